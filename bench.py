@@ -1,0 +1,385 @@
+#!/usr/bin/env python
+"""Benchmark of the fused-region path (BASELINE.json metric) — one JSON line.
+
+Default workload = BASELINE.json configs[1], Black-Scholes on 2^28 options in
+fp32 (the headline config; it fits one B200).  A "step" is one pass of the hot
+path over one batch: record the pricing expression on device-resident inputs
+and force call+put, which runs as ONE fused kernel.
+
+  value     elements/s with inputs resident in HBM, CUDA-event timed on the
+            runtime stream, K steps bracketed by barrier + sync, max over ranks
+  e2e       the same through the public API from pinned host buffers:
+            H2D of S,X,T + kernel + D2H of call,put every step
+  roofline  algorithmic bytes per launch / mean kernel time (CUDA events)
+            against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the oracle (eager NumPy, the paper's baseline) on a bounded
+            sample on this host, rank 0 only
+
+``--impl reference`` times the reference CPU path (eager NumPy evaluated over
+a blocked partition on all host cores) instead.
+
+Multi-GPU: launched by torchrun; one process per GPU; every rank prices its own
+2^28-option partition (weak scaling, no data-path collective for this map);
+timing barrier/max via a gloo process group.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+BASE = json.load(open(os.path.join(REPO, "BASELINE.json")))
+METRIC = BASE["metric"]
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (timing only)
+# ---------------------------------------------------------------------------
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch.distributed as td
+            td.init_process_group("gloo")
+            self.td = td
+
+    def barrier(self):
+        if self.world > 1:
+            self.td.barrier()
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.td.all_reduce(t, op=self.td.ReduceOp.MAX)
+        return float(t.item())
+
+    def close(self):
+        if self.world > 1:
+            self.td.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# workloads
+# ---------------------------------------------------------------------------
+def _bs_setup(n, dtype, seed):
+    from paper_1901_03771_b200 import workloads as wl
+    return wl.blackscholes_inputs(n=n, seed=seed, dtype=dtype)
+
+
+WORKLOADS = {
+    "blackscholes-f32": dict(n=1 << 28, dtype=np.float32, desc="Black-Scholes call+put, 2^28 options, fp32",
+                              bytes_per_elem=5 * 4, label="f32"),
+    "blackscholes-f64": dict(n=1 << 28, dtype=np.float64, desc="Black-Scholes call+put, 2^28 options, fp64",
+                              bytes_per_elem=5 * 8, label="f64"),
+    "listing1": dict(n=1 << 24, dtype=np.float64, desc="paper Listing 1 chain (4 mul + 2 add), 2^24 fp64",
+                     bytes_per_elem=4 * 8, label="f64"),
+}
+
+
+def make_program(name):
+    from paper_1901_03771_b200 import workloads as wl
+    if name.startswith("blackscholes"):
+        def prog(xp, arrs):
+            return wl.blackscholes(xp, *arrs)
+        return prog
+    if name == "listing1":
+        def prog(xp, arrs):
+            return (wl.listing1(xp, *arrs),)
+        return prog
+    raise KeyError(name)
+
+
+def make_inputs(name, n, seed):
+    from paper_1901_03771_b200 import workloads as wl
+    w = WORKLOADS[name]
+    if name.startswith("blackscholes"):
+        return wl.blackscholes_inputs(n=n, seed=seed, dtype=w["dtype"])
+    if name == "listing1":
+        return wl.listing1_inputs(n=n, seed=seed, dtype=w["dtype"])
+    raise KeyError(name)
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle = the paper's eager NumPy baseline)
+# ---------------------------------------------------------------------------
+def cpu_time(name, sample, threads, reps):
+    """Eager NumPy over a blocked partition of `sample` elements on `threads`
+    threads (NumPy releases the GIL inside ufunc loops)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    inputs = make_inputs(name, sample, seed=7)
+    prog = make_program(name)
+    blocks = max(threads, 1) * 4
+    edges = np.linspace(0, sample, blocks + 1).astype(np.int64)
+
+    def work(i):
+        lo, hi = edges[i], edges[i + 1]
+        return prog(np, [x[lo:hi] for x in inputs])
+
+    best = float("inf")
+    with ThreadPoolExecutor(max_workers=max(threads, 1)) as ex:
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            if threads <= 1:
+                prog(np, inputs)
+            else:
+                list(ex.map(work, range(blocks)))
+            best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def run_reference(args, dist):
+    """--impl reference: the reference's CPU path on all host cores (rank 0)."""
+    if dist.rank != 0:
+        return
+    w = WORKLOADS[args.workload]
+    cores = len(os.sched_getaffinity(0))
+    sample = args.cpu_sample or min(w["n"], 1 << 24)
+    for _ in range(args.warmup):
+        cpu_time(args.workload, sample, cores, 1)
+    times = [cpu_time(args.workload, sample, cores, 1) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    value = sample / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": w["label"],
+        "data": "synthetic (numpy default_rng)",
+        "config": {"workload": w["desc"], "sample_elements": sample},
+        "cpu_baseline": {"value": value, "unit": "elements/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} elements per step, eager NumPy over {cores} threads (blocked partition)"},
+        "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+def run_grumpy(args, dist):
+    import paper_1901_03771_b200 as gp
+    from paper_1901_03771_b200 import runtime
+
+    os.environ.setdefault("GRUMPY_DEVICE", str(dist.local_rank))
+    rt = runtime.get()
+    w = WORKLOADS[args.workload]
+    n = w["n"] if args.scaling == "weak" else w["n"] // dist.world
+    prog = make_program(args.workload)
+    sess = gp.Session()
+    gp.set_default_session(sess)
+
+    host = make_inputs(args.workload, n, seed=42 + dist.rank)
+    dev = [gp.asarray(x) for x in host]
+    for d in dev:  # upload once (not timed)
+        d.node.data.device = rt.upload(d.node.data.host)
+
+    # warmup (includes NVRTC compile on the first step)
+    t0 = time.perf_counter()
+    outs = prog(gp, dev)
+    gp.force(*outs)
+    rt.sync()
+    cold_s = time.perf_counter() - t0
+    for _ in range(max(args.warmup - 1, 0)):
+        outs = prog(gp, dev)
+        gp.force(*outs)
+    rt.sync()
+
+    # timed region: K steps, per-step events around each force
+    k0 = sess.stats.kernels_executed
+    clocks = Clocks(dist.local_rank)
+    evs = [(rt.event(), rt.event()) for _ in range(args.steps)]
+    e_all0, e_all1 = rt.event(), rt.event()
+    dist.barrier()
+    rt.sync()
+    clocks.start()
+    rt.record(e_all0)
+    keep = []
+    for i in range(args.steps):
+        rt.record(evs[i][0])
+        outs = prog(gp, dev)
+        gp.force(*outs)
+        rt.record(evs[i][1])
+        keep.append(outs)
+        if len(keep) > 2:
+            keep.pop(0)
+    rt.record(e_all1)
+    rt.sync()
+    clk = clocks.stop()
+    dist.barrier()
+    launches = sess.stats.kernels_executed - k0
+    total_ms = rt.elapsed_ms(e_all0, e_all1)
+    kern_ms = [rt.elapsed_ms(a, b) for a, b in evs]
+    total_ms = dist.max(total_ms)
+    kmean = statistics.mean(kern_ms)
+    del keep
+
+    elements = n * dist.world
+    value = elements / (total_ms / 1e3)
+    peak, peak_src = peaks()
+    alg_bytes = n * w["bytes_per_elem"]
+    achieved = alg_bytes / (kmean / 1e3) / 1e9
+
+    # e2e through the public API from pinned host memory
+    pinned_in = []
+    for x in host:
+        p = rt.pinned_empty(x.shape, x.dtype)
+        p[...] = x
+        pinned_in.append(p)
+    outs0 = prog(gp, dev)
+    pinned_out = [rt.pinned_empty(o.shape, o.dtype) for o in outs0]
+    del outs0
+    h2d = sum(x.nbytes for x in pinned_in)
+    d2h = sum(x.nbytes for x in pinned_out)
+    e2e_steps = max(1, min(args.steps, args.e2e_steps))
+    for it in range(1 + e2e_steps):
+        if it == 1:
+            dist.barrier()
+            rt.sync()
+            t0 = time.perf_counter()
+        arrs = [gp.asarray(x) for x in pinned_in]
+        outs = prog(gp, arrs)
+        gp.force(*outs)
+        for o, dst in zip(outs, pinned_out):
+            o.numpy(out=dst)
+    rt.sync()
+    e2e_s = dist.max(time.perf_counter() - t0)
+    e2e_value = elements * e2e_steps / e2e_s
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": dist.world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": w["label"],
+        "data": "synthetic (numpy default_rng, seed 42+rank)",
+        "config": {"workload": w["desc"], "elements_per_gpu": n, "parallelism": f"shard{dist.world}",
+                   "l2": "inputs (%.1f GiB/GPU) larger than the 126 MB L2; no flush" % (alg_bytes / 2**30)},
+        "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _traffic(args.workload),
+                     "peak_source": peak_src, "kernel_ms": kmean,
+                     "algorithmic_bytes_per_launch": alg_bytes},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "cold_first_step_s": cold_s,
+        "device": rt.name,
+    }
+    if dist.rank == 0 and not args.no_cpu_baseline:
+        sample = args.cpu_sample or min(n, 1 << 24)
+        t = cpu_time(args.workload, sample, 1, 2)
+        line["cpu_baseline"] = {"value": sample / t, "unit": "elements/s", "cores": 1, "kind": "port",
+                                "sample": f"{sample} elements, eager NumPy (oracle) single thread, best of 2"}
+    if dist.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def _traffic(workload):
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(workload)
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="grumpy", choices=["grumpy", "reference"])
+    ap.add_argument("--workload", default="blackscholes-f32", choices=sorted(WORKLOADS))
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, dist)
+        else:
+            run_grumpy(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,709 @@
+"""kernel-lowering + code generation: region → CUDA C++ for the sm_100a skeletons.
+
+Reference module ``kernel-lowering``:
+``lower`` builds an iteration space from the root shape
+and composes index maps root→leaves for transpose, slice, broadcast and reshape
+(PAPER.md:463-483); constants are splatted into the body
+(SPEC.md:337).  The spec then interprets or natively emits the point program
+("execution strategy ... is an implementation decision").
+
+The B200 path always emits native code: the point program becomes C++ calls to
+the hand-written device-function templates in ``csrc/kernels/gr_ops.cuh`` and is
+instantiated into a hand-written fused-loop skeleton (``gr_map.cuh`` …), then
+compiled by NVRTC for sm_100a through the C-ABI shim.
+
+Index maps are kept *symbolic and affine* (``Aff``: Σ coef·var + const over the
+kernel's coordinate variables); reshapes that cannot stay affine introduce
+derived div/mod variables.  Every emitted value records the set of loop
+variables it depends on and is placed in the outermost scope where those are
+bound — constants at kernel scope, per-group values once per group, per-point
+values inside the vector-lane loop — so broadcast operands and row-level
+values are computed once, not once per point.
+"""
+
+from __future__ import annotations
+
+import math
+import struct
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from .dag import ElemCode, Node, OpKind
+from .errors import UnsupportedNodeInFusedStep
+from .tensor import DType, element_count, row_major_strides
+
+# ---------------------------------------------------------------------------
+# Coordinate algebra
+# ---------------------------------------------------------------------------
+
+
+class Var:
+    """A coordinate variable of the generated kernel.
+
+    ``level`` is the scope that binds it (0 kernel, 1 group, 2 lane, 3+ loops);
+    ``align`` a known divisor of its value.
+    """
+
+    __slots__ = ("name", "level", "align", "ctype")
+
+    def __init__(self, name, level, align=1, ctype="long long"):
+        self.name = name
+        self.level = level
+        self.align = align
+        self.ctype = ctype
+
+    def __repr__(self):
+        return self.name
+
+
+class Aff:
+    """Affine integer expression Σ coef·var + const (immutable)."""
+
+    __slots__ = ("terms", "const")
+
+    def __init__(self, terms=(), const=0):
+        # terms: tuple of (Var, coef) with coef != 0, sorted by name
+        self.terms = terms
+        self.const = const
+
+    @staticmethod
+    def of(x):
+        if isinstance(x, Aff):
+            return x
+        if isinstance(x, Var):
+            return Aff(((x, 1),), 0)
+        return Aff((), int(x))
+
+    def __add__(self, other):
+        o = Aff.of(other)
+        d = {v.name: [v, c] for v, c in self.terms}
+        for v, c in o.terms:
+            if v.name in d:
+                d[v.name][1] += c
+            else:
+                d[v.name] = [v, c]
+        terms = tuple(sorted(((v, c) for v, c in d.values() if c != 0), key=lambda t: t[0].name))
+        return Aff(terms, self.const + o.const)
+
+    def scale(self, k):
+        k = int(k)
+        if k == 0:
+            return Aff((), 0)
+        return Aff(tuple((v, c * k) for v, c in self.terms), self.const * k)
+
+    def coef(self, var):
+        for v, c in self.terms:
+            if v is var:
+                return c
+        return 0
+
+    @property
+    def is_const(self):
+        return not self.terms
+
+    @property
+    def level(self):
+        return max((v.level for v, _ in self.terms), default=0)
+
+    def without(self, var):
+        return Aff(tuple((v, c) for v, c in self.terms if v is not var), self.const)
+
+    def alignment(self):
+        """Largest known divisor of the value (0 when identically 0)."""
+        g = abs(self.const)
+        for v, c in self.terms:
+            g = math.gcd(g, abs(c) * v.align)
+        return g
+
+    def key(self):
+        return (tuple((v.name, c) for v, c in self.terms), self.const)
+
+    def c(self, ctype="long long"):
+        parts = []
+        for v, c in self.terms:
+            if c == 1:
+                parts.append(v.name)
+            elif c == -1:
+                parts.append(f"-{v.name}")
+            else:
+                parts.append(f"{c}*{v.name}")
+        if self.const or not parts:
+            parts.append(str(self.const))
+        s = " + ".join(parts).replace("+ -", "- ")
+        return f"({s})"
+
+
+def bcast_coords(coords: Sequence[Aff], out_shape, in_shape) -> List[Aff]:
+    """Right-aligned broadcast index map (SPEC.md:70, 284 'constant 0')."""
+    off = len(out_shape) - len(in_shape)
+    return [Aff.of(0) if in_shape[d] == 1 else coords[off + d] for d in range(len(in_shape))]
+
+
+# ---------------------------------------------------------------------------
+# Literal formatting (bit-exact constants)
+# ---------------------------------------------------------------------------
+
+
+def c_literal(value, dtype: DType) -> str:
+    if dtype is DType.f32:
+        (u,) = struct.unpack("<I", struct.pack("<f", float(value)))
+        return f"gr::f32_bits(0x{u:08x}u)"
+    if dtype is DType.f64:
+        (u,) = struct.unpack("<Q", struct.pack("<d", float(value)))
+        return f"gr::f64_bits(0x{u:016x}ull)"
+    if dtype is DType.i32:
+        v = int(value)
+        return "(-2147483647 - 1)" if v == -(2**31) else f"{v}"
+    if dtype is DType.i64:
+        v = int(value)
+        return "(-9223372036854775807LL - 1)" if v == -(2**63) else f"{v}LL"
+    return "true" if value else "false"
+
+
+_BIN = {
+    ElemCode.add: "gr::add<{T}>", ElemCode.sub: "gr::sub<{T}>", ElemCode.mul: "gr::mul<{T}>",
+    ElemCode.div: "gr::div<{T}>", ElemCode.floordiv: "gr::floordiv<{T}>", ElemCode.mod: "gr::mod<{T}>",
+    ElemCode.pow: "gr::pow_<{T}>", ElemCode.maximum: "gr::maximum<{T}>", ElemCode.minimum: "gr::minimum<{T}>",
+    ElemCode.cmp_lt: "gr::lt<{T}>", ElemCode.cmp_gt: "gr::gt<{T}>", ElemCode.cmp_le: "gr::le<{T}>",
+    ElemCode.cmp_ge: "gr::ge<{T}>", ElemCode.cmp_eq: "gr::eq<{T}>", ElemCode.cmp_ne: "gr::ne<{T}>",
+    ElemCode.logical_and: "gr::land<{T}>", ElemCode.logical_or: "gr::lor<{T}>",
+    ElemCode.logical_xor: "gr::lxor<{T}>",
+}
+_UN = {
+    ElemCode.neg: "gr::neg<{T}>", ElemCode.abs: "gr::abs_", ElemCode.exp: "gr::exp_",
+    ElemCode.log: "gr::log_", ElemCode.sqrt: "gr::sqrt_", ElemCode.square: "gr::square<{T}>",
+    ElemCode.sin: "gr::sin_", ElemCode.cos: "gr::cos_", ElemCode.tanh: "gr::tanh_",
+    ElemCode.erf: "gr::erf_", ElemCode.floor: "gr::floor_", ElemCode.ceil: "gr::ceil_",
+    ElemCode.isnan: "gr::isnan_<{T}>", ElemCode.logical_not: "gr::lnot<{T}>",
+}
+
+
+# ---------------------------------------------------------------------------
+# Region descriptor
+# ---------------------------------------------------------------------------
+
+
+class Region:
+    """A fused step: roots (outputs), interior nodes, leaves (inputs).
+
+    Leaves are nodes whose values come from buffers at execution time
+    (materialized before the step runs, SPEC.md:195 leaves-only invariant).
+    """
+
+    def __init__(self, roots: Sequence[Node], leaves: Sequence[Node], nodes: Sequence[Node]):
+        self.roots = list(roots)
+        self.leaves = list(leaves)
+        self.nodes = list(nodes)
+        self.leaf_ids = {n.id for n in self.leaves}
+
+    def __repr__(self):
+        return f"Region(roots={[r.id for r in self.roots]}, leaves={[l.id for l in self.leaves]}, n={len(self.nodes)})"
+
+
+# ---------------------------------------------------------------------------
+# Generated kernel description
+# ---------------------------------------------------------------------------
+
+
+class KernelSource:
+    """Generated source plus everything the executor needs to launch it."""
+
+    def __init__(self, family, source, name, leaf_slots, root_slots, block, groups, vec, unroll,
+                 scratch_bytes=0, meta=None):
+        self.family = family
+        self.source = source
+        self.name = name
+        self.leaf_slots = leaf_slots    # list of leaf positions (index into region.leaves)
+        self.root_slots = root_slots    # list of root positions (index into region.roots)
+        self.block = block
+        self.groups = groups            # number of work items the grid walks
+        self.vec = vec
+        self.unroll = unroll
+        self.scratch_bytes = scratch_bytes
+        self.meta = meta or {}
+
+
+# ---------------------------------------------------------------------------
+# Value emission shared by all families
+# ---------------------------------------------------------------------------
+
+
+class ValueEmitter:
+    """Emits C++ for node values at symbolic coordinates.
+
+    Subclasses decide where statements go (``place``) and how leaves are
+    loaded (``load_leaf``).  A value is (expr, level): the C expression naming
+    it and the deepest scope level it depends on.
+    """
+
+    def __init__(self, region: Region):
+        self.region = region
+        self.memo: Dict[tuple, Tuple[str, int]] = {}
+        self.counter = 0
+        self.leaf_index = {n.id: i for i, n in enumerate(region.leaves)}
+        self.consts: List[str] = []
+        self.const_memo: Dict[tuple, str] = {}
+
+    def fresh(self, prefix="t"):
+        self.counter += 1
+        return f"{prefix}{self.counter}"
+
+    # -- to implement
+    def emit(self, level: int, ctype: str, expr: str) -> str:
+        raise NotImplementedError
+
+    def load_leaf(self, leaf: Node, offset: Aff) -> Tuple[str, int]:
+        raise NotImplementedError
+
+    # -- shared
+    def const(self, value, dtype: DType) -> Tuple[str, int]:
+        key = (value, dtype)
+        if key not in self.const_memo:
+            name = self.fresh("k")
+            self.consts.append(f"const {dtype.ctype} {name} = {c_literal(value, dtype)};  // {value!r}")
+            self.const_memo[key] = name
+        return self.const_memo[key], 0
+
+    def cast(self, val: Tuple[str, int], frm: DType, to: DType) -> Tuple[str, int]:
+        if frm is to:
+            return val
+        expr, lvl = val
+        return self.emit(lvl, to.ctype, f"gr::cast<{to.ctype}, {frm.ctype}>({expr})"), lvl
+
+    def value(self, n: Node, coords: Sequence[Aff]) -> Tuple[str, int]:
+        key = (n.id, tuple(c.key() for c in coords))
+        hit = self.memo.get(key)
+        if hit is not None:
+            return hit
+        v = self._value(n, list(coords))
+        self.memo[key] = v
+        return v
+
+    def _value(self, n: Node, coords: List[Aff]) -> Tuple[str, int]:
+        if n.id in self.leaf_index:
+            st = row_major_strides(n.shape)
+            off = Aff.of(0)
+            for c, s, ext in zip(coords, st, n.shape):
+                if ext != 1:
+                    off = off + c.scale(s)
+            return self.load_leaf(n, off)
+        k = n.op.kind
+        if k is OpKind.MAP:
+            code = n.op.code
+            if code is ElemCode.const_splat:
+                return self.const(n.op.attrs[0], n.dtype)
+            args = []
+            for p, lt in zip(n.preds, n.loop):
+                v = self.value(p, bcast_coords(coords, n.shape, p.shape))
+                args.append(self.cast(v, p.dtype, lt))
+            lvl = max(a[1] for a in args)
+            names = [a[0] for a in args]
+            if code is ElemCode.select:
+                T = n.dtype.ctype
+                expr = f"gr::select<{T}>({names[0]}, {names[1]}, {names[2]})"
+            elif code in _BIN:
+                T = n.loop[0].ctype
+                expr = _BIN[code].format(T=T) + f"({names[0]}, {names[1]})"
+            else:
+                T = n.loop[0].ctype
+                expr = _UN[code].format(T=T) + f"({names[0]})"
+            return self.emit(lvl, n.dtype.ctype, expr), lvl
+        if k is OpKind.CAST:
+            (p,) = n.preds
+            return self.cast(self.value(p, coords), p.dtype, n.dtype)
+        if k is OpKind.TRANSPOSE:
+            (perm,) = n.op.attrs
+            (p,) = n.preds
+            pc = [None] * len(perm)
+            for i, ax in enumerate(perm):
+                pc[ax] = coords[i]
+            return self.value(p, pc)
+        if k is OpKind.BROADCAST:
+            (p,) = n.preds
+            return self.value(p, bcast_coords(coords, n.shape, p.shape))
+        if k is OpKind.SLICE:
+            (sl,) = n.op.attrs
+            (p,) = n.preds
+            pc = [c.scale(step) + start for c, (start, step, _l) in zip(coords, sl)]
+            return self.value(p, pc)
+        if k is OpKind.RESHAPE:
+            (p,) = n.preds
+            return self.value(p, self.reshape_coords(coords, n.shape, p.shape))
+        if k is OpKind.SLICE_ASSIGN:
+            return self.slice_assign(n, coords)
+        raise UnsupportedNodeInFusedStep(f"{n.op!r} cannot appear inside this fused step")
+
+    def reshape_coords(self, coords, out_shape, in_shape) -> List[Aff]:
+        """Index map through Reshape: linearize over the
+        output shape, delinearize over the input shape; stays affine when the
+        dims regroup without merging (splits, unit dims)."""
+        out_shape = list(out_shape)
+        in_shape = list(in_shape)
+        res: List[Optional[Aff]] = [None] * len(in_shape)
+        i = j = 0
+        while i < len(out_shape) or j < len(in_shape):
+            # grow blocks until products match
+            bi, bj = [i], [j]
+            po = out_shape[i] if i < len(out_shape) else 1
+            pi = in_shape[j] if j < len(in_shape) else 1
+            i += 1
+            j += 1
+            while po != pi:
+                if po < pi:
+                    bi.append(i)
+                    po *= out_shape[i]
+                    i += 1
+                else:
+                    bj.append(j)
+                    pi *= in_shape[j]
+                    j += 1
+            bi = [x for x in bi if x < len(out_shape)]
+            bj = [x for x in bj if x < len(in_shape)]
+            # linear index within the block over the output dims
+            lin = Aff.of(0)
+            acc = 1
+            for x in reversed(bi):
+                lin = lin + coords[x].scale(acc)
+                acc *= out_shape[x]
+            nonunit = [x for x in bj if in_shape[x] != 1]
+            for x in bj:
+                res[x] = Aff.of(0)
+            if len(nonunit) <= 1:
+                if nonunit:
+                    res[nonunit[0]] = lin
+                continue
+            # merge: delinearize with div/mod (derived variables)
+            lvl = lin.level
+            rest = lin
+            for x in reversed(nonunit):
+                ext = in_shape[x]
+                if x == nonunit[0]:
+                    res[x] = rest
+                else:
+                    q = self.derived_var(lvl, f"{rest.c()} % {ext}")
+                    res[x] = Aff.of(q)
+                    rest = Aff.of(self.derived_var(lvl, f"{rest.c()} / {ext}"))
+        return [r if r is not None else Aff.of(0) for r in res]
+
+    def derived_var(self, level, expr) -> Var:
+        name = self.emit(level, "long long", expr)
+        return Var(name, level)
+
+    def slice_assign(self, n: Node, coords):
+        """SliceAssign lowers to select(in-region, value-branch, target-branch)
+        (SPEC.md:304, 336).  Value-branch coordinates are clamped so the load
+        stays in bounds when the predicate is false."""
+        (region,) = n.op.attrs
+        target, val = n.preds
+        conds = []
+        vcoords = []
+        lvl = 0
+        for c, (start, step, length) in zip(coords, region):
+            rel = (c + (-start))
+            lvl = max(lvl, c.level)
+            if step == 1:
+                conds.append(f"({rel.c()} >= 0 && {rel.c()} < {length})")
+                q = self.derived_var(c.level, f"min(max({rel.c()}, 0LL), {max(length - 1, 0)}LL)")
+            else:
+                conds.append(f"({rel.c()} % {step} == 0 && {rel.c()} / {step} >= 0 && {rel.c()} / {step} < {length})")
+                q = self.derived_var(c.level, f"min(max({rel.c()} / {step}, 0LL), {max(length - 1, 0)}LL)")
+            vcoords.append(Aff.of(q))
+        pred = self.emit(lvl, "bool", " && ".join(conds) if conds else "true")
+        vv = self.cast(self.value(val, bcast_coords(vcoords, tuple(r[2] for r in region), val.shape)),
+                       val.dtype, n.dtype)
+        tv = self.value(target, coords)
+        lv = max(lvl, vv[1], tv[1])
+        return self.emit(lv, n.dtype.ctype, f"gr::select<{n.dtype.ctype}>({pred}, {vv[0]}, {tv[0]})"), lv
+
+
+# ---------------------------------------------------------------------------
+# Family K1: flat map
+# ---------------------------------------------------------------------------
+
+HEADER = '#include "gr_ops.cuh"\n#include "gr_mem.cuh"\n'
+
+LEVEL_KERNEL, LEVEL_GROUP, LEVEL_LANE = 0, 1, 2
+
+
+class MapEmitter(ValueEmitter):
+    """Three scopes: kernel constants, per-group (arrays indexed by u), per-lane."""
+
+    def __init__(self, region, vec, vars_group, lane_var):
+        super().__init__(region)
+        self.vec = vec
+        self.group_lines: List[str] = []   # executed for each u, values stored in [u] arrays
+        self.group_decls: List[str] = []   # array declarations
+        self.lane_lines: List[str] = []
+        self.lane_var = lane_var
+
+    def emit(self, level, ctype, expr):
+        name = self.fresh()
+        if level <= LEVEL_KERNEL:
+            self.consts.append(f"const {ctype} {name} = {expr};")
+            return name
+        if level == LEVEL_GROUP:
+            self.group_decls.append(f"{ctype} {name}[N];")
+            self.group_lines.append(f"{name}[u] = {expr};")
+            return f"{name}[u]"
+        self.lane_lines.append(f"const {ctype} {name} = {expr};")
+        return name
+
+    def derived_var(self, level, expr):
+        name = self.emit(level, "long long", expr)
+        return Var(name, level)
+
+    def load_leaf(self, leaf: Node, off: Aff):
+        idx = self.leaf_index[leaf.id]
+        T = leaf.dtype.ctype
+        ptr = f"p.in{idx}"
+        lvl = off.level
+        lane = self.lane_var
+        if lvl < LEVEL_LANE:
+            return self.emit(lvl, T, f"gr::ld<{T}>({ptr} + {off.c()})"), lvl
+        cv = off.coef(lane)
+        rest = off.without(lane)
+        if cv == 1 and self.vec > 1 and rest.level < LEVEL_LANE and (rest.alignment() % self.vec == 0):
+            name = self.fresh("L")
+            self.group_decls.append(f"{T} {name}[N][{self.vec}];")
+            self.group_lines.append(f"gr::ldv<{T}, {self.vec}>({name}[u], {ptr} + {rest.c()});")
+            return f"{name}[u][v]", LEVEL_LANE
+        return self.emit(LEVEL_LANE, T, f"gr::ld<{T}>({ptr} + {off.c()})"), LEVEL_LANE
+
+
+def _index_ctype(region: Region) -> str:
+    big = max([element_count(r.shape) for r in region.roots] + [element_count(l.shape) for l in region.leaves])
+    return "long long" if big >= 2**31 - 64 else "int"
+
+
+def choose_vec(region: Region, shape) -> int:
+    sizes = [r.dtype.itemsize for r in region.roots] + [l.dtype.itemsize for l in region.leaves]
+    vec = max(1, 16 // max(sizes))
+    n = element_count(shape)
+    if not shape or n == 0:
+        return 1
+    if len(shape) > 1 and shape[-1] % vec != 0:
+        # fall back to the largest power of two dividing the innermost extent
+        v = vec
+        while v > 1 and shape[-1] % v != 0:
+            v //= 2
+        vec = v
+    return vec
+
+
+def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> KernelSource:
+    """Family K1: every root has the same shape S; out[p] = point(p)."""
+    shape = tuple(region.roots[0].shape)
+    for r in region.roots:
+        if tuple(r.shape) != shape:
+            raise UnsupportedNodeInFusedStep("map roots must share one shape")
+    n = element_count(shape)
+    vec = choose_vec(region, shape)
+    ngroups = n // vec
+    tail = n - ngroups * vec
+    ictype = _index_ctype(region)
+    # dtype-dependent unroll: keep ~64 B in flight per thread per leaf stream
+    if unroll is None:
+        unroll = 2 if max(r.dtype.itemsize for r in region.roots) >= 8 else 1
+    rank = len(shape)
+
+    def build(mode):
+        lane = Var("v", LEVEL_LANE)
+        em = MapEmitter(region, vec if mode == "group" else 1, None, lane)
+        coords: List[Aff] = []
+        if rank == 0:
+            lin0 = Aff.of(0)
+        else:
+            # group-level coordinates from the linear start of the group
+            pass
+            inner = shape[-1]
+            if rank == 1:
+                cin = Var("lin", LEVEL_GROUP if mode == "group" else LEVEL_LANE, align=vec if mode == "group" else 1)
+                coords = [Aff.of(cin) + (Aff.of(lane) if mode == "group" else Aff.of(0))]
+            else:
+                base = em.emit(LEVEL_GROUP if mode == "group" else LEVEL_LANE, ictype, f"lin % {inner}")
+                cin = Var(base, LEVEL_GROUP if mode == "group" else LEVEL_LANE,
+                          align=vec if mode == "group" else 1)
+                outer: List[Aff] = []
+                rest = em.emit(LEVEL_GROUP if mode == "group" else LEVEL_LANE, ictype, f"lin / {inner}")
+                for d in range(rank - 2, -1, -1):
+                    ext = shape[d]
+                    lvl = LEVEL_GROUP if mode == "group" else LEVEL_LANE
+                    if ext == 1:
+                        outer.append(Aff.of(0))
+                        continue
+                    if d == 0:
+                        outer.append(Aff.of(Var(rest, lvl)))
+                    else:
+                        c = em.emit(lvl, ictype, f"{rest} % {ext}")
+                        outer.append(Aff.of(Var(c, lvl)))
+                        rest = em.emit(lvl, ictype, f"{rest} / {ext}")
+                outer.reverse()
+                coords = outer + [Aff.of(cin) + (Aff.of(lane) if mode == "group" else Aff.of(0))]
+        outs = []
+        for ri, r in enumerate(region.roots):
+            val = em.value(r, coords)
+            outs.append(val)
+        return em, outs
+
+    # ---- group body (vectorised)
+    em, outs = build("group")
+    lines = []
+    lines.append("template <int N> static __device__ __forceinline__ void group(const Params& p, long long g0, long long stride) {")
+    for d in em.group_decls:
+        lines.append("  " + d)
+    lines.append("#pragma unroll")
+    lines.append("  for (int u = 0; u < N; ++u) {")
+    lines.append(f"    const {ictype} lin = ({ictype})(g0 + u * stride) * {vec}; (void)lin;")
+    for l in em.group_lines:
+        lines.append("    " + l)
+    lines.append("  }")
+    lines.append("#pragma unroll")
+    lines.append("  for (int u = 0; u < N; ++u) {")
+    lines.append(f"    const {ictype} lin = ({ictype})(g0 + u * stride) * {vec}; (void)lin;")
+    for ri, r in enumerate(region.roots):
+        lines.append(f"    {r.dtype.ctype} o{ri}[{vec}];")
+    lines.append("#pragma unroll")
+    lines.append(f"    for (int v = 0; v < {vec}; ++v) {{")
+    for l in em.lane_lines:
+        lines.append("      " + l)
+    for ri, (r, (expr, _lvl)) in enumerate(zip(region.roots, outs)):
+        lines.append(f"      o{ri}[v] = {expr};")
+    lines.append("    }")
+    for ri, r in enumerate(region.roots):
+        T = r.dtype.ctype
+        if vec > 1:
+            lines.append(f"    gr::stv<{T}, {vec}>(p.out{ri} + lin, o{ri});")
+        else:
+            lines.append(f"    gr::st<{T}>(p.out{ri} + lin, o{ri}[0]);")
+    lines.append("  }")
+    lines.append("}")
+    consts = list(em.consts)
+
+    # ---- scalar tail (rank-1 spaces whose length is not a multiple of VEC)
+    tail_lines = ["static __device__ __forceinline__ void tail(const Params& p) {"]
+    if tail:
+        em2, outs2 = build("tail")
+        consts2 = em2.consts
+        tail_lines.append(f"  for (int v = 0; v < {tail}; ++v) {{")
+        tail_lines.append("    const int u = 0; (void)u;")
+        tail_lines.append(f"    const {ictype} lin = ({ictype}){ngroups * vec} + v; (void)lin;")
+        for l in consts2:
+            tail_lines.append("    " + l)
+        for d in em2.group_decls:
+            tail_lines.append("    " + d.replace("[N]", "[1]"))
+        for l in em2.group_lines:
+            tail_lines.append("    " + l)
+        for l in em2.lane_lines:
+            tail_lines.append("    " + l)
+        for ri, (r, (expr, _)) in enumerate(zip(region.roots, outs2)):
+            tail_lines.append(f"    gr::st<{r.dtype.ctype}>(p.out{ri} + lin, {expr});")
+        tail_lines.append("  }")
+    tail_lines.append("}")
+
+    params = _params_struct(region)
+    src = [HEADER, '#include "gr_map.cuh"\n', "struct K {", params,
+           f"  static constexpr long long NGROUPS = {ngroups}LL;",
+           f"  static constexpr int U = {unroll};",
+           f"  static constexpr bool TAIL = {'true' if tail else 'false'};"]
+    src.append("  " + "\n  ".join(_wrap_consts(lines, consts)))
+    src.append("  " + "\n  ".join(tail_lines))
+    src.append("};")
+    src.append(f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{ gr::map_kernel<K>(p); }}')
+    return KernelSource("map", "\n".join(src) + "\n", kname,
+                        leaf_slots=list(range(len(region.leaves))),
+                        root_slots=list(range(len(region.roots))),
+                        block=block, groups=ngroups, vec=vec, unroll=unroll,
+                        meta={"shape": shape, "tail": tail})
+
+
+def _wrap_consts(fn_lines, consts):
+    """Insert kernel-level constants at the top of a generated function body."""
+    out = [fn_lines[0]]
+    out += ["  " + c for c in consts]
+    out += fn_lines[1:]
+    return out
+
+
+def _params_struct(region: Region) -> str:
+    fields = []
+    for i, l in enumerate(region.leaves):
+        fields.append(f"const {l.dtype.ctype}* __restrict__ in{i};")
+    for i, r in enumerate(region.roots):
+        fields.append(f"{r.dtype.ctype}* __restrict__ out{i};")
+    fields.append("void* __restrict__ scratch;")
+    return "  struct Params {\n    " + "\n    ".join(fields) + "\n  };"
+
+
+# ---------------------------------------------------------------------------
+# Region canonicalisation, signatures, dispatch
+# ---------------------------------------------------------------------------
+
+
+def canonicalize(region: Region) -> Region:
+    """Order leaves by first visit in a DFS from the roots so structurally equal
+    regions produce identical kernels and parameter layouts."""
+    leaf_ids = {l.id: l for l in region.leaves}
+    order: List[Node] = []
+    seen = set()
+    stack = list(reversed(region.roots))
+    while stack:
+        n = stack.pop()
+        if n.id in seen:
+            continue
+        seen.add(n.id)
+        if n.id in leaf_ids:
+            order.append(n)
+            continue
+        for p in reversed(n.preds):
+            stack.append(p)
+    for l in region.leaves:  # leaves only reachable through pruned paths
+        if l.id not in seen:
+            order.append(l)
+    return Region(region.roots, order, region.nodes)
+
+
+def signature(region: Region) -> tuple:
+    """Structural key: equal keys ⇒ identical generated source."""
+    local: Dict[int, int] = {}
+    items = []
+    leaf_pos = {l.id: i for i, l in enumerate(region.leaves)}
+
+    def visit(n: Node) -> int:
+        if n.id in local:
+            return local[n.id]
+        if n.id in leaf_pos:
+            idx = len(items)
+            items.append(("leaf", leaf_pos[n.id], n.shape, n.dtype.value))
+        else:
+            ps = tuple(visit(p) for p in n.preds)
+            idx = len(items)
+            items.append((repr(n.op), n.shape, n.dtype.value, ps,
+                          tuple(d.value for d in n.loop) if n.loop else None))
+        local[n.id] = idx
+        return idx
+
+    roots = tuple(visit(r) for r in region.roots)
+    return (tuple(items), roots)
+
+
+def needs_launch_when_empty(region: Region) -> bool:
+    return False
+
+
+def row_fusable(reduction: Node, consumer: Node) -> bool:
+    """Planner hook: may ``reduction`` stay inside ``consumer``'s kernel?"""
+    return False
+
+
+def generate(region: Region) -> KernelSource:
+    kinds = {r.op.kind for r in region.roots}
+    if kinds & {OpKind.REDUCE, OpKind.ARGREDUCE, OpKind.SCAN, OpKind.KEYED_SUM}:
+        raise UnsupportedNodeInFusedStep(f"no kernel family for roots {kinds} yet")
+    return gen_map(region)
+
+
+def grid_for(ks: KernelSource, sm_count: int, blocks_per_sm: int) -> int:
+    """Persistent grid: enough CTAs to cover the work, capped at one full wave
+    (SM count × resident CTAs per SM)."""
+    per_cta = ks.block * max(ks.unroll, 1)
+    need = max(1, -(-ks.groups // per_cta))
+    return int(max(1, min(need, sm_count * max(blocks_per_sm, 1))))

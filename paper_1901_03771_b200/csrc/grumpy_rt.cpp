@@ -1,0 +1,764 @@
+// libgrumpy_rt.so — C-ABI runtime shim for the fused-region path.
+//
+// Declared in include/grumpy_rt.h (which cites the reference interfaces each
+// export replaces).  Design:
+//   * CUDA driver API, loaded with dlopen("libcuda.so.1") + cuGetProcAddress so
+//     the library itself loads on machines without a driver (CPU CI checks the
+//     exports) and fails with GR_ENOINIT only when used;
+//   * one device, its primary context and ONE non-blocking stream per process
+//     (one process per GPU); kernels, copies, cuBLAS and NCCL all run on it, so
+//     stream order is the only synchronisation the pool needs;
+//   * NVRTC → cubin → cuModuleLoadData, cached in-process and on disk;
+//   * a caching device allocator with size classes;
+//   * cuBLAS for run_library (linked), NCCL via dlopen.
+#include "../../include/grumpy_rt.h"
+
+#include <cuda.h>
+#include <cublas_v2.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <sys/stat.h>
+#include <unistd.h>
+#include <unordered_map>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+// ---------------------------------------------------------------------------
+// Driver API table (resolved with cuGetProcAddress)
+// ---------------------------------------------------------------------------
+#define GR_CU_FUNCS(X)               \
+  X(cuInit)                          \
+  X(cuDeviceGetCount)                \
+  X(cuDeviceGet)                     \
+  X(cuDeviceGetAttribute)            \
+  X(cuDeviceGetName)                 \
+  X(cuDeviceTotalMem)                \
+  X(cuDevicePrimaryCtxRetain)        \
+  X(cuCtxSetCurrent)                 \
+  X(cuStreamCreate)                  \
+  X(cuStreamSynchronize)             \
+  X(cuMemAlloc)                      \
+  X(cuMemFree)                       \
+  X(cuMemcpyHtoDAsync)               \
+  X(cuMemcpyDtoHAsync)               \
+  X(cuMemcpyDtoDAsync)               \
+  X(cuMemsetD8Async)                 \
+  X(cuMemHostAlloc)                  \
+  X(cuMemFreeHost)                   \
+  X(cuMemHostRegister)               \
+  X(cuMemHostUnregister)             \
+  X(cuModuleLoadData)                \
+  X(cuModuleGetFunction)             \
+  X(cuFuncGetAttribute)              \
+  X(cuFuncSetAttribute)              \
+  X(cuOccupancyMaxActiveBlocksPerMultiprocessor) \
+  X(cuLaunchKernel)                  \
+  X(cuLaunchKernelEx)                \
+  X(cuEventCreate)                   \
+  X(cuEventRecord)                   \
+  X(cuEventSynchronize)              \
+  X(cuEventElapsedTime)              \
+  X(cuEventDestroy)                  \
+  X(cuGetErrorString)
+
+#define GR_DECL(name) decltype(&::name) p_##name = nullptr;
+struct Driver {
+  GR_CU_FUNCS(GR_DECL)
+  void* handle = nullptr;
+  bool loaded = false;
+};
+#undef GR_DECL
+Driver D;
+
+struct State {
+  bool init = false;
+  int device = -1;
+  CUdevice dev = 0;
+  CUcontext ctx = nullptr;
+  CUstream stream = nullptr;
+  int sm_count = 0;
+  cublasHandle_t cublas = nullptr;
+  std::mutex mu;
+} S;
+
+std::string cu_msg(CUresult r, const char* what) {
+  const char* s = nullptr;
+  if (D.p_cuGetErrorString) D.p_cuGetErrorString(r, &s);
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s failed: CUresult %d (%s)", what, (int)r, s ? s : "?");
+  return buf;
+}
+
+#define CU_CHECK(call, what)                                 \
+  do {                                                       \
+    CUresult _r = (call);                                    \
+    if (_r != CUDA_SUCCESS) return fail(GR_ECUDA, cu_msg(_r, what)); \
+  } while (0)
+
+int load_driver() {
+  if (D.loaded) return GR_OK;
+  D.handle = dlopen("libcuda.so.1", RTLD_NOW | RTLD_GLOBAL);
+  if (!D.handle) return fail(GR_EDLOPEN, std::string("dlopen(libcuda.so.1): ") + dlerror());
+  using GetProc = CUresult (*)(const char*, void**, int, cuuint64_t, CUdriverProcAddressQueryResult*);
+  auto gp = (GetProc)dlsym(D.handle, "cuGetProcAddress_v2");
+  if (!gp) return fail(GR_EDLOPEN, "libcuda.so.1 has no cuGetProcAddress_v2");
+#define GR_RESOLVE(name)                                                           \
+  {                                                                                \
+    void* fp = nullptr;                                                            \
+    CUdriverProcAddressQueryResult st;                                             \
+    CUresult r = gp(#name, &fp, 12080, CU_GET_PROC_ADDRESS_DEFAULT, &st);          \
+    if (r != CUDA_SUCCESS || !fp) return fail(GR_EDLOPEN, "cannot resolve " #name); \
+    D.p_##name = (decltype(D.p_##name))fp;                                         \
+  }
+  GR_CU_FUNCS(GR_RESOLVE)
+#undef GR_RESOLVE
+  D.loaded = true;
+  return GR_OK;
+}
+
+int need_init() {
+  if (!S.init) return fail(GR_ENOINIT, "grumpy_rt_init has not been called");
+  CUresult r = D.p_cuCtxSetCurrent(S.ctx);
+  if (r != CUDA_SUCCESS) return fail(GR_ECUDA, cu_msg(r, "cuCtxSetCurrent"));
+  return GR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Caching allocator.  Sizes are rounded to classes (256 B .. 1 MiB powers of
+// two, then 2 MiB multiples) so iterative workloads with fixed shapes hit the
+// cache exactly; large blocks may be reused with <= 1/8 slack.  Blocks return
+// to the cache on free; ordering is guaranteed by the single stream.
+// ---------------------------------------------------------------------------
+struct Pool {
+  std::multimap<size_t, CUdeviceptr> free_blocks;
+  std::unordered_map<CUdeviceptr, size_t> live;
+  size_t in_use = 0, cached = 0, peak = 0, n_allocs = 0;
+} P;
+
+size_t round_size(size_t b) {
+  if (b == 0) b = 1;
+  if (b <= (1u << 20)) {
+    size_t s = 256;
+    while (s < b) s <<= 1;
+    return s;
+  }
+  const size_t two_mib = size_t(2) << 20;
+  return (b + two_mib - 1) / two_mib * two_mib;
+}
+
+int pool_release_cached() {
+  for (auto& kv : P.free_blocks) D.p_cuMemFree(kv.second);
+  P.free_blocks.clear();
+  P.cached = 0;
+  return GR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NVRTC module cache
+// ---------------------------------------------------------------------------
+uint64_t fnv1a(const void* data, size_t n, uint64_t h = 1469598103934665603ull) {
+  const unsigned char* p = (const unsigned char*)data;
+  for (size_t i = 0; i < n; ++i) {
+    h ^= p[i];
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+std::unordered_map<uint64_t, CUmodule> g_modules;
+
+bool read_file(const std::string& path, std::vector<char>& out) {
+  FILE* f = fopen(path.c_str(), "rb");
+  if (!f) return false;
+  fseek(f, 0, SEEK_END);
+  long n = ftell(f);
+  fseek(f, 0, SEEK_SET);
+  out.resize(n > 0 ? (size_t)n : 0);
+  bool ok = n > 0 && fread(out.data(), 1, (size_t)n, f) == (size_t)n;
+  fclose(f);
+  return ok;
+}
+
+void write_file_atomic(const std::string& path, const std::vector<char>& data) {
+  std::string tmp = path + ".tmp." + std::to_string(getpid());
+  FILE* f = fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  bool ok = fwrite(data.data(), 1, data.size(), f) == data.size();
+  fclose(f);
+  if (ok) rename(tmp.c_str(), path.c_str());
+  else unlink(tmp.c_str());
+}
+
+
+// NVRTC source -> cubin (no device needed)
+int nvrtc_compile(const char* src, const char* const* opts, int n_opts, std::vector<char>& cubin, double* ms) {
+  auto t0 = std::chrono::steady_clock::now();
+  nvrtcProgram prog;
+  nvrtcResult nr = nvrtcCreateProgram(&prog, src, "grumpy_region.cu", 0, nullptr, nullptr);
+  if (nr != NVRTC_SUCCESS) return fail(GR_ENVRTC, std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(nr));
+  nr = nvrtcCompileProgram(prog, n_opts, opts);
+  if (nr != NVRTC_SUCCESS) {
+    size_t log_size = 0;
+    nvrtcGetProgramLogSize(prog, &log_size);
+    std::string log(log_size, '\0');
+    if (log_size) nvrtcGetProgramLog(prog, &log[0]);
+    nvrtcDestroyProgram(&prog);
+    return fail(GR_ENVRTC, std::string("NVRTC compile failed: ") + nvrtcGetErrorString(nr) + "\n" + log);
+  }
+  size_t n = 0;
+  nr = nvrtcGetCUBINSize(prog, &n);
+  if (nr != NVRTC_SUCCESS || n == 0) {
+    nvrtcDestroyProgram(&prog);
+    return fail(GR_ENVRTC, "nvrtcGetCUBINSize failed (is --gpu-architecture=sm_100a set?)");
+  }
+  cubin.resize(n);
+  nvrtcGetCUBIN(prog, cubin.data());
+  nvrtcDestroyProgram(&prog);
+  auto t1 = std::chrono::steady_clock::now();
+  if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  return GR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL via dlopen
+// ---------------------------------------------------------------------------
+struct NcclUid { char internal[128]; };
+typedef void* NcclComm;
+struct Nccl {
+  void* handle = nullptr;
+  int (*GetUniqueId)(NcclUid*) = nullptr;
+  int (*CommInitRank)(NcclComm*, int, NcclUid, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, CUstream) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, NcclComm, CUstream) = nullptr;
+  int (*CommDestroy)(NcclComm) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  NcclComm comm = nullptr;
+} N;
+
+// ncclDataType_t / ncclRedOp_t values (nccl.h)
+int nccl_dtype(int gr) {
+  switch (gr) {
+    case GR_F32: return 7;   // ncclFloat32
+    case GR_F64: return 8;   // ncclFloat64
+    case GR_I32: return 2;   // ncclInt32
+    case GR_I64: return 4;   // ncclInt64
+    case GR_BOOL: return 0;  // ncclInt8
+  }
+  return -1;
+}
+
+int nccl_fail(int r, const char* what) {
+  std::string s = std::string(what) + " failed: ncclResult " + std::to_string(r);
+  if (N.GetErrorString) s += std::string(" (") + N.GetErrorString(r) + ")";
+  return fail(GR_ENCCL, s);
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case GR_F32: case GR_I32: return 4;
+    case GR_F64: case GR_I64: return 8;
+    case GR_BOOL: return 1;
+  }
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int grumpy_rt_version(int* version) {
+  if (version) *version = 1;
+  return GR_OK;
+}
+
+const char* grumpy_rt_last_error(void) { return g_err.c_str(); }
+
+int grumpy_rt_device_count(int* count) {
+  int r = load_driver();
+  if (r) return r;
+  CU_CHECK(D.p_cuInit(0), "cuInit");
+  int n = 0;
+  CU_CHECK(D.p_cuDeviceGetCount(&n), "cuDeviceGetCount");
+  *count = n;
+  return GR_OK;
+}
+
+int grumpy_rt_init(int device) {
+  std::lock_guard<std::mutex> lk(S.mu);
+  if (S.init) {
+    if (device != S.device)
+      return fail(GR_EINVAL, "runtime already initialised on device " + std::to_string(S.device));
+    return need_init();
+  }
+  int r = load_driver();
+  if (r) return r;
+  CU_CHECK(D.p_cuInit(0), "cuInit");
+  int n = 0;
+  CU_CHECK(D.p_cuDeviceGetCount(&n), "cuDeviceGetCount");
+  if (device < 0 || device >= n)
+    return fail(GR_ENOINIT, "device " + std::to_string(device) + " not present (" + std::to_string(n) + " devices)");
+  CU_CHECK(D.p_cuDeviceGet(&S.dev, device), "cuDeviceGet");
+  CU_CHECK(D.p_cuDevicePrimaryCtxRetain(&S.ctx, S.dev), "cuDevicePrimaryCtxRetain");
+  CU_CHECK(D.p_cuCtxSetCurrent(S.ctx), "cuCtxSetCurrent");
+  CU_CHECK(D.p_cuStreamCreate(&S.stream, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  CU_CHECK(D.p_cuDeviceGetAttribute(&S.sm_count, CU_DEVICE_ATTRIBUTE_MULTIPROCESSOR_COUNT, S.dev),
+           "cuDeviceGetAttribute");
+  S.device = device;
+  S.init = true;
+  return GR_OK;
+}
+
+int grumpy_rt_device_info(int* sm_count, int* cc_major, int* cc_minor, size_t* total_mem, char* name) {
+  int r = need_init();
+  if (r) return r;
+  if (sm_count) *sm_count = S.sm_count;
+  if (cc_major) CU_CHECK(D.p_cuDeviceGetAttribute(cc_major, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MAJOR, S.dev), "attr");
+  if (cc_minor) CU_CHECK(D.p_cuDeviceGetAttribute(cc_minor, CU_DEVICE_ATTRIBUTE_COMPUTE_CAPABILITY_MINOR, S.dev), "attr");
+  if (total_mem) CU_CHECK(D.p_cuDeviceTotalMem(total_mem, S.dev), "cuDeviceTotalMem");
+  if (name) CU_CHECK(D.p_cuDeviceGetName(name, 255, S.dev), "cuDeviceGetName");
+  return GR_OK;
+}
+
+int grumpy_rt_stream(uint64_t* stream) {
+  int r = need_init();
+  if (r) return r;
+  *stream = (uint64_t)(uintptr_t)S.stream;
+  return GR_OK;
+}
+
+// ---- pool -------------------------------------------------------------------
+int grumpy_rt_alloc(size_t bytes, uint64_t* dptr) {
+  int r = need_init();
+  if (r) return r;
+  std::lock_guard<std::mutex> lk(S.mu);
+  size_t sz = round_size(bytes);
+  auto it = P.free_blocks.lower_bound(sz);
+  if (it != P.free_blocks.end() && (it->first == sz || (sz > (1u << 20) && it->first <= sz + sz / 8))) {
+    CUdeviceptr p = it->second;
+    size_t bsz = it->first;
+    P.free_blocks.erase(it);
+    P.cached -= bsz;
+    P.live[p] = bsz;
+    P.in_use += bsz;
+    if (P.in_use > P.peak) P.peak = P.in_use;
+    *dptr = (uint64_t)p;
+    return GR_OK;
+  }
+  CUdeviceptr p = 0;
+  CUresult cr = D.p_cuMemAlloc(&p, sz);
+  if (cr == CUDA_ERROR_OUT_OF_MEMORY) {
+    D.p_cuStreamSynchronize(S.stream);
+    pool_release_cached();
+    cr = D.p_cuMemAlloc(&p, sz);
+  }
+  if (cr == CUDA_ERROR_OUT_OF_MEMORY)
+    return fail(GR_ENOMEM, "device out of memory allocating " + std::to_string(sz) + " bytes (in use " +
+                               std::to_string(P.in_use) + ")");
+  if (cr != CUDA_SUCCESS) return fail(GR_ECUDA, cu_msg(cr, "cuMemAlloc"));
+  P.live[p] = sz;
+  P.in_use += sz;
+  P.n_allocs += 1;
+  if (P.in_use > P.peak) P.peak = P.in_use;
+  *dptr = (uint64_t)p;
+  return GR_OK;
+}
+
+int grumpy_rt_free(uint64_t dptr) {
+  if (!S.init) return GR_OK;  // interpreter shutdown after teardown
+  std::lock_guard<std::mutex> lk(S.mu);
+  auto it = P.live.find((CUdeviceptr)dptr);
+  if (it == P.live.end()) return fail(GR_EINVAL, "free of unknown pointer");
+  size_t sz = it->second;
+  P.live.erase(it);
+  P.in_use -= sz;
+  P.free_blocks.emplace(sz, (CUdeviceptr)dptr);
+  P.cached += sz;
+  return GR_OK;
+}
+
+int grumpy_rt_pool_stats(size_t* in_use, size_t* cached, size_t* peak, size_t* n_allocs) {
+  std::lock_guard<std::mutex> lk(S.mu);
+  if (in_use) *in_use = P.in_use;
+  if (cached) *cached = P.cached;
+  if (peak) *peak = P.peak;
+  if (n_allocs) *n_allocs = P.n_allocs;
+  return GR_OK;
+}
+
+int grumpy_rt_pool_trim(void) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuStreamSynchronize(S.stream), "cuStreamSynchronize");
+  std::lock_guard<std::mutex> lk(S.mu);
+  return pool_release_cached();
+}
+
+// ---- transfers ----------------------------------------------------------------
+int grumpy_rt_h2d(uint64_t dst, const void* src, size_t bytes) {
+  int r = need_init();
+  if (r) return r;
+  if (!bytes) return GR_OK;
+  CU_CHECK(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, S.stream), "cuMemcpyHtoDAsync");
+  return GR_OK;
+}
+
+int grumpy_rt_d2h(void* dst, uint64_t src, size_t bytes) {
+  int r = need_init();
+  if (r) return r;
+  if (bytes) CU_CHECK(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, S.stream), "cuMemcpyDtoHAsync");
+  CU_CHECK(D.p_cuStreamSynchronize(S.stream), "cuStreamSynchronize");
+  return GR_OK;
+}
+
+int grumpy_rt_d2d(uint64_t dst, uint64_t src, size_t bytes) {
+  int r = need_init();
+  if (r) return r;
+  if (!bytes) return GR_OK;
+  CU_CHECK(D.p_cuMemcpyDtoDAsync((CUdeviceptr)dst, (CUdeviceptr)src, bytes, S.stream), "cuMemcpyDtoDAsync");
+  return GR_OK;
+}
+
+int grumpy_rt_memset(uint64_t dst, int byte_value, size_t bytes) {
+  int r = need_init();
+  if (r) return r;
+  if (!bytes) return GR_OK;
+  CU_CHECK(D.p_cuMemsetD8Async((CUdeviceptr)dst, (unsigned char)byte_value, bytes, S.stream), "cuMemsetD8Async");
+  return GR_OK;
+}
+
+int grumpy_rt_host_alloc(size_t bytes, void** ptr) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuMemHostAlloc(ptr, bytes ? bytes : 1, CU_MEMHOSTALLOC_PORTABLE), "cuMemHostAlloc");
+  return GR_OK;
+}
+
+int grumpy_rt_host_free(void* ptr) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuMemFreeHost(ptr), "cuMemFreeHost");
+  return GR_OK;
+}
+
+int grumpy_rt_host_register(void* ptr, size_t bytes) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuMemHostRegister(ptr, bytes, CU_MEMHOSTREGISTER_PORTABLE), "cuMemHostRegister");
+  return GR_OK;
+}
+
+int grumpy_rt_host_unregister(void* ptr) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuMemHostUnregister(ptr), "cuMemHostUnregister");
+  return GR_OK;
+}
+
+// ---- compile ------------------------------------------------------------------
+int grumpy_rt_compile(const char* src, const char* const* opts, int n_opts, const char* cache_dir,
+                      uint64_t* module, double* compile_ms, int* cache_hit) {
+  int r = need_init();
+  if (r) return r;
+  if (compile_ms) *compile_ms = 0.0;
+  if (cache_hit) *cache_hit = 0;
+  uint64_t h = fnv1a(src, strlen(src));
+  for (int i = 0; i < n_opts; ++i) {
+    h = fnv1a(opts[i], strlen(opts[i]), h);
+    h = fnv1a("\x1f", 1, h);
+  }
+  int nv_major = 0, nv_minor = 0;
+  nvrtcVersion(&nv_major, &nv_minor);
+  h = fnv1a(&nv_major, sizeof(nv_major), h);
+  h = fnv1a(&nv_minor, sizeof(nv_minor), h);
+  {
+    std::lock_guard<std::mutex> lk(S.mu);
+    auto it = g_modules.find(h);
+    if (it != g_modules.end()) {
+      *module = (uint64_t)(uintptr_t)it->second;
+      if (cache_hit) *cache_hit = 1;
+      return GR_OK;
+    }
+  }
+  char key[32];
+  snprintf(key, sizeof(key), "%016llx", (unsigned long long)h);
+  std::string path;
+  std::vector<char> cubin;
+  bool have = false;
+  if (cache_dir && cache_dir[0]) {
+    path = std::string(cache_dir) + "/" + key + ".cubin";
+    have = read_file(path, cubin);
+    if (have && cache_hit) *cache_hit = 2;
+  }
+  if (!have) {
+    int rc = nvrtc_compile(src, opts, n_opts, cubin, compile_ms);
+    if (rc) return rc;
+    if (!path.empty()) {
+      mkdir(cache_dir, 0755);
+      write_file_atomic(path, cubin);
+    }
+  }
+  CUmodule mod;
+  CU_CHECK(D.p_cuModuleLoadData(&mod, cubin.data()), "cuModuleLoadData");
+  {
+    std::lock_guard<std::mutex> lk(S.mu);
+    g_modules[h] = mod;
+  }
+  *module = (uint64_t)(uintptr_t)mod;
+  return GR_OK;
+}
+
+int grumpy_rt_compile_cubin(const char* src, const char* const* opts, int n_opts, void* out, size_t cap,
+                            size_t* size, double* compile_ms) {
+  std::vector<char> cubin;
+  int rc = nvrtc_compile(src, opts, n_opts, cubin, compile_ms);
+  if (rc) return rc;
+  *size = cubin.size();
+  if (out && cap >= cubin.size()) memcpy(out, cubin.data(), cubin.size());
+  return GR_OK;
+}
+
+int grumpy_rt_get_function(uint64_t module, const char* name, uint64_t* fn) {
+  int r = need_init();
+  if (r) return r;
+  CUfunction f;
+  CU_CHECK(D.p_cuModuleGetFunction(&f, (CUmodule)(uintptr_t)module, name), "cuModuleGetFunction");
+  *fn = (uint64_t)(uintptr_t)f;
+  return GR_OK;
+}
+
+int grumpy_rt_function_info(uint64_t fn, int* num_regs, int* local_bytes, int* static_smem, int* max_threads) {
+  int r = need_init();
+  if (r) return r;
+  CUfunction f = (CUfunction)(uintptr_t)fn;
+  if (num_regs) CU_CHECK(D.p_cuFuncGetAttribute(num_regs, CU_FUNC_ATTRIBUTE_NUM_REGS, f), "attr");
+  if (local_bytes) CU_CHECK(D.p_cuFuncGetAttribute(local_bytes, CU_FUNC_ATTRIBUTE_LOCAL_SIZE_BYTES, f), "attr");
+  if (static_smem) CU_CHECK(D.p_cuFuncGetAttribute(static_smem, CU_FUNC_ATTRIBUTE_SHARED_SIZE_BYTES, f), "attr");
+  if (max_threads) CU_CHECK(D.p_cuFuncGetAttribute(max_threads, CU_FUNC_ATTRIBUTE_MAX_THREADS_PER_BLOCK, f), "attr");
+  return GR_OK;
+}
+
+int grumpy_rt_occupancy(uint64_t fn, int block, size_t dyn_smem, int* blocks_per_sm) {
+  int r = need_init();
+  if (r) return r;
+  CUfunction f = (CUfunction)(uintptr_t)fn;
+  if (dyn_smem > 48 * 1024)
+    CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem), "attr");
+  CU_CHECK(D.p_cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, dyn_smem), "occupancy");
+  return GR_OK;
+}
+
+// ---- launch -----------------------------------------------------------------
+int grumpy_rt_launch(uint64_t fn, unsigned gx, unsigned gy, unsigned gz, unsigned bx, unsigned by, unsigned bz,
+                     unsigned dyn_smem, unsigned cluster_x, const void* params, size_t params_size) {
+  int r = need_init();
+  if (r) return r;
+  CUfunction f = (CUfunction)(uintptr_t)fn;
+  if (dyn_smem > 48 * 1024)
+    CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem), "attr");
+  size_t sz = params_size;
+  void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void*>(params), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
+                   CU_LAUNCH_PARAM_END};
+  if (cluster_x > 1) {
+    CUlaunchConfig cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDimX = gx; cfg.gridDimY = gy; cfg.gridDimZ = gz;
+    cfg.blockDimX = bx; cfg.blockDimY = by; cfg.blockDimZ = bz;
+    cfg.sharedMemBytes = dyn_smem;
+    cfg.hStream = S.stream;
+    CUlaunchAttribute attr;
+    memset(&attr, 0, sizeof(attr));
+    attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+    attr.value.clusterDim.x = cluster_x;
+    attr.value.clusterDim.y = 1;
+    attr.value.clusterDim.z = 1;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    CU_CHECK(D.p_cuLaunchKernelEx(&cfg, f, nullptr, extra), "cuLaunchKernelEx");
+    return GR_OK;
+  }
+  CU_CHECK(D.p_cuLaunchKernel(f, gx, gy, gz, bx, by, bz, dyn_smem, S.stream, nullptr, extra), "cuLaunchKernel");
+  return GR_OK;
+}
+
+int grumpy_rt_sync(void) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuStreamSynchronize(S.stream), "cuStreamSynchronize");
+  return GR_OK;
+}
+
+// ---- events -------------------------------------------------------------------
+int grumpy_rt_event_create(uint64_t* ev) {
+  int r = need_init();
+  if (r) return r;
+  CUevent e;
+  CU_CHECK(D.p_cuEventCreate(&e, CU_EVENT_DEFAULT), "cuEventCreate");
+  *ev = (uint64_t)(uintptr_t)e;
+  return GR_OK;
+}
+
+int grumpy_rt_event_record(uint64_t ev) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuEventRecord((CUevent)(uintptr_t)ev, S.stream), "cuEventRecord");
+  return GR_OK;
+}
+
+int grumpy_rt_event_elapsed(uint64_t ev_start, uint64_t ev_end, float* ms) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuEventSynchronize((CUevent)(uintptr_t)ev_end), "cuEventSynchronize");
+  CU_CHECK(D.p_cuEventElapsedTime(ms, (CUevent)(uintptr_t)ev_start, (CUevent)(uintptr_t)ev_end),
+           "cuEventElapsedTime");
+  return GR_OK;
+}
+
+int grumpy_rt_event_destroy(uint64_t ev) {
+  if (!S.init) return GR_OK;
+  CU_CHECK(D.p_cuEventDestroy((CUevent)(uintptr_t)ev), "cuEventDestroy");
+  return GR_OK;
+}
+
+// ---- cuBLAS -------------------------------------------------------------------
+static int ensure_cublas() {
+  if (S.cublas) return GR_OK;
+  cublasStatus_t st = cublasCreate(&S.cublas);
+  if (st != CUBLAS_STATUS_SUCCESS) return fail(GR_ECUBLAS, "cublasCreate: status " + std::to_string((int)st));
+  cublasSetStream(S.cublas, S.stream);
+  // FP32 stays FP32 (no TF32): NumPy/OpenBLAS parity.
+  cublasSetMathMode(S.cublas, CUBLAS_DEFAULT_MATH);
+  return GR_OK;
+}
+
+int grumpy_rt_gemm(int trans_a, int trans_b, int m, int n, int k, int dtype, uint64_t a, int lda, uint64_t b,
+                   int ldb, uint64_t c, int ldc) {
+  int r = need_init();
+  if (r) return r;
+  r = ensure_cublas();
+  if (r) return r;
+  // Row-major C = op(A) op(B)  <=>  column-major C^T = op(B)^T op(A)^T.
+  cublasOperation_t opa = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
+  cublasOperation_t opb = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
+  cublasStatus_t st;
+  if (dtype == GR_F32) {
+    const float one = 1.f, zero = 0.f;
+    st = cublasSgemm(S.cublas, opb, opa, n, m, k, &one, (const float*)b, ldb, (const float*)a, lda, &zero,
+                     (float*)c, ldc);
+  } else if (dtype == GR_F64) {
+    const double one = 1.0, zero = 0.0;
+    st = cublasDgemm(S.cublas, opb, opa, n, m, k, &one, (const double*)b, ldb, (const double*)a, lda, &zero,
+                     (double*)c, ldc);
+  } else {
+    return fail(GR_EINVAL, "gemm dtype must be f32 or f64");
+  }
+  if (st != CUBLAS_STATUS_SUCCESS) return fail(GR_ECUBLAS, "cublas gemm: status " + std::to_string((int)st));
+  return GR_OK;
+}
+
+int grumpy_rt_gemv(int trans, int rows, int cols, int dtype, uint64_t a, int lda, uint64_t x, uint64_t y) {
+  int r = need_init();
+  if (r) return r;
+  r = ensure_cublas();
+  if (r) return r;
+  // Column-major view of row-major A[rows, cols] is A^T[cols, rows].
+  // trans = 0: y = A x  = (A^T)^T x -> OP_T;  trans = 1: y = A^T x -> OP_N.
+  cublasOperation_t op = trans ? CUBLAS_OP_N : CUBLAS_OP_T;
+  cublasStatus_t st;
+  if (dtype == GR_F32) {
+    const float one = 1.f, zero = 0.f;
+    st = cublasSgemv(S.cublas, op, cols, rows, &one, (const float*)a, lda, (const float*)x, 1, &zero, (float*)y, 1);
+  } else if (dtype == GR_F64) {
+    const double one = 1.0, zero = 0.0;
+    st = cublasDgemv(S.cublas, op, cols, rows, &one, (const double*)a, lda, (const double*)x, 1, &zero,
+                     (double*)y, 1);
+  } else {
+    return fail(GR_EINVAL, "gemv dtype must be f32 or f64");
+  }
+  if (st != CUBLAS_STATUS_SUCCESS) return fail(GR_ECUBLAS, "cublas gemv: status " + std::to_string((int)st));
+  return GR_OK;
+}
+
+// ---- NCCL ---------------------------------------------------------------------
+int grumpy_rt_nccl_load(const char* path) {
+  if (N.handle) return GR_OK;
+  N.handle = dlopen(path && path[0] ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!N.handle) return fail(GR_EDLOPEN, std::string("dlopen(libnccl): ") + dlerror());
+#define GR_NSYM(field, sym)                                                  \
+  N.field = (decltype(N.field))dlsym(N.handle, sym);                         \
+  if (!N.field) return fail(GR_EDLOPEN, std::string("libnccl lacks ") + sym);
+  GR_NSYM(GetUniqueId, "ncclGetUniqueId")
+  GR_NSYM(CommInitRank, "ncclCommInitRank")
+  GR_NSYM(AllReduce, "ncclAllReduce")
+  GR_NSYM(AllGather, "ncclAllGather")
+  GR_NSYM(CommDestroy, "ncclCommDestroy")
+  GR_NSYM(GetErrorString, "ncclGetErrorString")
+#undef GR_NSYM
+  return GR_OK;
+}
+
+int grumpy_rt_nccl_unique_id(char* id128) {
+  if (!N.handle) return fail(GR_ENOINIT, "grumpy_rt_nccl_load first");
+  NcclUid uid;
+  int rr = N.GetUniqueId(&uid);
+  if (rr) return nccl_fail(rr, "ncclGetUniqueId");
+  memcpy(id128, uid.internal, 128);
+  return GR_OK;
+}
+
+int grumpy_rt_nccl_init(int rank, int nranks, const char* id128) {
+  int r = need_init();
+  if (r) return r;
+  if (!N.handle) return fail(GR_ENOINIT, "grumpy_rt_nccl_load first");
+  NcclUid uid;
+  memcpy(uid.internal, id128, 128);
+  int rr = N.CommInitRank(&N.comm, nranks, uid, rank);
+  if (rr) return nccl_fail(rr, "ncclCommInitRank");
+  return GR_OK;
+}
+
+int grumpy_rt_nccl_allreduce(uint64_t send, uint64_t recv, size_t count, int dtype, int op) {
+  int r = need_init();
+  if (r) return r;
+  if (!N.comm) return fail(GR_ENOINIT, "NCCL communicator not initialised");
+  int nd = nccl_dtype(dtype);
+  if (nd < 0 || op < 0 || op > 3) return fail(GR_EINVAL, "bad dtype/op");
+  // grumpy op codes match ncclSum=0, ncclProd=1, ncclMax=2, ncclMin=3
+  int rr = N.AllReduce((const void*)send, (void*)recv, count, nd, op, N.comm, S.stream);
+  if (rr) return nccl_fail(rr, "ncclAllReduce");
+  return GR_OK;
+}
+
+int grumpy_rt_nccl_allgather(uint64_t send, uint64_t recv, size_t count_per_rank, int dtype) {
+  int r = need_init();
+  if (r) return r;
+  if (!N.comm) return fail(GR_ENOINIT, "NCCL communicator not initialised");
+  int nd = nccl_dtype(dtype);
+  if (nd < 0) return fail(GR_EINVAL, "bad dtype");
+  (void)dtype_size;
+  int rr = N.AllGather((const void*)send, (void*)recv, count_per_rank, nd, N.comm, S.stream);
+  if (rr) return nccl_fail(rr, "ncclAllGather");
+  return GR_OK;
+}
+
+int grumpy_rt_nccl_destroy(void) {
+  if (N.comm && N.CommDestroy) N.CommDestroy(N.comm);
+  N.comm = nullptr;
+  return GR_OK;
+}
+
+}  // extern "C"

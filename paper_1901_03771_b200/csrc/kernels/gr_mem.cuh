@@ -1,0 +1,45 @@
+// gr_mem.cuh — vectorised global-memory access for the fused-loop skeletons.
+//
+// Leaves are read-only for the lifetime of a kernel (regions never write a
+// buffer they read: outputs are fresh pool allocations), so loads go through
+// the non-coherent path (__ldg / LDG.E.CONSTANT) and can be hoisted above the
+// region's stores.  Vector width is chosen by the code generator so every
+// access is one 16-byte LDG.128/STG.128 when the leaf is contiguous along the
+// innermost iteration axis and 16-byte aligned (SURVEY.md §2.2 "128-bit-vector").
+#pragma once
+
+namespace gr {
+
+template <int BYTES> struct RawVec;
+template <> struct RawVec<1> { typedef unsigned char T; };
+template <> struct RawVec<2> { typedef unsigned short T; };
+template <> struct RawVec<4> { typedef unsigned int T; };
+template <> struct RawVec<8> { typedef uint2 T; };
+template <> struct RawVec<16> { typedef uint4 T; };
+
+template <class T, int V> union VecU {
+  typename RawVec<sizeof(T) * V>::T raw;
+  T v[V];
+};
+
+// dst[0..V) = src[0..V); src aligned to sizeof(T)*V
+template <class T, int V> __device__ __forceinline__ void ldv(T (&dst)[V], const T* __restrict__ src) {
+  VecU<T, V> u;
+  u.raw = __ldg(reinterpret_cast<const typename RawVec<sizeof(T) * V>::T*>(src));
+#pragma unroll
+  for (int i = 0; i < V; ++i) dst[i] = u.v[i];
+}
+template <class T> __device__ __forceinline__ T ld(const T* __restrict__ src) { return __ldg(src); }
+template <> __device__ __forceinline__ bool ld(const bool* __restrict__ src) {
+  return __ldg(reinterpret_cast<const unsigned char*>(src)) != 0;
+}
+
+template <class T, int V> __device__ __forceinline__ void stv(T* __restrict__ dst, const T (&src)[V]) {
+  VecU<T, V> u;
+#pragma unroll
+  for (int i = 0; i < V; ++i) u.v[i] = src[i];
+  *reinterpret_cast<typename RawVec<sizeof(T) * V>::T*>(dst) = u.raw;
+}
+template <class T> __device__ __forceinline__ void st(T* __restrict__ dst, T x) { *dst = x; }
+
+}  // namespace gr

@@ -1,0 +1,187 @@
+// gr_ops.cuh — hand-written device-function templates for the point program.
+//
+// One function per ElemCode with NumPy's
+// semantics, so a fused region computes what the eager NumPy baseline computes
+// ("semantics ... match the corresponding numpy operations"):
+//   * IEEE +,-,*,/ and sqrt, never contracted (NVRTC --fmad=false) and never
+//     flushed (no fast-math): bit-identical to NumPy on x86;
+//   * maximum/minimum propagate NaN and return the second operand on ties
+//     (np.maximum(-0.,0.) == 0., np.maximum(0.,-0.) == -0.);
+//   * integer +,-,* wrap (two's complement); // and % follow Python floor
+//     semantics with x//0 == x%0 == 0 as NumPy does;
+//   * float->int casts reproduce x86 cvtt*: NaN/out-of-range -> INT_MIN;
+//   * transcendentals use CUDA's accurate (non-intrinsic) libm: within a few
+//     ulp of NumPy/SciPy, not bit-identical (tolerances in DESIGN.md).
+// Compiled by NVRTC together with the generated region source; no system
+// headers are used so compilation stays fast.
+#pragma once
+
+namespace gr {
+
+typedef long long i64;
+typedef unsigned long long u64;
+
+template <class T> struct is_float { static constexpr bool value = false; };
+template <> struct is_float<float> { static constexpr bool value = true; };
+template <> struct is_float<double> { static constexpr bool value = true; };
+
+// ---- casts (Op CAST, ufunc loop casts) ------------------------------------
+template <class To, class From> struct Cast {
+  static __device__ __forceinline__ To run(From x) { return (To)x; }
+};
+template <class From> struct Cast<bool, From> {
+  static __device__ __forceinline__ bool run(From x) { return x != From(0); }
+};
+template <> struct Cast<bool, bool> {
+  static __device__ __forceinline__ bool run(bool x) { return x; }
+};
+#define GR_F2I(FT, IT, MINV)                                                \
+  template <> struct Cast<IT, FT> {                                         \
+    static __device__ __forceinline__ IT run(FT x) {                        \
+      FT t = trunc(x);                                                      \
+      const FT lo = (FT)(MINV);                                             \
+      return (t >= lo && t < -lo) ? (IT)t : (IT)(MINV);                     \
+    }                                                                       \
+  };
+GR_F2I(float, int, (-2147483647 - 1))
+GR_F2I(double, int, (-2147483647 - 1))
+GR_F2I(float, i64, (-9223372036854775807LL - 1))
+GR_F2I(double, i64, (-9223372036854775807LL - 1))
+#undef GR_F2I
+template <class To, class From> __device__ __forceinline__ To cast(From x) { return Cast<To, From>::run(x); }
+
+// ---- arithmetic -----------------------------------------------------------
+template <class T> __device__ __forceinline__ T add(T a, T b) { return a + b; }
+template <> __device__ __forceinline__ int add(int a, int b) { return (int)((unsigned)a + (unsigned)b); }
+template <> __device__ __forceinline__ i64 add(i64 a, i64 b) { return (i64)((u64)a + (u64)b); }
+template <> __device__ __forceinline__ bool add(bool a, bool b) { return a || b; }
+
+template <class T> __device__ __forceinline__ T sub(T a, T b) { return a - b; }
+template <> __device__ __forceinline__ int sub(int a, int b) { return (int)((unsigned)a - (unsigned)b); }
+template <> __device__ __forceinline__ i64 sub(i64 a, i64 b) { return (i64)((u64)a - (u64)b); }
+
+template <class T> __device__ __forceinline__ T mul(T a, T b) { return a * b; }
+template <> __device__ __forceinline__ int mul(int a, int b) { return (int)((unsigned)a * (unsigned)b); }
+template <> __device__ __forceinline__ i64 mul(i64 a, i64 b) { return (i64)((u64)a * (u64)b); }
+template <> __device__ __forceinline__ bool mul(bool a, bool b) { return a && b; }
+
+template <class T> __device__ __forceinline__ T div(T a, T b) { return a / b; }
+
+template <class T> __device__ __forceinline__ T neg(T a) { return -a; }
+template <> __device__ __forceinline__ int neg(int a) { return (int)(0u - (unsigned)a); }
+template <> __device__ __forceinline__ i64 neg(i64 a) { return (i64)(0ull - (u64)a); }
+
+template <class T> __device__ __forceinline__ T square(T a) { return mul<T>(a, a); }
+
+__device__ __forceinline__ float abs_(float a) { return fabsf(a); }
+__device__ __forceinline__ double abs_(double a) { return fabs(a); }
+__device__ __forceinline__ int abs_(int a) { return a < 0 ? neg<int>(a) : a; }
+__device__ __forceinline__ i64 abs_(i64 a) { return a < 0 ? neg<i64>(a) : a; }
+__device__ __forceinline__ bool abs_(bool a) { return a; }
+
+// npy_divmod (numpy/_core/src/npymath/npy_math_internal.h.src)
+template <class T> __device__ __forceinline__ T fdivmod(T a, T b, T* modulus) {
+  T mod = fmod(a, b);
+  if (b == T(0)) {
+    *modulus = mod;
+    return a / b;
+  }
+  T dv = (a - mod) / b;
+  if (mod != T(0)) {
+    if ((b < T(0)) != (mod < T(0))) {
+      mod += b;
+      dv -= T(1);
+    }
+  } else {
+    mod = copysign(T(0), b);
+  }
+  T fl;
+  if (dv != T(0)) {
+    fl = floor(dv);
+    if (dv - fl > T(0.5)) fl += T(1);
+  } else {
+    fl = copysign(T(0), a / b);
+  }
+  *modulus = mod;
+  return fl;
+}
+template <class T> __device__ __forceinline__ T floordiv(T a, T b) {
+  // integers: Python floor division, x // 0 == 0, INT_MIN // -1 wraps
+  if (b == T(0)) return T(0);
+  if (b == T(-1)) return neg<T>(a);
+  T q = a / b;
+  if ((a % b != T(0)) && ((a < T(0)) != (b < T(0)))) q -= T(1);
+  return q;
+}
+template <> __device__ __forceinline__ float floordiv(float a, float b) { float m; return fdivmod<float>(a, b, &m); }
+template <> __device__ __forceinline__ double floordiv(double a, double b) { double m; return fdivmod<double>(a, b, &m); }
+
+template <class T> __device__ __forceinline__ T mod(T a, T b) {
+  if (b == T(0) || b == T(-1)) return T(0);
+  T r = a % b;
+  if (r != T(0) && ((r < T(0)) != (b < T(0)))) r += b;
+  return r;
+}
+template <> __device__ __forceinline__ float mod(float a, float b) { float m; fdivmod<float>(a, b, &m); return m; }
+template <> __device__ __forceinline__ double mod(double a, double b) { double m; fdivmod<double>(a, b, &m); return m; }
+
+template <class T> __device__ __forceinline__ T pow_(T a, T b) {
+  // integer power by squaring (wraps); negative exponents give 0 (NumPy raises)
+  if (b < T(0)) return T(0);
+  T r = T(1), base = a;
+  u64 e = (u64)b;
+  while (e) {
+    if (e & 1) r = mul<T>(r, base);
+    base = mul<T>(base, base);
+    e >>= 1;
+  }
+  return r;
+}
+template <> __device__ __forceinline__ float pow_(float a, float b) { return powf(a, b); }
+template <> __device__ __forceinline__ double pow_(double a, double b) { return pow(a, b); }
+
+// NaN-propagating, second-operand-on-tie (np.maximum / np.minimum)
+template <class T> __device__ __forceinline__ T maximum(T a, T b) { return (a > b || a != a) ? a : b; }
+template <class T> __device__ __forceinline__ T minimum(T a, T b) { return (a < b || a != a) ? a : b; }
+
+// ---- transcendentals (accurate libm; not intrinsics) ------------------------
+__device__ __forceinline__ float exp_(float a) { return expf(a); }
+__device__ __forceinline__ double exp_(double a) { return exp(a); }
+__device__ __forceinline__ float log_(float a) { return logf(a); }
+__device__ __forceinline__ double log_(double a) { return log(a); }
+__device__ __forceinline__ float sqrt_(float a) { return sqrtf(a); }  // IEEE (prec-sqrt)
+__device__ __forceinline__ double sqrt_(double a) { return sqrt(a); }
+__device__ __forceinline__ float sin_(float a) { return sinf(a); }
+__device__ __forceinline__ double sin_(double a) { return sin(a); }
+__device__ __forceinline__ float cos_(float a) { return cosf(a); }
+__device__ __forceinline__ double cos_(double a) { return cos(a); }
+__device__ __forceinline__ float tanh_(float a) { return tanhf(a); }
+__device__ __forceinline__ double tanh_(double a) { return tanh(a); }
+__device__ __forceinline__ float erf_(float a) { return erff(a); }
+__device__ __forceinline__ double erf_(double a) { return erf(a); }
+__device__ __forceinline__ float floor_(float a) { return floorf(a); }
+__device__ __forceinline__ double floor_(double a) { return floor(a); }
+__device__ __forceinline__ float ceil_(float a) { return ceilf(a); }
+__device__ __forceinline__ double ceil_(double a) { return ceil(a); }
+template <class T> __device__ __forceinline__ T floor_(T a) { return a; }
+template <class T> __device__ __forceinline__ T ceil_(T a) { return a; }
+template <class T> __device__ __forceinline__ bool isnan_(T a) { return a != a; }
+
+// ---- comparisons / logic ----------------------------------------------------
+template <class T> __device__ __forceinline__ bool lt(T a, T b) { return a < b; }
+template <class T> __device__ __forceinline__ bool gt(T a, T b) { return a > b; }
+template <class T> __device__ __forceinline__ bool le(T a, T b) { return a <= b; }
+template <class T> __device__ __forceinline__ bool ge(T a, T b) { return a >= b; }
+template <class T> __device__ __forceinline__ bool eq(T a, T b) { return a == b; }
+template <class T> __device__ __forceinline__ bool ne(T a, T b) { return a != b; }
+template <class T> __device__ __forceinline__ bool land(T a, T b) { return (a != T(0)) && (b != T(0)); }
+template <class T> __device__ __forceinline__ bool lor(T a, T b) { return (a != T(0)) || (b != T(0)); }
+template <class T> __device__ __forceinline__ bool lxor(T a, T b) { return (a != T(0)) != (b != T(0)); }
+template <class T> __device__ __forceinline__ bool lnot(T a) { return !(a != T(0)); }
+template <class T> __device__ __forceinline__ T select(bool c, T a, T b) { return c ? a : b; }
+
+// ---- bit-exact constants ----------------------------------------------------
+__device__ __forceinline__ float f32_bits(unsigned u) { return __uint_as_float(u); }
+__device__ __forceinline__ double f64_bits(u64 u) { return __longlong_as_double((i64)u); }
+
+}  // namespace gr

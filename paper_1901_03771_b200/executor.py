@@ -1,0 +1,141 @@
+"""parallel-executor on B200: runs plan steps through the C-ABI shim.
+
+Reference module ``parallel-executor``:
+``run_map`` / ``run_map_reduce`` / ``run_map_scan`` over a blocked partition
+of the iteration space on a CPU worker pool, and ``run_library`` for
+gemm/gemv with transpose flags.  Here every fused step is ONE generated
+sm_100a kernel launched on the runtime's stream, and library steps are cuBLAS
+calls on the same stream.  Nothing synchronises the host
+until an external consumer reads data (to_external), so consecutive steps and
+consecutive forces pipeline on the device.
+"""
+
+from __future__ import annotations
+
+import time
+from typing import Dict, List
+
+from . import codegen, runtime
+from .dag import Node, OpKind
+from .errors import ShapeMismatch, UnsupportedNodeInFusedStep
+from .planner import PlanStep
+from .tensor import DType, TensorBuffer, element_count
+
+
+class Executor:
+    def __init__(self, session):
+        self.session = session
+        self.rt = runtime.get()      # raises NativeLibraryMissing: no CPU fallback
+        self._gen_cache: Dict[tuple, codegen.KernelSource] = {}
+        self.last_steps: List[PlanStep] = []
+        self.launch_log = []          # (kernel name, family) per launch, for tests/bench
+
+    # -- planner hook ---------------------------------------------------------------
+    def row_fusion(self, reduction: Node, consumer: Node) -> bool:
+        return codegen.row_fusable(reduction, consumer)
+
+    # -- buffers --------------------------------------------------------------------
+    def device_ptr(self, n: Node) -> int:
+        buf = n.data
+        if buf.device is None:
+            buf.device = self.rt.upload(buf.host)
+            self.session.stats.h2d_bytes += buf.host.nbytes
+        return buf.device.ptr
+
+    def new_buffer(self, n: Node) -> TensorBuffer:
+        nbytes = element_count(n.shape) * n.dtype.itemsize
+        return TensorBuffer(n.dtype, n.shape, device=self.rt.alloc(nbytes))
+
+    # -- steps ------------------------------------------------------------------------
+    def run(self, steps: List[PlanStep]):
+        self.last_steps = steps
+        g = self.session.graph
+        for st in steps:
+            if st.kind == "Library":
+                out = self.run_library(st)
+                g.mark_materialized(st.root, out)
+                self.session.stats.library_calls += 1
+                self.session.stats.nodes_materialized += 1
+            else:
+                outs = self.run_fused(st)
+                for r, b in zip(st.roots, outs):
+                    g.mark_materialized(r, b)
+                self.session.stats.nodes_materialized += len(st.roots)
+
+    def kernel_source(self, region: codegen.Region) -> codegen.KernelSource:
+        sig = codegen.signature(region)
+        ks = self._gen_cache.get(sig)
+        if ks is None:
+            ks = codegen.generate(region)
+            self._gen_cache[sig] = ks
+        return ks
+
+    def run_fused(self, st: PlanStep) -> List[TensorBuffer]:
+        region = codegen.Region(st.roots, st.leaves, st.nodes)
+        region = codegen.canonicalize(region)
+        outs = [self.new_buffer(r) for r in region.roots]
+        if all(element_count(r.shape) == 0 for r in region.roots) and not codegen.needs_launch_when_empty(region):
+            return self._reorder(st, region, outs)
+        ks = self.kernel_source(region)
+        k = self.rt.kernel(ks.source, ks.name, ks.block)
+        self.session.stats.compile_ms += k.compile_ms if k.cache_hit == 0 else 0.0
+        k.compile_ms = 0.0
+        ptrs = [self.device_ptr(l) for l in region.leaves] + [b.device.ptr for b in outs]
+        scratch = None
+        if ks.scratch_bytes:
+            scratch = self.rt.alloc(ks.scratch_bytes)
+            if ks.meta.get("scratch_zero"):
+                self.rt.memset(scratch, 0)
+            ptrs.append(scratch.ptr)
+        else:
+            ptrs.append(0)
+        grid = codegen.grid_for(ks, self.rt.sm_count, k.blocks_per_sm)
+        self.rt.launch(k, grid, ks.block, runtime.pack_params(ptrs), smem=ks.meta.get("smem", 0))
+        self.session.stats.kernels_executed += 1
+        self.launch_log.append((ks.family, ks.name))
+        # scratch is stream-ordered: freeing it now returns it to the pool for
+        # later launches on the same stream
+        del scratch
+        return self._reorder(st, region, outs)
+
+    @staticmethod
+    def _reorder(st, region, outs):
+        by_id = {r.id: b for r, b in zip(region.roots, outs)}
+        return [by_id[r.id] for r in st.roots]
+
+    def run_library(self, st: PlanStep) -> TensorBuffer:
+        """run_library → cuBLAS on the runtime stream."""
+        n = st.root
+        ops = st.operands
+        flags = st.trans_flags
+        out = self.new_buffer(n)
+        dt = n.dtype
+        for o in ops:
+            if o.dtype is not dt:
+                raise ShapeMismatch(f"library operand dtype {o.dtype} != {dt}")
+        if n.kind is OpKind.MATMUL:
+            a, b = ops
+            ta, tb = flags
+            m, nn = n.shape
+            k = a.shape[0] if ta else a.shape[1]
+            if m and nn:
+                if k == 0:
+                    self.rt.memset(out.device, 0)
+                else:
+                    self.rt.gemm(ta, tb, m, nn, k, dt, self.device_ptr(a), a.shape[1],
+                                 self.device_ptr(b), b.shape[1], out.device.ptr, nn)
+        else:
+            (vec_mat,) = n.op.attrs
+            mat, x = ops
+            tm = flags[0]
+            rows, cols = mat.shape
+            # effective operation: y = M x (vec_mat False) or y = M^T x (True);
+            # an absorbed transpose flips it once more.
+            trans = bool(vec_mat) != bool(tm)
+            if element_count(n.shape):
+                if (cols if not trans else rows) == 0:
+                    self.rt.memset(out.device, 0)
+                else:
+                    self.rt.gemv(trans, rows, cols, dt, self.device_ptr(mat), cols, self.device_ptr(x), out.device.ptr)
+        self.launch_log.append(("library", st.call))
+        return out

@@ -1,0 +1,115 @@
+"""The BASELINE.json configs written as NumPy programs over a module ``xp``.
+
+Each function is the user program: run it with ``xp=numpy`` (+ scipy erf) and
+it is the reference's eager NumPy baseline; run it with
+``xp=grumpy`` and every region materializes as one fused B200 kernel.  Input
+generators use ``numpy.random.default_rng(seed)`` (SURVEY.md
+§8(d)).
+
+C1 Listing 1 chain     (reconstructed)
+C2 Black-Scholes       (erf normal CDF)
+C3 row-normalise + sum (BASELINE.json configs[2])
+C4 MNIST-style MLP     (np.dot -> library)
+C5 k-means assignment
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _erf(xp):
+    if xp is np:
+        from scipy.special import erf
+        return erf
+    return xp.erf
+
+
+# ---- C1 -----------------------------------------------------------------------
+def listing1_inputs(n=1 << 24, seed=42, dtype=np.float64):
+    rng = np.random.default_rng(seed)
+    W = rng.random(n, dtype=np.float64).astype(dtype)
+    a = rng.random(n, dtype=np.float64).astype(dtype)
+    b = rng.random(n, dtype=np.float64).astype(dtype)
+    return W, a, b
+
+
+def listing1(xp, W, a, b):
+    """4 multiplies + 2 adds (SURVEY.md §8(d) C1 reconstruction)."""
+    x = a * W
+    y = b * W
+    z = x * y
+    return z * W + a + b
+
+
+# ---- C2 -----------------------------------------------------------------------
+BS_R = 0.02
+BS_V = 0.30
+
+
+def blackscholes_inputs(n=1 << 28, seed=42, dtype=np.float32):
+    rng = np.random.default_rng(seed)
+    S = rng.uniform(5.0, 30.0, n).astype(dtype)
+    X = rng.uniform(1.0, 100.0, n).astype(dtype)
+    T = rng.uniform(0.25, 10.0, n).astype(dtype)
+    return S, X, T
+
+
+def blackscholes(xp, S, X, T, r=BS_R, v=BS_V):
+    """European call/put with the erf-based CND."""
+    erf = _erf(xp)
+    sqT = xp.sqrt(T)
+    d1 = (xp.log(S / X) + (r + 0.5 * v * v) * T) / (v * sqT)
+    d2 = d1 - v * sqT
+    cnd1 = 0.5 * (1.0 + erf(d1 * 0.7071067811865476))
+    cnd2 = 0.5 * (1.0 + erf(d2 * 0.7071067811865476))
+    e = xp.exp(-r * T)
+    call = S * cnd1 - X * e * cnd2
+    put = X * e * (1.0 - cnd2) - S * (1.0 - cnd1)
+    return call, put
+
+
+# ---- C3 -----------------------------------------------------------------------
+def rownorm_inputs(rows=65536, cols=4096, seed=42, dtype=np.float32):
+    rng = np.random.default_rng(seed)
+    x = (rng.standard_normal((rows, cols), dtype=np.float32) * 2 + 5).astype(dtype)
+    return (x,)
+
+
+def rownorm(xp, x):
+    y = (x - x.mean(1)[:, None]) / x.std(1)[:, None]
+    return y, y.sum()
+
+
+# ---- C4 -----------------------------------------------------------------------
+def mlp_inputs(batch=65536, hidden=1024, seed=42):
+    rng = np.random.default_rng(seed)
+    X = rng.random((batch, 784), dtype=np.float32)
+    W1 = (rng.standard_normal((784, hidden), dtype=np.float32) / np.float32(np.sqrt(784))).astype(np.float32)
+    b1 = rng.uniform(-0.1, 0.1, hidden).astype(np.float32)
+    W2 = (rng.standard_normal((hidden, 10), dtype=np.float32) / np.float32(np.sqrt(hidden))).astype(np.float32)
+    b2 = rng.uniform(-0.1, 0.1, 10).astype(np.float32)
+    return X, W1, b1, W2, b2
+
+
+def mlp(xp, X, W1, b1, W2, b2):
+    h = xp.maximum(X @ W1 + b1, 0)
+    z = h @ W2 + b2
+    p = xp.exp(z - z.max(1)[:, None])
+    p = p / p.sum(1)[:, None]
+    return p, p.argmax(1)
+
+
+# ---- C5 -----------------------------------------------------------------------
+def kmeans_inputs(n=1 << 26, k=64, d=4, seed=42):
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(-10, 10, (k, d)).astype(np.float32)
+    lab = rng.integers(0, k, n)
+    P = (centres[lab] + rng.standard_normal((n, d), dtype=np.float32)).astype(np.float32)
+    C0 = P[rng.choice(n, k, replace=False)].copy()
+    return P, C0
+
+
+def kmeans_assign(xp, P, C):
+    d = ((P[:, None, :] - C[None]) ** 2).sum(-1)
+    return d.argmin(1)
