@@ -101,6 +101,17 @@ class Clocks:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout):
+        t0 = time.time()
+        while self.proc is not None and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self):
+        self.mark_at = len(self.lines)
+
+    def since_mark(self):
+        return len(self.lines) - getattr(self, "mark_at", 0) if self.proc is not None else 99
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -111,7 +122,7 @@ class Clocks:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for l in self.lines:
+        for l in self.lines[getattr(self, "mark_at", 0):]:
             parts = [p.strip() for p in l.split(",")]
             if len(parts) < 6:
                 continue
@@ -250,6 +261,11 @@ def run_grumpy(args, dist):
     for d in dev:  # upload once (not timed)
         d.node.data.device = rt.upload(d.node.data.host)
 
+    # clocks sampler runs from before warm-up so it has samples under load
+    clocks = Clocks(dist.local_rank)
+    clocks.start()
+    clocks.wait_first(3.0)
+
     # warmup (includes NVRTC compile on the first step)
     t0 = time.perf_counter()
     outs = prog(gp, dev)
@@ -260,38 +276,42 @@ def run_grumpy(args, dist):
         outs = prog(gp, dev)
         gp.force(*outs)
     rt.sync()
+    del outs
 
-    # timed region: K steps, per-step events around each force
+    # timed region: exactly K steps; per-launch events inside the executor
     k0 = sess.stats.kernels_executed
-    clocks = Clocks(dist.local_rank)
-    evs = [(rt.event(), rt.event()) for _ in range(args.steps)]
     e_all0, e_all1 = rt.event(), rt.event()
+    sess.executor.enable_profile()
     dist.barrier()
     rt.sync()
-    clocks.start()
+    clocks.mark()
     rt.record(e_all0)
     keep = []
     for i in range(args.steps):
-        rt.record(evs[i][0])
         outs = prog(gp, dev)
         gp.force(*outs)
-        rt.record(evs[i][1])
         keep.append(outs)
         if len(keep) > 2:
             keep.pop(0)
     rt.record(e_all1)
     rt.sync()
+    launches = sess.stats.kernels_executed - k0
+    prof = sess.executor.take_profile()
+    sess.executor.profile = None
+    # keep the GPU loaded (untimed) until the sampler has enough points
+    t_load = time.perf_counter()
+    while clocks.since_mark() < 5 and time.perf_counter() - t_load < 3.0:
+        outs = prog(gp, dev)
+        gp.force(*outs)
+        rt.sync()
     clk = clocks.stop()
     dist.barrier()
-    launches = sess.stats.kernels_executed - k0
-    total_ms = rt.elapsed_ms(e_all0, e_all1)
-    kern_ms = [rt.elapsed_ms(a, b) for a, b in evs]
-    total_ms = dist.max(total_ms)
+    total_ms = dist.max(rt.elapsed_ms(e_all0, e_all1))
+    kern_ms = [ms for _f, _l, ms in prof]
     kmean = statistics.mean(kern_ms)
     del keep
-
     elements = n * dist.world
-    value = elements / (total_ms / 1e3)
+    value = elements * args.steps / (total_ms / 1e3)
     peak, peak_src = peaks()
     alg_bytes = n * w["bytes_per_elem"]
     achieved = alg_bytes / (kmean / 1e3) / 1e9

@@ -268,8 +268,22 @@ def _resolve_loop(code: ElemCode, in_dtypes: Sequence[Any]):
     return tuple(dtype_of(r) for r in res[:-1]), dtype_of(res[-1])
 
 
+_LOOP_CACHE: dict = {}
+
+
 def resolve_map(code: ElemCode, in_dtypes: Sequence[Any]):
-    """Public wrapper used by the session (weak Python scalars allowed)."""
+    """Public wrapper used by the session (weak Python scalars allowed).
+
+    Memoised: NumPy's resolution is a pure function of (ufunc, dtypes)."""
+    key = (code, tuple(in_dtypes))
+    hit = _LOOP_CACHE.get(key)
+    if hit is None:
+        hit = _resolve_map(code, key[1])
+        _LOOP_CACHE[key] = hit
+    return hit
+
+
+def _resolve_map(code: ElemCode, in_dtypes: Sequence[Any]):
     if code is ElemCode.select:
         cond, a, b = in_dtypes
         args = [x.np if isinstance(x, DType) else x for x in (a, b)]
@@ -302,7 +316,8 @@ def infer(op: Op, pred_shapes: Sequence[Shape], pred_dtypes: Sequence[DType]) ->
             raise ShapeMismatch(f"{code.value} takes {arity(code)} operands, got {len(pred_shapes)}")
         if code is ElemCode.const_splat:
             raise ShapeMismatch("const_splat nodes are created with add_const")
-        shape = broadcast_many(pred_shapes)
+        s0 = pred_shapes[0]
+        shape = s0 if all(s == s0 for s in pred_shapes) else broadcast_many(pred_shapes)
         loop, out = resolve_map(code, pred_dtypes)
         return shape, out, loop
     if k is OpKind.CAST:

@@ -12,6 +12,7 @@ consecutive forces pipeline on the device.
 
 from __future__ import annotations
 
+import collections
 import time
 from typing import Dict, List
 
@@ -28,7 +29,8 @@ class Executor:
         self.rt = runtime.get()      # raises NativeLibraryMissing: no CPU fallback
         self._gen_cache: Dict[tuple, codegen.KernelSource] = {}
         self.last_steps: List[PlanStep] = []
-        self.launch_log = []          # (kernel name, family) per launch, for tests/bench
+        self.launch_log = collections.deque(maxlen=4096)  # (family, kernel name) per launch
+        self.profile = None           # per-launch CUDA events when enabled
 
     # -- planner hook ---------------------------------------------------------------
     def row_fusion(self, reduction: Node, consumer: Node) -> bool:
@@ -71,16 +73,26 @@ class Executor:
         return ks
 
     def run_fused(self, st: PlanStep) -> List[TensorBuffer]:
-        region = codegen.Region(st.roots, st.leaves, st.nodes)
-        region = codegen.canonicalize(region)
-        outs = [self.new_buffer(r) for r in region.roots]
-        if all(element_count(r.shape) == 0 for r in region.roots) and not codegen.needs_launch_when_empty(region):
-            return self._reorder(st, region, outs)
-        ks = self.kernel_source(region)
-        k = self.rt.kernel(ks.source, ks.name, ks.block)
-        self.session.stats.compile_ms += k.compile_ms if k.cache_hit == 0 else 0.0
-        k.compile_ms = 0.0
-        ptrs = [self.device_ptr(l) for l in region.leaves] + [b.device.ptr for b in outs]
+        c = st.cache
+        if "perm" not in c:
+            region = codegen.canonicalize(codegen.Region(st.roots, st.leaves, st.nodes))
+            pos = {l.id: i for i, l in enumerate(st.leaves)}
+            c["perm"] = [pos[l.id] for l in region.leaves]
+            empty = all(element_count(r.shape) == 0 for r in region.roots)
+            c["ks"] = None if empty else self.kernel_source(region)
+        leaves = [st.leaves[i] for i in c["perm"]]
+        outs = [self.new_buffer(r) for r in st.roots]
+        ks = c["ks"]
+        if ks is None:
+            return outs
+        k = c.get("kernel")
+        if k is None:
+            k = self.rt.kernel(ks.source, ks.name, ks.block)
+            if k.cache_hit == 0:
+                self.session.stats.compile_ms += k.compile_ms
+            c["kernel"] = k
+            c["grid"] = codegen.grid_for(ks, self.rt.sm_count, k.blocks_per_sm)
+        ptrs = [self.device_ptr(l) for l in leaves] + [b.device.ptr for b in outs]
         scratch = None
         if ks.scratch_bytes:
             scratch = self.rt.alloc(ks.scratch_bytes)
@@ -89,19 +101,38 @@ class Executor:
             ptrs.append(scratch.ptr)
         else:
             ptrs.append(0)
-        grid = codegen.grid_for(ks, self.rt.sm_count, k.blocks_per_sm)
-        self.rt.launch(k, grid, ks.block, runtime.pack_params(ptrs), smem=ks.meta.get("smem", 0))
+        params = runtime.pack_params(ptrs)
+        if self.profile is not None:
+            e0, e1 = self._event_pair()
+            self.rt.record(e0)
+            self.rt.launch(k, c["grid"], ks.block, params, smem=ks.meta.get("smem", 0))
+            self.rt.record(e1)
+            self.profile.append((ks.family, ks.meta.get("label", ks.name), e0, e1))
+        else:
+            self.rt.launch(k, c["grid"], ks.block, params, smem=ks.meta.get("smem", 0))
         self.session.stats.kernels_executed += 1
         self.launch_log.append((ks.family, ks.name))
-        # scratch is stream-ordered: freeing it now returns it to the pool for
+        # scratch is stream-ordered: returning it to the pool now is safe for
         # later launches on the same stream
         del scratch
-        return self._reorder(st, region, outs)
+        return outs
 
-    @staticmethod
-    def _reorder(st, region, outs):
-        by_id = {r.id: b for r, b in zip(region.roots, outs)}
-        return [by_id[r.id] for r in st.roots]
+    # -- optional per-launch device timing (bench.py) ----------------------------------
+    def enable_profile(self):
+        self.profile = []
+        self._events = []
+
+    def _event_pair(self):
+        i = len(self.profile)
+        while len(self._events) <= i:
+            self._events.append((self.rt.event(), self.rt.event()))
+        return self._events[i]
+
+    def take_profile(self):
+        """[(family, label, ms)] for launches since enable_profile(); syncs."""
+        out = [(f, l, self.rt.elapsed_ms(a, b)) for f, l, a, b in self.profile]
+        self.profile = []
+        return out
 
     def run_library(self, st: PlanStep) -> TensorBuffer:
         """run_library → cuBLAS on the runtime stream."""

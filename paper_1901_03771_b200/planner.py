@@ -61,6 +61,9 @@ class PlanStep:
     trans_flags: Tuple[bool, ...] = ()
     operands: List[Node] = dataclasses.field(default_factory=list)
     order_index: int = 0
+    # executor-owned memo shared by every instantiation of a cached plan
+    # (canonical leaf order, generated kernel source)
+    cache: dict = dataclasses.field(default_factory=dict)
 
     @property
     def root(self) -> Node:
@@ -447,3 +450,69 @@ def _merge_into(m: PlanStep, c: PlanStep):
     m.nodes = sorted(m.nodes + [n for n in c.nodes if n.id not in ids], key=lambda x: x.id)
     lids = {n.id for n in m.leaves}
     m.leaves = m.leaves + [l for l in c.leaves if l.id not in lids]
+
+
+# ---------------------------------------------------------------------------
+# Plan cache: structural DAG signatures and step templates
+# ---------------------------------------------------------------------------
+
+
+def dag_signature(roots: Sequence[Node]):
+    """Structural key of the demanded DAG plus its nodes in visit order.
+
+    Materialized nodes are leaves keyed by (shape, dtype) only, so a loop that
+    rebuilds the same expression on fresh inputs hits the same key; node
+    identity inside the DAG (sharing) is captured by local indices."""
+    local: Dict[int, int] = {}
+    order: List[Node] = []
+    items = []
+    for r in roots:
+        if r.id in local:
+            continue
+        stack = [(r, False)]
+        while stack:
+            n, expanded = stack.pop()
+            if n.id in local:
+                continue
+            if n.is_materialized:
+                local[n.id] = len(order)
+                order.append(n)
+                items.append(("L", n.shape, n.dtype))
+                continue
+            if not expanded:
+                stack.append((n, True))
+                for p in reversed(n.preds):
+                    if p.id not in local:
+                        stack.append((p, False))
+                continue
+            local[n.id] = len(order)
+            order.append(n)
+            items.append((n.op, n.shape, n.dtype, tuple(local[p.id] for p in n.preds)))
+    return (tuple(items), tuple(local[r.id] for r in roots)), order
+
+
+def make_template(steps: List[PlanStep], order: List[Node]):
+    idx = {n.id: i for i, n in enumerate(order)}
+    tmpl = []
+    for st in steps:
+        tmpl.append({
+            "kind": st.kind, "kernel_kind": st.kernel_kind, "call": st.call,
+            "trans_flags": st.trans_flags,
+            "roots": [idx[n.id] for n in st.roots],
+            "nodes": [idx[n.id] for n in st.nodes],
+            "leaves": [idx[n.id] for n in st.leaves],
+            "operands": [idx[n.id] for n in st.operands],
+            "cache": st.cache,
+        })
+    return tmpl
+
+
+def instantiate(tmpl, order: List[Node]) -> List[PlanStep]:
+    steps = []
+    for i, t in enumerate(tmpl):
+        st = PlanStep(t["kind"], [order[j] for j in t["roots"]], [order[j] for j in t["nodes"]],
+                      [order[j] for j in t["leaves"]], kernel_kind=t["kernel_kind"], call=t["call"],
+                      trans_flags=t["trans_flags"], operands=[order[j] for j in t["operands"]], order_index=i)
+        st.cache = t["cache"]
+        steps.append(st)
+    return steps

@@ -67,6 +67,8 @@ class Session:
         self.planner = planner
         self.limits = limits or _planner.PlannerLimits()
         self._executor = None
+        self._consts = {}
+        self._plan_cache = {}
         self.comm = None  # distributed.Comm when sharded
 
     @property
@@ -89,13 +91,36 @@ class Session:
             return steps
         return _planner.plan_regions(roots, row_fusion=self.executor.row_fusion)
 
+    def const(self, value, dtype: DType) -> Node:
+        """Interned rank-0 const_splat node (constants are immutable)."""
+        key = (type(value), value, dtype)
+        n = self._consts.get(key)
+        if n is None:
+            if len(self._consts) > 4096:
+                self._consts.clear()
+            n = self.graph.add_const(value, dtype, ())
+            self._consts[key] = n
+        return n
+
     # -- materialization -----------------------------------------------------
     def force_nodes(self, nodes: Sequence[Node]):
+        """Plan (or reuse a cached plan for a structurally identical DAG) and
+        execute.  The plan cache turns the per-force host cost into one DAG
+        traversal for iterative programs (SPEC.md:521 warm vs cold)."""
         pending = [n for n in nodes if not n.is_materialized]
         if not pending:
             return
         t0 = time.perf_counter()
-        steps = self.plan(pending)
+        key, order = _planner.dag_signature(pending)
+        tmpl = self._plan_cache.get(key)
+        if tmpl is None:
+            steps = self.plan(pending)
+            tmpl = _planner.make_template(steps, order)
+            if len(self._plan_cache) > 1024:
+                self._plan_cache.clear()
+            self._plan_cache[key] = tmpl
+        else:
+            steps = _planner.instantiate(tmpl, order)
         t1 = time.perf_counter()
         self.stats.plan_time += t1 - t0
         self.executor.run(steps)
@@ -173,21 +198,40 @@ def _check_int_range(v, dt: DType):
             raise OverflowError(f"Python integer {v} out of bounds for {dt.np}")
 
 
+_MAP_OPS = {c: Op(OpKind.MAP, c) for c in ElemCode}
+_WEAK = {float: float, int: int, bool: DType.bool8}
+
+
 def elementwise(code: ElemCode, *args, sess: Optional[Session] = None) -> "ndarray":
-    """Record MapElementwise(code) with NumPy's ufunc type resolution."""
-    sess = sess or _session_of(args)
-    dts = [_dt_arg(a) for a in args]
-    dts = [np.dtype(np.bool_) if d is bool else d for d in dts]
-    dts = [dtype_of(d) if isinstance(d, np.dtype) else d for d in dts]
+    """Record MapElementwise(code) with NumPy's ufunc type resolution.
+
+    Hot path of recording: weak Python scalars (NEP 50) resolve with their
+    Python type and become const_splat nodes of the loop dtype."""
+    if sess is None:
+        sess = _session_of(args)
+    dts = []
+    for a in args:
+        t = type(a)
+        if t is ndarray:
+            dts.append(a._node.dtype)
+        elif t in _WEAK:
+            dts.append(_WEAK[t])
+        else:
+            d = _dt_arg(a)
+            dts.append(DType.bool8 if d is bool else d)
     loop, out = resolve_map(code, dts)
     preds = []
+    g = sess.graph
     for a, lt in zip(args, loop):
-        if _is_weak_scalar(a):
+        t = type(a)
+        if t is ndarray:
+            preds.append(a._node)
+        elif t in _WEAK:
             _check_int_range(a, lt)
-            preds.append(sess.graph.add_const(a, lt, ()))
+            preds.append(sess.const(a, lt))
         else:
             preds.append(_as_node(a, sess))
-    return _wrap(sess.graph.add_op(Op(OpKind.MAP, code), preds), sess)
+    return ndarray(g.add_op(_MAP_OPS[code], preds), sess)
 
 
 def _session_of(args) -> Session:
