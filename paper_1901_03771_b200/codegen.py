@@ -690,15 +690,52 @@ def needs_launch_when_empty(region: Region) -> bool:
 
 
 def row_fusable(reduction: Node, consumer: Node) -> bool:
-    """Planner hook: may ``reduction`` stay inside ``consumer``'s kernel?"""
+    """Planner hook (optimistic): may ``reduction`` stay inside ``consumer``'s
+    kernel?  Row-local reductions (leading axis kept) are proposed; the code
+    generator has the last word and raises NotFusable otherwise."""
+    if reduction.kind is OpKind.REDUCE:
+        axes = reduction.op.attrs[1]
+        return bool(axes) and min(axes) > 0
+    if reduction.kind is OpKind.ARGREDUCE:
+        ax = reduction.op.attrs[1]
+        return ax is not None and ax > 0
     return False
 
 
 def generate(region: Region) -> KernelSource:
-    kinds = {r.op.kind for r in region.roots}
-    if kinds & {OpKind.REDUCE, OpKind.ARGREDUCE, OpKind.SCAN, OpKind.KEYED_SUM}:
-        raise UnsupportedNodeInFusedStep(f"no kernel family for roots {kinds} yet")
+    """Pick the kernel family for a region and emit its source."""
+    from . import codegen_rows
+    kinds = {n.op.kind for n in region.nodes}
+    if kinds & {OpKind.SCAN, OpKind.KEYED_SUM}:
+        from . import codegen_scan
+        return codegen_scan.generate(region)
+    if kinds & {OpKind.REDUCE, OpKind.ARGREDUCE}:
+        from . import codegen_coop
+        ks = codegen_coop.try_generate(region)
+        if ks is not None:
+            return ks
+        return codegen_rows.gen_rows(region)
     return gen_map(region)
+
+
+_GEN_CACHE: Dict[tuple, KernelSource] = {}
+
+
+def cached_generate(region: Region) -> KernelSource:
+    """generate() memoised by structural signature (region must be canonical)."""
+    sig = signature(region)
+    ks = _GEN_CACHE.get(sig)
+    if ks is None:
+        ks = generate(region)
+        if len(_GEN_CACHE) > 4096:
+            _GEN_CACHE.clear()
+        _GEN_CACHE[sig] = ks
+    return ks
+
+
+def check_step(step) -> None:
+    """Planner feedback: raise NotFusable if the step's region cannot be generated."""
+    cached_generate(canonicalize(Region(step.roots, step.leaves, step.nodes)))
 
 
 def grid_for(ks: KernelSource, sm_count: int, blocks_per_sm: int) -> int:

@@ -1,0 +1,672 @@
+"""Row family: fused regions that contain reductions (K2 / K3 / K4 / K5).
+
+Reference: run_map_reduce (per-thread fold
+from the identity, partials folded in a fixed order), arg-reductions as
+"reduce + select" and the paper's GPU reduction with a
+separate final kernel.  The B200 design replaces the
+"cut at every reduction" of Algorithm 1 with loop nests:
+
+* the region's *thread space* T is the leading shape every reduction keeps
+  (rows); one thread owns one row and evaluates the whole region for it;
+* a reduction is evaluated where its kept coordinates live — values depending
+  only on the row are computed once per row and reused by every element of the
+  row (mean/std broadcast back in row-normalise, max/sum in softmax);
+* float sums follow NumPy's association exactly (``gr::pairwise`` along the
+  contiguous axis, sequential along the others, identity-initialised), so
+  reductions of IEEE-exact terms are bit-identical to the oracle; arg-
+  reductions keep the first index and treat NaN as extreme like np.argmax;
+* full reductions of the region ("totals", e.g. ``y.sum()``) are accumulated
+  as one partial per row and folded by the last CTA to finish (atomic ticket,
+  no float atomics) in a fixed tree: one launch, deterministic.
+
+The cooperative variant for long rows (one CTA per row, row staged in
+registers) lives in ``codegen_coop.py``.
+"""
+
+from __future__ import annotations
+
+from typing import Dict, List, Optional, Sequence, Tuple
+
+from .codegen import (
+    HEADER, Aff, KernelSource, Region, ValueEmitter, Var, _params_struct, bcast_coords, c_literal,
+)
+from .dag import Node, OpKind, ReduceOp
+from .errors import UnsupportedNodeInFusedStep
+from .tensor import DType, element_count, row_major_strides
+
+
+class NotFusable(UnsupportedNodeInFusedStep):
+    """Raised when ``node`` cannot live inside this region; the planner cuts it."""
+
+    def __init__(self, node: Node, why: str):
+        super().__init__(f"node {node.id} ({node.op!r}) not fusable here: {why}")
+        self.node = node
+
+
+def is_total(n: Node) -> bool:
+    """A reduction to a single value (all axes), e.g. y.sum() or argmax(axis=None)."""
+    if n.kind is OpKind.REDUCE:
+        return len(n.op.attrs[1]) == len(n.preds[0].shape) if n.preds else element_count(n.shape) == 1
+    if n.kind is OpKind.ARGREDUCE:
+        return n.op.attrs[1] is None
+    return False
+
+
+_IDENT = {
+    ReduceOp.sum: lambda dt: 0,
+    ReduceOp.prod: lambda dt: 1,
+    ReduceOp.max: lambda dt: float("-inf") if dt.is_float else (False if dt.is_bool else (-(2**31) if dt is DType.i32 else -(2**63))),
+    ReduceOp.min: lambda dt: float("inf") if dt.is_float else (True if dt.is_bool else (2**31 - 1 if dt is DType.i32 else 2**63 - 1)),
+}
+_COMBINE = {ReduceOp.sum: "gr::add", ReduceOp.prod: "gr::mul", ReduceOp.max: "gr::maximum", ReduceOp.min: "gr::minimum"}
+_OPS = {ReduceOp.sum: "gr::OpSum", ReduceOp.prod: "gr::OpProd", ReduceOp.max: "gr::OpMax", ReduceOp.min: "gr::OpMin"}
+
+SMALL_RECOMPUTE = 64   # a reduction re-evaluated per column may reduce at most this many points
+
+
+class Scope:
+    __slots__ = ("level", "kind", "header", "lines", "ret", "unroll", "var", "trip")
+
+    def __init__(self, level, kind="block", header="", unroll=False, var=None, trip=None):
+        self.level = level
+        self.kind = kind
+        self.header = header
+        self.lines: list = []
+        self.ret = None
+        self.unroll = unroll
+        self.var = var
+        self.trip = trip
+
+
+def render(scope: Scope, indent: int) -> List[str]:
+    pad = "  " * indent
+    out = []
+    for l in scope.lines:
+        if isinstance(l, Scope):
+            if l.kind == "for":
+                if l.unroll:
+                    out.append("#pragma unroll")
+                out.append(f"{pad}{l.header} {{")
+                out += render(l, indent + 1)
+                out.append(f"{pad}}}")
+            elif l.kind == "lambda":
+                out.append(f"{pad}{l.header} {{")
+                out += render(l, indent + 1)
+                out.append(f"{pad}  return {l.ret};")
+                out.append(f"{pad}}};")
+            else:
+                out.append(f"{pad}{{")
+                out += render(l, indent + 1)
+                out.append(f"{pad}}}")
+        else:
+            out.append(pad + l)
+    return out
+
+
+class LoopEmitter(ValueEmitter):
+    """Scoped emitter: level 0 kernel constants, level 1 the row, 2+ loops."""
+
+    def __init__(self, region: Region, vec_loads=True):
+        super().__init__(region)
+        self.row = Scope(1)
+        self.stack: List[Optional[Scope]] = [None, self.row]
+        self.vec_loads = vec_loads
+
+    # -- scopes ------------------------------------------------------------------
+    def emit(self, level, ctype, expr):
+        name = self.fresh()
+        if level <= 0:
+            self.consts.append(f"const {ctype} {name} = {expr};")
+            return name
+        self.stack[level].lines.append(f"const {ctype} {name} = {expr};")
+        return name
+
+    def stmt(self, level, text):
+        if level <= 0:
+            self.consts.append(text)
+        else:
+            self.stack[level].lines.append(text)
+
+    def var_decl(self, level, ctype, init) -> str:
+        name = self.fresh("a")
+        self.stmt(level, f"{ctype} {name} = {init};")
+        return name
+
+    def open(self, parent_level, kind, trip=None, unroll=False, ret_type=None):
+        saved = self.stack[parent_level + 1:]
+        del self.stack[parent_level + 1:]
+        lvl = parent_level + 1
+        name = self.fresh("i")
+        var = Var(name, lvl)
+        if kind == "for":
+            header = f"for (long long {name} = 0; {name} < {trip}LL; ++{name})"
+        else:
+            header = f"auto f{name} = [&](long long {name}) -> {ret_type}"
+        s = Scope(lvl, kind, header, unroll=unroll, var=var, trip=trip)
+        self.stack.append(s)
+        return var, s, saved
+
+    def close(self, s: Scope, saved, ret=None):
+        assert self.stack[-1] is s
+        self.stack.pop()
+        s.ret = ret
+        self.stack[-1].lines.append(s)
+        self.stack.extend(saved)
+
+    def value(self, n: Node, coords):
+        key = (n.id, tuple(c.key() for c in coords))
+        hit = self.memo.get(key)
+        if hit is not None:
+            expr, lvl, sc = hit
+            if lvl == 0 or (lvl < len(self.stack) and self.stack[lvl] is sc):
+                return expr, lvl
+        v = self._value(n, list(coords))
+        self.memo[key] = (v[0], v[1], self.stack[v[1]] if 0 < v[1] < len(self.stack) else None)
+        return v
+
+    def derived_var(self, level, expr) -> Var:
+        name = self.emit(level, "long long", expr)
+        return Var(name, level)
+
+    # -- loads ----------------------------------------------------------------------
+    def load_leaf(self, leaf: Node, off: Aff):
+        idx = self.leaf_index[leaf.id]
+        T = leaf.dtype.ctype
+        ptr = f"p.in{idx}"
+        lvl = off.level
+        if self.vec_loads and lvl >= 2:
+            sc = self.stack[lvl]
+            if sc.kind == "for" and sc.unroll and sc.var is not None:
+                cv = off.coef(sc.var)
+                rest = off.without(sc.var)
+                trip = sc.trip
+                nbytes = trip * leaf.dtype.itemsize
+                if (cv == 1 and rest.level < lvl and trip in (2, 4, 8, 16) and nbytes in (2, 4, 8, 16)
+                        and rest.alignment() % trip == 0):
+                    key = ("vec", leaf.id, rest.key(), trip)
+                    hit = self.memo.get(key)
+                    if hit is not None and (hit[1] == 0 or self.stack[hit[1]] is hit[2]):
+                        return f"{hit[0]}[{sc.var.name}]", lvl
+                    name = self.fresh("L")
+                    plvl = max(rest.level, 1)
+                    self.stmt(plvl, f"{T} {name}[{trip}];")
+                    self.stmt(plvl, f"gr::ldv<{T}, {trip}>({name}, {ptr} + {rest.c()});")
+                    self.memo[key] = (name, plvl, self.stack[plvl] if plvl > 0 else None)
+                    return f"{name}[{sc.var.name}]", lvl
+        return self.emit(lvl, T, f"gr::ld<{T}>({ptr} + {off.c()})"), lvl
+
+    # -- reductions -------------------------------------------------------------------
+    def _value(self, n: Node, coords):
+        if n.id not in self.leaf_index:
+            if n.kind is OpKind.REDUCE:
+                return self.reduce(n, coords)
+            if n.kind is OpKind.ARGREDUCE:
+                return self.argreduce(n, coords)
+        return super()._value(n, coords)
+
+    def _operand_coords(self, r: Node, coords, axes, keepdims):
+        x = r.preds[0]
+        if keepdims:
+            kept = [c for i, c in enumerate(coords) if i not in axes]
+        else:
+            kept = list(coords)
+        lvl = max((c.level for c in kept), default=0)
+        return x, kept, lvl
+
+    def loop_coords(self, level, dims, trip_unroll=16):
+        """Open nested for-loops over ``dims`` (C order) under ``level``;
+        returns (vars, scopes)."""
+        vars_, opened = [], []
+        cur = level
+        for ext in dims:
+            v, s, saved = self.open(cur, "for", trip=ext, unroll=(ext <= trip_unroll))
+            vars_.append(v)
+            opened.append((s, saved))
+            cur = v.level
+        return vars_, opened
+
+    def close_all(self, opened):
+        for s, saved in reversed(opened):
+            self.close(s, saved)
+
+    def reduce(self, r: Node, coords):
+        rop, axes, keepdims, odt = r.op.attrs
+        x, kept, L = self._operand_coords(r, coords, axes, keepdims)
+        T = r.dtype
+        ct = T.ctype
+        So = x.shape
+        red_sizes = [So[a] for a in axes]
+        nred = element_count(red_sizes)
+        if L >= 2 and nred > SMALL_RECOMPUTE:
+            raise NotFusable(r, f"reduction over {nred} points would be recomputed per column")
+        if nred == 0:
+            return self.const(_IDENT[rop](T), T)
+        ident = c_literal(_IDENT[rop](T), T)
+        acc = self.var_decl(L, ct, ident)
+        # coalesce: NumPy merges adjacent reduced axes; the innermost group is
+        # pairwise-summed when it contains the last (contiguous) axis.
+        groups: List[List[int]] = []
+        for a in axes:
+            if groups and groups[-1][-1] == a - 1:
+                groups[-1].append(a)
+            else:
+                groups.append([a])
+        pairwise = (rop is ReduceOp.sum and T.is_float and groups and groups[-1][-1] == len(So) - 1
+                    and element_count([So[a] for a in groups[-1]]) > 1)
+        outer_axes = [a for g in (groups[:-1] if pairwise else groups) for a in g]
+        # sequential loops over outer reduced axes (C order)
+        ovars, opened = self.loop_coords(L, [So[a] for a in outer_axes])
+        loop_lvl = ovars[-1].level if ovars else L
+        amap = dict(zip(outer_axes, ovars))
+
+        def full_coords(inner_map):
+            out = []
+            k = 0
+            for i in range(len(So)):
+                if i in amap:
+                    out.append(Aff.of(amap[i]))
+                elif i in inner_map:
+                    out.append(inner_map[i])
+                else:
+                    out.append(kept[k])
+                    k += 1
+            return out
+
+        comb = _COMBINE[rop]
+        if pairwise and element_count([So[a] for a in groups[-1]]) < 8:
+            # NumPy: n < 8 is a sequential fold from -0.0 — an unrolled loop, so
+            # contiguous operands become one vector load
+            g = groups[-1]
+            gdims = [So[a] for a in g]
+            Lg = element_count(gdims)
+            part = self.var_decl(loop_lvl, ct, c_literal(-0.0, T))
+            iv, s, saved = self.open(loop_lvl, "for", trip=Lg, unroll=True)
+            inner = self._delin(iv, g, gdims)
+            v = self.cast(self.value(x, full_coords(inner)), x.dtype, T)
+            self.stmt(iv.level, f"{part} = gr::add<{ct}>({part}, {v[0]});")
+            self.close(s, saved)
+            self.stmt(loop_lvl, f"{acc} = gr::add<{ct}>({acc}, {part});")
+        elif pairwise:
+            g = groups[-1]
+            gdims = [So[a] for a in g]
+            Lg = element_count(gdims)
+            iv, s, saved = self.open(loop_lvl, "lambda", ret_type=ct)
+            inner = self._delin(iv, g, gdims)
+            v = self.cast(self.value(x, full_coords(inner)), x.dtype, T)
+            self.close(s, saved, ret=v[0])
+            self.stmt(loop_lvl, f"{acc} = gr::add<{ct}>({acc}, gr::pairwise<{ct}, {Lg}LL>(f{iv.name}, 0));")
+        else:
+            v = self.cast(self.value(x, full_coords({})), x.dtype, T)
+            self.stmt(loop_lvl, f"{acc} = {comb}<{ct}>({acc}, {v[0]});")
+        self.close_all(opened)
+        return acc, L
+
+    def _delin(self, iv: Var, group, gdims) -> Dict[int, Aff]:
+        if len(group) == 1:
+            return {group[0]: Aff.of(iv)}
+        out = {}
+        rest = Aff.of(iv)
+        for a, ext in zip(reversed(group), reversed(gdims)):
+            if a == group[0]:
+                out[a] = rest
+            else:
+                out[a] = Aff.of(self.derived_var(iv.level, f"{rest.c()} % {ext}"))
+                rest = Aff.of(self.derived_var(iv.level, f"{rest.c()} / {ext}"))
+        return out
+
+    def argreduce(self, r: Node, coords):
+        which, axis, keepdims = r.op.attrs
+        x = r.preds[0]
+        So = x.shape
+        if axis is None:
+            axes = tuple(range(len(So)))
+            kept = []
+        else:
+            axes = (axis,)
+            kept = [c for i, c in enumerate(coords) if i != axis] if keepdims else list(coords)
+        L = max((c.level for c in kept), default=0)
+        n = element_count([So[a] for a in axes])
+        if L >= 2 and n > SMALL_RECOMPUTE:
+            raise NotFusable(r, f"arg-reduction over {n} points would be recomputed per column")
+        T = x.dtype.ctype
+        best = self.var_decl(L, T, "0")
+        bi = self.var_decl(L, "long long", "0")
+        iv, s, saved = self.open(L, "for", trip=n, unroll=(n <= 16))
+        inner = self._delin(iv, list(axes), [So[a] for a in axes])
+        full = []
+        k = 0
+        for i in range(len(So)):
+            if i in inner:
+                full.append(inner[i])
+            else:
+                full.append(kept[k])
+                k += 1
+        v = self.value(x, full)
+        pred = "gr::arg_better_max" if which == "max" else "gr::arg_better_min"
+        self.stmt(iv.level, f"if ({iv.name} == 0 || {pred}<{T}>({v[0]}, {best})) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
+        self.close(s, saved)
+        return bi, L
+
+
+# ---------------------------------------------------------------------------
+# Thread space analysis
+# ---------------------------------------------------------------------------
+
+
+def _reductions(region: Region):
+    return [n for n in region.nodes if n.kind in (OpKind.REDUCE, OpKind.ARGREDUCE)]
+
+
+def thread_space(region: Region):
+    """(Ts, totals, rows_roots): the row shape every non-total reduction keeps."""
+    totals = [r for r in region.roots if is_total(r)]
+    tot_ids = {t.id for t in totals}
+    reds = [n for n in _reductions(region) if n.id not in tot_ids]
+    for n in _reductions(region):
+        if n.id not in tot_ids and is_total(n):
+            raise NotFusable(n, "a full reduction consumed inside the region")
+    if len(reds) == 1 and reds[0] in region.roots and len(region.roots) == 1 + len(totals) and not totals:
+        # a lone reduction root: one thread per output element, loops over the
+        # reduced axes in NumPy order (covers sum(axis=0) and middle axes)
+        return tuple(reds[0].shape), totals, None
+    if reds:
+        prefixes = []
+        for r in reds:
+            x = r.preds[0]
+            if r.kind is OpKind.REDUCE:
+                lo = min(r.op.attrs[1])
+            else:
+                lo = r.op.attrs[1]
+            prefixes.append((r, tuple(x.shape[:lo])))
+        Ts = min((p for _, p in prefixes), key=len)
+        for r, p in prefixes:
+            if p[:len(Ts)] != Ts:
+                raise NotFusable(r, f"keeps {p}, not the row shape {Ts}")
+        if not Ts:
+            bad = next(r for r, p in prefixes if not p)
+            raise NotFusable(bad, "reduction over the leading axis shares a region with other outputs")
+        virtual = None
+    else:
+        # maps + totals: rows are chunks of the flattened space
+        shapes = [t.preds[0].shape for t in totals] + [r.shape for r in region.roots if r.id not in tot_ids]
+        S = max(shapes, key=len)
+        N = element_count(S)
+        C = _chunk(N)
+        Ts = (N // C,)
+        virtual = (tuple(S), C)
+    return tuple(Ts), totals, virtual
+
+
+def _chunk(N: int) -> int:
+    if N <= 2048:
+        return max(N, 1)
+    c = 2048
+    while c >= 128:
+        if N % c == 0:
+            return c
+        c //= 2
+    for c in range(2048, 0, -1):
+        if N % c == 0:
+            return c
+    return 1
+
+
+# ---------------------------------------------------------------------------
+# Generator
+# ---------------------------------------------------------------------------
+
+
+def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
+    Ts, totals, virtual = thread_space(region)
+    tot_ids = {t.id for t in totals}
+    R = element_count(Ts)
+    em = LoopEmitter(region)
+    rvar = Var("r", 1)
+    # row coordinates
+    if virtual is None:
+        if len(Ts) == 1:
+            row_coords = [Aff.of(rvar)]
+        else:
+            row_coords = []
+            rest = "r"
+            for d in range(len(Ts) - 1, -1, -1):
+                if d == 0:
+                    row_coords.append(Aff.of(Var(rest, 1)))
+                else:
+                    c = em.emit(1, "long long", f"{rest} % {Ts[d]}")
+                    row_coords.append(Aff.of(Var(c, 1)))
+                    rest = em.emit(1, "long long", f"{rest} / {Ts[d]}")
+            row_coords.reverse()
+    body_stores: List[Tuple[int, str]] = []
+
+    def full_root_coords(shape):
+        """Open loops over the columns of a root of ``shape`` (shape[:len(Ts)] == Ts)."""
+        cols = shape[len(Ts):]
+        vars_, opened = em.loop_coords(1, list(cols))
+        return row_coords + [Aff.of(v) for v in vars_], opened, cols
+
+    def virtual_coords(S, C):
+        iv, s, saved = em.open(1, "for", trip=C, unroll=(C <= 16))
+        lin = Aff.of(rvar).scale(C) + Aff.of(iv)
+        coords = []
+        if len(S) == 1:
+            coords = [lin]
+        else:
+            rest = lin
+            for d in range(len(S) - 1, -1, -1):
+                if d == 0:
+                    coords.append(rest)
+                else:
+                    coords.append(Aff.of(em.derived_var(iv.level, f"{rest.c()} % {S[d]}")))
+                    rest = Aff.of(em.derived_var(iv.level, f"{rest.c()} / {S[d]}"))
+            coords.reverse()
+        return coords, [(s, saved)], iv
+
+    partial_info = []
+    for ri, r in enumerate(region.roots):
+        if r.id in tot_ids:
+            continue
+        T = r.dtype.ctype
+        if virtual is not None:
+            S, C = virtual
+            if tuple(r.shape) != S:
+                raise NotFusable(r, "map root shape differs from the reduced space")
+            coords, opened, iv = virtual_coords(S, C)
+            v = em.value(r, coords)
+            em.stmt(iv.level, f"gr::st<{T}>(p.out{ri} + r * {C}LL + {iv.name}, {v[0]});")
+            em.close_all(opened)
+            continue
+        if tuple(r.shape[:len(Ts)]) != Ts:
+            raise NotFusable(r, f"root shape {r.shape} does not start with the row shape {Ts}")
+        cols = r.shape[len(Ts):]
+        if element_count(cols) == 1:
+            v = em.value(r, row_coords + [Aff.of(0)] * len(cols))
+            em.stmt(1, f"gr::st<{T}>(p.out{ri} + r, {v[0]});")
+        else:
+            coords, opened, cols = full_root_coords(r.shape)
+            v = em.value(r, coords)
+            st = row_major_strides(cols)
+            off = Aff.of(rvar).scale(element_count(cols))
+            for c, s_ in zip(coords[len(Ts):], st):
+                off = off + c.scale(s_)
+            em.stmt(max(v[1], opened[-1][0].level), f"gr::st<{T}>(p.out{ri} + {off.c()}, {v[0]});")
+            em.close_all(opened)
+
+    # totals: one partial per row
+    scratch_off = 0
+    tot_meta = []
+    for ri, r in enumerate(region.roots):
+        if r.id not in tot_ids:
+            continue
+        x = r.preds[0]
+        if r.kind is OpKind.ARGREDUCE:
+            which = r.op.attrs[0]
+            xt = x.dtype
+            if virtual is not None:
+                S, C = virtual
+                if tuple(x.shape) != S:
+                    raise NotFusable(r, "total operand shape differs")
+                best, bi = _arg_partial(em, x, which, None, S, C)
+                glob = f"r * {C}LL + {bi}"
+            else:
+                if tuple(x.shape[:len(Ts)]) != Ts:
+                    raise NotFusable(r, f"total operand {x.shape} does not start with rows {Ts}")
+                cols = x.shape[len(Ts):]
+                C = element_count(cols)
+                best, bi = _arg_partial(em, x, which, row_coords, None, C, cols)
+                glob = f"r * {C}LL + {bi}"
+            voff = scratch_off
+            scratch_off += ((R * xt.itemsize + 255) // 256) * 256
+            ioff = scratch_off
+            scratch_off += ((R * 8 + 255) // 256) * 256
+            em.stmt(1, f"reinterpret_cast<{xt.ctype}*>(static_cast<char*>(p.scratch) + {voff})[r] = {best};")
+            em.stmt(1, f"reinterpret_cast<long long*>(static_cast<char*>(p.scratch) + {ioff})[r] = {glob};")
+            tot_meta.append((ri, ("arg", which), xt, (voff, ioff)))
+            continue
+        rop = r.op.attrs[0]
+        T = r.dtype
+        ct = T.ctype
+        if virtual is not None:
+            S, C = virtual
+            if tuple(x.shape) != S:
+                raise NotFusable(r, "total operand shape differs")
+            # partial = NumPy pairwise over this row's chunk of the flat space
+            part = _chunk_partial(em, x, rop, T, S, C)
+        else:
+            if tuple(x.shape[:len(Ts)]) != Ts:
+                raise NotFusable(r, f"total operand {x.shape} does not start with rows {Ts}")
+            cols = x.shape[len(Ts):]
+            if element_count(cols) == 1:
+                v = em.cast(em.value(x, row_coords + [Aff.of(0)] * len(cols)), x.dtype, T)
+                part = v[0]
+            else:
+                part = _row_partial(em, x, rop, T, row_coords, cols)
+        off = scratch_off
+        em.stmt(1, f"reinterpret_cast<{ct}*>(static_cast<char*>(p.scratch) + {off})[r] = {part};")
+        tot_meta.append((ri, rop, T, off))
+        scratch_off += ((R * T.itemsize + 255) // 256) * 256
+
+    lines = ["static __device__ __forceinline__ void row(const Params& p, const long long r) {"]
+    lines += ["  " + c for c in em.consts]
+    lines += render(em.row, 1)
+    lines.append("}")
+    params = _params_struct(region).replace("    void* __restrict__ scratch;",
+                                             "    void* __restrict__ scratch;\n    unsigned int* ticket;")
+    src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params,
+           f"  static constexpr long long NROWS = {R}LL;"]
+    src.append("  " + "\n  ".join(lines))
+    src.append("};")
+    kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
+            "  const long long stride = (long long)gridDim.x * blockDim.x;",
+            "  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride)",
+            "    K::row(p, r);"]
+    if tot_meta:
+        kern.append("  if (gr::last_block(p.ticket)) {")
+        for ri, rop, T, off in tot_meta:
+            ct = T.ctype
+            if isinstance(rop, tuple):
+                mx = "true" if rop[1] == "max" else "false"
+                voff, ioff = off
+                kern.append(f"    const long long v{ri} = gr::block_arg<{mx}, {ct}>("
+                            f"reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {voff}), "
+                            f"reinterpret_cast<const long long*>(static_cast<const char*>(p.scratch) + {ioff}), K::NROWS);")
+                kern.append(f"    if (threadIdx.x == 0) p.out{ri}[0] = v{ri};")
+                continue
+            ident = c_literal(_IDENT[rop](T), T)
+            kern.append(f"    const {ct} v{ri} = gr::block_tree<{_OPS[rop]}, {ct}>("
+                        f"reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {off}), K::NROWS, {ident});")
+            fin = f"gr::add<{ct}>({c_literal(0, T)}, v{ri})" if rop is ReduceOp.sum else f"v{ri}"
+            kern.append(f"    if (threadIdx.x == 0) p.out{ri}[0] = {fin};")
+        kern.append("  }")
+    kern.append("}")
+    src += kern
+    return KernelSource("rows", "\n".join(src) + "\n", kname,
+                        leaf_slots=list(range(len(region.leaves))),
+                        root_slots=list(range(len(region.roots))),
+                        block=block, groups=R, vec=1, unroll=1, scratch_bytes=scratch_off,
+                        meta={"rows": R, "row_shape": Ts, "totals": len(tot_meta), "ticket": bool(tot_meta),
+                              "virtual": virtual, "block_pow2": True})
+
+
+def _row_partial(em: LoopEmitter, x: Node, rop, T: DType, row_coords, cols):
+    """Reduction of x over the row's columns with NumPy order (a total's partial)."""
+    ct = T.ctype
+    ident = c_literal(_IDENT[rop](T), T)
+    if rop is ReduceOp.sum and T.is_float:
+        C = element_count(cols)
+        iv, s, saved = em.open(1, "lambda", ret_type=ct)
+        inner = em._delin(iv, list(range(len(row_coords), len(row_coords) + len(cols))), list(cols))
+        coords = row_coords + [inner[i] for i in range(len(row_coords), len(row_coords) + len(cols))]
+        v = em.cast(em.value(x, coords), x.dtype, T)
+        em.close(s, saved, ret=v[0])
+        return em.emit(1, ct, f"gr::pairwise<{ct}, {C}LL>(f{iv.name}, 0)")
+    acc = em.var_decl(1, ct, ident)
+    vars_, opened = em.loop_coords(1, list(cols))
+    v = em.cast(em.value(x, row_coords + [Aff.of(v_) for v_ in vars_]), x.dtype, T)
+    em.stmt(max(v[1], vars_[-1].level), f"{acc} = {_COMBINE[rop]}<{ct}>({acc}, {v[0]});")
+    em.close_all(opened)
+    return acc
+
+
+def _chunk_partial(em: LoopEmitter, x: Node, rop, T: DType, S, C):
+    ct = T.ctype
+    ident = c_literal(_IDENT[rop](T), T)
+    pw = rop is ReduceOp.sum and T.is_float
+    if pw:
+        iv, s, saved = em.open(1, "lambda", ret_type=ct)
+    else:
+        acc = em.var_decl(1, ct, ident)
+        iv, s, saved = em.open(1, "for", trip=C, unroll=(C <= 16))
+    lin = Aff.of(Var("r", 1)).scale(C) + Aff.of(iv)
+    coords = []
+    if len(S) == 1:
+        coords = [lin]
+    else:
+        rest = lin
+        for d in range(len(S) - 1, -1, -1):
+            if d == 0:
+                coords.append(rest)
+            else:
+                coords.append(Aff.of(em.derived_var(iv.level, f"{rest.c()} % {S[d]}")))
+                rest = Aff.of(em.derived_var(iv.level, f"{rest.c()} / {S[d]}"))
+        coords.reverse()
+    v = em.cast(em.value(x, coords), x.dtype, T)
+    if pw:
+        em.close(s, saved, ret=v[0])
+        return em.emit(1, ct, f"gr::pairwise<{ct}, {C}LL>(f{iv.name}, 0)")
+    em.stmt(iv.level, f"{acc} = {_COMBINE[rop]}<{ct}>({acc}, {v[0]});")
+    em.close(s, saved)
+    return acc
+
+
+def _arg_partial(em: LoopEmitter, x: Node, which, row_coords, S, C, cols=None):
+    """First-index arg-reduction of x over this row's columns (row mode) or its
+    chunk of the flattened space (virtual mode); returns (best, local index)."""
+    T = x.dtype.ctype
+    best = em.var_decl(1, T, "0")
+    bi = em.var_decl(1, "long long", "0")
+    iv, s, saved = em.open(1, "for", trip=C, unroll=(C <= 16))
+    if row_coords is None:
+        lin = Aff.of(Var("r", 1)).scale(C) + Aff.of(iv)
+        shape = S
+        coords = []
+        if len(shape) == 1:
+            coords = [lin]
+        else:
+            rest = lin
+            for d in range(len(shape) - 1, -1, -1):
+                if d == 0:
+                    coords.append(rest)
+                else:
+                    coords.append(Aff.of(em.derived_var(iv.level, f"{rest.c()} % {shape[d]}")))
+                    rest = Aff.of(em.derived_var(iv.level, f"{rest.c()} / {shape[d]}"))
+            coords.reverse()
+    else:
+        nrow = len(row_coords)
+        inner = em._delin(iv, list(range(nrow, nrow + len(cols))), list(cols))
+        coords = list(row_coords) + [inner[i] for i in range(nrow, nrow + len(cols))]
+    v = em.value(x, coords)
+    pred = "gr::arg_better_max" if which == "max" else "gr::arg_better_min"
+    em.stmt(iv.level, f"if ({iv.name} == 0 || {pred}<{T}>({v[0]}, {best})) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
+    em.close(s, saved)
+    return best, bi

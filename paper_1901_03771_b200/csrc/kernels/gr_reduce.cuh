@@ -1,0 +1,238 @@
+// gr_reduce.cuh — reduction templates with NumPy's association order.
+//
+// The reference reduces with per-thread sequential folds combined in thread
+// order; its baseline is NumPy, whose float add.reduce
+// is *pairwise* along the contiguous axis (numpy/_core/src/umath/
+// loops_utils.h.src pairwise_sum: n < 8 sequential from -0.0; 8 <= n <= 128
+// eight strided accumulators combined ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) plus
+// a sequential tail; n > 128 split at n2 = n/2 - (n/2)%8) and sequential along
+// the other axes, starting from the identity 0.0.  Restated and pinned in
+// oracle/pairwise.py.  These templates reproduce that order exactly, so a
+// fused reduction of IEEE-exact terms is bit-identical to NumPy.
+#pragma once
+
+namespace gr {
+
+template <class T> __device__ __forceinline__ T shfl_xor(T v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+template <> __device__ __forceinline__ bool shfl_xor(bool v, int m) { return __shfl_xor_sync(0xffffffffu, (int)v, m) != 0; }
+
+template <class T> struct Zero { static __device__ __forceinline__ T neg() { return T(0); } };
+template <> struct Zero<float> { static __device__ __forceinline__ float neg() { return -0.0f; } };
+template <> struct Zero<double> { static __device__ __forceinline__ double neg() { return -0.0; } };
+
+// True when NumPy's recursion over N splits in exact halves down to 128-leaves.
+__host__ __device__ constexpr bool pw_regular(long long n) {
+  return n == 128 || (n > 128 && n % 256 == 0 && pw_regular(n / 2));
+}
+__host__ __device__ constexpr int pw_log2(long long n) { return n <= 1 ? 0 : 1 + pw_log2(n / 2); }
+
+// NumPy pairwise_sum over f(off .. off+N); N is a compile-time extent.
+template <class T, long long N, class F>
+__device__ __forceinline__ T pairwise(const F& f, long long off) {
+  if constexpr (N < 8) {
+    T r = Zero<T>::neg();
+#pragma unroll
+    for (long long i = 0; i < N; ++i) r = add<T>(r, f(off + i));
+    return r;
+  } else if constexpr (N <= 128) {
+    T r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = f(off + j);
+    constexpr long long NB = N - (N % 8);
+#pragma unroll 2
+    for (long long i = 8; i < NB; i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = add<T>(r[j], f(off + i + j));
+    }
+    T res = add<T>(add<T>(add<T>(r[0], r[1]), add<T>(r[2], r[3])), add<T>(add<T>(r[4], r[5]), add<T>(r[6], r[7])));
+#pragma unroll
+    for (long long i = NB; i < N; ++i) res = add<T>(res, f(off + i));
+    return res;
+  } else if constexpr (pw_regular(N)) {
+    // perfect binary tree over N/128 leaves: fold leaves left to right with a
+    // binary-counter stack (stack[l] holds a finished subtree of 2^l leaves)
+    constexpr long long NL = N / 128;
+    constexpr int D = pw_log2(NL) + 1;
+    T stack[D];
+#pragma unroll 1
+    for (long long b = 0; b < NL; ++b) {
+      T v = pairwise<T, 128>(f, off + b * 128);
+      int l = 0;
+      long long c = b;
+      while (c & 1) {
+        v = add<T>(stack[l], v);
+        ++l;
+        c >>= 1;
+      }
+      stack[l] = v;
+    }
+    return stack[D - 1];
+  } else {
+    constexpr long long H = N / 2;
+    constexpr long long N2 = H - (H % 8);
+    return add<T>(pairwise<T, N2>(f, off), pairwise<T, N - N2>(f, off + N2));
+  }
+}
+
+// first-index arg-reduction predicates (np.argmax / np.argmin: the first
+// maximal element wins; a NaN is maximal and minimal, the first NaN wins)
+template <class T> __device__ __forceinline__ bool arg_better_max(T x, T best) {
+  return (x > best) || (x != x && best == best);
+}
+template <class T> __device__ __forceinline__ bool arg_better_min(T x, T best) {
+  return (x < best) || (x != x && best == best);
+}
+template <> __device__ __forceinline__ bool arg_better_max(bool x, bool best) { return x && !best; }
+template <> __device__ __forceinline__ bool arg_better_min(bool x, bool best) { return !x && best; }
+
+// Is candidate (bv, bi) a better np.argmax/argmin answer than (av, ai)?
+// NaN beats numbers; among equals (or NaNs) the lower index wins.
+template <bool MAX, class T> __device__ __forceinline__ bool arg_take_b(T av, long long ai, T bv, long long bi) {
+  const bool an = av != av, bn = bv != bv;
+  if (an || bn) return bn && (!an || bi < ai);
+  if (MAX ? (bv > av) : (bv < av)) return true;
+  if (bv == av) return bi < ai;
+  return false;
+}
+
+// CTA-wide first-index arg-reduction over n (value, index) candidates.
+template <bool MAX, class T> __device__ long long block_arg(const T* v, const long long* ix, long long n) {
+  __shared__ T sv[32];
+  __shared__ long long si[32];
+  const long long nt = blockDim.x;
+  const long long chunk = (n + nt - 1) / nt;
+  const long long lo = threadIdx.x * chunk;
+  const long long hi = lo + chunk < n ? lo + chunk : n;
+  T best = T(0);
+  long long bi = -1;
+  for (long long i = lo; i < hi; ++i) {
+    if (bi < 0 || arg_take_b<MAX, T>(best, bi, v[i], ix[i])) {
+      best = v[i];
+      bi = ix[i];
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    T ov = shfl_xor<T>(best, m);
+    long long oi = __shfl_xor_sync(0xffffffffu, bi, m);
+    if (oi >= 0 && (bi < 0 || arg_take_b<MAX, T>(best, bi, ov, oi))) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  if (lane == 0) {
+    sv[w] = best;
+    si[w] = bi;
+  }
+  __syncthreads();
+  if (w == 0) {
+    best = lane < nw ? sv[lane] : T(0);
+    bi = lane < nw ? si[lane] : -1;
+#pragma unroll
+    for (int m = 1; m < 32; m <<= 1) {
+      T ov = shfl_xor<T>(best, m);
+      long long oi = __shfl_xor_sync(0xffffffffu, bi, m);
+      if (oi >= 0 && (bi < 0 || arg_take_b<MAX, T>(best, bi, ov, oi))) {
+        best = ov;
+        bi = oi;
+      }
+    }
+    if (lane == 0) si[0] = bi;
+  }
+  __syncthreads();
+  long long r = si[0];
+  __syncthreads();
+  return r;
+}
+
+// ---- combine ops for cross-thread / cross-block trees -----------------------
+struct OpSum {
+  template <class T> static __device__ __forceinline__ T c(T a, T b) { return add<T>(a, b); }
+};
+struct OpProd {
+  template <class T> static __device__ __forceinline__ T c(T a, T b) { return mul<T>(a, b); }
+};
+struct OpMax {
+  template <class T> static __device__ __forceinline__ T c(T a, T b) { return (a != a) ? a : ((b != b) ? b : (b > a ? b : a)); }
+};
+struct OpMin {
+  template <class T> static __device__ __forceinline__ T c(T a, T b) { return (a != a) ? a : ((b != b) ? b : (b < a ? b : a)); }
+};
+
+// Perfect binary tree over the lanes of a warp in lane order (pairs (0,1),
+// (2,3), ... then (01,23), ...): the association of NumPy's pairwise split for
+// power-of-two counts.  Every lane ends with the full result.
+template <class Op, class T> __device__ __forceinline__ T warp_tree(T v, int width = 32) {
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    if (m < width) {
+      T o = shfl_xor<T>(v, m);
+      // lower lane's value is the left operand (add/mul commute exactly in IEEE)
+      v = Op::template c<T>(v, o);
+    }
+  }
+  return v;
+}
+
+// Tree over n partials p[0..n) in index order, by one CTA (blockDim.x a power
+// of two <= 1024, n arbitrary).  Each thread folds a contiguous power-of-two
+// chunk as a perfect binary tree (binary-counter stack), then warp and CTA
+// trees: for power-of-two n this is exactly the perfect binary tree over p,
+// i.e. NumPy's pairwise split above row granularity.
+template <class Op, class T> __device__ T block_tree(const T* p, long long n, T ident) {
+  __shared__ T sh[32];
+  const int t = threadIdx.x, nt = blockDim.x;
+  long long chunk = 1;
+  while (chunk * nt < n) chunk <<= 1;
+  const long long lo = (long long)t * chunk;
+  T stack[40];
+  long long cnt = 0;
+  for (long long i = 0; i < chunk; ++i) {
+    T v = (lo + i < n) ? p[lo + i] : ident;
+    int lvl = 0;
+    while ((cnt >> lvl) & 1) {
+      v = Op::template c<T>(stack[lvl], v);
+      ++lvl;
+    }
+    stack[lvl] = v;
+    ++cnt;
+  }
+  int top = 0;
+  while ((1ll << top) < chunk) ++top;
+  T acc = stack[top];
+  acc = warp_tree<Op, T>(acc);
+  const int lane = t & 31, w = t >> 5, nw = (nt + 31) >> 5;
+  if (lane == 0) sh[w] = acc;
+  __syncthreads();
+  if (w == 0) {
+    T v = lane < nw ? sh[lane] : ident;
+    v = warp_tree<Op, T>(v);
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  T r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Grid completion ticket: returns true in exactly one (the last) block, after
+// every block's partials are visible.  The ticket self-resets for the next
+// launch of the same kernel (stream order serialises launches).
+__device__ __forceinline__ bool last_block(unsigned int* ticket) {
+  __shared__ bool am_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    unsigned int prev = atomicAdd(ticket, 1u);
+    am_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (am_last) {
+    __threadfence();
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+  return am_last;
+}
+
+}  // namespace gr

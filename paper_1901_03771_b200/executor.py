@@ -31,6 +31,7 @@ class Executor:
         self.last_steps: List[PlanStep] = []
         self.launch_log = collections.deque(maxlen=4096)  # (family, kernel name) per launch
         self.profile = None           # per-launch CUDA events when enabled
+        self._tickets = {}
 
     # -- planner hook ---------------------------------------------------------------
     def row_fusion(self, reduction: Node, consumer: Node) -> bool:
@@ -65,12 +66,7 @@ class Executor:
                 self.session.stats.nodes_materialized += len(st.roots)
 
     def kernel_source(self, region: codegen.Region) -> codegen.KernelSource:
-        sig = codegen.signature(region)
-        ks = self._gen_cache.get(sig)
-        if ks is None:
-            ks = codegen.generate(region)
-            self._gen_cache[sig] = ks
-        return ks
+        return codegen.cached_generate(region)
 
     def run_fused(self, st: PlanStep) -> List[TensorBuffer]:
         c = st.cache
@@ -101,6 +97,15 @@ class Executor:
             ptrs.append(scratch.ptr)
         else:
             ptrs.append(0)
+        if ks.meta.get("ticket"):
+            # grid-completion counter: zeroed once, reset by the last CTA of
+            # every launch (launches of one kernel are stream-ordered)
+            tk = self._tickets.get(id(ks))
+            if tk is None:
+                tk = self.rt.alloc(256)
+                self.rt.memset(tk, 0)
+                self._tickets[id(ks)] = tk
+            ptrs.append(tk.ptr)
         params = runtime.pack_params(ptrs)
         if self.profile is not None:
             e0, e1 = self._event_pair()

@@ -324,10 +324,38 @@ def _is_view(n: Node) -> bool:
     return n.kind in (OpKind.TRANSPOSE, OpKind.RESHAPE, OpKind.SLICE, OpKind.BROADCAST)
 
 
-def plan_regions(roots: Sequence[Node], row_fusion=None) -> List[PlanStep]:
-    """B200 region planner (module docstring).  ``row_fusion(reduction, consumer)``
-    is the code generator's predicate for keeping a reduction inside its
-    consumer's kernel; None disables row fusion (every reduction is a root)."""
+def plan_regions(roots: Sequence[Node], row_fusion=None, check=None) -> List[PlanStep]:
+    """B200 region planner (module docstring).
+
+    ``row_fusion(reduction, consumer)`` proposes keeping a reduction inside its
+    consumer's kernel (None: every reduction is its own step).  ``check(step)``
+    is the code generator's verdict; when it raises an exception carrying
+    ``.node`` that node becomes a materialization point and planning repeats.
+    """
+    extra: Set[int] = set()
+    for _ in range(256):
+        steps = _plan_once(roots, row_fusion, extra, check)
+        if check is None:
+            return steps
+        bad = None
+        for st in steps:
+            if st.kind != "Fused":
+                continue
+            try:
+                check(st)
+            except Exception as e:  # NotFusable
+                node = getattr(e, "node", None)
+                if node is None or node.id in extra or node.id in {r.id for r in st.roots}:
+                    raise
+                bad = node
+                break
+        if bad is None:
+            return steps
+        extra.add(bad.id)
+    raise RuntimeError("region planning did not converge")
+
+
+def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check) -> List[PlanStep]:
     roots = [r for r in dict((r.id, r) for r in roots).values() if not r.is_materialized]
     if not roots:
         return []
@@ -352,6 +380,9 @@ def plan_regions(roots: Sequence[Node], row_fusion=None) -> List[PlanStep]:
     points: Dict[int, Node] = {r.id: r for r in roots}
     for n in demand.values():
         if n.is_materialized:
+            continue
+        if n.id in extra:
+            points[n.id] = n
             continue
         if n.kind in LIBRARY_KINDS:
             points[n.id] = n
@@ -405,6 +436,34 @@ def plan_regions(roots: Sequence[Node], row_fusion=None) -> List[PlanStep]:
                 merged.append(c)
         else:
             merged.append(c)
+    # 4b. fold a reduction step into the step producing its operand (y and
+    # y.sum() in one kernel), or fuse cones sharing inputs with a reduction
+    # step; each candidate merge is kept only if the code generator accepts it
+    if check is not None:
+        changed = True
+        while changed:
+            changed = False
+            for a in list(merged):
+                if a.kind != "Fused" or a.kernel_kind != "MapReduce":
+                    continue
+                for b in merged:
+                    if b is a or b.kind != "Fused":
+                        continue
+                    if not (_depends(a, b) or (_shares(a, b) and not _depends(b, a))):
+                        continue
+                    if _depends(b, a):
+                        continue
+                    trial = _merged_copy(b, a)
+                    try:
+                        check(trial)
+                    except Exception:
+                        continue
+                    b.roots, b.nodes, b.leaves, b.kernel_kind = trial.roots, trial.nodes, trial.leaves, trial.kernel_kind
+                    merged.remove(a)
+                    changed = True
+                    break
+                if changed:
+                    break
 
     # 5. topological order over steps
     produced = {}
@@ -442,6 +501,22 @@ def _depends(a: PlanStep, b: PlanStep) -> bool:
     """True if a reads any root of b."""
     rb = {r.id for r in b.roots}
     return any(l.id in rb for l in a.leaves)
+
+
+def _merged_copy(b: PlanStep, a: PlanStep) -> PlanStep:
+    """b ∪ a where a may read b's roots (they become interior)."""
+    broots = {r.id for r in b.roots}
+    ids = {n.id for n in b.nodes}
+    nodes = sorted(b.nodes + [n for n in a.nodes if n.id not in ids], key=lambda x: x.id)
+    nids = {n.id for n in nodes}
+    leaves = [l for l in b.leaves]
+    lids = {l.id for l in leaves}
+    for l in a.leaves:
+        if l.id not in lids and l.id not in broots and l.id not in nids:
+            leaves.append(l)
+            lids.add(l.id)
+    kind = "MapReduce" if "MapReduce" in (a.kernel_kind, b.kernel_kind) else b.kernel_kind
+    return PlanStep("Fused", b.roots + a.roots, nodes, leaves, kernel_kind=kind)
 
 
 def _merge_into(m: PlanStep, c: PlanStep):

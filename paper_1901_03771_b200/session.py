@@ -89,7 +89,8 @@ class Session:
                         steps.append(st)
                         done.add(st.root.id)
             return steps
-        return _planner.plan_regions(roots, row_fusion=self.executor.row_fusion)
+        from . import codegen
+        return _planner.plan_regions(roots, row_fusion=codegen.row_fusable, check=codegen.check_step)
 
     def const(self, value, dtype: DType) -> Node:
         """Interned rank-0 const_splat node (constants are immutable)."""

@@ -1,0 +1,89 @@
+"""GPU parity for regions with reductions (K2-K5) against the NumPy oracle.
+
+Float sums are generated in NumPy's pairwise order, so sums of IEEE-exact
+terms are asserted bit-exact; transcendental terms use the stated tolerance.
+"""
+import numpy as np
+import pytest
+
+import paper_1901_03771_b200 as gp
+from paper_1901_03771_b200 import workloads as wl
+from oracle import eager
+
+pytestmark = pytest.mark.gpu
+
+
+def test_rownorm_exact(sess):
+    (x,) = wl.rownorm_inputs(rows=512, cols=256)
+    y, tot = wl.rownorm(gp, gp.asarray(x))
+    gp.force(y, tot)
+    assert sess.stats.kernels_executed == 1
+    ey, et = wl.rownorm(np, x)
+    assert np.array_equal(np.asarray(y), ey)
+    assert np.asarray(tot) == et
+
+
+def test_softmax_argmax(sess):
+    rng = np.random.default_rng(3)
+    z = rng.standard_normal((1000, 10)).astype(np.float32)
+    gz = gp.asarray(z)
+    p = gp.exp(gz - gz.max(1)[:, None])
+    p = p / p.sum(1)[:, None]
+    lab = p.argmax(1)
+    gp.force(p, lab)
+    assert sess.stats.kernels_executed == 1
+    ep = np.exp(z - z.max(1)[:, None])
+    ep = ep / ep.sum(1)[:, None]
+    np.testing.assert_allclose(np.asarray(p), ep, rtol=1e-5, atol=1e-7)
+    assert np.array_equal(np.asarray(lab), ep.argmax(1))
+
+
+def test_kmeans_labels_exact(sess):
+    P, C = wl.kmeans_inputs(n=1 << 14, k=64, d=4)
+    lab = wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C))
+    assert np.array_equal(np.asarray(lab), wl.kmeans_assign(np, P, C))
+    assert sess.stats.kernels_executed == 1
+
+
+@pytest.mark.parametrize("shape,axis", [((300, 50), 0), ((300, 50), 1), ((7, 9, 11), (0, 2)),
+                                        ((7, 9, 11), 1), ((1 << 16,), None), ((512, 256), None),
+                                        ((1000, 3), None)])
+def test_sum_axes_exact(sess, shape, axis):
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal(shape).astype(np.float32)
+    g = gp.asarray(x).sum(axis=axis)
+    assert np.array_equal(np.asarray(g), x.sum(axis=axis))
+
+
+@pytest.mark.parametrize("op", ["max", "min", "argmax", "argmin", "mean", "std", "prod"])
+def test_reductions_misc(sess, op):
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((257, 33))
+    x[3, 7] = np.nan
+    for axis in (None, 0, 1):
+        got = np.asarray(getattr(gp.asarray(x), op)(axis=axis))
+        exp = getattr(x, op)(axis=axis)
+        if op in ("argmax", "argmin", "max", "min"):
+            assert np.array_equal(got, exp, equal_nan=True), (op, axis)
+        else:
+            np.testing.assert_allclose(got, exp, rtol=1e-12, equal_nan=True)
+
+
+def test_int_and_bool_reductions(sess):
+    rng = np.random.default_rng(6)
+    a = rng.integers(-1000, 1000, (123, 45)).astype(np.int32)
+    g = gp.asarray(a)
+    assert np.array_equal(np.asarray(g.sum(1)), a.sum(1))
+    assert np.asarray(g.sum()) == a.sum()
+    assert np.array_equal(np.asarray((g > 0).any(0)), (a > 0).any(0))
+    assert np.array_equal(np.asarray((g > -990).all(1)), (a > -990).all(1))
+    assert np.array_equal(np.asarray(g.max(0)), a.max(0))
+
+
+def test_region_against_eager_oracle(sess):
+    rng = np.random.default_rng(7)
+    x = gp.asarray(rng.standard_normal((64, 48)))
+    y = gp.asarray(rng.standard_normal(48))
+    r = (x * y - (x * y).mean(1, keepdims=True)).max(1) + x.sum() * 0.0
+    expect = eager.evaluate(r.node)
+    np.testing.assert_allclose(np.asarray(r), expect, rtol=1e-12)
