@@ -1,11 +1,315 @@
-"""Cooperative row family (K3): one thread group per long row, row in registers.
+"""Cooperative row family (K3): a thread group per long row, row in registers.
 
-Filled in by the row-normalise work; ``try_generate`` returns None when the
-region does not qualify, and the thread-per-row family handles it.
+Used for regions whose reductions all reduce the full (single) column axis
+of long rows — row-normalise (x - mean)/std and its total, softmax over wide
+rows, row-wise argmax.  The thread-per-row family (codegen_rows.py) would
+serialise a 4096-element row in one thread with uncoalesced loads; here:
+
+* a row of C = 128·2^k elements is spread over TPR = (C/128)·P threads; thread
+  (leaf l, part h) owns elements 128·l + 8·m + h·VEC + v (m < 16, v < VEC),
+  i.e. VEC of NumPy's eight leaf accumulators, so every leaf access is one
+  16-byte load and each warp instruction covers whole 32-byte sectors;
+* every leaf the region reads along the row is loaded ONCE into registers
+  (``S[16][VEC]``) and reused by every phase (sum for the mean, sum of
+  squares, the normalised store, the total) — HBM sees x exactly once;
+* row sums are combined as NumPy's pairwise_sum does: the 8 accumulators of a
+  leaf as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), leaves in a perfect binary tree
+  (``gr::row_sum``) — bit-identical to numpy.add.reduce along the row;
+* totals fold one partial per row with the last-CTA tree of gr_reduce.cuh.
 """
 
 from __future__ import annotations
 
+from typing import List, Optional
 
-def try_generate(region):
-    return None
+from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, c_literal
+from .codegen_rows import (
+    _COMBINE, _IDENT, _OPS, LoopEmitter, NotFusable, is_total, render, thread_space,
+)
+from .dag import Node, OpKind, ReduceOp
+from .tensor import DType, element_count
+
+MAX_TPR = 512
+
+
+def _regular(c: int) -> bool:
+    return c == 128 or (c > 128 and c % 256 == 0 and _regular(c // 2))
+
+
+class CoopEmitter(LoopEmitter):
+    def __init__(self, region, vec, tpr, rpc, row_shape, C):
+        super().__init__(region, vec_loads=False)
+        self.vec = vec
+        self.tpr = tpr
+        self.rpc = rpc
+        self.P = 8 // vec
+        self.Ts = row_shape
+        self.C = C
+        self.cb = Var("cb", 1, align=vec)     # thread's first column (128*l + h*VEC)
+        self.coop_m: Optional[Var] = None
+        self.coop_v: Optional[Var] = None
+        self.staged = {}
+        self.n_sh = 0
+
+    # col coordinate of the current coop loops
+    def coop_col(self, m: Var, v: Var) -> Aff:
+        return Aff.of(self.cb) + Aff.of(m).scale(8) + Aff.of(v)
+
+    def close_coop(self, mm, vv):
+        self.close(vv[1], vv[2])
+        self.close(mm[1], mm[2])
+
+    def load_leaf(self, leaf: Node, off: Aff):
+        # staged row segment: offset = rest + cb + 8*m + v with m, v the coop loop vars
+        for m, v in self._coop_pairs():
+            if off.coef(v) == 1 and off.coef(m) == 8 and off.coef(self.cb) == 1:
+                rest = off.without(v).without(m).without(self.cb)
+                if rest.level <= 1 and rest.alignment() % self.vec == 0:
+                    key = (leaf.id, rest.key())
+                    name = self.staged.get(key)
+                    if name is None:
+                        name = self.fresh("S")
+                        T = leaf.dtype.ctype
+                        idx = self.leaf_index[leaf.id]
+                        self.stmt(1, f"{T} {name}[16][{self.vec}];")
+                        self.stmt(1, f"#pragma unroll\n    for (int mm = 0; mm < 16; ++mm) "
+                                     f"gr::ldv<{T}, {self.vec}>({name}[mm], p.in{idx} + {rest.c()} + cb + 8 * mm);")
+                        self.staged[key] = name
+                    return f"{name}[{m.name}][{v.name}]", max(v.level, off.level)
+        return super().load_leaf(leaf, off)
+
+    def _coop_pairs(self):
+        out = []
+        for i in range(2, len(self.stack) - 1):
+            a, b = self.stack[i], self.stack[i + 1]
+            if (a is not None and b is not None and a.kind == "for" and b.kind == "for" and a.trip == 16
+                    and b.trip == self.vec and getattr(a, "coop", False)):
+                out.append((a.var, b.var))
+        return out
+
+    def open_coop(self, level):
+        """Open the (m < 16, v < VEC) loops over this thread's row elements."""
+        m, sm, savm = self.open(level, "for", trip=16, unroll=True)
+        sm.coop = True
+        v, sv, savv = self.open(m.level, "for", trip=self.vec, unroll=True)
+        return (m, sm, savm), (v, sv, savv)
+
+    # -- row-complete reductions ---------------------------------------------------
+    def _row_complete(self, r: Node, axes) -> bool:
+        x = r.preds[0]
+        return (tuple(x.shape[:len(self.Ts)]) == self.Ts and len(x.shape) == len(self.Ts) + 1
+                and x.shape[-1] == self.C and tuple(axes) == (len(self.Ts),))
+
+    def reduce(self, r: Node, coords):
+        rop, axes, keepdims, odt = r.op.attrs
+        if not self._row_complete(r, axes):
+            return super().reduce(r, coords)
+        kept = [c for i, c in enumerate(coords) if i not in axes] if keepdims else list(coords)
+        if any(c.level > 1 for c in kept):
+            raise NotFusable(r, "row reduction consumed per column")
+        return self.coop_reduce(r.preds[0], rop, r.dtype, kept), 1
+
+    def coop_reduce(self, x: Node, rop, T: DType, row_coords, identity=True):
+        """Reduce x over this row's C columns across the TPR threads; float sums
+        in NumPy pairwise order (``identity``: apply NumPy's 0.0 start)."""
+        ct = T.ctype
+        acc = self.fresh("acc")
+        self.stmt(1, f"{ct} {acc}[{self.vec}];")
+        mm, vv = self.open_coop(1)
+        m, v = mm[0], vv[0]
+        val = self.cast(self.value(x, list(row_coords) + [self.coop_col(m, v)]), x.dtype, T)
+        comb = _COMBINE[rop]
+        self.stmt(v.level, f"{acc}[{v.name}] = ({m.name} == 0) ? {val[0]} : {comb}<{ct}>({acc}[{v.name}], {val[0]});")
+        self.close_coop(mm, vv)
+        sh = self._sh(T)
+        if rop is ReduceOp.sum and T.is_float:
+            tree = self.emit(1, ct, f"gr::row_sum<{ct}, {self.vec}, {self.P}, {self.tpr}>({acc}, {sh}, ri)")
+            if not identity:
+                return tree
+            return self.emit(1, ct, f"gr::add<{ct}>({c_literal(0, T)}, {tree})")
+        loc = self.fresh("lo")
+        self.stmt(1, f"{ct} {loc} = {acc}[0];")
+        for i in range(1, self.vec):
+            self.stmt(1, f"{loc} = {comb}<{ct}>({loc}, {acc}[{i}]);")
+        return self.emit(1, ct, f"gr::row_tree<{_OPS[rop]}, {ct}, {self.tpr}>({loc}, {sh}, ri)")
+
+    def _sh(self, T: DType) -> str:
+        self.n_sh += 1
+        nw = max(self.tpr // 32, 1)
+        name = f"sh{self.n_sh}"
+        self.stmt(1, f"__shared__ {T.ctype} {name}[{self.rpc * nw}];")
+        return name
+
+    def argreduce(self, r: Node, coords):
+        which, axis, keepdims = r.op.attrs
+        x = r.preds[0]
+        if axis is None or not self._row_complete(r, (axis,)):
+            return super().argreduce(r, coords)
+        kept = [c for i, c in enumerate(coords) if i != axis] if keepdims else list(coords)
+        if any(c.level > 1 for c in kept):
+            raise NotFusable(r, "row arg-reduction consumed per column")
+        T = x.dtype.ctype
+        best = self.fresh("bv")
+        bi = self.fresh("bi")
+        self.stmt(1, f"{T} {best} = 0; long long {bi} = -1;")
+        mm, vv = self.open_coop(1)
+        m, v = mm[0], vv[0]
+        col = self.coop_col(m, v)
+        val = self.value(x, list(kept) + [col])
+        pred = "gr::arg_better_max" if which == "max" else "gr::arg_better_min"
+        # within a thread the columns visit in increasing order per v lane, so
+        # combine with the index-aware predicate
+        self.stmt(v.level, f"{{ const long long ci = {col.c()}; if ({bi} < 0 || gr::arg_take_b<{'true' if which == 'max' else 'false'}, {T}>({best}, {bi}, {val[0]}, ci)) {{ {best} = {val[0]}; {bi} = ci; }} }}")
+        self.close_coop(mm, vv)
+        nw = max(self.tpr // 32, 1)
+        self.n_sh += 1
+        shv, shi = f"shv{self.n_sh}", f"shi{self.n_sh}"
+        self.stmt(1, f"__shared__ {T} {shv}[{self.rpc * nw}]; __shared__ long long {shi}[{self.rpc * nw}];")
+        mx = "true" if which == "max" else "false"
+        return self.emit(1, "long long", f"gr::row_arg<{mx}, {T}, {self.tpr}>({best}, {bi}, {shv}, {shi}, ri)"), 1
+
+
+def _qualifies(region: Region):
+    try:
+        Ts, totals, virtual = thread_space(region)
+    except NotFusable:
+        return None
+    if virtual is not None or not Ts:
+        return None
+    tot_ids = {t.id for t in totals}
+    C = None
+    for n in region.nodes:
+        if n.kind in (OpKind.REDUCE, OpKind.ARGREDUCE) and n.id not in tot_ids:
+            x = n.preds[0]
+            if len(x.shape) != len(Ts) + 1 or tuple(x.shape[:len(Ts)]) != Ts:
+                return None
+            axes = n.op.attrs[1] if n.kind is OpKind.REDUCE else (n.op.attrs[1],)
+            if tuple(axes) != (len(Ts),):
+                return None
+            if C is None:
+                C = x.shape[-1]
+            elif C != x.shape[-1]:
+                return None
+    if C is None or C < 256 or not _regular(C):
+        return None
+    for r in region.roots:
+        if r.id in tot_ids:
+            x = r.preds[0]
+            if tuple(x.shape) not in (Ts, Ts + (C,)) and element_count(x.shape[len(Ts):]) != 1:
+                return None
+            continue
+        if tuple(r.shape) not in (Ts, Ts + (C,)) and not (tuple(r.shape[:len(Ts)]) == Ts and element_count(r.shape[len(Ts):]) == 1):
+            return None
+    sizes = [n.dtype.itemsize for n in region.nodes + region.leaves]
+    vec = 4 if max(sizes) <= 4 else 2
+    tpr = (C // 128) * (8 // vec)
+    if tpr > MAX_TPR:
+        return None
+    return Ts, totals, C, vec, tpr
+
+
+def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
+    q = _qualifies(region)
+    if q is None:
+        return None
+    Ts, totals, C, vec, tpr = q
+    tot_ids = {t.id for t in totals}
+    block = max(256, tpr)
+    rpc = block // tpr
+    R = element_count(Ts)
+    em = CoopEmitter(region, vec, tpr, rpc, Ts, C)
+    rvar = Var("r", 1)
+    if len(Ts) == 1:
+        row_coords = [Aff.of(rvar)]
+    else:
+        row_coords = []
+        rest = "r"
+        for d in range(len(Ts) - 1, -1, -1):
+            if d == 0:
+                row_coords.append(Aff.of(Var(rest, 1)))
+            else:
+                c = em.emit(1, "long long", f"{rest} % {Ts[d]}")
+                row_coords.append(Aff.of(Var(c, 1)))
+                rest = em.emit(1, "long long", f"{rest} / {Ts[d]}")
+        row_coords.reverse()
+
+    for ri, r in enumerate(region.roots):
+        if r.id in tot_ids:
+            continue
+        T = r.dtype.ctype
+        if tuple(r.shape) == Ts + (C,):
+            o = em.fresh("O")
+            mm, vv = None, None
+            m, sm, savm = em.open(1, "for", trip=16, unroll=True)
+            sm.coop = True
+            em.stmt(m.level, f"{T} {o}[{vec}];")
+            v, sv, savv = em.open(m.level, "for", trip=vec, unroll=True)
+            val = em.value(r, row_coords + [em.coop_col(m, v)])
+            em.stmt(v.level, f"{o}[{v.name}] = {val[0]};")
+            em.close(sv, savv)
+            em.stmt(m.level, f"if (valid) gr::stv<{T}, {vec}>(p.out{ri} + r * {C}LL + cb + 8 * {m.name}, {o});")
+            em.close(sm, savm)
+        else:
+            val = em.value(r, row_coords + [Aff.of(0)] * (len(r.shape) - len(Ts)))
+            em.stmt(1, f"if (valid && tr == 0) gr::st<{T}>(p.out{ri} + r, {val[0]});")
+
+    scratch_off = 0
+    tot_meta = []
+    for ri, r in enumerate(region.roots):
+        if r.id not in tot_ids:
+            continue
+        x = r.preds[0]
+        if r.kind is OpKind.ARGREDUCE:
+            raise NotFusable(r, "argmax over all axes with cooperative rows")
+        rop = r.op.attrs[0]
+        T = r.dtype
+        ct = T.ctype
+        if tuple(x.shape) == Ts + (C,):
+            # the partial is the bare pairwise row sum: NumPy's 0.0 start is
+            # applied once, to the grand total
+            part = em.coop_reduce(x, rop, T, row_coords, identity=False)
+        else:
+            part = em.cast(em.value(x, row_coords + [Aff.of(0)] * (len(x.shape) - len(Ts))), x.dtype, T)[0]
+        off = scratch_off
+        em.stmt(1, f"if (valid && tr == 0) reinterpret_cast<{ct}*>(static_cast<char*>(p.scratch) + {off})[r] = {part};")
+        tot_meta.append((ri, rop, T, off))
+        scratch_off += ((R * T.itemsize + 255) // 256) * 256
+
+    P = 8 // vec
+    lines = ["static __device__ __forceinline__ void rows(const Params& p, const long long rb) {",
+             f"  const int tr = threadIdx.x % {tpr};",
+             f"  const int ri = threadIdx.x / {tpr};",
+             "  const bool valid = rb + ri < NROWS;",
+             "  const long long r = valid ? rb + ri : NROWS - 1;",
+             f"  const long long cb = (long long)(tr / {P}) * 128 + (tr % {P}) * {vec};"]
+    lines += ["  " + c for c in em.consts]
+    lines += render(em.row, 1)
+    lines.append("}")
+    params = _params_struct(region).replace("    void* __restrict__ scratch;",
+                                             "    void* __restrict__ scratch;\n    unsigned int* ticket;")
+    src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params,
+           f"  static constexpr long long NROWS = {R}LL;"]
+    src.append("  " + "\n  ".join(lines))
+    src.append("};")
+    kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
+            f"  for (long long rb = (long long)blockIdx.x * {rpc}; rb < K::NROWS; rb += (long long)gridDim.x * {rpc})",
+            "    K::rows(p, rb);"]
+    if tot_meta:
+        kern.append("  if (gr::last_block(p.ticket)) {")
+        for ri, rop, T, off in tot_meta:
+            ct = T.ctype
+            ident = c_literal(_IDENT[rop](T), T)
+            kern.append(f"    const {ct} v{ri} = gr::block_tree<{_OPS[rop]}, {ct}>("
+                        f"reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {off}), K::NROWS, {ident});")
+            fin = f"gr::add<{ct}>({c_literal(0, T)}, v{ri})" if rop is ReduceOp.sum else f"v{ri}"
+            kern.append(f"    if (threadIdx.x == 0) p.out{ri}[0] = {fin};")
+        kern.append("  }")
+    kern.append("}")
+    src += kern
+    groups = -(-R // rpc)
+    return KernelSource("coop", "\n".join(src) + "\n", kname,
+                        leaf_slots=list(range(len(region.leaves))),
+                        root_slots=list(range(len(region.roots))),
+                        block=block, groups=groups * block, vec=vec, unroll=1, scratch_bytes=scratch_off,
+                        meta={"rows": R, "row_shape": Ts, "cols": C, "tpr": tpr, "rows_per_cta": rpc,
+                              "totals": len(tot_meta), "ticket": bool(tot_meta)})

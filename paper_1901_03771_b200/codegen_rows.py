@@ -65,9 +65,10 @@ SMALL_RECOMPUTE = 64   # a reduction re-evaluated per column may reduce at most 
 
 
 class Scope:
-    __slots__ = ("level", "kind", "header", "lines", "ret", "unroll", "var", "trip")
+    __slots__ = ("level", "kind", "header", "lines", "ret", "unroll", "var", "trip", "coop")
 
     def __init__(self, level, kind="block", header="", unroll=False, var=None, trip=None):
+        self.coop = False
         self.level = level
         self.kind = kind
         self.header = header
@@ -139,7 +140,8 @@ class LoopEmitter(ValueEmitter):
         name = self.fresh("i")
         var = Var(name, lvl)
         if kind == "for":
-            header = f"for (long long {name} = 0; {name} < {trip}LL; ++{name})"
+            tstr = f"{trip}LL" if isinstance(trip, int) else trip
+            header = f"for (long long {name} = 0; {name} < {tstr}; ++{name})"
         else:
             header = f"auto f{name} = [&](long long {name}) -> {ret_type}"
         s = Scope(lvl, kind, header, unroll=unroll, var=var, trip=trip)
@@ -387,28 +389,41 @@ def thread_space(region: Region):
             raise NotFusable(bad, "reduction over the leading axis shares a region with other outputs")
         virtual = None
     else:
-        # maps + totals: rows are chunks of the flattened space
+        # maps + totals: rows are the subtrees of NumPy's pairwise tree over the
+        # flattened space at depth D, so per-row partials combined by a
+        # perfect binary tree reproduce np.sum exactly for any length
         shapes = [t.preds[0].shape for t in totals] + [r.shape for r in region.roots if r.id not in tot_ids]
         S = max(shapes, key=len)
         N = element_count(S)
-        C = _chunk(N)
-        Ts = (N // C,)
-        virtual = (tuple(S), C)
+        D, sizes = tree_chunks(N)
+        Ts = (1 << D,)
+        virtual = (tuple(S), D, sizes)
     return tuple(Ts), totals, virtual
 
 
-def _chunk(N: int) -> int:
-    if N <= 2048:
-        return max(N, 1)
-    c = 2048
-    while c >= 128:
-        if N % c == 0:
-            return c
-        c //= 2
-    for c in range(2048, 0, -1):
-        if N % c == 0:
-            return c
-    return 1
+def _split(n: int) -> int:
+    h = n // 2
+    return h - h % 8
+
+
+def tree_chunks(N: int, cmax: int = 2048):
+    """(D, sorted distinct chunk sizes) for the depth-D nodes of NumPy's
+    pairwise recursion over N elements (oracle/pairwise.py), D the smallest
+    depth whose nodes all hold <= cmax elements.  All nodes above depth D have
+    > 128 elements, so every one of them splits and there are exactly 2^D."""
+    D = 0
+    level = {N}
+    while max(level) > cmax:
+        nxt = set()
+        for n in level:
+            if n <= 256:
+                return D, sorted(level)
+            a = _split(n)
+            nxt.add(a)
+            nxt.add(n - a)
+        level = nxt
+        D += 1
+    return D, sorted(level)
 
 
 # ---------------------------------------------------------------------------
@@ -437,7 +452,15 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
                     row_coords.append(Aff.of(Var(c, 1)))
                     rest = em.emit(1, "long long", f"{rest} / {Ts[d]}")
             row_coords.reverse()
-    body_stores: List[Tuple[int, str]] = []
+    else:
+        # descend NumPy's pairwise tree along the bits of r: (vo, vn) = this
+        # row's chunk of the flattened space
+        S, D, sizes = virtual
+        N = element_count(S)
+        em.stmt(1, f"long long vo = 0, vn = {N}LL;")
+        if D:
+            em.stmt(1, f"for (int d = {D - 1}; d >= 0; --d) {{ const long long h = vn / 2, n2 = h - h % 8; "
+                       f"if ((r >> d) & 1) {{ vo += n2; vn -= n2; }} else {{ vn = n2; }} }}")
 
     def full_root_coords(shape):
         """Open loops over the columns of a root of ``shape`` (shape[:len(Ts)] == Ts)."""
@@ -445,36 +468,25 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
         vars_, opened = em.loop_coords(1, list(cols))
         return row_coords + [Aff.of(v) for v in vars_], opened, cols
 
-    def virtual_coords(S, C):
-        iv, s, saved = em.open(1, "for", trip=C, unroll=(C <= 16))
-        lin = Aff.of(rvar).scale(C) + Aff.of(iv)
-        coords = []
-        if len(S) == 1:
-            coords = [lin]
+    def virtual_coords(S, kind="for", ret_type=None):
+        if kind == "for":
+            iv, s, saved = em.open(1, "for", trip="vn")
         else:
-            rest = lin
-            for d in range(len(S) - 1, -1, -1):
-                if d == 0:
-                    coords.append(rest)
-                else:
-                    coords.append(Aff.of(em.derived_var(iv.level, f"{rest.c()} % {S[d]}")))
-                    rest = Aff.of(em.derived_var(iv.level, f"{rest.c()} / {S[d]}"))
-            coords.reverse()
-        return coords, [(s, saved)], iv
+            iv, s, saved = em.open(1, "lambda", ret_type=ret_type)
+        return _flat_coords(em, S, Aff.of(Var("vo", 1)) + Aff.of(iv), iv), (s, saved), iv
 
-    partial_info = []
     for ri, r in enumerate(region.roots):
         if r.id in tot_ids:
             continue
         T = r.dtype.ctype
         if virtual is not None:
-            S, C = virtual
+            S = virtual[0]
             if tuple(r.shape) != S:
                 raise NotFusable(r, "map root shape differs from the reduced space")
-            coords, opened, iv = virtual_coords(S, C)
+            coords, (s, saved), iv = virtual_coords(S)
             v = em.value(r, coords)
-            em.stmt(iv.level, f"gr::st<{T}>(p.out{ri} + r * {C}LL + {iv.name}, {v[0]});")
-            em.close_all(opened)
+            em.stmt(iv.level, f"gr::st<{T}>(p.out{ri} + vo + {iv.name}, {v[0]});")
+            em.close(s, saved)
             continue
         if tuple(r.shape[:len(Ts)]) != Ts:
             raise NotFusable(r, f"root shape {r.shape} does not start with the row shape {Ts}")
@@ -503,11 +515,11 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
             which = r.op.attrs[0]
             xt = x.dtype
             if virtual is not None:
-                S, C = virtual
+                S = virtual[0]
                 if tuple(x.shape) != S:
                     raise NotFusable(r, "total operand shape differs")
-                best, bi = _arg_partial(em, x, which, None, S, C)
-                glob = f"r * {C}LL + {bi}"
+                best, bi = _arg_partial(em, x, which, None, S, "vn")
+                glob = f"vo + {bi}"
             else:
                 if tuple(x.shape[:len(Ts)]) != Ts:
                     raise NotFusable(r, f"total operand {x.shape} does not start with rows {Ts}")
@@ -527,11 +539,11 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
         T = r.dtype
         ct = T.ctype
         if virtual is not None:
-            S, C = virtual
+            S, D, sizes = virtual
             if tuple(x.shape) != S:
                 raise NotFusable(r, "total operand shape differs")
-            # partial = NumPy pairwise over this row's chunk of the flat space
-            part = _chunk_partial(em, x, rop, T, S, C)
+            # partial = NumPy pairwise over this row's subtree of the flat space
+            part = _chunk_partial(em, x, rop, T, S, sizes)
         else:
             if tuple(x.shape[:len(Ts)]) != Ts:
                 raise NotFusable(r, f"total operand {x.shape} does not start with rows {Ts}")
@@ -608,7 +620,24 @@ def _row_partial(em: LoopEmitter, x: Node, rop, T: DType, row_coords, cols):
     return acc
 
 
-def _chunk_partial(em: LoopEmitter, x: Node, rop, T: DType, S, C):
+def _flat_coords(em: LoopEmitter, S, lin: Aff, iv: Var):
+    """Coordinates in S of the flat (row-major) index ``lin``."""
+    if len(S) == 1:
+        return [lin]
+    coords = []
+    rest = lin
+    for d in range(len(S) - 1, -1, -1):
+        if d == 0:
+            coords.append(rest)
+        else:
+            coords.append(Aff.of(em.derived_var(iv.level, f"{rest.c()} % {S[d]}")))
+            rest = Aff.of(em.derived_var(iv.level, f"{rest.c()} / {S[d]}"))
+    coords.reverse()
+    return coords
+
+
+def _chunk_partial(em: LoopEmitter, x: Node, rop, T: DType, S, sizes):
+    """Reduction of x over this row's subtree (vo, vn) of the flattened space."""
     ct = T.ctype
     ident = c_literal(_IDENT[rop](T), T)
     pw = rop is ReduceOp.sum and T.is_float
@@ -616,24 +645,15 @@ def _chunk_partial(em: LoopEmitter, x: Node, rop, T: DType, S, C):
         iv, s, saved = em.open(1, "lambda", ret_type=ct)
     else:
         acc = em.var_decl(1, ct, ident)
-        iv, s, saved = em.open(1, "for", trip=C, unroll=(C <= 16))
-    lin = Aff.of(Var("r", 1)).scale(C) + Aff.of(iv)
-    coords = []
-    if len(S) == 1:
-        coords = [lin]
-    else:
-        rest = lin
-        for d in range(len(S) - 1, -1, -1):
-            if d == 0:
-                coords.append(rest)
-            else:
-                coords.append(Aff.of(em.derived_var(iv.level, f"{rest.c()} % {S[d]}")))
-                rest = Aff.of(em.derived_var(iv.level, f"{rest.c()} / {S[d]}"))
-        coords.reverse()
+        iv, s, saved = em.open(1, "for", trip="vn")
+    coords = _flat_coords(em, S, Aff.of(Var("vo", 1)) + Aff.of(iv), iv)
     v = em.cast(em.value(x, coords), x.dtype, T)
     if pw:
         em.close(s, saved, ret=v[0])
-        return em.emit(1, ct, f"gr::pairwise<{ct}, {C}LL>(f{iv.name}, 0)")
+        part = em.var_decl(1, ct, ident)
+        cases = " ".join(f"case {n}LL: {part} = gr::pairwise<{ct}, {n}LL>(f{iv.name}, 0); break;" for n in sizes)
+        em.stmt(1, f"switch (vn) {{ {cases} default: break; }}")
+        return part
     em.stmt(iv.level, f"{acc} = {_COMBINE[rop]}<{ct}>({acc}, {v[0]});")
     em.close(s, saved)
     return acc
@@ -641,26 +661,13 @@ def _chunk_partial(em: LoopEmitter, x: Node, rop, T: DType, S, C):
 
 def _arg_partial(em: LoopEmitter, x: Node, which, row_coords, S, C, cols=None):
     """First-index arg-reduction of x over this row's columns (row mode) or its
-    chunk of the flattened space (virtual mode); returns (best, local index)."""
+    chunk (vo, vn) of the flattened space (virtual mode); returns (best, local index)."""
     T = x.dtype.ctype
     best = em.var_decl(1, T, "0")
     bi = em.var_decl(1, "long long", "0")
-    iv, s, saved = em.open(1, "for", trip=C, unroll=(C <= 16))
+    iv, s, saved = em.open(1, "for", trip=C, unroll=(isinstance(C, int) and C <= 16))
     if row_coords is None:
-        lin = Aff.of(Var("r", 1)).scale(C) + Aff.of(iv)
-        shape = S
-        coords = []
-        if len(shape) == 1:
-            coords = [lin]
-        else:
-            rest = lin
-            for d in range(len(shape) - 1, -1, -1):
-                if d == 0:
-                    coords.append(rest)
-                else:
-                    coords.append(Aff.of(em.derived_var(iv.level, f"{rest.c()} % {shape[d]}")))
-                    rest = Aff.of(em.derived_var(iv.level, f"{rest.c()} / {shape[d]}"))
-            coords.reverse()
+        coords = _flat_coords(em, S, Aff.of(Var("vo", 1)) + Aff.of(iv), iv)
     else:
         nrow = len(row_coords)
         inner = em._delin(iv, list(range(nrow, nrow + len(cols))), list(cols))

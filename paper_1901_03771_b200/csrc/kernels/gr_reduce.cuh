@@ -216,6 +216,114 @@ template <class Op, class T> __device__ T block_tree(const T* p, long long n, T 
   return r;
 }
 
+// ---- cooperative rows (codegen_coop.py) --------------------------------------
+// A row of C = 128 * 2^k elements is held by TPR = (C/128) * P threads; thread
+// (leaf l, part h) owns accumulators j = h*VEC .. h*VEC+VEC-1 of NumPy's
+// 8-accumulator leaf loop (element 128*l + 8*m + j, m = 0..15), so:
+//   leaf sum  = ((r0+r1)+(r2+r3)) + ((r4+r5)+(r6+r7))   (local + shfl over P)
+//   row sum   = perfect binary tree over leaves          (shfl, then smem)
+// which is exactly numpy.add.reduce along a contiguous row of that length.
+
+template <class T, int VEC> __device__ __forceinline__ T leaf_local(const T (&a)[VEC]) {
+  if constexpr (VEC == 1) {
+    return a[0];
+  } else if constexpr (VEC == 2) {
+    return add<T>(a[0], a[1]);
+  } else if constexpr (VEC == 4) {
+    return add<T>(add<T>(a[0], a[1]), add<T>(a[2], a[3]));
+  } else {
+    return add<T>(add<T>(add<T>(a[0], a[1]), add<T>(a[2], a[3])), add<T>(add<T>(a[4], a[5]), add<T>(a[6], a[7])));
+  }
+}
+
+// Combine a per-thread value over the TPR threads of a row (lanes grouped in
+// aligned runs of TPR, tr = thread index within the row) in perfect-tree
+// order; for TPR > 32 the warp results meet in shared memory `sh`
+// (>= rows_per_cta * TPR/32 elements).  Every thread of the row gets the result.
+template <class Op, class T, int TPR> __device__ __forceinline__ T row_tree(T v, T* sh, int ri) {
+  constexpr int W = TPR < 32 ? TPR : 32;
+#pragma unroll
+  for (int m = 1; m < W; m <<= 1) v = Op::template c<T>(v, shfl_xor<T>(v, m));
+  if constexpr (TPR > 32) {
+    constexpr int NW = TPR / 32;
+    const int tr = threadIdx.x % TPR;
+    if ((threadIdx.x & 31) == 0) sh[ri * NW + tr / 32] = v;
+    __syncthreads();
+    T buf[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) buf[w] = sh[ri * NW + w];
+#pragma unroll
+    for (int s = 1; s < NW; s <<= 1)
+#pragma unroll
+      for (int w = 0; w + s < NW; w += 2 * s) buf[w] = Op::template c<T>(buf[w], buf[w + s]);
+    __syncthreads();
+    v = buf[0];
+  }
+  return v;
+}
+
+// Leaf-level combine over the P parts then the row tree (float sums).
+template <class T, int VEC, int P, int TPR> __device__ __forceinline__ T row_sum(const T (&acc)[VEC], T* sh, int ri) {
+  T s = leaf_local<T, VEC>(acc);
+#pragma unroll
+  for (int m = 1; m < P; m <<= 1) s = add<T>(s, shfl_xor<T>(s, m));
+  // leaves: lanes P apart
+  constexpr int W = TPR < 32 ? TPR : 32;
+#pragma unroll
+  for (int m = P; m < W; m <<= 1) s = add<T>(s, shfl_xor<T>(s, m));
+  if constexpr (TPR > 32) {
+    constexpr int NW = TPR / 32;
+    const int tr = threadIdx.x % TPR;
+    if ((threadIdx.x & 31) == 0) sh[ri * NW + tr / 32] = s;
+    __syncthreads();
+    T buf[NW];
+#pragma unroll
+    for (int w = 0; w < NW; ++w) buf[w] = sh[ri * NW + w];
+#pragma unroll
+    for (int st = 1; st < NW; st <<= 1)
+#pragma unroll
+      for (int w = 0; w + st < NW; w += 2 * st) buf[w] = add<T>(buf[w], buf[w + st]);
+    __syncthreads();
+    s = buf[0];
+  }
+  return s;
+}
+
+// First-index arg combine over the row's threads.
+template <bool MAX, class T, int TPR>
+__device__ __forceinline__ long long row_arg(T best, long long bi, T* shv, long long* shi, int ri) {
+  constexpr int W = TPR < 32 ? TPR : 32;
+#pragma unroll
+  for (int m = 1; m < W; m <<= 1) {
+    T ov = shfl_xor<T>(best, m);
+    long long oi = __shfl_xor_sync(0xffffffffu, bi, m);
+    if (arg_take_b<MAX, T>(best, bi, ov, oi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  if constexpr (TPR > 32) {
+    constexpr int NW = TPR / 32;
+    const int tr = threadIdx.x % TPR;
+    if ((threadIdx.x & 31) == 0) {
+      shv[ri * NW + tr / 32] = best;
+      shi[ri * NW + tr / 32] = bi;
+    }
+    __syncthreads();
+    best = shv[ri * NW];
+    bi = shi[ri * NW];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      if (arg_take_b<MAX, T>(best, bi, shv[ri * NW + w], shi[ri * NW + w])) {
+        best = shv[ri * NW + w];
+        bi = shi[ri * NW + w];
+      }
+    }
+    __syncthreads();
+  }
+  return bi;
+}
+
 // Grid completion ticket: returns true in exactly one (the last) block, after
 // every block's partials are visible.  The ticket self-resets for the next
 // launch of the same kernel (stream order serialises launches).
