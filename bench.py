@@ -149,42 +149,81 @@ def peaks():
 # ---------------------------------------------------------------------------
 # workloads
 # ---------------------------------------------------------------------------
-def _bs_setup(n, dtype, seed):
+def _wl():
     from paper_1901_03771_b200 import workloads as wl
-    return wl.blackscholes_inputs(n=n, seed=seed, dtype=dtype)
+    return wl
 
 
+MLP_H = 1024   # hidden width (unpinned by BASELINE.json; SURVEY.md §8(d) C4 recommends 1024)
+KM_D = 4       # k-means dimensionality (SURVEY.md §8(d) C5 recommends 4)
+
+# n = leading-axis extent at full size (the sharded / sampled axis).
+# elements(n): iteration-space points per step; bytes(n): algorithmic HBM bytes
+# of the dominant fused kernel per launch (inputs read once, outputs written once).
 WORKLOADS = {
-    "blackscholes-f32": dict(n=1 << 28, dtype=np.float32, desc="Black-Scholes call+put, 2^28 options, fp32",
-                              bytes_per_elem=5 * 4, label="f32"),
-    "blackscholes-f64": dict(n=1 << 28, dtype=np.float64, desc="Black-Scholes call+put, 2^28 options, fp64",
-                              bytes_per_elem=5 * 8, label="f64"),
-    "listing1": dict(n=1 << 24, dtype=np.float64, desc="paper Listing 1 chain (4 mul + 2 add), 2^24 fp64",
-                     bytes_per_elem=4 * 8, label="f64"),
+    "blackscholes-f32": dict(
+        n=1 << 28, label="f32", desc="Black-Scholes call+put, 2^28 options, fp32 (BASELINE configs[1])",
+        inputs=lambda n, s: _wl().blackscholes_inputs(n=n, seed=s, dtype=np.float32),
+        program=lambda xp, a: _wl().blackscholes(xp, *a),
+        elements=lambda n: n, bytes=lambda n: 5 * 4 * n, bound="hbm"),
+    "blackscholes-f64": dict(
+        n=1 << 28, label="f64", desc="Black-Scholes call+put, 2^28 options, fp64 (BASELINE configs[1])",
+        inputs=lambda n, s: _wl().blackscholes_inputs(n=n, seed=s, dtype=np.float64),
+        program=lambda xp, a: _wl().blackscholes(xp, *a),
+        elements=lambda n: n, bytes=lambda n: 5 * 8 * n, bound="hbm (fp64 pipe limits)"),
+    "listing1": dict(
+        n=1 << 24, label="f64", desc="paper Listing 1 chain (4 mul + 2 add), 2^24 fp64 (BASELINE configs[0])",
+        inputs=lambda n, s: _wl().listing1_inputs(n=n, seed=s),
+        program=lambda xp, a: (_wl().listing1(xp, *a),),
+        elements=lambda n: n, bytes=lambda n: 4 * 8 * n, bound="hbm"),
+    "rownorm": dict(
+        n=65536, label="f32", desc="row-normalise 65536x4096 fp32 then sum; total forced (BASELINE configs[2])",
+        inputs=lambda n, s: _wl().rownorm_inputs(rows=n, cols=4096, seed=s),
+        program=lambda xp, a: (_wl().rownorm(xp, *a)[1],),
+        elements=lambda n: n * 4096, bytes=lambda n: n * 4096 * 4 + 4, bound="hbm"),
+    "rownorm-y": dict(
+        n=65536, label="f32", desc="row-normalise 65536x4096 fp32, y and total forced",
+        inputs=lambda n, s: _wl().rownorm_inputs(rows=n, cols=4096, seed=s),
+        program=lambda xp, a: _wl().rownorm(xp, *a),
+        elements=lambda n: n * 4096, bytes=lambda n: 2 * n * 4096 * 4 + 4, bound="hbm"),
+    "mlp": dict(
+        n=65536, label="f32", desc=f"MNIST-style MLP inference batch 65536, 784-{MLP_H}-10, cuBLAS GEMMs + fused epilogues (BASELINE configs[3])",
+        inputs=lambda n, s: _mlp_inputs(n, s),
+        program=lambda xp, a: _wl().mlp(xp, *a),
+        elements=lambda n: n * (MLP_H + 10), bytes=lambda n: 2 * n * MLP_H * 4 + MLP_H * 4,
+        bound="hbm (R1 bias+ReLU region); GEMMs are cuBLAS"),
+    "kmeans": dict(
+        n=1 << 26, label="f32", desc=f"k-means assignment, 2^26 points x 64 centroids, D={KM_D} (BASELINE configs[4])",
+        inputs=lambda n, s: _km_inputs(n, s),
+        program=lambda xp, a: (_wl().kmeans_assign(xp, *a),),
+        elements=lambda n: n, bytes=lambda n: n * (KM_D * 4 + 8) + 64 * KM_D * 4, bound="fp32 issue (no FMA, NumPy order)"),
 }
+
+_CACHE_IN = {}
+
+
+def _mlp_inputs(n, s):
+    X, W1, b1, W2, b2 = _wl().mlp_inputs(batch=n, hidden=MLP_H, seed=s)
+    return [X, W1, b1, W2, b2]
+
+
+def _km_inputs(n, s):
+    P, C = _wl().kmeans_inputs(n=n, k=64, d=KM_D, seed=s)
+    return [P, C]
 
 
 def make_program(name):
-    from paper_1901_03771_b200 import workloads as wl
-    if name.startswith("blackscholes"):
-        def prog(xp, arrs):
-            return wl.blackscholes(xp, *arrs)
-        return prog
-    if name == "listing1":
-        def prog(xp, arrs):
-            return (wl.listing1(xp, *arrs),)
-        return prog
-    raise KeyError(name)
+    return WORKLOADS[name]["program"]
+
+
+def cpu_sample_n(name):
+    """Leading extent of the bounded CPU sample (~5-20 s of single-thread NumPy)."""
+    return {"blackscholes-f32": 1 << 24, "blackscholes-f64": 1 << 24, "listing1": 1 << 24,
+            "rownorm": 16384, "rownorm-y": 16384, "mlp": 16384, "kmeans": 1 << 20}[name]
 
 
 def make_inputs(name, n, seed):
-    from paper_1901_03771_b200 import workloads as wl
-    w = WORKLOADS[name]
-    if name.startswith("blackscholes"):
-        return wl.blackscholes_inputs(n=n, seed=seed, dtype=w["dtype"])
-    if name == "listing1":
-        return wl.listing1_inputs(n=n, seed=seed, dtype=w["dtype"])
-    raise KeyError(name)
+    return list(WORKLOADS[name]["inputs"](n, seed))
 
 
 # ---------------------------------------------------------------------------
@@ -201,8 +240,10 @@ def cpu_time(name, sample, threads, reps):
     edges = np.linspace(0, sample, blocks + 1).astype(np.int64)
 
     def work(i):
+        # blocked partition of the leading axis;
+        # arrays without that axis (weights, centroids) are shared
         lo, hi = edges[i], edges[i + 1]
-        return prog(np, [x[lo:hi] for x in inputs])
+        return prog(np, [x[lo:hi] if x.shape and x.shape[0] == sample else x for x in inputs])
 
     best = float("inf")
     with ThreadPoolExecutor(max_workers=max(threads, 1)) as ex:
@@ -222,12 +263,12 @@ def run_reference(args, dist):
         return
     w = WORKLOADS[args.workload]
     cores = len(os.sched_getaffinity(0))
-    sample = args.cpu_sample or min(w["n"], 1 << 24)
+    sample = args.cpu_sample or cpu_sample_n(args.workload)
     for _ in range(args.warmup):
         cpu_time(args.workload, sample, cores, 1)
     times = [cpu_time(args.workload, sample, cores, 1) for _ in range(args.steps)]
     t = sum(times) / len(times)
-    value = sample / t
+    value = w["elements"](sample) / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "elements/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
@@ -310,10 +351,17 @@ def run_grumpy(args, dist):
     kern_ms = [ms for _f, _l, ms in prof]
     kmean = statistics.mean(kern_ms)
     del keep
-    elements = n * dist.world
+    # dominant fused kernel = largest share of device time in the timed region
+    by_label = {}
+    for fam, lab, ms in prof:
+        by_label.setdefault((fam, lab), []).append(ms)
+    dom = max(by_label.items(), key=lambda kv: sum(kv[1]))
+    kmean = statistics.mean(dom[1])
+    share = sum(dom[1]) / max(total_ms, 1e-9)
+    elements = w["elements"](n) * dist.world
     value = elements * args.steps / (total_ms / 1e3)
     peak, peak_src = peaks()
-    alg_bytes = n * w["bytes_per_elem"]
+    alg_bytes = w["bytes"](n)
     achieved = alg_bytes / (kmean / 1e3) / 1e9
 
     # e2e through the public API from pinned host memory
@@ -348,23 +396,26 @@ def run_grumpy(args, dist):
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": w["label"],
         "data": "synthetic (numpy default_rng, seed 42+rank)",
         "config": {"workload": w["desc"], "elements_per_gpu": n, "parallelism": f"shard{dist.world}",
-                   "l2": "inputs (%.1f GiB/GPU) larger than the 126 MB L2; no flush" % (alg_bytes / 2**30)},
+                   "l2": "inputs %.2f GiB/GPU vs 126 MB L2 (no flush; dominant kernel streams %.2f GiB)"
+                         % (sum(x.nbytes for x in host) / 2**30, alg_bytes / 2**30)},
         "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "steps": e2e_steps},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(args.workload),
-                     "peak_source": peak_src, "kernel_ms": kmean,
-                     "algorithmic_bytes_per_launch": alg_bytes},
+                     "peak_source": peak_src, "kernel_ms": kmean, "kernel": f"{dom[0][0]}:{dom[0][1]}",
+                     "kernel_share_of_step": share, "launches_per_step": len(prof) / args.steps,
+                     "algorithmic_bytes_per_launch": alg_bytes, "limiter": w["bound"]},
         "gpu_launches": launches,
         "clocks": clk,
         "cold_first_step_s": cold_s,
         "device": rt.name,
     }
     if dist.rank == 0 and not args.no_cpu_baseline:
-        sample = args.cpu_sample or min(n, 1 << 24)
+        sample = args.cpu_sample or cpu_sample_n(args.workload)
         t = cpu_time(args.workload, sample, 1, 2)
-        line["cpu_baseline"] = {"value": sample / t, "unit": "elements/s", "cores": 1, "kind": "port",
-                                "sample": f"{sample} elements, eager NumPy (oracle) single thread, best of 2"}
+        line["cpu_baseline"] = {"value": w["elements"](sample) / t, "unit": "elements/s", "cores": 1,
+                                "kind": "port",
+                                "sample": f"leading extent {sample} (of {w['n']}), eager NumPy (oracle) single thread, best of 2"}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
 
