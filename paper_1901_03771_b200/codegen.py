@@ -242,6 +242,19 @@ class ValueEmitter:
         self.leaf_index = {n.id: i for i, n in enumerate(region.leaves)}
         self.consts: List[str] = []
         self.const_memo: Dict[tuple, str] = {}
+        # hash-consing: structurally identical nodes (same op over the same
+        # operands) share one value — e.g. the two mean computations of
+        # (x - x.mean(1)) / x.std(1).  Evaluation is pure, so this is exact.
+        self.canon: Dict[int, int] = {}
+        seen: Dict[tuple, int] = {}
+        for n in sorted(region.nodes, key=lambda x: x.id):
+            if n.id in self.leaf_index:
+                continue
+            key = (n.op, n.shape, n.dtype, tuple(self.canon.get(p.id, p.id) for p in n.preds))
+            self.canon[n.id] = seen.setdefault(key, n.id)
+
+    def cid(self, n: Node) -> int:
+        return self.canon.get(n.id, n.id)
 
     def fresh(self, prefix="t"):
         self.counter += 1
@@ -270,7 +283,7 @@ class ValueEmitter:
         return self.emit(lvl, to.ctype, f"gr::cast<{to.ctype}, {frm.ctype}>({expr})"), lvl
 
     def value(self, n: Node, coords: Sequence[Aff]) -> Tuple[str, int]:
-        key = (n.id, tuple(c.key() for c in coords))
+        key = (self.cid(n), tuple(c.key() for c in coords))
         hit = self.memo.get(key)
         if hit is not None:
             return hit

@@ -107,7 +107,11 @@ class CoopEmitter(LoopEmitter):
         kept = [c for i, c in enumerate(coords) if i not in axes] if keepdims else list(coords)
         if any(c.level > 1 for c in kept):
             raise NotFusable(r, "row reduction consumed per column")
-        return self.coop_reduce(r.preds[0], rop, r.dtype, kept), 1
+        rk = self.reduction_key(r, kept)
+        hit = self.memo_get(rk)
+        if hit is not None:
+            return hit
+        return self.memo_put(rk, (self.coop_reduce(r.preds[0], rop, r.dtype, kept), 1))
 
     def coop_reduce(self, x: Node, rop, T: DType, row_coords, identity=True):
         """Reduce x over this row's C columns across the TPR threads; float sums
@@ -121,6 +125,12 @@ class CoopEmitter(LoopEmitter):
         comb = _COMBINE[rop]
         self.stmt(v.level, f"{acc}[{v.name}] = ({m.name} == 0) ? {val[0]} : {comb}<{ct}>({acc}[{v.name}], {val[0]});")
         self.close_coop(mm, vv)
+        return self.finish_coop(acc, rop, T, identity)
+
+    def finish_coop(self, acc: str, rop, T: DType, identity=True):
+        """Cross-thread combine of per-thread accumulators acc[VEC] for one row."""
+        ct = T.ctype
+        comb = _COMBINE[rop]
         sh = self._sh(T)
         if rop is ReduceOp.sum and T.is_float:
             tree = self.emit(1, ct, f"gr::row_sum<{ct}, {self.vec}, {self.P}, {self.tpr}>({acc}, {sh}, ri)")
@@ -233,22 +243,41 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
                 rest = em.emit(1, "long long", f"{rest} / {Ts[d]}")
         row_coords.reverse()
 
+    # totals whose operand is itself a stored root accumulate in the store loop
+    # (the value is computed once per element)
+    fused_tot = {}
+    for t in totals:
+        x = t.preds[0]
+        if (t.kind is OpKind.REDUCE and tuple(x.shape) == Ts + (C,)
+                and any(x is r for r in region.roots if r.id not in tot_ids)):
+            fused_tot.setdefault(x.id, []).append(t)
+    tot_partials = {}
     for ri, r in enumerate(region.roots):
         if r.id in tot_ids:
             continue
         T = r.dtype.ctype
         if tuple(r.shape) == Ts + (C,):
             o = em.fresh("O")
-            mm, vv = None, None
+            accs = []
+            for t in fused_tot.get(r.id, []):
+                a = em.fresh("acc")
+                em.stmt(1, f"{t.dtype.ctype} {a}[{vec}];")
+                accs.append((t, a))
             m, sm, savm = em.open(1, "for", trip=16, unroll=True)
             sm.coop = True
             em.stmt(m.level, f"{T} {o}[{vec}];")
             v, sv, savv = em.open(m.level, "for", trip=vec, unroll=True)
             val = em.value(r, row_coords + [em.coop_col(m, v)])
             em.stmt(v.level, f"{o}[{v.name}] = {val[0]};")
+            for t, a in accs:
+                tv = em.cast(val, r.dtype, t.dtype)
+                comb = _COMBINE[t.op.attrs[0]]
+                em.stmt(v.level, f"{a}[{v.name}] = ({m.name} == 0) ? {tv[0]} : {comb}<{t.dtype.ctype}>({a}[{v.name}], {tv[0]});")
             em.close(sv, savv)
             em.stmt(m.level, f"if (valid) gr::stv<{T}, {vec}>(p.out{ri} + r * {C}LL + cb + 8 * {m.name}, {o});")
             em.close(sm, savm)
+            for t, a in accs:
+                tot_partials[t.id] = em.finish_coop(a, t.op.attrs[0], t.dtype, identity=False)
         else:
             val = em.value(r, row_coords + [Aff.of(0)] * (len(r.shape) - len(Ts)))
             em.stmt(1, f"if (valid && tr == 0) gr::st<{T}>(p.out{ri} + r, {val[0]});")
@@ -264,7 +293,9 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
         rop = r.op.attrs[0]
         T = r.dtype
         ct = T.ctype
-        if tuple(x.shape) == Ts + (C,):
+        if r.id in tot_partials:
+            part = tot_partials[r.id]
+        elif tuple(x.shape) == Ts + (C,):
             # the partial is the bare pairwise row sum: NumPy's 0.0 start is
             # applied once, to the grand total
             part = em.coop_reduce(x, rop, T, row_coords, identity=False)

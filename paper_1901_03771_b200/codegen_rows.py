@@ -156,7 +156,7 @@ class LoopEmitter(ValueEmitter):
         self.stack.extend(saved)
 
     def value(self, n: Node, coords):
-        key = (n.id, tuple(c.key() for c in coords))
+        key = (self.cid(n), tuple(c.key() for c in coords))
         hit = self.memo.get(key)
         if hit is not None:
             expr, lvl, sc = hit
@@ -169,6 +169,24 @@ class LoopEmitter(ValueEmitter):
     def derived_var(self, level, expr) -> Var:
         name = self.emit(level, "long long", expr)
         return Var(name, level)
+
+    def memo_get(self, key):
+        hit = self.memo.get(key)
+        if hit is not None:
+            expr, lvl, sc = hit
+            if lvl == 0 or (lvl < len(self.stack) and self.stack[lvl] is sc):
+                return expr, lvl
+        return None
+
+    def memo_put(self, key, v):
+        self.memo[key] = (v[0], v[1], self.stack[v[1]] if 0 < v[1] < len(self.stack) else None)
+        return v
+
+    def reduction_key(self, r: Node, kept) -> tuple:
+        """keepdims-independent identity of a reduction value: the same fold of
+        the same operand at the same kept coordinates."""
+        a = r.op.attrs
+        return ("red", r.kind, self.cid(r.preds[0]), a[0], a[1], r.dtype, tuple(k.key() for k in kept))
 
     # -- loads ----------------------------------------------------------------------
     def load_leaf(self, leaf: Node, off: Aff):
@@ -234,6 +252,14 @@ class LoopEmitter(ValueEmitter):
     def reduce(self, r: Node, coords):
         rop, axes, keepdims, odt = r.op.attrs
         x, kept, L = self._operand_coords(r, coords, axes, keepdims)
+        rk = self.reduction_key(r, kept)
+        hit = self.memo_get(rk)
+        if hit is not None:
+            return hit
+        return self.memo_put(rk, self._reduce(r, x, kept, L))
+
+    def _reduce(self, r: Node, x: Node, kept, L):
+        rop, axes, keepdims, odt = r.op.attrs
         T = r.dtype
         ct = T.ctype
         So = x.shape
