@@ -216,6 +216,38 @@ template <class Op, class T> __device__ T block_tree(const T* p, long long n, T 
   return r;
 }
 
+// Perfect binary tree over N (power of two) register values in index order.
+template <class Op, class T, int N> __device__ __forceinline__ T lane_tree(const T (&a)[N]) {
+  if constexpr (N == 1) {
+    return a[0];
+  } else {
+    T b[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) b[i] = a[i];
+#pragma unroll
+    for (int s = 1; s < N; s <<= 1)
+#pragma unroll
+      for (int i = 0; i + s < N; i += 2 * s) b[i] = Op::template c<T>(b[i], b[i + s]);
+    return b[0];
+  }
+}
+
+// First-index (value, index) combine over aligned groups of `width` lanes.
+template <bool MAX, class T> __device__ __forceinline__ long long warp_arg(T best, long long bi, int width) {
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    if (m < width) {
+      T ov = shfl_xor<T>(best, m);
+      long long oi = __shfl_xor_sync(0xffffffffu, bi, m);
+      if (arg_take_b<MAX, T>(best, bi, ov, oi)) {
+        best = ov;
+        bi = oi;
+      }
+    }
+  }
+  return bi;
+}
+
 // ---- cooperative rows (codegen_coop.py) --------------------------------------
 // A row of C = 128 * 2^k elements is held by TPR = (C/128) * P threads; thread
 // (leaf l, part h) owns accumulators j = h*VEC .. h*VEC+VEC-1 of NumPy's

@@ -1,0 +1,97 @@
+// gr_tma.cuh — bulk asynchronous copies (TMA bulk engine) and mbarriers.
+//
+// The row-streaming family (codegen_wrow.py) moves each row of a region's
+// inputs from HBM into a shared-memory ring with `cp.async.bulk` (SASS
+// UBLKCP), completion signalled on an mbarrier (expect_tx / complete_tx), so
+// the next rows are in flight while the current one is reduced — no register
+// staging, no LSU traffic for the stream (PTX ISA: cp.async.bulk, mbarrier).
+#pragma once
+
+namespace gr {
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// order this thread's prior generic-proxy smem accesses before later
+// async-proxy (bulk copy) writes to the same smem
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, unsigned parity) {
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+
+// global -> shared bulk copy; bytes % 16 == 0, both addresses 16-byte aligned
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// 8 consecutive elements from shared memory (16-byte aligned) into registers
+template <class T> __device__ __forceinline__ void lds8(T (&d)[8], const T* s) {
+  static_assert(sizeof(T) == 4 || sizeof(T) == 8, "lds8");
+  if constexpr (sizeof(T) == 4) {
+    const uint4 a = reinterpret_cast<const uint4*>(s)[0];
+    const uint4 b = reinterpret_cast<const uint4*>(s)[1];
+    d[0] = __uint_as_float(a.x); d[1] = __uint_as_float(a.y); d[2] = __uint_as_float(a.z); d[3] = __uint_as_float(a.w);
+    d[4] = __uint_as_float(b.x); d[5] = __uint_as_float(b.y); d[6] = __uint_as_float(b.z); d[7] = __uint_as_float(b.w);
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 a = reinterpret_cast<const double2*>(s)[i];
+      d[2 * i] = a.x;
+      d[2 * i + 1] = a.y;
+    }
+  }
+}
+template <> __device__ __forceinline__ void lds8<int>(int (&d)[8], const int* s) {
+  const int4 a = reinterpret_cast<const int4*>(s)[0];
+  const int4 b = reinterpret_cast<const int4*>(s)[1];
+  d[0] = a.x; d[1] = a.y; d[2] = a.z; d[3] = a.w; d[4] = b.x; d[5] = b.y; d[6] = b.z; d[7] = b.w;
+}
+template <> __device__ __forceinline__ void lds8<long long>(long long (&d)[8], const long long* s) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) d[i] = s[i];
+}
+
+// 8 consecutive elements to global memory (32/64-byte aligned run)
+template <class T> __device__ __forceinline__ void st8(T* dst, const T (&v)[8]) {
+  constexpr int V = 16 / sizeof(T);
+#pragma unroll
+  for (int i = 0; i < 8; i += V) {
+    T tmp[V];
+#pragma unroll
+    for (int k = 0; k < V; ++k) tmp[k] = v[i + k];
+    stv<T, V>(dst + i, tmp);
+  }
+}
+
+}  // namespace gr

@@ -83,7 +83,7 @@ class Executor:
             return outs
         k = c.get("kernel")
         if k is None:
-            k = self.rt.kernel(ks.source, ks.name, ks.block)
+            k = self.rt.kernel(ks.source, ks.name, ks.block, ks.meta.get("smem", 0))
             if k.cache_hit == 0:
                 self.session.stats.compile_ms += k.compile_ms
             c["kernel"] = k

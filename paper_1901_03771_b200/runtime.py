@@ -267,7 +267,7 @@ class Runtime:
         return arr
 
     # -- compile / launch
-    def kernel(self, source: str, name: str, block: int) -> Kernel:
+    def kernel(self, source: str, name: str, block: int, smem: int = 0) -> Kernel:
         k = self._kernels.get((source, name))
         if k is not None:
             return k
@@ -281,7 +281,7 @@ class Runtime:
         fn = ctypes.c_uint64(0)
         _check(self.lib.grumpy_rt_get_function(mod.value, name.encode(), ctypes.byref(fn)))
         occ = ctypes.c_int(0)
-        _check(self.lib.grumpy_rt_occupancy(fn.value, block, 0, ctypes.byref(occ)))
+        _check(self.lib.grumpy_rt_occupancy(fn.value, block, smem, ctypes.byref(occ)))
         regs = ctypes.c_int(0)
         _check(self.lib.grumpy_rt_function_info(fn.value, ctypes.byref(regs), None, None, None))
         self.compile_ms_total += ms.value
