@@ -724,10 +724,10 @@ def generate(region: Region) -> KernelSource:
         return codegen_scan.generate(region)
     if kinds & {OpKind.REDUCE, OpKind.ARGREDUCE}:
         from . import codegen_coop, codegen_wrow
-        ks = codegen_wrow.try_generate(region)
+        ks = codegen_coop.try_generate(region)
         if ks is not None:
             return ks
-        ks = codegen_coop.try_generate(region)
+        ks = codegen_wrow.try_generate(region)
         if ks is not None:
             return ks
         return codegen_rows.gen_rows(region)

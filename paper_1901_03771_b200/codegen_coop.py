@@ -49,6 +49,7 @@ class CoopEmitter(LoopEmitter):
         self.coop_m: Optional[Var] = None
         self.coop_v: Optional[Var] = None
         self.staged = {}
+        self.discovered = []
         self.n_sh = 0
 
     # col coordinate of the current coop loops
@@ -59,6 +60,27 @@ class CoopEmitter(LoopEmitter):
         self.close(vv[1], vv[2])
         self.close(mm[1], mm[2])
 
+    def prestage(self, leaves, tma_layout=None):
+        """Load whole row segments of ``leaves`` into registers up front: from
+        the shared-memory stage filled by bulk copies (``tma_layout``: leaf id ->
+        (byte offset of the leaf block, leaf stride in elements, row bytes)) or
+        from global memory."""
+        rowkey = Aff.of(Var("r", 1)).scale(self.C).key()
+        for leaf in leaves:
+            name = self.fresh("S")
+            T = leaf.dtype.ctype
+            self.stmt(1, f"{T} {name}[16][{self.vec}];")
+            if tma_layout is not None and leaf.id in tma_layout:
+                boff, ls, rowb = tma_layout[leaf.id]
+                self.stmt(1, f"{{ const {T}* sp = reinterpret_cast<const {T}*>(stage + {boff} + (long long)ri * {rowb}) + "
+                             f"(tr / {self.P}) * {ls} + (tr % {self.P}) * {self.vec};")
+                self.stmt(1, f"#pragma unroll\n    for (int mm = 0; mm < 16; ++mm) gr::ldsv<{T}, {self.vec}>({name}[mm], sp + 8 * mm); }}")
+            else:
+                idx = self.leaf_index[leaf.id]
+                self.stmt(1, f"#pragma unroll\n    for (int mm = 0; mm < 16; ++mm) "
+                             f"gr::ldv<{T}, {self.vec}>({name}[mm], p.in{idx} + r * {self.C}LL + cb + 8 * mm);")
+            self.staged[(leaf.id, rowkey)] = name
+
     def load_leaf(self, leaf: Node, off: Aff):
         # staged row segment: offset = rest + cb + 8*m + v with m, v the coop loop vars
         for m, v in self._coop_pairs():
@@ -68,6 +90,7 @@ class CoopEmitter(LoopEmitter):
                     key = (leaf.id, rest.key())
                     name = self.staged.get(key)
                     if name is None:
+                        self.discovered.append((leaf, rest.key()))
                         name = self.fresh("S")
                         T = leaf.dtype.ctype
                         idx = self.leaf_index[leaf.id]
@@ -218,10 +241,53 @@ def _qualifies(region: Region):
     return Ts, totals, C, vec, tpr
 
 
+SMEM_PER_CTA = 110 * 1024   # two CTAs per SM keep 16 warps resident
+
+
+def _pad_bytes(isz: int, P: int) -> int:
+    """Leaf padding so a warp's 16-byte reads of the staged leaves are
+    conflict-free: (leaf stride / 16) ≡ P (mod 8)."""
+    base = 128 * isz // 16
+    pad = 0
+    while (base + pad) % 8 != P % 8:
+        pad += 1
+    return pad * 16
+
+
 def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
     q = _qualifies(region)
     if q is None:
         return None
+    # pass 1 discovers the row-contiguous leaves; pass 2 stages them up front,
+    # through a bulk-copy ring when they fit in shared memory
+    first = _generate(region, q, kname, None, None)
+    if first is None:
+        return None
+    ks, em = first
+    Ts, totals, C, vec, tpr = q
+    rowkey = Aff.of(Var("r", 1)).scale(C).key()
+    leaves = []
+    for leaf, key in em.discovered:
+        if key == rowkey and tuple(leaf.shape) == Ts + (C,) and leaf not in leaves:
+            leaves.append(leaf)
+    if not leaves:
+        return ks
+    block = max(256, tpr)
+    rpc = block // tpr
+    P = 8 // vec
+    layout = {}
+    off = 0
+    for l in leaves:
+        lsb = 128 * l.dtype.itemsize + _pad_bytes(l.dtype.itemsize, P)
+        rowb = (C // 128) * lsb
+        layout[l.id] = (off, lsb // l.dtype.itemsize, rowb)
+        off += rpc * rowb
+    tma = layout if off <= SMEM_PER_CTA else None
+    second = _generate(region, q, kname, leaves, tma, smem_bytes=off if tma else 0)
+    return second[0] if second is not None else ks
+
+
+def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0):
     Ts, totals, C, vec, tpr = q
     tot_ids = {t.id for t in totals}
     block = max(256, tpr)
@@ -242,6 +308,14 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
                 row_coords.append(Aff.of(Var(c, 1)))
                 rest = em.emit(1, "long long", f"{rest} / {Ts[d]}")
         row_coords.reverse()
+
+    if prestage:
+        em.prestage(prestage, tma)
+        if tma:
+            # the stage is in registers now: release it and start the bulk copy
+            # of the next row group, which then overlaps this group's compute
+            em.stmt(1, "__syncthreads();")
+            em.stmt(1, "if (threadIdx.x < 32) { gr::fence_proxy_async(); if (gnext < NG) issue(p, stage, bar, gnext, threadIdx.x); }")
 
     # totals whose operand is itself a stored root accumulate in the store loop
     # (the value is computed once per element)
@@ -307,24 +381,60 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
         scratch_off += ((R * T.itemsize + 255) // 256) * 256
 
     P = 8 // vec
-    lines = ["static __device__ __forceinline__ void rows(const Params& p, const long long rb) {",
+    NG = -(-R // rpc)
+    lines = ["static __device__ __forceinline__ void rows(const Params& p, const long long rb, "
+             "unsigned char* stage, unsigned long long* bar, const long long gnext) {",
              f"  const int tr = threadIdx.x % {tpr};",
              f"  const int ri = threadIdx.x / {tpr};",
              "  const bool valid = rb + ri < NROWS;",
              "  const long long r = valid ? rb + ri : NROWS - 1;",
-             f"  const long long cb = (long long)(tr / {P}) * 128 + (tr % {P}) * {vec};"]
+             f"  const long long cb = (long long)(tr / {P}) * 128 + (tr % {P}) * {vec};",
+             "  (void)stage; (void)bar; (void)gnext;"]
     lines += ["  " + c for c in em.consts]
     lines += render(em.row, 1)
     lines.append("}")
+    issue = []
+    if tma:
+        nleaf = C // 128
+        total = sum(nleaf * 128 * l.dtype.itemsize for l in prestage)
+        issue = ["static __device__ __forceinline__ void issue(const Params& p, unsigned char* stage, unsigned long long* bar, const long long g, const int lane) {",
+                 f"  const long long nvalid = (g * {rpc} + {rpc} <= NROWS) ? {rpc} : (NROWS - g * {rpc});",
+                 f"  if (lane == 0) gr::mbar_arrive_expect_tx(bar, (unsigned)(nvalid * {total}));"]
+        for l in prestage:
+            boff, ls, rowb = tma[l.id]
+            lsb = ls * l.dtype.itemsize
+            idx = region.leaves.index(l)
+            issue += [f"  for (int c = lane; c < {rpc * nleaf}; c += 32) {{",
+                      f"    const int qq = c / {nleaf}, lf = c % {nleaf};",
+                      f"    if (qq < nvalid) gr::bulk_g2s(stage + {boff} + (long long)qq * {rowb} + (long long)lf * {lsb}, "
+                      f"p.in{idx} + (g * {rpc} + qq) * {C}LL + (long long)lf * 128, {128 * l.dtype.itemsize}u, bar);",
+                      "  }"]
+        issue.append("}")
     params = _params_struct(region).replace("    void* __restrict__ scratch;",
                                              "    void* __restrict__ scratch;\n    unsigned int* ticket;")
-    src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params,
-           f"  static constexpr long long NROWS = {R}LL;"]
+    src = [HEADER, '#include "gr_reduce.cuh"\n#include "gr_tma.cuh"\n', "struct K {", params,
+           f"  static constexpr long long NROWS = {R}LL;",
+           f"  static constexpr long long NG = {NG}LL;"]
+    if issue:
+        src.append("  " + "\n  ".join(issue))
     src.append("  " + "\n  ".join(lines))
     src.append("};")
-    kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
-            f"  for (long long rb = (long long)blockIdx.x * {rpc}; rb < K::NROWS; rb += (long long)gridDim.x * {rpc})",
-            "    K::rows(p, rb);"]
+    if tma:
+        kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
+                "  extern __shared__ __align__(128) unsigned char smem[];",
+                "  __shared__ unsigned long long bar;",
+                "  if (threadIdx.x == 0) { gr::mbar_init(&bar, 1); gr::fence_mbar_init(); }",
+                "  __syncthreads();",
+                "  long long g = blockIdx.x;",
+                "  if (threadIdx.x < 32 && g < K::NG) K::issue(p, smem, &bar, g, threadIdx.x);",
+                "  for (int it = 0; g < K::NG; g += gridDim.x, ++it) {",
+                "    gr::mbar_wait(&bar, (unsigned)(it & 1));",
+                f"    K::rows(p, g * {rpc}, smem, &bar, g + gridDim.x);",
+                "  }"]
+    else:
+        kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
+                f"  for (long long g = blockIdx.x; g < K::NG; g += gridDim.x)",
+                f"    K::rows(p, g * {rpc}, nullptr, nullptr, 0);"]
     if tot_meta:
         kern.append("  if (gr::last_block(p.ticket)) {")
         for ri, rop, T, off in tot_meta:
@@ -337,10 +447,11 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
         kern.append("  }")
     kern.append("}")
     src += kern
-    groups = -(-R // rpc)
-    return KernelSource("coop", "\n".join(src) + "\n", kname,
-                        leaf_slots=list(range(len(region.leaves))),
-                        root_slots=list(range(len(region.roots))),
-                        block=block, groups=groups * block, vec=vec, unroll=1, scratch_bytes=scratch_off,
-                        meta={"rows": R, "row_shape": Ts, "cols": C, "tpr": tpr, "rows_per_cta": rpc,
-                              "totals": len(tot_meta), "ticket": bool(tot_meta)})
+    ks = KernelSource("coop", "\n".join(src) + "\n", kname,
+                      leaf_slots=list(range(len(region.leaves))),
+                      root_slots=list(range(len(region.roots))),
+                      block=block, groups=NG * block, vec=vec, unroll=1, scratch_bytes=scratch_off,
+                      meta={"rows": R, "row_shape": Ts, "cols": C, "tpr": tpr, "rows_per_cta": rpc,
+                            "totals": len(tot_meta), "ticket": bool(tot_meta), "smem": smem_bytes,
+                            "bulk_copy": bool(tma), "label": "coop-tma" if tma else "coop"})
+    return ks, em

@@ -55,6 +55,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// V consecutive elements (16 bytes) from shared memory into registers
+template <class T, int V> __device__ __forceinline__ void ldsv(T (&d)[V], const T* s) {
+  VecU<T, V> u;
+  u.raw = *reinterpret_cast<const typename RawVec<sizeof(T) * V>::T*>(s);
+#pragma unroll
+  for (int i = 0; i < V; ++i) d[i] = u.v[i];
+}
+
 // 8 consecutive elements from shared memory (16-byte aligned) into registers
 template <class T> __device__ __forceinline__ void lds8(T (&d)[8], const T* s) {
   static_assert(sizeof(T) == 4 || sizeof(T) == 8, "lds8");
