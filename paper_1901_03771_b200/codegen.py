@@ -313,6 +313,17 @@ class ValueEmitter:
             if code is ElemCode.select:
                 T = n.dtype.ctype
                 expr = f"gr::select<{T}>({names[0]}, {names[1]}, {names[2]})"
+            elif code is ElemCode.div and n.loop[0].is_float and args[1][1] < args[0][1]:
+                # divisor hoisted out of the dividend's scope: one reciprocal per
+                # divisor, exact Markstein correction per element
+                T = n.loop[0].ctype
+                rk = ("rcp", names[1])
+                r = self.const_memo.get(rk)
+                if r is None or args[1][1] > 0:
+                    r = self.emit(args[1][1], f"gr::DivShared<{T}>", f"gr::div_prep<{T}>({names[1]})")
+                    if args[1][1] == 0:
+                        self.const_memo[rk] = r
+                expr = f"gr::div_shared<{T}>({names[0]}, {r})"
             elif code in _BIN:
                 T = n.loop[0].ctype
                 expr = _BIN[code].format(T=T) + f"({names[0]}, {names[1]})"

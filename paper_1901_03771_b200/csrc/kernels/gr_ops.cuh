@@ -67,6 +67,51 @@ template <> __device__ __forceinline__ bool mul(bool a, bool b) { return a && b;
 
 template <class T> __device__ __forceinline__ T div(T a, T b) { return a / b; }
 
+// Division by a divisor shared by many dividends (a row's std, a constant):
+// r = RN(1/s) once, then per element Markstein's correction
+//   q0 = RN(x*r); e = x - q0*s (exact with FMA); q = RN(q0 + e*r)
+// which is the correctly rounded x/s whenever no intermediate leaves the
+// normal range (Markstein 1990).  Outside a conservative exponent window (and
+// for zeros, inf, NaN) the IEEE division is used, so the result is always
+// bit-identical to x / s.
+template <class T> struct DivWin;
+template <> struct DivWin<float> {
+  static __device__ __forceinline__ float lo() { return 7.8886091e-31f; }   // 2^-100
+  static __device__ __forceinline__ float hi() { return 1.2676506e+30f; }   // 2^100
+};
+template <> struct DivWin<double> {
+  static __device__ __forceinline__ double lo() { return 1.4916681462400413e-154; }  // 2^-510
+  static __device__ __forceinline__ double hi() { return 6.7039039649712985e+153; }  // 2^510
+};
+template <class T> struct DivShared {
+  T s, r, xlo, xhi;   // |x| in [xlo, xhi]  =>  x, q and the residual stay normal
+};
+template <class T> __device__ __forceinline__ DivShared<T> div_prep(T s) {
+  DivShared<T> d;
+  const T as = s < T(0) ? -s : s;
+  d.s = s;
+  if (as >= DivWin<T>::lo() && as <= DivWin<T>::hi()) {
+    d.r = T(1) / s;
+    const T a = DivWin<T>::lo() * as * T(4), b = DivWin<T>::hi() * as * T(0.25);
+    d.xlo = a > DivWin<T>::lo() ? a : DivWin<T>::lo();
+    d.xhi = b < DivWin<T>::hi() ? b : DivWin<T>::hi();
+  } else {
+    d.r = T(0);
+    d.xlo = T(1);
+    d.xhi = T(0);  // empty window: always the IEEE path
+  }
+  return d;
+}
+__device__ __noinline__ float div_slow(float x, float s) { return x / s; }
+__device__ __noinline__ double div_slow(double x, double s) { return x / s; }
+template <class T> __device__ __forceinline__ T div_shared(T x, const DivShared<T>& d) {
+  const T q0 = x * d.r;
+  const T e = fma(-q0, d.s, x);
+  const T q = fma(e, d.r, q0);
+  const T ax = fabs(x);
+  return (ax >= d.xlo && ax <= d.xhi) ? q : div_slow(x, d.s);
+}
+
 template <class T> __device__ __forceinline__ T neg(T a) { return -a; }
 template <> __device__ __forceinline__ int neg(int a) { return (int)(0u - (unsigned)a); }
 template <> __device__ __forceinline__ i64 neg(i64 a) { return (i64)(0ull - (u64)a); }

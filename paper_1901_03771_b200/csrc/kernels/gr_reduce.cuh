@@ -272,6 +272,16 @@ template <class T, int VEC> __device__ __forceinline__ T leaf_local(const T (&a)
 // aligned runs of TPR, tr = thread index within the row) in perfect-tree
 // order; for TPR > 32 the warp results meet in shared memory `sh`
 // (>= rows_per_cta * TPR/32 elements).  Every thread of the row gets the result.
+// Barrier over the TPR threads of row slot ri only (named barrier 1 + ri):
+// the warps of one row wait for each other, not for the whole CTA.
+template <int TPR> __device__ __forceinline__ void row_bar(int ri) {
+  if constexpr (TPR >= 1024) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + ri), "n"(TPR) : "memory");
+  }
+}
+
 template <class Op, class T, int TPR> __device__ __forceinline__ T row_tree(T v, T* sh, int ri) {
   constexpr int W = TPR < 32 ? TPR : 32;
 #pragma unroll
@@ -280,7 +290,7 @@ template <class Op, class T, int TPR> __device__ __forceinline__ T row_tree(T v,
     constexpr int NW = TPR / 32;
     const int tr = threadIdx.x % TPR;
     if ((threadIdx.x & 31) == 0) sh[ri * NW + tr / 32] = v;
-    __syncthreads();
+    row_bar<TPR>(ri);
     T buf[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) buf[w] = sh[ri * NW + w];
@@ -288,7 +298,7 @@ template <class Op, class T, int TPR> __device__ __forceinline__ T row_tree(T v,
     for (int s = 1; s < NW; s <<= 1)
 #pragma unroll
       for (int w = 0; w + s < NW; w += 2 * s) buf[w] = Op::template c<T>(buf[w], buf[w + s]);
-    __syncthreads();
+    row_bar<TPR>(ri);
     v = buf[0];
   }
   return v;
@@ -307,7 +317,7 @@ template <class T, int VEC, int P, int TPR> __device__ __forceinline__ T row_sum
     constexpr int NW = TPR / 32;
     const int tr = threadIdx.x % TPR;
     if ((threadIdx.x & 31) == 0) sh[ri * NW + tr / 32] = s;
-    __syncthreads();
+    row_bar<TPR>(ri);
     T buf[NW];
 #pragma unroll
     for (int w = 0; w < NW; ++w) buf[w] = sh[ri * NW + w];
@@ -315,7 +325,7 @@ template <class T, int VEC, int P, int TPR> __device__ __forceinline__ T row_sum
     for (int st = 1; st < NW; st <<= 1)
 #pragma unroll
       for (int w = 0; w + st < NW; w += 2 * st) buf[w] = add<T>(buf[w], buf[w + st]);
-    __syncthreads();
+    row_bar<TPR>(ri);
     s = buf[0];
   }
   return s;
@@ -341,7 +351,7 @@ __device__ __forceinline__ long long row_arg(T best, long long bi, T* shv, long 
       shv[ri * NW + tr / 32] = best;
       shi[ri * NW + tr / 32] = bi;
     }
-    __syncthreads();
+    row_bar<TPR>(ri);
     best = shv[ri * NW];
     bi = shi[ri * NW];
 #pragma unroll
@@ -351,7 +361,7 @@ __device__ __forceinline__ long long row_arg(T best, long long bi, T* shv, long 
         bi = shi[ri * NW + w];
       }
     }
-    __syncthreads();
+    row_bar<TPR>(ri);
   }
   return bi;
 }
