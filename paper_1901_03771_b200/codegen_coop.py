@@ -20,6 +20,8 @@ serialise a 4096-element row in one thread with uncoalesced loads; here:
 
 from __future__ import annotations
 
+import os
+
 from typing import List, Optional
 
 from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, c_literal
@@ -242,6 +244,7 @@ def _qualifies(region: Region):
 
 
 SMEM_PER_CTA = 110 * 1024   # two CTAs per SM keep 16 warps resident
+PREFETCH_GROUPS = int(os.environ.get("GRUMPY_PREFETCH_GROUPS", "2"))
 
 
 def _pad_bytes(isz: int, P: int) -> int:
@@ -282,12 +285,14 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
         rowb = (C // 128) * lsb
         layout[l.id] = (off, lsb // l.dtype.itemsize, rowb)
         off += rpc * rowb
-    tma = layout if off <= SMEM_PER_CTA else None
-    second = _generate(region, q, kname, leaves, tma, smem_bytes=off if tma else 0)
+    mode = os.environ.get("GRUMPY_COOP_MODE", "l2")
+    tma = layout if (off <= SMEM_PER_CTA and mode == "tma") else None
+    second = _generate(region, q, kname, leaves, tma, smem_bytes=off if tma else 0,
+                       l2_prefetch=(mode == "l2" and tma is None))
     return second[0] if second is not None else ks
 
 
-def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0):
+def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch=False):
     Ts, totals, C, vec, tpr = q
     tot_ids = {t.id for t in totals}
     block = max(256, tpr)
@@ -309,6 +314,15 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0):
                 rest = em.emit(1, "long long", f"{rest} / {Ts[d]}")
         row_coords.reverse()
 
+    if prestage and l2_prefetch:
+        # bulk-prefetch this row's segment of the group PREFETCH_GROUPS ahead into
+        # L2 (cp.async.bulk.prefetch.L2): the register staging loads of later
+        # groups then hit L2, keeping HBM busy while this group is reduced
+        for l in prestage:
+            idx = em.leaf_index[l.id]
+            isz = l.dtype.itemsize
+            em.stmt(1, f"if (tr == 0) {{ const long long rp = (rb / {rpc} + {PREFETCH_GROUPS}LL * gridDim.x) * {rpc} + ri; "
+                       f"if (rp < NROWS) gr::prefetch_l2(p.in{idx} + rp * {C}LL, {C * isz}u); }}")
     if prestage:
         em.prestage(prestage, tma)
         if tma:

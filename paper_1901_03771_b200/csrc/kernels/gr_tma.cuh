@@ -55,6 +55,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion):
+// later LDGs of that range hit L2 instead of HBM.
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // V consecutive elements (16 bytes) from shared memory into registers
 template <class T, int V> __device__ __forceinline__ void ldsv(T (&d)[V], const T* s) {
   VecU<T, V> u;
