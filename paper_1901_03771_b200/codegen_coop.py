@@ -285,7 +285,9 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
         rowb = (C // 128) * lsb
         layout[l.id] = (off, lsb // l.dtype.itemsize, rowb)
         off += rpc * rowb
-    mode = os.environ.get("GRUMPY_COOP_MODE", "l2")
+    # measured on B200 (profiles/r01_rownorm_modes.md): plain register staging
+    # 0.312 ms, + L2 bulk prefetch 0.333 ms, smem bulk-copy ring 0.427 ms
+    mode = os.environ.get("GRUMPY_COOP_MODE", "plain")
     tma = layout if (off <= SMEM_PER_CTA and mode == "tma") else None
     second = _generate(region, q, kname, leaves, tma, smem_bytes=off if tma else 0,
                        l2_prefetch=(mode == "l2" and tma is None))
