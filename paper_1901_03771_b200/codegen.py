@@ -730,9 +730,11 @@ def generate(region: Region) -> KernelSource:
     """Pick the kernel family for a region and emit its source."""
     from . import codegen_rows
     kinds = {n.op.kind for n in region.nodes}
-    if kinds & {OpKind.SCAN, OpKind.KEYED_SUM}:
+    if OpKind.SCAN in kinds:
         from . import codegen_scan
         return codegen_scan.generate(region)
+    if OpKind.KEYED_SUM in kinds:
+        return codegen_rows.gen_rows(region)
     if kinds & {OpKind.REDUCE, OpKind.ARGREDUCE}:
         from . import codegen_coop, codegen_wrow
         ks = codegen_coop.try_generate(region)
@@ -770,4 +772,7 @@ def grid_for(ks: KernelSource, sm_count: int, blocks_per_sm: int) -> int:
     (SM count × resident CTAs per SM)."""
     per_cta = ks.block * max(ks.unroll, 1)
     need = max(1, -(-ks.groups // per_cta))
-    return int(max(1, min(need, sm_count * max(blocks_per_sm, 1))))
+    g = min(need, sm_count * max(blocks_per_sm, 1))
+    if ks.meta.get("max_grid"):
+        g = min(g, ks.meta["max_grid"])
+    return int(max(1, g))

@@ -62,6 +62,7 @@ _COMBINE = {ReduceOp.sum: "gr::add", ReduceOp.prod: "gr::mul", ReduceOp.max: "gr
 _OPS = {ReduceOp.sum: "gr::OpSum", ReduceOp.prod: "gr::OpProd", ReduceOp.max: "gr::OpMax", ReduceOp.min: "gr::OpMin"}
 
 SMALL_RECOMPUTE = 64   # a reduction re-evaluated per column may reduce at most this many points
+MAX_GRID = 148 * 16    # grid cap for kernels with per-CTA partial slots (keyed sums)
 
 
 class Scope:
@@ -393,6 +394,9 @@ def thread_space(region: Region):
     for n in _reductions(region):
         if n.id not in tot_ids and is_total(n):
             raise NotFusable(n, "a full reduction consumed inside the region")
+    keyed = [r for r in region.roots if r.kind is OpKind.KEYED_SUM]
+    if keyed and not reds:
+        return tuple(keyed[0].preds[0].shape), totals, None
     if len(reds) == 1 and reds[0] in region.roots and len(region.roots) == 1 + len(totals) and not totals:
         # a lone reduction root: one thread per output element, loops over the
         # reduced axes in NumPy order (covers sum(axis=0) and middle axes)
@@ -502,7 +506,7 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
         return _flat_coords(em, S, Aff.of(Var("vo", 1)) + Aff.of(iv), iv), (s, saved), iv
 
     for ri, r in enumerate(region.roots):
-        if r.id in tot_ids:
+        if r.id in tot_ids or r.kind is OpKind.KEYED_SUM:
             continue
         T = r.dtype.ctype
         if virtual is not None:
@@ -584,7 +588,51 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
         tot_meta.append((ri, rop, T, off))
         scratch_off += ((R * T.itemsize + 255) // 256) * 256
 
-    lines = ["static __device__ __forceinline__ void row(const Params& p, const long long r) {"]
+    # keyed sums (np.bincount): deterministic warp histograms.  Each warp owns
+    # a private shared-memory histogram; per 32 rows the (key, weight) pairs
+    # are broadcast in lane order and lane (key % 32) adds them — no atomics,
+    # fixed order.  Warps fold in warp order, CTAs in CTA order (last CTA).
+    keyed = [(ri, r) for ri, r in enumerate(region.roots) if r.kind is OpKind.KEYED_SUM]
+    warps = block // 32
+    kmeta = []
+    if keyed:
+        NB = max(r.op.attrs[0] for _, r in keyed)
+        if warps * NB * 8 * len(keyed) > 40 * 1024:
+            raise UnsupportedNodeInFusedStep(f"bincount with {NB} bins exceeds the shared-memory histogram")
+        key_node = keyed[0][1].preds[0]
+        kv = em.cast(em.value(key_node, row_coords), key_node.dtype, DType.i64)
+        em.stmt(1, f"const long long kkey = valid ? {kv[0]} : -1LL;")
+        wnames = []
+        for j, (ri, r) in enumerate(keyed):
+            if r.preds[0] is not key_node and r.preds[0].id != key_node.id:
+                raise NotFusable(r, "bincounts of one region must share their keys")
+            if len(r.preds) == 2:
+                wv = em.cast(em.value(r.preds[1], row_coords), r.preds[1].dtype, DType.f64)
+                em.stmt(1, f"const double kw{j} = {wv[0]};")
+            else:
+                em.stmt(1, f"const long long kw{j} = 1LL;")
+            wnames.append((j, r))
+        body = [f"for (int src = 0; src < 32; ++src) {{",
+                "  const long long kk = __shfl_sync(0xffffffffu, kkey, src);"]
+        for j, r in wnames:
+            body.append(f"  const {r.dtype.ctype} w{j} = __shfl_sync(0xffffffffu, kw{j}, src);")
+        conds = []
+        for j, r in wnames:
+            NBj = r.op.attrs[0]
+            body.append(f"  if (kk >= 0 && kk < {NBj}LL && (int)(kk & 31) == (threadIdx.x & 31)) "
+                        f"khist{j}[(threadIdx.x >> 5) * {NBj} + kk] += w{j};")
+        body.append("}")
+        for line in body:
+            em.stmt(1, line)
+        for j, r in wnames:
+            NBj = r.op.attrs[0]
+            off = scratch_off
+            scratch_off += ((MAX_GRID * NBj * 8 + 255) // 256) * 256
+            kmeta.append((j, r, NBj, off))
+
+    lines = ["static __device__ __forceinline__ void row(const Params& p, const long long r, const bool valid"
+             + "".join(f", {r.dtype.ctype}* khist{j}" for j, r, _, _ in kmeta) + ") {",
+             "  (void)valid;"]
     lines += ["  " + c for c in em.consts]
     lines += render(em.row, 1)
     lines.append("}")
@@ -595,11 +643,38 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
     src.append("  " + "\n  ".join(lines))
     src.append("};")
     kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
-            "  const long long stride = (long long)gridDim.x * blockDim.x;",
-            "  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride)",
-            "    K::row(p, r);"]
-    if tot_meta:
+            "  const long long stride = (long long)gridDim.x * blockDim.x;"]
+    if kmeta:
+        for j, r, NBj, off in kmeta:
+            kern.append(f"  __shared__ {r.dtype.ctype} khist{j}[{warps * NBj}];")
+            kern.append(f"  for (int i = threadIdx.x; i < {warps * NBj}; i += blockDim.x) khist{j}[i] = 0;")
+        kern.append("  __syncthreads();")
+        hargs = "".join(f", khist{j}" for j, _, _, _ in kmeta)
+        kern += ["  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < K::NROWS; base += stride) {",
+                 "    const long long r = base + (threadIdx.x & 31);",
+                 f"    K::row(p, r < K::NROWS ? r : K::NROWS - 1, r < K::NROWS{hargs});",
+                 "  }",
+                 "  __syncthreads();"]
+        for j, r, NBj, off in kmeta:
+            ct = r.dtype.ctype
+            kern += [f"  for (int b = threadIdx.x; b < {NBj}; b += blockDim.x) {{",
+                     f"    {ct} s = khist{j}[b];",
+                     f"    for (int w = 1; w < {warps}; ++w) s += khist{j}[w * {NBj} + b];",
+                     f"    reinterpret_cast<{ct}*>(static_cast<char*>(p.scratch) + {off})[(long long)blockIdx.x * {NBj} + b] = s;",
+                     "  }"]
+    else:
+        kern += ["  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride)",
+                 "    K::row(p, r, true);"]
+    if tot_meta or kmeta:
         kern.append("  if (gr::last_block(p.ticket)) {")
+        for j, r, NBj, off in kmeta:
+            ri = region.roots.index(r)
+            ct = r.dtype.ctype
+            kern += [f"    for (int b = threadIdx.x; b < {NBj}; b += blockDim.x) {{",
+                     f"      {ct} s = 0;",
+                     f"      for (unsigned c = 0; c < gridDim.x; ++c) s += reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {off})[(long long)c * {NBj} + b];",
+                     f"      p.out{ri}[b] = s;",
+                     "    }"]
         for ri, rop, T, off in tot_meta:
             ct = T.ctype
             if isinstance(rop, tuple):
@@ -622,8 +697,9 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
                         leaf_slots=list(range(len(region.leaves))),
                         root_slots=list(range(len(region.roots))),
                         block=block, groups=R, vec=1, unroll=1, scratch_bytes=scratch_off,
-                        meta={"rows": R, "row_shape": Ts, "totals": len(tot_meta), "ticket": bool(tot_meta),
-                              "virtual": virtual, "block_pow2": True})
+                        meta={"rows": R, "row_shape": Ts, "totals": len(tot_meta), "ticket": bool(tot_meta or kmeta),
+                              "virtual": virtual, "block_pow2": True, "keyed": len(kmeta),
+                              "max_grid": MAX_GRID if kmeta else None})
 
 
 def _row_partial(em: LoopEmitter, x: Node, rop, T: DType, row_coords, cols):

@@ -207,9 +207,10 @@ class Node:
     nodes (operands are cast to these before the op, as NumPy does).
     """
 
-    __slots__ = ("id", "op", "preds", "pred_ids", "shape", "dtype", "data", "loop", "__weakref__")
+    __slots__ = ("id", "op", "preds", "pred_ids", "shape", "dtype", "data", "loop", "dist", "__weakref__")
 
     def __init__(self, op: Op, preds: Sequence["Node"], shape: Shape, dtype: DType, loop=None, data=None):
+        self.dist = None   # distribution tag after a sharded force (distributed.py)
         self.id = next(_ids)
         self.op = op
         self.preds: Tuple[Node, ...] = tuple(preds)

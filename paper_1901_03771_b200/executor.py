@@ -50,20 +50,30 @@ class Executor:
         return TensorBuffer(n.dtype, n.shape, device=self.rt.alloc(nbytes))
 
     # -- steps ------------------------------------------------------------------------
-    def run(self, steps: List[PlanStep]):
+    def run(self, steps: List[PlanStep], dist=None, comm=None):
         self.last_steps = steps
         g = self.session.graph
         for st in steps:
             if st.kind == "Library":
-                out = self.run_library(st)
-                g.mark_materialized(st.root, out)
+                outs = [self.run_library(st)]
                 self.session.stats.library_calls += 1
-                self.session.stats.nodes_materialized += 1
             else:
                 outs = self.run_fused(st)
-                for r, b in zip(st.roots, outs):
-                    g.mark_materialized(r, b)
-                self.session.stats.nodes_materialized += len(st.roots)
+            if dist is not None:
+                self._combine_partials(st.roots, outs, dist, comm)
+            for r, b in zip(st.roots, outs):
+                g.mark_materialized(r, b)
+            self.session.stats.nodes_materialized += len(st.roots)
+
+    def _combine_partials(self, roots, outs, dist, comm):
+        """Allreduce partial roots in place on the runtime stream (NCCL), right
+        after the kernel that produced them (distributed.py)."""
+        from .dag import ReduceOp
+        for r, b in zip(roots, outs):
+            d = dist.get(r.id, "R")
+            if d.startswith("P:") and element_count(r.shape):
+                comm.allreduce_device(b.device, element_count(r.shape), r.dtype, ReduceOp(d[2:]))
+                self.session.stats.collectives += 1
 
     def kernel_source(self, region: codegen.Region) -> codegen.KernelSource:
         return codegen.cached_generate(region)

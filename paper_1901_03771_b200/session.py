@@ -69,6 +69,7 @@ class Session:
         self._executor = None
         self._consts = {}
         self._plan_cache = {}
+        self._arg_operand_shape = {}
         self.comm = None  # distributed.Comm when sharded
 
     @property
@@ -111,6 +112,8 @@ class Session:
         pending = [n for n in nodes if not n.is_materialized]
         if not pending:
             return
+        if self.comm is not None:
+            return self._force_sharded(pending)
         t0 = time.perf_counter()
         key, order = _planner.dag_signature(pending)
         tmpl = self._plan_cache.get(key)
@@ -126,6 +129,59 @@ class Session:
         self.stats.plan_time += t1 - t0
         self.executor.run(steps)
         self.stats.exec_time += time.perf_counter() - t1
+
+    def _force_sharded(self, pending):
+        """Leading-axis sharded execution (distributed.py): partial nodes become
+        step roots and are allreduced after their kernel; arg-reductions over
+        the sharded axis are combined from (value, global index) pairs."""
+        from . import distributed as D
+        t0 = time.perf_counter()
+        dist = D.classify(pending)
+        nodes = {}
+        stack = list(pending)
+        while stack:
+            n = stack.pop()
+            if n.id in nodes:
+                continue
+            nodes[n.id] = n
+            if not n.is_materialized:
+                stack.extend(n.preds)
+        partial = [n for n in nodes.values() if not n.is_materialized and dist.get(n.id, "R")[0] in "PA"]
+        aux = {}
+        for n in partial:
+            if dist[n.id][0] == "A":
+                info = D.shard_of(n.preds[0])
+                self._arg_operand_shape[n.id] = (n.preds[0].shape, info[1] if info else 0)
+                which, axis, keepdims = n.op.attrs
+                x = n.preds[0]
+                axes = tuple(range(len(x.shape))) if axis is None else (axis,)
+                rop = ReduceOp.max if which == "max" else ReduceOp.min
+                aux[n.id] = self.graph.add_op(Op(OpKind.REDUCE, None, (rop, axes, bool(keepdims), None)), [x])
+        roots = list(dict((n.id, n) for n in list(pending) + partial + list(aux.values())).values())
+        steps = self.plan(roots)
+        self.stats.plan_time += time.perf_counter() - t0
+        t1 = time.perf_counter()
+        self.executor.run(steps, dist=dist, comm=self.comm)
+        for n in partial:
+            if dist[n.id][0] == "A":
+                self._combine_arg(n, aux[n.id], dist[n.id][2:])
+            n.dist = "R"
+        self.stats.exec_time += time.perf_counter() - t1
+
+    def _combine_arg(self, n, aux, which):
+        from . import distributed as D
+        local_idx = self.to_numpy(n)
+        local_val = self.to_numpy(aux)
+        src_shape, off_rows = self._arg_operand_shape[n.id]
+        if n.op.attrs[1] is None:
+            # flat index over the local [n_local, ...] block -> global
+            offset = off_rows * int(np.prod(src_shape[1:]))
+        else:
+            offset = off_rows
+        g = D.combine_arg(which, local_idx, local_val, offset, self.comm)
+        g = np.ascontiguousarray(g.astype(np.int64).reshape(n.shape))
+        n.data.host = g
+        n.data.device.copy_from_host(g)
 
     def to_numpy(self, node: Node) -> np.ndarray:
         self.force_nodes([node])
@@ -656,9 +712,16 @@ def _reduce(a, rop: ReduceOp, axis, dtype, keepdims) -> ndarray:
 
 
 def _count(a: ndarray, axes) -> int:
+    """Number of reduced elements; the sharded leading axis counts globally."""
     n = 1
+    glob = None
+    if 0 in axes and a._session.comm is not None:
+        from . import distributed as D
+        if D.classify([a._node]).get(a._node.id) == "S":
+            info = D.shard_of(a._node)
+            glob = info[0] if info else None
     for ax in axes:
-        n *= a.shape[ax]
+        n *= glob if (ax == 0 and glob is not None) else a.shape[ax]
     return n
 
 

@@ -113,3 +113,24 @@ def kmeans_inputs(n=1 << 26, k=64, d=4, seed=42):
 def kmeans_assign(xp, P, C):
     d = ((P[:, None, :] - C[None]) ** 2).sum(-1)
     return d.argmin(1)
+
+
+def kmeans_partials(xp, P, C):
+    """Assignment + per-cluster partial sums (fp64) and counts: the quantities
+    each shard allreduces before the centroid update."""
+    k, D = C.shape
+    lab = kmeans_assign(xp, P, C)
+    sums = [xp.bincount(lab, weights=P[:, d], minlength=k) for d in range(D)]
+    counts = xp.bincount(lab, minlength=k)
+    return lab, sums, counts
+
+
+def kmeans_centroids(sums, counts, C_old):
+    """Host-side centroid update from (allreduced) partials; empty clusters keep
+    their previous centre."""
+    S = np.stack([np.asarray(s) for s in sums], axis=1)
+    n = np.asarray(counts)
+    out = np.array(C_old, dtype=np.float64, copy=True)
+    nz = n > 0
+    out[nz] = S[nz] / n[nz, None]
+    return out.astype(np.float32)

@@ -80,6 +80,29 @@ def test_int_and_bool_reductions(sess):
     assert np.array_equal(np.asarray(g.max(0)), a.max(0))
 
 
+def test_kmeans_partials_one_kernel(sess):
+    P, C = wl.kmeans_inputs(n=(1 << 15) + 17, k=64, d=4)
+    lab, sums, counts = wl.kmeans_partials(gp, gp.asarray(P), gp.asarray(C))
+    gp.force(lab, *sums, counts)
+    assert sess.stats.kernels_executed == 1
+    elab, esums, ecounts = wl.kmeans_partials(np, P, C)
+    assert np.array_equal(np.asarray(lab), elab)
+    assert np.array_equal(np.asarray(counts), ecounts)
+    for s, e in zip(sums, esums):
+        # fp64 sums of fp32 weights; order differs from NumPy's sequential loop
+        np.testing.assert_allclose(np.asarray(s), e, rtol=1e-12, atol=1e-9)
+
+
+def test_bincount_alone(sess):
+    rng = np.random.default_rng(9)
+    k = rng.integers(0, 100, 5000)
+    w = rng.standard_normal(5000)
+    g = gp.bincount(gp.asarray(k), weights=gp.asarray(w), minlength=100)
+    np.testing.assert_allclose(np.asarray(g), np.bincount(k, weights=w, minlength=100), rtol=1e-12, atol=1e-12)
+    c = gp.bincount(gp.asarray(k.astype(np.int32)), minlength=100)
+    assert np.array_equal(np.asarray(c), np.bincount(k, minlength=100))
+
+
 def test_region_against_eager_oracle(sess):
     rng = np.random.default_rng(7)
     x = gp.asarray(rng.standard_normal((64, 48)))
