@@ -195,9 +195,19 @@ WORKLOADS = {
     "kmeans": dict(
         n=1 << 26, label="f32", desc=f"k-means assignment, 2^26 points x 64 centroids, D={KM_D} (BASELINE configs[4])",
         inputs=lambda n, s: _km_inputs(n, s),
-        program=lambda xp, a: (_wl().kmeans_assign(xp, *a),),
-        elements=lambda n: n, bytes=lambda n: n * (KM_D * 4 + 8) + 64 * KM_D * 4, bound="fp32 issue (no FMA, NumPy order)"),
+        program=lambda xp, a: _km_step(xp, a),
+        elements=lambda n: n, bytes=lambda n: n * (KM_D * 4 + 8) + 64 * KM_D * 4, bound="fp32 issue (no FMA, NumPy order)",
+        sharded=(0,)),
 }
+WORKLOADS["rownorm"]["sharded"] = (0,)
+WORKLOADS["rownorm-y"]["sharded"] = (0,)
+
+
+def _km_step(xp, a):
+    """k-means step on this shard: labels + per-cluster fp64 partial sums and
+    counts (one fused kernel); sharded runs allreduce sums/counts over NCCL."""
+    lab, sums, counts = _wl().kmeans_partials(xp, *a)
+    return (lab, *sums, counts)
 
 _CACHE_IN = {}
 
@@ -298,7 +308,16 @@ def run_grumpy(args, dist):
     gp.set_default_session(sess)
 
     host = make_inputs(args.workload, n, seed=42 + dist.rank)
-    dev = [gp.asarray(x) for x in host]
+    sharded = w.get("sharded", ())
+    if dist.world > 1 and sharded:
+        # leading-axis sharding: this rank's rows are rows [rank*n, (rank+1)*n)
+        # of the global problem; reduction partials are allreduced over NCCL
+        import paper_1901_03771_b200.distributed as D
+        D.init(backend="nccl", session=sess)
+        dev = [D.local_input(x, n * dist.world, dist.rank * n, session=sess) if i in sharded else gp.asarray(x)
+               for i, x in enumerate(host)]
+    else:
+        dev = [gp.asarray(x) for x in host]
     for d in dev:  # upload once (not timed)
         d.node.data.device = rt.upload(d.node.data.host)
 
@@ -387,7 +406,11 @@ def run_grumpy(args, dist):
             dist.barrier()
             rt.sync()
             t0 = time.perf_counter()
-        arrs = [gp.asarray(x) for x in pinned_in]
+        if dist.world > 1 and sharded:
+            arrs = [D.local_input(x, n * dist.world, dist.rank * n, session=sess) if i in sharded else gp.asarray(x)
+                    for i, x in enumerate(pinned_in)]
+        else:
+            arrs = [gp.asarray(x) for x in pinned_in]
         outs = prog(gp, arrs)
         gp.force(*outs)
         for o, dst in zip(outs, pinned_out):
@@ -412,6 +435,7 @@ def run_grumpy(args, dist):
                      "kernel_share_of_step": share, "launches_per_step": len(prof) / args.steps,
                      "algorithmic_bytes_per_launch": alg_bytes, "limiter": w["bound"]},
         "gpu_launches": launches,
+        "collectives_per_step": sess.stats.collectives / max(1, args.warmup + args.steps + 1),
         "cuMemAlloc_in_timed_region": allocs_in_timed,
         "clocks": clk,
         "cold_first_step_s": cold_s,
