@@ -426,10 +426,10 @@ class ValueEmitter:
             lvl = max(lvl, c.level)
             if step == 1:
                 conds.append(f"({rel.c()} >= 0 && {rel.c()} < {length})")
-                q = self.derived_var(c.level, f"min(max({rel.c()}, 0LL), {max(length - 1, 0)}LL)")
+                q = self.derived_var(c.level, f"gr::clampll({rel.c()}, {max(length - 1, 0)}LL)")
             else:
                 conds.append(f"({rel.c()} % {step} == 0 && {rel.c()} / {step} >= 0 && {rel.c()} / {step} < {length})")
-                q = self.derived_var(c.level, f"min(max({rel.c()} / {step}, 0LL), {max(length - 1, 0)}LL)")
+                q = self.derived_var(c.level, f"gr::clampll({rel.c()} / {step}, {max(length - 1, 0)}LL)")
             vcoords.append(Aff.of(q))
         pred = self.emit(lvl, "bool", " && ".join(conds) if conds else "true")
         vv = self.cast(self.value(val, bcast_coords(vcoords, tuple(r[2] for r in region), val.shape)),

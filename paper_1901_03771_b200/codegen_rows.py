@@ -231,7 +231,8 @@ class LoopEmitter(ValueEmitter):
             kept = [c for i, c in enumerate(coords) if i not in axes]
         else:
             kept = list(coords)
-        lvl = max((c.level for c in kept), default=0)
+        # loops need a real scope: reductions at constant coordinates live in the row scope
+        lvl = max(max((c.level for c in kept), default=0), 1)
         return x, kept, lvl
 
     def loop_coords(self, level, dims, trip_unroll=16):
@@ -353,7 +354,7 @@ class LoopEmitter(ValueEmitter):
         else:
             axes = (axis,)
             kept = [c for i, c in enumerate(coords) if i != axis] if keepdims else list(coords)
-        L = max((c.level for c in kept), default=0)
+        L = max(max((c.level for c in kept), default=0), 1)
         n = element_count([So[a] for a in axes])
         if L >= 2 and n > SMALL_RECOMPUTE:
             raise NotFusable(r, f"arg-reduction over {n} points would be recomputed per column")
@@ -380,6 +381,17 @@ class LoopEmitter(ValueEmitter):
 # ---------------------------------------------------------------------------
 # Thread space analysis
 # ---------------------------------------------------------------------------
+
+
+def _blame(region: Region, node: Node) -> Node:
+    """The node the planner should cut: an interior reduction that fixed the
+    row space when possible (roots cannot be cut, only split off)."""
+    root_ids = {r.id for r in region.roots}
+    if node.id in root_ids:
+        inner = [n for n in _reductions(region) if n.id not in root_ids and not is_total(n)]
+        if inner:
+            return inner[0]
+    return node
 
 
 def _reductions(region: Region):
@@ -413,10 +425,10 @@ def thread_space(region: Region):
         Ts = min((p for _, p in prefixes), key=len)
         for r, p in prefixes:
             if p[:len(Ts)] != Ts:
-                raise NotFusable(r, f"keeps {p}, not the row shape {Ts}")
+                raise NotFusable(_blame(region, r), f"keeps {p}, not the row shape {Ts}")
         if not Ts:
             bad = next(r for r, p in prefixes if not p)
-            raise NotFusable(bad, "reduction over the leading axis shares a region with other outputs")
+            raise NotFusable(_blame(region, bad), "reduction over the leading axis shares a region with other outputs")
         virtual = None
     else:
         # maps + totals: rows are the subtrees of NumPy's pairwise tree over the
@@ -519,7 +531,7 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
             em.close(s, saved)
             continue
         if tuple(r.shape[:len(Ts)]) != Ts:
-            raise NotFusable(r, f"root shape {r.shape} does not start with the row shape {Ts}")
+            raise NotFusable(_blame(region, r), f"root shape {r.shape} does not start with the row shape {Ts}")
         cols = r.shape[len(Ts):]
         if element_count(cols) == 1:
             v = em.value(r, row_coords + [Aff.of(0)] * len(cols))
@@ -552,7 +564,7 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
                 glob = f"vo + {bi}"
             else:
                 if tuple(x.shape[:len(Ts)]) != Ts:
-                    raise NotFusable(r, f"total operand {x.shape} does not start with rows {Ts}")
+                    raise NotFusable(_blame(region, r), f"total operand {x.shape} does not start with rows {Ts}")
                 cols = x.shape[len(Ts):]
                 C = element_count(cols)
                 best, bi = _arg_partial(em, x, which, row_coords, None, C, cols)
@@ -576,7 +588,7 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
             part = _chunk_partial(em, x, rop, T, S, sizes)
         else:
             if tuple(x.shape[:len(Ts)]) != Ts:
-                raise NotFusable(r, f"total operand {x.shape} does not start with rows {Ts}")
+                raise NotFusable(_blame(region, r), f"total operand {x.shape} does not start with rows {Ts}")
             cols = x.shape[len(Ts):]
             if element_count(cols) == 1:
                 v = em.cast(em.value(x, row_coords + [Aff.of(0)] * len(cols)), x.dtype, T)

@@ -225,6 +225,9 @@ template <class T> __device__ __forceinline__ bool lxor(T a, T b) { return (a !=
 template <class T> __device__ __forceinline__ bool lnot(T a) { return !(a != T(0)); }
 template <class T> __device__ __forceinline__ T select(bool c, T a, T b) { return c ? a : b; }
 
+// clamp an index into [0, hi] (slice-assign value branch stays in bounds)
+__device__ __forceinline__ long long clampll(long long x, long long hi) { return x < 0 ? 0 : (x > hi ? hi : x); }
+
 // ---- bit-exact constants ----------------------------------------------------
 __device__ __forceinline__ float f32_bits(unsigned u) { return __uint_as_float(u); }
 __device__ __forceinline__ double f64_bits(u64 u) { return __longlong_as_double((i64)u); }

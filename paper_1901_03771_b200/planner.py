@@ -333,8 +333,9 @@ def plan_regions(roots: Sequence[Node], row_fusion=None, check=None) -> List[Pla
     ``.node`` that node becomes a materialization point and planning repeats.
     """
     extra: Set[int] = set()
+    solo: Set[int] = set()
     for _ in range(256):
-        steps = _plan_once(roots, row_fusion, extra, check)
+        steps = _plan_once(roots, row_fusion, extra, check, solo)
         if check is None:
             return steps
         bad = None
@@ -345,17 +346,25 @@ def plan_regions(roots: Sequence[Node], row_fusion=None, check=None) -> List[Pla
                 check(st)
             except Exception as e:  # NotFusable
                 node = getattr(e, "node", None)
-                if node is None or node.id in extra or node.id in {r.id for r in st.roots}:
+                root_ids = {r.id for r in st.roots}
+                if node is None:
                     raise
-                bad = node
+                if node.id in root_ids:
+                    if len(st.roots) == 1 or node.id in solo:
+                        raise
+                    bad = ("solo", node)      # a root that cannot share this kernel
+                elif node.id in extra:
+                    raise
+                else:
+                    bad = ("cut", node)       # an interior node: materialize it
                 break
         if bad is None:
             return steps
-        extra.add(bad.id)
+        (solo if bad[0] == "solo" else extra).add(bad[1].id)
     raise RuntimeError("region planning did not converge")
 
 
-def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check) -> List[PlanStep]:
+def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=frozenset()) -> List[PlanStep]:
     roots = [r for r in dict((r.id, r) for r in roots).values() if not r.is_materialized]
     if not roots:
         return []
@@ -426,10 +435,13 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check) -> Lis
     # 4. merge map cones with the same iteration space that share inputs or interior
     merged: List[PlanStep] = []
     for c in cones:
-        if c.kind == "Fused" and c.kernel_kind == "Map":
+        if c.kind == "Fused" and c.kernel_kind == "Map" and c.root.id not in solo:
             for m in merged:
                 if (m.kind == "Fused" and m.kernel_kind == "Map" and m.root.shape == c.root.shape
-                        and _shares(m, c) and not _depends(m, c) and not _depends(c, m)):
+                        and not any(r.id in solo for r in m.roots)
+                        and _shares(m, c) and not _depends(m, c) and not _depends(c, m)
+                        and not _cyclic([s for s in merged if s is not m] + [_merged_copy(m, c)]
+                                        + [s for s in cones if s is not c and s not in merged])):
                     _merge_into(m, c)
                     break
             else:
@@ -444,16 +456,19 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check) -> Lis
         while changed:
             changed = False
             for a in list(merged):
-                if a.kind != "Fused" or a.kernel_kind != "MapReduce":
+                if a.kind != "Fused" or a.kernel_kind != "MapReduce" or any(r.id in solo for r in a.roots):
                     continue
                 for b in merged:
-                    if b is a or b.kind != "Fused":
+                    if b is a or b.kind != "Fused" or any(r.id in solo for r in b.roots):
                         continue
                     if not (_depends(a, b) or (_shares(a, b) and not _depends(b, a))):
                         continue
                     if _depends(b, a):
                         continue
                     trial = _merged_copy(b, a)
+                    others = [s for s in merged if s is not a and s is not b]
+                    if _cyclic(others + [trial]):
+                        continue
                     try:
                         check(trial)
                     except Exception:
@@ -490,6 +505,34 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check) -> Lis
     for i, s in enumerate(out):
         s.order_index = i
     return out
+
+
+def _cyclic(steps: List[PlanStep]) -> bool:
+    """True if the steps' leaf -> producing-step dependencies contain a cycle."""
+    produced = {}
+    for i, s in enumerate(steps):
+        for r in s.roots:
+            produced[r.id] = i
+    deps = [{produced[l.id] for l in s.leaves if l.id in produced and produced[l.id] != i}
+            for i, s in enumerate(steps)]
+    state = [0] * len(steps)
+    for start in range(len(steps)):
+        if state[start]:
+            continue
+        stack = [(start, iter(deps[start]))]
+        state[start] = 1
+        while stack:
+            i, it = stack[-1]
+            j = next(it, None)
+            if j is None:
+                state[i] = 2
+                stack.pop()
+            elif state[j] == 1:
+                return True
+            elif state[j] == 0:
+                state[j] = 1
+                stack.append((j, iter(deps[j])))
+    return False
 
 
 def _shares(a: PlanStep, b: PlanStep) -> bool:

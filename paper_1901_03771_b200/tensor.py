@@ -231,7 +231,7 @@ class TensorBuffer:
     def from_numpy(cls, arr) -> "TensorBuffer":
         arr = np.asarray(arr)
         dt = dtype_of(arr.dtype)
-        arr = np.ascontiguousarray(arr, dtype=dt.np)
+        arr = np.asarray(arr, dtype=dt.np, order="C")   # keeps rank 0 (ascontiguousarray would not)
         return cls(dt, arr.shape, host=arr)
 
     def __repr__(self):

@@ -1,0 +1,168 @@
+"""fusion-planner: Algorithm 1 golden plans and region-pass
+invariants checked with a plan simulator (CPU only)."""
+import numpy as np
+import pytest
+
+import paper_1901_03771_b200 as gp
+from paper_1901_03771_b200 import codegen, planner, workloads as wl
+from paper_1901_03771_b200.dag import OpKind
+from paper_1901_03771_b200.planner import PlannerLimits, demand_set, materialize_node, materialize_pred_of_node, plan
+
+
+@pytest.fixture
+def sess():
+    s = gp.Session()
+    old = gp.set_default_session(s)
+    yield s
+    gp.set_default_session(old)
+
+
+def describe(steps):
+    out = []
+    for s in steps:
+        if s.kind == "Library":
+            out.append(("Library", s.call, s.trans_flags, s.root.id, frozenset(l.id for l in s.leaves)))
+        else:
+            out.append(("Fused", s.kernel_kind, s.root.id, frozenset(l.id for l in s.leaves)))
+    return out
+
+
+def simulate(steps, roots):
+    """Plan simulator: at each step, the leaves and only the
+    leaves are materialized; every root ends materialized."""
+    done = set()
+    for st in steps:
+        for l in st.leaves:
+            assert l.is_materialized or l.id in done, f"leaf {l.id} not ready before step {st.describe()}"
+        interior = {n.id for n in st.nodes}
+        for l in st.leaves:
+            assert l.id not in interior
+        for r in st.roots:
+            done.add(r.id)
+    for r in roots:
+        assert r.is_materialized or r.id in done
+
+
+def test_golden_mnist_pattern(sess):
+    """3 steps — Fused(Map) max, Library(Gemv, transA), Fused(Map) output."""
+    W = gp.asarray(np.ones((784, 10)))
+    x = gp.asarray(np.ones(784))
+    b = gp.asarray(np.ones(10))
+    m = gp.maximum(x, 0.0)
+    mv = W.T @ m
+    out = mv + b
+    steps = plan(out.node)
+    d = describe(steps)
+    assert d == [
+        ("Fused", "Map", m.node.id, frozenset({x.node.id})),
+        ("Library", "Gemv", (True, False), mv.node.id, frozenset({W.node.id, m.node.id})),
+        ("Fused", "Map", out.node.id, frozenset({mv.node.id, b.node.id})),
+    ]
+    simulate(steps, [out.node])
+
+
+def test_golden_listing1_one_step(sess):
+    """the pointwise DAG of Fig. 1 is one Fused(Map) step."""
+    W, a, b = (gp.asarray(np.ones(16)) for _ in range(3))
+    out = wl.listing1(gp, W, a, b)
+    steps = plan(out.node)
+    assert describe(steps) == [("Fused", "Map", out.node.id, frozenset({W.node.id, a.node.id, b.node.id}))]
+
+
+def test_golden_shared_exp_sum_add(sess):
+    """v=exp(x); s=sum(v); out=s+v → 3 steps (multiple-use rule)."""
+    x = gp.asarray(np.ones(8))
+    v = gp.exp(x)
+    s = v.sum()
+    out = s + v
+    steps = plan(out.node)
+    assert describe(steps) == [
+        ("Fused", "Map", v.node.id, frozenset({x.node.id})),
+        ("Fused", "MapReduce", s.node.id, frozenset({v.node.id})),
+        ("Fused", "Map", out.node.id, frozenset({s.node.id, v.node.id})),
+    ]
+    simulate(steps, [out.node])
+
+
+def test_plan_examples(sess):
+    x = gp.asarray(np.ones(4))
+    assert plan(x.node) == []
+    y = x
+    for _ in range(150):
+        y = gp.exp(y)
+    steps = plan(y.node, limits=PlannerLimits(100))
+    assert [s.kind for s in steps] == ["Fused", "Fused"]
+    assert all(len(s.nodes) <= 100 for s in steps)
+    simulate(steps, [y.node])
+
+
+def test_predicates(sess):
+    """SPEC.md:220-231."""
+    x = gp.asarray(np.ones((3, 3)))
+    assert materialize_node(x.sum().node)
+    assert not materialize_node((x + 1).node)
+    assert materialize_node((x @ x).node)
+    mv = x.T @ gp.asarray(np.ones(3))
+    assert not materialize_pred_of_node(mv.node, mv.node.preds[0])    # absorbed transpose
+    mm = gp.maximum(x, 0) @ x
+    assert materialize_pred_of_node(mm.node, mm.node.preds[0])
+    a = x + 1
+    assert not materialize_pred_of_node(a.node, a.node.preds[0])
+
+
+def test_demand_set(sess):
+    """SPEC.md:211-213."""
+    x = gp.asarray(np.ones(4))
+    e = gp.exp(x)
+    out = e + 1
+    ids = {n.id for n in demand_set(out.node)}
+    assert x.node.id in ids and e.node.id in ids and out.node.id in ids
+    assert {n.id for n in demand_set(x.node)} == {x.node.id}
+
+
+def region_plan(roots):
+    return planner.plan_regions([r.node for r in roots], row_fusion=codegen.row_fusable, check=codegen.check_step)
+
+
+def test_region_pass_fuses_configs(sess):
+    S, X, T = (gp.asarray(v) for v in wl.blackscholes_inputs(n=64))
+    c, p = wl.blackscholes(gp, S, X, T)
+    steps = region_plan([c, p])
+    assert len(steps) == 1 and len(steps[0].roots) == 2          # one multi-root kernel
+    (x,) = (gp.asarray(v) for v in wl.rownorm_inputs(rows=8, cols=256))
+    y, tot = wl.rownorm(gp, x)
+    steps = region_plan([y, tot])
+    assert len(steps) == 1                                      # Algorithm 1 would use 4
+    assert len(plan(tot.node)) >= 4
+    Xm, W1, b1, W2, b2 = (gp.asarray(v) for v in wl.mlp_inputs(batch=32, hidden=16))
+    pr, lab = wl.mlp(gp, Xm, W1, b1, W2, b2)
+    steps = region_plan([pr, lab])
+    kinds = [s.kind for s in steps]
+    assert kinds == ["Library", "Fused", "Library", "Fused"]    # GEMM, bias+ReLU, GEMM, softmax+argmax
+    simulate(steps, [pr.node, lab.node])
+    P, C = (gp.asarray(v) for v in wl.kmeans_inputs(n=256, k=8, d=4))
+    l, sums, counts = wl.kmeans_partials(gp, P, C)
+    steps = region_plan([l, *sums, counts])
+    assert len(steps) == 1
+
+
+def test_region_pass_cuts_nonlocal_reductions(sess):
+    x = gp.asarray(np.ones((16, 8)))
+    out = x - x.sum(0)               # column sums broadcast over rows: cut
+    steps = region_plan([out])
+    assert len(steps) == 2
+    simulate(steps, [out.node])
+    out2 = x - x.mean()              # full reduction consumed per element: cut
+    steps = region_plan([out2])
+    assert len(steps) == 2
+    simulate(steps, [out2.node])
+
+
+def test_plan_cache_reuses_structure(sess):
+    from paper_1901_03771_b200.planner import dag_signature
+    a = gp.asarray(np.ones(4))
+    b = gp.asarray(np.ones(4))
+    k1, _ = dag_signature([(a * b + 1).node])
+    k2, _ = dag_signature([(a * b + 1).node])
+    k3, _ = dag_signature([(a * a + 1).node])
+    assert k1 == k2 and k1 != k3
