@@ -37,6 +37,8 @@ def make_program(seed):
         pool.append(gp.asarray(np.asarray(a, dtype=dt)))
     depth = int(rng.integers(1, 13))
     cur = pool[0]
+    transcendental = False   # exp is ulp-accurate, not bit-exact: no branching on it afterwards
+    viewed = False
     for _ in range(depth):
         k = rng.integers(0, 11)
         other = pool[int(rng.integers(0, len(pool)))]
@@ -49,17 +51,23 @@ def make_program(seed):
                 cur = gp.maximum(cur, other)
             elif k == 3 and cur.dtype.kind == "f":
                 cur = gp.exp(cur * 0.1) + gp.sqrt(gp.abs(cur))
-            elif k == 4:
+                transcendental = True
+            elif k == 4 and not transcendental:
                 cur = gp.where(cur > other, cur, other * 2)
             elif k == 5 and cur.ndim >= 2:
                 cur = cur.transpose()
+                viewed = True
             elif k == 6 and cur.ndim >= 1 and cur.shape[-1] > 2:
                 cur = cur[..., 1:] if rng.random() < 0.5 else cur[..., ::2]
+                viewed = True
             elif k == 7 and cur.ndim >= 2:
                 cur = cur.reshape(-1, cur.shape[-1])
             elif k == 8 and cur.ndim >= 2:
                 ax = int(rng.integers(0, cur.ndim))
                 cur = cur.sum(axis=ax, keepdims=bool(rng.random() < 0.5))
+                # NumPy reduces a strided view in memory order, the kernel in C
+                # order: same value up to reassociation, so not bit-exact
+                transcendental = transcendental or (viewed and cur.dtype.kind == "f")
             elif k == 9 and cur.ndim >= 1:
                 ax = int(rng.integers(0, cur.ndim))
                 cur = cur.max(axis=ax) if rng.random() < 0.5 else cur.min(axis=ax)
@@ -68,30 +76,34 @@ def make_program(seed):
         except gp.LazyFuseError:
             continue
     finals = [cur]
-    if cur.ndim >= 1 and rng.random() < 0.5:
+    if cur.ndim >= 1 and rng.random() < 0.5 and not transcendental:
         finals.append(cur.argmax(axis=int(rng.integers(0, cur.ndim))))
     if rng.random() < 0.5:
         finals.append(cur.sum())
-    return finals
+    return finals, transcendental
 
 
-def _close(got, exp, dtype):
+def _close(got, exp, dtype, transcendental=False):
     if dtype.kind in "biu":
         return np.array_equal(got, exp)
-    rtol = 1e-5 if dtype == np.float32 else 1e-12
+    # f32 transcendental ancestry carries f32 ulp error into f64 results
+    rtol = 1e-5 if (dtype == np.float32 or transcendental) else 1e-12
     scale = np.max(np.abs(exp)) if exp.size else 0.0
     return np.allclose(got, exp, rtol=rtol, atol=rtol * max(1.0, scale) * 64, equal_nan=True)
 
 
 @pytest.mark.parametrize("seed", range(NPROG))
 def test_random_program(sess, seed):
-    outs = make_program(seed)
+    outs, transcendental = make_program(seed)
     expect = [eager.evaluate(o.node) for o in outs]
     gp.force(*outs)
     for o, e in zip(outs, expect):
         got = np.asarray(o)
         assert got.shape == e.shape and got.dtype == e.dtype
-        assert _close(got, e, e.dtype), (seed, o.node, got, e)
+        assert _close(got, e, e.dtype, transcendental), (seed, o.node, got, e)
+        if not transcendental and e.dtype.kind == "f" and o.node.kind.value == "MapElementwise":
+            # +,-,*,/,sqrt,max and casts are IEEE-exact: bit-identical to NumPy
+            assert np.array_equal(got, e, equal_nan=True), (seed, "not bit-exact", o.node)
 
 
 def test_config_fixtures(sess):
