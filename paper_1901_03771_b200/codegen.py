@@ -24,6 +24,7 @@ values are computed once, not once per point.
 from __future__ import annotations
 
 import math
+import os
 import struct
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -443,7 +444,7 @@ class ValueEmitter:
 # Family K1: flat map
 # ---------------------------------------------------------------------------
 
-HEADER = '#include "gr_ops.cuh"\n#include "gr_mem.cuh"\n'
+HEADER = '#include "gr_ops.cuh"\n#include "gr_mem.cuh"\n#include "gr_pair.cuh"\n'
 
 LEVEL_KERNEL, LEVEL_GROUP, LEVEL_LANE = 0, 1, 2
 
@@ -493,6 +494,124 @@ class MapEmitter(ValueEmitter):
         return self.emit(LEVEL_LANE, T, f"gr::ld<{T}>({ptr} + {off.c()})"), LEVEL_LANE
 
 
+class NotPairable(Exception):
+    pass
+
+
+_PAIR_BIN = {
+    ElemCode.add: "gr::p2::add", ElemCode.sub: "gr::p2::sub", ElemCode.mul: "gr::p2::mul",
+    ElemCode.div: "gr::p2::div", ElemCode.maximum: "gr::p2::maximum", ElemCode.minimum: "gr::p2::minimum",
+    ElemCode.cmp_lt: "gr::p2::lt", ElemCode.cmp_gt: "gr::p2::gt", ElemCode.cmp_le: "gr::p2::le",
+    ElemCode.cmp_ge: "gr::p2::ge", ElemCode.cmp_eq: "gr::p2::eq", ElemCode.cmp_ne: "gr::p2::ne",
+}
+_PAIR_UN = {
+    ElemCode.neg: "gr::p2::neg", ElemCode.abs: "gr::p2::abs_", ElemCode.exp: "gr::p2::exp_",
+    ElemCode.log: "gr::p2::log_", ElemCode.sqrt: "gr::p2::sqrt_", ElemCode.square: "gr::p2::square",
+    ElemCode.erf: "gr::p2::erf_",
+}
+_PAIR_BOOL = {ElemCode.logical_and: "gr::p2::land", ElemCode.logical_or: "gr::p2::lor"}
+
+
+class PairMapEmitter(MapEmitter):
+    """Map emitter whose lane loop walks lane PAIRS (v = 0 .. VEC/2-1) and
+    evaluates f32 lane values as packed ``gr::f2`` (FADD2/FMUL2/FFMA2), bools
+    as ``gr::b2``.  Values hoisted out of the lane loop stay scalar and are
+    splatted once where a lane pair consumes them."""
+
+    def emit(self, level, ctype, expr):
+        if level >= LEVEL_LANE:
+            ctype = {"float": "gr::f2", "bool": "gr::b2"}.get(ctype)
+            if ctype is None:
+                raise NotPairable("non-f32 lane value")
+        return super().emit(level, ctype, expr)
+
+    def splat(self, val, dtype: DType):
+        expr, lvl = val
+        if lvl >= LEVEL_LANE:
+            return val
+        if dtype is DType.f32:
+            key = ("splat", expr)
+            hit = self.const_memo.get(key)
+            if hit is None:
+                hit = MapEmitter.emit(self, lvl, "gr::f2", f"gr::splat({expr})")
+                if lvl == 0:
+                    self.const_memo[key] = hit
+            return hit, LEVEL_LANE
+        if dtype is DType.bool8:
+            return f"gr::b2{{{expr}, {expr}}}", LEVEL_LANE
+        raise NotPairable("splat of non-f32")
+
+    def cast(self, val, frm: DType, to: DType):
+        if frm is to:
+            return val
+        if val[1] >= LEVEL_LANE:
+            raise NotPairable("cast inside the lane loop")
+        return super().cast(val, frm, to)
+
+    def _value(self, n: Node, coords):
+        if n.id not in self.leaf_index and n.op.kind is OpKind.MAP and n.op.code is not ElemCode.const_splat:
+            code = n.op.code
+            args = []
+            for p, lt in zip(n.preds, n.loop):
+                v = self.value(p, bcast_coords(coords, n.shape, p.shape))
+                args.append((self.cast(v, p.dtype, lt), lt))
+            lvl = max(a[0][1] for a in args)
+            if lvl < LEVEL_LANE:
+                return super()._value(n, coords)
+            if any(lt not in (DType.f32, DType.bool8) for _, lt in args) or n.dtype not in (DType.f32, DType.bool8):
+                raise NotPairable(f"{code} on {n.loop}")
+            names = [self.splat(a, lt)[0] for a, lt in args]
+            if code is ElemCode.select:
+                expr = f"gr::p2::select({names[0]}, {names[1]}, {names[2]})"
+            elif code in _PAIR_BIN and n.loop[0] is DType.f32:
+                expr = f"{_PAIR_BIN[code]}({names[0]}, {names[1]})"
+            elif code in _PAIR_UN and n.loop[0] is DType.f32:
+                expr = f"{_PAIR_UN[code]}({names[0]})"
+            elif code in _PAIR_BOOL and n.loop[0] is DType.bool8:
+                expr = f"{_PAIR_BOOL[code]}({names[0]}, {names[1]})"
+            elif code is ElemCode.logical_not and n.loop[0] is DType.bool8:
+                expr = f"gr::p2::lnot({names[0]})"
+            else:
+                raise NotPairable(f"no packed form for {code}")
+            return self.emit(LEVEL_LANE, n.dtype.ctype, expr), LEVEL_LANE
+        if n.id not in self.leaf_index and n.op.kind not in (OpKind.MAP, OpKind.TRANSPOSE, OpKind.BROADCAST,
+                                                             OpKind.SLICE, OpKind.RESHAPE, OpKind.CAST):
+            raise NotPairable(f"{n.op!r}")
+        return super()._value(n, coords)
+
+    def derived_var(self, level, expr):
+        if level >= LEVEL_LANE:
+            raise NotPairable("per-lane index arithmetic")
+        return super().derived_var(level, expr)
+
+    def load_leaf(self, leaf: Node, off: Aff):
+        idx = self.leaf_index[leaf.id]
+        T = leaf.dtype.ctype
+        lvl = off.level
+        if lvl < LEVEL_LANE:
+            return super().load_leaf(leaf, off)
+        if leaf.dtype not in (DType.f32, DType.bool8):
+            raise NotPairable("non-f32 leaf in the lane loop")
+        lane = self.lane_var
+        cv = off.coef(lane)
+        rest = off.without(lane)
+        if cv == 1 and rest.level < LEVEL_LANE and rest.alignment() % self.vec == 0:
+            name = self.fresh("L")
+            self.group_decls.append(f"{T} {name}[N][{self.vec}];")
+            self.group_lines.append(f"gr::ldv<{T}, {self.vec}>({name}[u], p.in{idx} + {rest.c()});")
+            if leaf.dtype is DType.f32:
+                return f"gr::pk({name}[u][2 * v], {name}[u][2 * v + 1])", LEVEL_LANE
+            return f"gr::b2{{{name}[u][2 * v], {name}[u][2 * v + 1]}}", LEVEL_LANE
+        # gather: lane 2v and 2v+1 (the lane variable counts pairs)
+        o0 = rest + Aff.of(lane).scale(2 * cv)
+        o1 = o0 + cv
+        a = f"gr::ld<{T}>(p.in{idx} + {o0.c()})"
+        b = f"gr::ld<{T}>(p.in{idx} + {o1.c()})"
+        if leaf.dtype is DType.f32:
+            return self.emit(LEVEL_LANE, T, f"gr::pk({a}, {b})"), LEVEL_LANE
+        return self.emit(LEVEL_LANE, T, f"gr::b2{{{a}, {b}}}"), LEVEL_LANE
+
+
 def _index_ctype(region: Region) -> str:
     big = max([element_count(r.shape) for r in region.roots] + [element_count(l.shape) for l in region.leaves])
     return "long long" if big >= 2**31 - 64 else "int"
@@ -529,9 +648,10 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
         unroll = 2 if max(r.dtype.itemsize for r in region.roots) >= 8 else 1
     rank = len(shape)
 
-    def build(mode):
+    def build(mode, pair=False):
         lane = Var("v", LEVEL_LANE)
-        em = MapEmitter(region, vec if mode == "group" else 1, None, lane)
+        cls = PairMapEmitter if pair else MapEmitter
+        em = cls(region, vec if mode == "group" else 1, None, lane)
         coords: List[Aff] = []
         if rank == 0:
             lin0 = Aff.of(0)
@@ -568,8 +688,17 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
             outs.append(val)
         return em, outs
 
-    # ---- group body (vectorised)
-    em, outs = build("group")
+    # ---- group body (vectorised); f32 regions evaluate lane pairs packed
+    pair = False
+    if vec % 2 == 0 and os.environ.get("GRUMPY_PAIR", "1") != "0":
+        try:
+            em, outs = build("group", pair=True)
+            pair = True
+        except NotPairable:
+            pair = False
+    if not pair:
+        em, outs = build("group")
+    nl = vec // 2 if pair else vec
     lines = []
     lines.append("template <int N> static __device__ __forceinline__ void group(const Params& p, long long g0, long long stride) {")
     for d in em.group_decls:
@@ -586,11 +715,19 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
     for ri, r in enumerate(region.roots):
         lines.append(f"    {r.dtype.ctype} o{ri}[{vec}];")
     lines.append("#pragma unroll")
-    lines.append(f"    for (int v = 0; v < {vec}; ++v) {{")
+    lines.append(f"    for (int v = 0; v < {nl}; ++v) {{")
     for l in em.lane_lines:
         lines.append("      " + l)
     for ri, (r, (expr, _lvl)) in enumerate(zip(region.roots, outs)):
-        lines.append(f"      o{ri}[v] = {expr};")
+        if not pair:
+            lines.append(f"      o{ri}[v] = {expr};")
+            continue
+        if _lvl < LEVEL_LANE:
+            lines.append(f"      o{ri}[2 * v] = {expr}; o{ri}[2 * v + 1] = {expr};")
+        elif r.dtype is DType.f32:
+            lines.append(f"      o{ri}[2 * v] = gr::lo({expr}); o{ri}[2 * v + 1] = gr::hi({expr});")
+        else:
+            lines.append(f"      o{ri}[2 * v] = ({expr}).lo; o{ri}[2 * v + 1] = ({expr}).hi;")
     lines.append("    }")
     for ri, r in enumerate(region.roots):
         T = r.dtype.ctype
