@@ -8,6 +8,51 @@
 #include "gr_ops.cuh"
 #include "gr_mem.cuh"
 #include "gr_map.cuh"
+#include "gr_reduce.cuh"
+#include "gr_tma.cuh"
+#include "gr_pair.cuh"
+
+// reductions, packed pairs, bulk copies: one instantiation each
+extern "C" __global__ void aot_reduce(const float* x, float* o, unsigned* ticket, long long* oi) {
+  auto f = [&](long long i) -> float { return x[i]; };
+  float s = gr::pairwise<float, 4096>(f, 0) + gr::pairwise<float, 1000>(f, 0);
+  float acc[4] = {x[0], x[1], x[2], x[3]};
+  __shared__ float sh[8];
+  s += gr::row_sum<float, 4, 2, 64>(acc, sh, 0) + gr::row_tree<gr::OpMax, float, 64>(s, sh, 0);
+  float ls[4] = {s, s, s, s};
+  s += gr::lane_tree<gr::OpSum, float, 4>(ls) + gr::warp_tree<gr::OpSum, float>(s, 8);
+  long long bi = gr::warp_arg<true, float>(s, threadIdx.x, 32);
+  if (gr::last_block(ticket)) {
+    o[0] = gr::block_tree<gr::OpSum, float>(o + 1, 1000, 0.0f);
+    oi[0] = gr::block_arg<true, float>(o + 1, oi + 1, 1000) + bi;
+  }
+  const gr::DivShared<float> d = gr::div_prep<float>(s);
+  o[threadIdx.x + 2000] = gr::div_shared<float>(x[threadIdx.x], d);
+}
+
+extern "C" __global__ void aot_pair(const float4* x, float4* o) {
+  const float4 a = x[threadIdx.x];
+  const gr::f2 p = gr::pk(a.x, a.y), q = gr::pk(a.z, a.w);
+  const gr::f2 r = gr::p2::add(gr::p2::exp_(p), gr::p2::mul(gr::p2::log_(q), gr::p2::erf_(gr::p2::div(p, q))));
+  o[threadIdx.x] = make_float4(gr::lo(r), gr::hi(r), gr::lo(gr::p2::sqrt_(q)), gr::hi(gr::p2::select(gr::p2::lt(p, q), p, q)));
+}
+
+extern "C" __global__ void aot_bulk(const float* x, float* o) {
+  __shared__ __align__(128) float buf[128];
+  __shared__ unsigned long long bar;
+  if (threadIdx.x == 0) {
+    gr::mbar_init(&bar, 1);
+    gr::fence_mbar_init();
+    gr::mbar_arrive_expect_tx(&bar, 512);
+    gr::bulk_g2s(buf, x, 512, &bar);
+    gr::prefetch_l2(x + 128, 512);
+  }
+  __syncthreads();
+  gr::mbar_wait(&bar, 0);
+  float v[8];
+  gr::lds8<float>(v, buf + 8 * (threadIdx.x % 16));
+  gr::st8<float>(o + 8 * threadIdx.x, v);
+}
 
 
 template <class T> __device__ T all_ops(T a, T b, bool c) {
