@@ -366,6 +366,49 @@ __device__ __forceinline__ long long row_arg(T best, long long bi, T* shv, long 
   return bi;
 }
 
+// ---- single-pass scan with decoupled look-back (codegen_scan.py) -------------
+// Tile t publishes (flag, value): flag 1 = tile aggregate, 2 = inclusive prefix.
+// Tile ids come from an atomic counter so earlier tiles are always scheduled
+// first (forward progress); the look-back folds predecessors right to left.
+template <class T> struct ScanState {
+  unsigned long long* flags;   // per tile: 0 empty, 1 aggregate, 2 inclusive
+  T* agg;
+  T* inc;
+};
+
+template <class Op, class T>
+__device__ __forceinline__ T scan_lookback(const ScanState<T>& st, long long tile, T tile_agg) {
+  // called by one thread; returns the exclusive prefix of `tile`
+  if (tile == 0) {
+    st.inc[0] = tile_agg;
+    __threadfence();
+    atomicExch(&st.flags[0], 2ull);
+    return T(0);
+  }
+  st.agg[tile] = tile_agg;
+  __threadfence();
+  atomicExch(&st.flags[tile], 1ull);
+  T excl;
+  bool have = false;
+  long long p = tile - 1;
+  while (true) {
+    unsigned long long f;
+    do {
+      f = atomicAdd(&st.flags[p], 0ull);
+    } while (f == 0ull);
+    __threadfence();
+    const T v = (f == 2ull) ? st.inc[p] : st.agg[p];
+    excl = have ? Op::template c<T>(v, excl) : v;
+    have = true;
+    if (f == 2ull) break;
+    --p;
+  }
+  st.inc[tile] = Op::template c<T>(excl, tile_agg);
+  __threadfence();
+  atomicExch(&st.flags[tile], 2ull);
+  return excl;
+}
+
 // Grid completion ticket: returns true in exactly one (the last) block, after
 // every block's partials are visible.  The ticket self-resets for the next
 // launch of the same kernel (stream order serialises launches).

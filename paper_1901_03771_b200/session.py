@@ -626,8 +626,9 @@ class ndarray:
                 if name.startswith("logical") and x._node.dtype is not DType.bool8:
                     x = x.astype(np.bool_)
                 return _reduce(x, rop, kwargs.get("axis", 0), kwargs.get("dtype"), kwargs.get("keepdims", False))
-        if method == "accumulate" and name in ("add", "multiply") and set(kwargs) <= {"axis", "dtype"}:
-            rop = ReduceOp.sum if name == "add" else ReduceOp.prod
+        if method == "accumulate" and name in ("add", "multiply", "maximum", "minimum") and set(kwargs) <= {"axis", "dtype"}:
+            rop = {"add": ReduceOp.sum, "multiply": ReduceOp.prod, "maximum": ReduceOp.max,
+                   "minimum": ReduceOp.min}[name]
             return _scan(_as_array(inputs[0]), rop, kwargs.get("axis", 0), kwargs.get("dtype"))
         return _fallback(getattr(ufunc, method), inputs, kwargs)
 

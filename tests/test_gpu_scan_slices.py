@@ -1,0 +1,59 @@
+"""GPU parity for map-scan kernels and slice / slice-assign
+regions (the Jacobi sweep)."""
+import numpy as np
+import pytest
+
+import paper_1901_03771_b200 as gp
+
+pytestmark = pytest.mark.gpu
+
+
+def test_scan_kats(sess):
+    """SPEC.md:388-390."""
+    assert np.asarray(gp.asarray(np.array([1, 2, 3])).cumsum()).tolist() == [1, 3, 6]
+    assert np.asarray(gp.asarray(np.zeros(4)).cumsum()).tolist() == [0, 0, 0, 0]
+    assert np.asarray(np.maximum.accumulate(gp.asarray(np.array([3, 1, 4, 1, 5])))).tolist() == [3, 3, 4, 4, 5]
+
+
+@pytest.mark.parametrize("shape,axis", [((300, 50), 0), ((30, 500), 1), ((7, 9, 11), 1), ((3, 4, 5), None)])
+def test_scan_lines_exact(sess, shape, axis):
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(shape)
+    g = (gp.asarray(x) * 2 + 1).cumsum(axis=axis)
+    assert np.array_equal(np.asarray(g), (x * 2 + 1).cumsum(axis=axis))   # sequential fold = NumPy
+
+
+@pytest.mark.parametrize("n", [8193, 100000, 1 << 22])
+def test_scan_lookback(sess, n):
+    rng = np.random.default_rng(6)
+    xi = rng.integers(-100, 100, n)
+    assert np.array_equal(np.asarray(gp.asarray(xi).cumsum()), xi.cumsum())          # integers exact
+    xf = rng.standard_normal(n)
+    got = np.asarray(gp.exp(gp.asarray(xf) * 0.1).cumsum())
+    ref = np.exp(xf * 0.1).cumsum()
+    # reassociated fp64 prefix sums: |err| <= n * eps * sum|x|
+    assert np.max(np.abs(got - ref)) <= 4 * np.log2(n) * 2.2e-16 * np.abs(np.exp(xf * 0.1)).sum()
+    m = np.asarray(np.maximum.accumulate(gp.asarray(xf)))
+    assert np.array_equal(m, np.maximum.accumulate(xf))
+
+
+def test_jacobi_sweep_one_kernel(sess):
+    """one slice-assign sweep is exactly one fused map kernel."""
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((66, 66))
+    b = rng.standard_normal((66, 66))
+    ga, gb = gp.asarray(a), gp.asarray(b)
+    gb[1:-1, 1:-1] = 0.2 * (ga[1:-1, 1:-1] + ga[1:-1, :-2] + ga[1:-1, 2:] + ga[:-2, 1:-1] + ga[2:, 1:-1])
+    k0 = sess.stats.kernels_executed
+    got = np.asarray(gb)
+    assert sess.stats.kernels_executed - k0 == 1
+    b[1:-1, 1:-1] = 0.2 * (a[1:-1, 1:-1] + a[1:-1, :-2] + a[1:-1, 2:] + a[:-2, 1:-1] + a[2:, 1:-1])
+    assert np.array_equal(got, b)
+
+
+def test_views_strided(sess):
+    rng = np.random.default_rng(8)
+    t = rng.standard_normal((8, 6, 4)).astype(np.float32)
+    g = gp.asarray(t).transpose(2, 0, 1).reshape(4, 48)[:, ::3] * 2 + gp.asarray(t)[::-1, 0, :].T.sum(1)[:, None]
+    e = t.transpose(2, 0, 1).reshape(4, 48)[:, ::3] * 2 + t[::-1, 0, :].T.sum(1)[:, None]
+    np.testing.assert_allclose(np.asarray(g), e, rtol=1e-6)
