@@ -31,8 +31,13 @@ def test_scan_lookback(sess, n):
     xf = rng.standard_normal(n)
     got = np.asarray(gp.exp(gp.asarray(xf) * 0.1).cumsum())
     ref = np.exp(xf * 0.1).cumsum()
-    # reassociated fp64 prefix sums: |err| <= n * eps * sum|x|
-    assert np.max(np.abs(got - ref)) <= 4 * np.log2(n) * 2.2e-16 * np.abs(np.exp(xf * 0.1)).sum()
+    # reassociated fp64 prefix sums: measured against an extended-precision
+    # prefix, the look-back scan must be no less accurate than NumPy's own
+    # sequential fold (within 2x, plus one ulp of the running total)
+    exact = np.cumsum(np.exp(xf * 0.1).astype(np.longdouble))
+    err_ref = float(np.max(np.abs(ref - exact)))
+    err_got = float(np.max(np.abs(got - exact)))
+    assert err_got <= 2 * err_ref + 2.2e-16 * float(exact[-1])
     m = np.asarray(np.maximum.accumulate(gp.asarray(xf)))
     assert np.array_equal(m, np.maximum.accumulate(xf))
 
@@ -56,4 +61,11 @@ def test_views_strided(sess):
     t = rng.standard_normal((8, 6, 4)).astype(np.float32)
     g = gp.asarray(t).transpose(2, 0, 1).reshape(4, 48)[:, ::3] * 2 + gp.asarray(t)[::-1, 0, :].T.sum(1)[:, None]
     e = t.transpose(2, 0, 1).reshape(4, 48)[:, ::3] * 2 + t[::-1, 0, :].T.sum(1)[:, None]
-    np.testing.assert_allclose(np.asarray(g), e, rtol=1e-6)
+    # the strided views themselves are exact (gathers); the f32 sum over a
+    # reversed, non-contiguous axis is summed by NumPy's iterator in MEMORY
+    # order (it flips negative strides), which a logical-order fold does not
+    # reproduce bit-for-bit: f32 tolerance (rel 1e-5)
+    assert np.array_equal(np.asarray(gp.asarray(t).transpose(2, 0, 1).reshape(4, 48)[:, ::3]),
+                          t.transpose(2, 0, 1).reshape(4, 48)[:, ::3])
+    assert np.array_equal(np.asarray(gp.asarray(t)[::-1, 0, :].T), t[::-1, 0, :].T)
+    np.testing.assert_allclose(np.asarray(g), e, rtol=1e-5, atol=1e-6)
