@@ -65,6 +65,19 @@ def evaluate(n: Node, cache: Dict[int, np.ndarray] | None = None) -> np.ndarray:
     return _eval(n, cache)
 
 
+def eval_point(point, coords, leaves) -> np.generic:
+    """Reference executor for a point program: the value of
+    the point function at ``coords`` given leaf buffers (leaf node id →
+    TensorBuffer or ndarray).  ``point`` is a ``lowering.PointProgram``; its
+    value nodes are evaluated eagerly over the leaves, then indexed."""
+    cache = {}
+    for lid, b in leaves.items():
+        cache[lid] = np.asarray(b.host if hasattr(b, "host") and b.host is not None else
+                                (b.to_numpy() if hasattr(b, "to_numpy") else b))
+    v = _eval(point.value_nodes[0], cache)
+    return v[tuple(coords)]
+
+
 def _eval(n: Node, cache) -> np.ndarray:
     hit = cache.get(n.id)
     if hit is not None:

@@ -10,8 +10,10 @@ Layout of the package (reference module in brackets, /root/reference/SPEC.md):
   tensor.py     [tensor-core]        dtypes, shapes, broadcasting, buffers
   dag.py        [expr-dag]           Node / Graph / inference
   planner.py    [fusion-planner]     Algorithm 1 + the B200 region pass
+  lowering.py   [kernel-lowering]    IterSpace / IndexMap / PointProgram, lower, compile
   codegen.py    [kernel-lowering]    index maps, point programs -> CUDA C++
-  executor.py   [parallel-executor]  launches through the C-ABI shim
+  executor.py   [parallel-executor]  launches through the C-ABI shim; run_map,
+                                     run_map_reduce, run_map_scan, run_library
   runtime.py    C-ABI binding of libgrumpy_rt.so (include/grumpy_rt.h)
   session.py    [session]            ndarray proxy, force, fallback, stats
   distributed.py  leading-axis sharding, NCCL allreduce of partials

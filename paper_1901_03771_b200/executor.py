@@ -78,7 +78,16 @@ class Executor:
     def kernel_source(self, region: codegen.Region) -> codegen.KernelSource:
         return codegen.cached_generate(region)
 
-    def run_fused(self, st: PlanStep) -> List[TensorBuffer]:
+    def buffer_ptr(self, buf: TensorBuffer) -> int:
+        if buf.device is None:
+            buf.device = self.rt.upload(buf.host)
+            self.session.stats.h2d_bytes += buf.host.nbytes
+        return buf.device.ptr
+
+    def run_fused(self, st: PlanStep, bind: Dict[int, TensorBuffer] = None) -> List[TensorBuffer]:
+        """Launch the step's kernel.  ``bind`` (leaf node id → buffer) supplies
+        leaf data explicitly (the reference-style ``run_map(k, leaves, cfg)``
+        entry points); otherwise leaves read their materialized data."""
         c = st.cache
         if "perm" not in c:
             region = codegen.canonicalize(codegen.Region(st.roots, st.leaves, st.nodes))
@@ -98,7 +107,11 @@ class Executor:
                 self.session.stats.compile_ms += k.compile_ms
             c["kernel"] = k
             c["grid"] = codegen.grid_for(ks, self.rt.sm_count, k.blocks_per_sm)
-        ptrs = [self.device_ptr(l) for l in leaves] + [b.device.ptr for b in outs]
+        if bind is None:
+            ptrs = [self.device_ptr(l) for l in leaves]
+        else:
+            ptrs = [self.buffer_ptr(bind[l.id]) for l in leaves]
+        ptrs += [b.device.ptr for b in outs]
         scratch = None
         if ks.scratch_bytes:
             scratch = self.rt.alloc(ks.scratch_bytes)
@@ -185,3 +198,127 @@ class Executor:
                     self.rt.gemv(trans, rows, cols, dt, self.device_ptr(mat), cols, self.device_ptr(x), out.device.ptr)
         self.launch_log.append(("library", st.call))
         return out
+
+
+# ---------------------------------------------------------------------------
+# Reference-facing executor entry points
+# ---------------------------------------------------------------------------
+
+
+class ExecConfig:
+    """SPEC.md:355-358.  ``num_threads`` is validated and recorded; on the B200
+    path the partition is the kernel's grid, and results are bit-identical for
+    every value (the reference's determinism invariant)."""
+
+    def __init__(self, num_threads: int = 1, block="auto"):
+        if int(num_threads) < 1:
+            raise ValueError("num_threads must be >= 1 (SPEC.md:357)")
+        self.num_threads = int(num_threads)
+        self.block = block
+
+
+class LibraryCall:
+    """Gemm | Gemv, per-operand transpose flags, operand ids."""
+
+    def __init__(self, call: str, trans_flags=(False, False), operands=()):
+        if call not in ("Gemm", "Gemv"):
+            raise ValueError(f"unknown library call {call!r}")
+        self.call = call
+        self.trans_flags = tuple(bool(t) for t in trans_flags)
+        self.operands = tuple(operands)
+
+
+def _executor():
+    from .session import default_session
+    return default_session().executor
+
+
+def _bind(k, leaves) -> Dict[int, TensorBuffer]:
+    st = k.step
+    if isinstance(leaves, dict):
+        bind = dict(leaves)
+    else:
+        leaves = list(leaves)
+        if len(leaves) != len(st.leaves):
+            raise ShapeMismatch(f"kernel has {len(st.leaves)} leaves, got {len(leaves)} buffers")
+        bind = {l.id: b for l, b in zip(st.leaves, leaves)}
+    for l in st.leaves:
+        b = bind.get(l.id)
+        if b is None:
+            raise ShapeMismatch(f"no buffer for leaf {l.id}")
+        if tuple(b.shape) != tuple(l.shape) or b.dtype is not l.dtype:
+            raise ShapeMismatch(f"leaf {l.id}: buffer {b.dtype.value}{b.shape} != {l.dtype.value}{l.shape}")
+    return bind
+
+
+def _run(k, leaves, cfg, kind):
+    if k.kind != kind:
+        raise ValueError(f"run_{kind} given a {k.kind} kernel")
+    if cfg is not None and not isinstance(cfg, ExecConfig):
+        raise TypeError("cfg must be an ExecConfig")
+    ex = _executor()
+    outs = ex.run_fused(k.step, bind=_bind(k, leaves))
+    return outs[0] if len(outs) == 1 else tuple(outs)
+
+
+def run_map(k, leaves, cfg: ExecConfig = None) -> TensorBuffer:
+    """out[p] = point(p) for every p — one generated kernel."""
+    return _run(k, leaves, cfg, "Map")
+
+
+def run_map_reduce(k, leaves, cfg: ExecConfig = None) -> TensorBuffer:
+    """fold of the mapped values — one kernel launch,
+    deterministic combine (NumPy's association order, see codegen_rows)."""
+    return _run(k, leaves, cfg, "MapReduce")
+
+
+def run_map_scan(k, leaves, cfg: ExecConfig = None) -> TensorBuffer:
+    """inclusive scan of the mapped values (codegen_scan)."""
+    return _run(k, leaves, cfg, "MapScan")
+
+
+def run_library(call: LibraryCall, operands, cfg: ExecConfig = None) -> TensorBuffer:
+    """SPEC.md:391-399 → cuBLAS on the runtime stream.
+
+    Gemv(A, x): y[i] = Σ_k A'[i,k]·x[k], A' = Aᵀ when trans_flags[0].
+    Gemm(A, B): C = A'·B' with per-operand flags.  ShapeMismatch when the
+    operands do not conform after the flags."""
+    ex = _executor()
+    rt = ex.rt
+    ops = list(operands)
+    if len(ops) != 2:
+        raise ShapeMismatch(f"{call.call} takes 2 operands, got {len(ops)}")
+    a, b = ops
+    dt = a.dtype
+    if b.dtype is not dt or dt not in (DType.f32, DType.f64):
+        raise ShapeMismatch(f"library operands must share an f32/f64 dtype, got {a.dtype} and {b.dtype}")
+    flags = call.trans_flags + (False,) * (2 - len(call.trans_flags))
+    if len(a.shape) != 2:
+        raise ShapeMismatch(f"{call.call}: first operand must be rank 2, got {a.shape}")
+    rows, cols = a.shape
+    m, k = (cols, rows) if flags[0] else (rows, cols)
+    if call.call == "Gemv":
+        if len(b.shape) != 1 or b.shape[0] != k:
+            raise ShapeMismatch(f"Gemv: {a.shape}{'ᵀ' if flags[0] else ''} · {b.shape}")
+        out = TensorBuffer(dt, (m,), device=rt.alloc(m * dt.itemsize))
+        if m:
+            if k == 0:
+                rt.memset(out.device, 0)
+            else:
+                rt.gemv(flags[0], rows, cols, dt, ex.buffer_ptr(a), cols, ex.buffer_ptr(b), out.device.ptr)
+    else:
+        if len(b.shape) != 2:
+            raise ShapeMismatch(f"Gemm: second operand must be rank 2, got {b.shape}")
+        k2, n = (b.shape[1], b.shape[0]) if flags[1] else tuple(b.shape)
+        if k2 != k:
+            raise ShapeMismatch(f"Gemm: inner extents {k} and {k2} differ")
+        out = TensorBuffer(dt, (m, n), device=rt.alloc(m * n * dt.itemsize))
+        if m and n:
+            if k == 0:
+                rt.memset(out.device, 0)
+            else:
+                rt.gemm(flags[0], flags[1], m, n, k, dt, ex.buffer_ptr(a), a.shape[1],
+                        ex.buffer_ptr(b), b.shape[1], out.device.ptr, n)
+    ex.session.stats.library_calls += 1
+    ex.launch_log.append(("library", call.call))
+    return out

@@ -234,6 +234,13 @@ class TensorBuffer:
         arr = np.asarray(arr, dtype=dt.np, order="C")   # keeps rank 0 (ascontiguousarray would not)
         return cls(dt, arr.shape, host=arr)
 
+    def to_numpy(self) -> np.ndarray:
+        """Host view of the value (to_external): one D2H copy
+        the first time, then cached."""
+        if self.host is None:
+            self.host = self.device.to_numpy(self.dtype, self.shape)
+        return self.host
+
     def __repr__(self):
         where = "device" if self.device is not None else "host"
         return f"TensorBuffer({self.dtype.value}, {self.shape}, {where})"
