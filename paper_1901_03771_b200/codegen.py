@@ -243,6 +243,10 @@ class ValueEmitter:
         self.leaf_index = {n.id: i for i, n in enumerate(region.leaves)}
         self.consts: List[str] = []
         self.const_memo: Dict[tuple, str] = {}
+        # families that can redo a work item emit the two-pass division
+        # (gr::div_sh<FAST>) and set this before emission
+        self.div_fast = False
+        self.used_div_fast = False
         # hash-consing: structurally identical nodes (same op over the same
         # operands) share one value — e.g. the two mean computations of
         # (x - x.mean(1)) / x.std(1).  Evaluation is pure, so this is exact.
@@ -324,7 +328,11 @@ class ValueEmitter:
                     r = self.emit(args[1][1], f"gr::DivShared<{T}>", f"gr::div_prep<{T}>({names[1]})")
                     if args[1][1] == 0:
                         self.const_memo[rk] = r
-                expr = f"gr::div_shared<{T}>({names[0]}, {r})"
+                if self.div_fast:
+                    expr = f"gr::div_sh<FAST, {T}>({names[0]}, {r}, bad)"
+                    self.used_div_fast = True
+                else:
+                    expr = f"gr::div_shared<{T}>({names[0]}, {r})"
             elif code in _BIN:
                 T = n.loop[0].ctype
                 expr = _BIN[code].format(T=T) + f"({names[0]}, {names[1]})"

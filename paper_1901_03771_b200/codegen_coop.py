@@ -62,12 +62,37 @@ class CoopEmitter(LoopEmitter):
         self.close(vv[1], vv[2])
         self.close(mm[1], mm[2])
 
-    def prestage(self, leaves, tma_layout=None):
+    def prestage(self, leaves, tma_layout=None, async_layout=None, block=256):
         """Load whole row segments of ``leaves`` into registers up front: from
         the shared-memory stage filled by bulk copies (``tma_layout``: leaf id ->
-        (byte offset of the leaf block, leaf stride in elements, row bytes)) or
-        from global memory."""
+        (byte offset of the leaf block, leaf stride in elements, row bytes)),
+        from the per-thread cp.async stage (``async_layout``: leaf id -> byte
+        offset; the fast pass reads it, then starts the next row group's
+        copies), or from global memory."""
         rowkey = Aff.of(Var("r", 1)).scale(self.C).key()
+        if async_layout is not None:
+            names = []
+            for leaf in leaves:
+                name = self.fresh("S")
+                self.stmt(1, f"{leaf.dtype.ctype} {name}[16][{self.vec}];")
+                names.append(name)
+                self.staged[(leaf.id, rowkey)] = name
+            self.stmt(1, "if constexpr (FAST) {")
+            self.stmt(1, "  gr::cp_async_wait_all();")
+            for leaf, name in zip(leaves, names):
+                T = leaf.dtype.ctype
+                self.stmt(1, f"  #pragma unroll\n    for (int mm = 0; mm < 16; ++mm) gr::ldsv<{T}, {self.vec}>({name}[mm], "
+                             f"reinterpret_cast<const {T}*>(stage + {async_layout[leaf.id]}) + "
+                             f"((long long)mm * {block} + threadIdx.x) * {self.vec});")
+            self.stmt(1, "  if (gnext < NG) copy_group(p, stage, gnext);")
+            self.stmt(1, "} else {")
+            for leaf, name in zip(leaves, names):
+                T = leaf.dtype.ctype
+                idx = self.leaf_index[leaf.id]
+                self.stmt(1, f"  #pragma unroll\n    for (int mm = 0; mm < 16; ++mm) "
+                             f"gr::ldv<{T}, {self.vec}>({name}[mm], p.in{idx} + r * {self.C}LL + cb + 8 * mm);")
+            self.stmt(1, "}")
+            return
         for leaf in leaves:
             name = self.fresh("S")
             T = leaf.dtype.ctype
@@ -237,6 +262,7 @@ def _qualifies(region: Region):
             return None
     sizes = [n.dtype.itemsize for n in region.nodes + region.leaves]
     vec = 4 if max(sizes) <= 4 else 2
+    vec = min(vec, int(os.environ.get("GRUMPY_COOP_VEC", vec)))
     tpr = (C // 128) * (8 // vec)
     if tpr > MAX_TPR:
         return None
@@ -244,6 +270,7 @@ def _qualifies(region: Region):
 
 
 SMEM_PER_CTA = 110 * 1024   # two CTAs per SM keep 16 warps resident
+ASYNC_SMEM_PER_CTA = 72 * 1024   # cp.async stage: three CTAs per SM
 PREFETCH_GROUPS = int(os.environ.get("GRUMPY_PREFETCH_GROUPS", "2"))
 
 
@@ -285,22 +312,35 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
         rowb = (C // 128) * lsb
         layout[l.id] = (off, lsb // l.dtype.itemsize, rowb)
         off += rpc * rowb
-    # measured on B200 (profiles/r01_rownorm_modes.md): plain register staging
-    # 0.312 ms, + L2 bulk prefetch 0.333 ms, smem bulk-copy ring 0.427 ms
+    # measured (profiles/r01_rownorm_modes.md): register staging at 3 CTAs/SM
+    # 0.270 ms; per-thread cp.async stage 0.371 ms (MIO-bound); bulk-copy ring
+    # 0.427 ms; L2 bulk prefetch 0.333 ms
     mode = os.environ.get("GRUMPY_COOP_MODE", "plain")
     tma = layout if (off <= SMEM_PER_CTA and mode == "tma") else None
-    second = _generate(region, q, kname, leaves, tma, smem_bytes=off if tma else 0,
-                       l2_prefetch=(mode == "l2" and tma is None))
+    async_layout = None
+    if mode == "async" and all(vec * l.dtype.itemsize == 16 for l in leaves):
+        async_layout, aoff = {}, 0
+        for l in leaves:
+            async_layout[l.id] = aoff
+            aoff += 16 * block * 16
+        if aoff > ASYNC_SMEM_PER_CTA:
+            async_layout = None
+    if async_layout is not None:
+        second = _generate(region, q, kname, leaves, None, smem_bytes=aoff, async_layout=async_layout)
+    else:
+        second = _generate(region, q, kname, leaves, tma, smem_bytes=off if tma else 0,
+                           l2_prefetch=(mode == "l2" and tma is None))
     return second[0] if second is not None else ks
 
 
-def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch=False):
+def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch=False, async_layout=None):
     Ts, totals, C, vec, tpr = q
     tot_ids = {t.id for t in totals}
     block = max(256, tpr)
     rpc = block // tpr
     R = element_count(Ts)
     em = CoopEmitter(region, vec, tpr, rpc, Ts, C)
+    em.div_fast = tma is None and os.environ.get("GRUMPY_DIV_TWO_PASS", "1") != "0"
     rvar = Var("r", 1)
     if len(Ts) == 1:
         row_coords = [Aff.of(rvar)]
@@ -326,7 +366,7 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
             em.stmt(1, f"if (tr == 0) {{ const long long rp = (rb / {rpc} + {PREFETCH_GROUPS}LL * gridDim.x) * {rpc} + ri; "
                        f"if (rp < NROWS) gr::prefetch_l2(p.in{idx} + rp * {C}LL, {C * isz}u); }}")
     if prestage:
-        em.prestage(prestage, tma)
+        em.prestage(prestage, tma, async_layout, block)
         if tma:
             # the stage is in registers now: release it and start the bulk copy
             # of the next row group, which then overlaps this group's compute
@@ -398,18 +438,38 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
 
     P = 8 // vec
     NG = -(-R // rpc)
-    lines = ["static __device__ __forceinline__ void rows(const Params& p, const long long rb, "
-             "unsigned char* stage, unsigned long long* bar, const long long gnext) {",
+    two_pass = em.used_div_fast
+    templ = two_pass or async_layout is not None
+    lines = [("template <bool FAST> static __device__ __forceinline__ bool rows(" if templ else
+              "static __device__ __forceinline__ void rows(") +
+             "const Params& p, const long long rb, unsigned char* stage, unsigned long long* bar, const long long gnext) {",
              f"  const int tr = threadIdx.x % {tpr};",
              f"  const int ri = threadIdx.x / {tpr};",
              "  const bool valid = rb + ri < NROWS;",
              "  const long long r = valid ? rb + ri : NROWS - 1;",
              f"  const long long cb = (long long)(tr / {P}) * 128 + (tr % {P}) * {vec};",
              "  (void)stage; (void)bar; (void)gnext;"]
+    if templ:
+        lines.append("  bool bad = false;")
     lines += ["  " + c for c in em.consts]
     lines += render(em.row, 1)
+    if templ:
+        lines.append("  return bad;")
     lines.append("}")
     issue = []
+    if async_layout is not None:
+        issue = ["static __device__ __forceinline__ void copy_group(const Params& p, unsigned char* stage, const long long g) {",
+                 f"  const int tr = threadIdx.x % {tpr};",
+                 f"  const int ri = threadIdx.x / {tpr};",
+                 f"  const long long r0 = g * {rpc} + ri;",
+                 "  const long long r = r0 < NROWS ? r0 : NROWS - 1;",
+                 f"  const long long cb = (long long)(tr / {P}) * 128 + (tr % {P}) * {vec};"]
+        for l in prestage:
+            idx = region.leaves.index(l)
+            issue += ["#pragma unroll",
+                      f"  for (int mm = 0; mm < 16; ++mm) gr::cp_async16(stage + {async_layout[l.id]} + "
+                      f"((long long)mm * {block} + threadIdx.x) * 16, p.in{idx} + r * {C}LL + cb + 8 * mm);"]
+        issue += ["  gr::cp_async_commit();", "}"]
     if tma:
         nleaf = C // 128
         total = sum(nleaf * 128 * l.dtype.itemsize for l in prestage)
@@ -447,10 +507,34 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
                 "    gr::mbar_wait(&bar, (unsigned)(it & 1));",
                 f"    K::rows(p, g * {rpc}, smem, &bar, g + gridDim.x);",
                 "  }"]
+    elif async_layout is not None:
+        minb = int(os.environ.get("GRUMPY_COOP_MINBLOCKS", "3"))
+        kern = [f'extern "C" __global__ void __launch_bounds__({block}, {minb}) {kname}(const K::Params p) {{',
+                "  extern __shared__ __align__(128) unsigned char smem[];",
+                "  if (blockIdx.x < K::NG) K::copy_group(p, smem, blockIdx.x);",
+                "  for (long long g = blockIdx.x; g < K::NG; g += gridDim.x) {"]
+        if two_pass:
+            kern += [f"    if (__syncthreads_or(K::rows<true>(p, g * {rpc}, smem, nullptr, g + gridDim.x)))",
+                     f"      K::rows<false>(p, g * {rpc}, smem, nullptr, g + gridDim.x);"]
+        else:
+            kern.append(f"    K::rows<true>(p, g * {rpc}, smem, nullptr, g + gridDim.x);")
+        kern.append("  }")
     else:
-        kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
-                f"  for (long long g = blockIdx.x; g < K::NG; g += gridDim.x)",
-                f"    K::rows(p, g * {rpc}, nullptr, nullptr, 0);"]
+        # register staging holds 16*VEC elements per staged leaf; with one f32
+        # leaf (64 registers) capping the kernel at 80 registers fits three
+        # CTAs per SM: 0.270 ms vs 0.307 ms at two (profiles/r01_rownorm_modes.md)
+        data_regs = sum(16 * vec * l.dtype.itemsize // 4 for l in (prestage or []))
+        minb = int(os.environ.get("GRUMPY_COOP_MINBLOCKS", "3" if 0 < data_regs <= 64 else "0"))
+        lb = f"{block}, {minb}" if minb else f"{block}"
+        kern = [f'extern "C" __global__ void __launch_bounds__({lb}) {kname}(const K::Params p) {{',
+                f"  for (long long g = blockIdx.x; g < K::NG; g += gridDim.x)"]
+        if two_pass:
+            # fast pass; the CTA redoes the row group exactly if any dividend
+            # left the shared-divisor window (gr::div_sh)
+            kern += [f"    if (__syncthreads_or(K::rows<true>(p, g * {rpc}, nullptr, nullptr, 0)))",
+                     f"      K::rows<false>(p, g * {rpc}, nullptr, nullptr, 0);"]
+        else:
+            kern.append(f"    K::rows(p, g * {rpc}, nullptr, nullptr, 0);")
     if tot_meta:
         kern.append("  if (gr::last_block(p.ticket)) {")
         for ri, rop, T, off in tot_meta:
@@ -469,5 +553,6 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
                       block=block, groups=NG * block, vec=vec, unroll=1, scratch_bytes=scratch_off,
                       meta={"rows": R, "row_shape": Ts, "cols": C, "tpr": tpr, "rows_per_cta": rpc,
                             "totals": len(tot_meta), "ticket": bool(tot_meta), "smem": smem_bytes,
-                            "bulk_copy": bool(tma), "label": "coop-tma" if tma else "coop"})
+                            "bulk_copy": bool(tma), "cp_async": async_layout is not None,
+                            "label": "coop-tma" if tma else ("coop-async" if async_layout is not None else "coop")})
     return ks, em

@@ -429,6 +429,18 @@ def thread_space(region: Region):
         if not Ts:
             bad = next(r for r, p in prefixes if not p)
             raise NotFusable(_blame(region, bad), "reduction over the leading axis shares a region with other outputs")
+        # a float total folds one pairwise partial per row with a perfect
+        # binary tree: exact only when NumPy's pairwise recursion over the
+        # flattened operand splits on row boundaries all the way down.
+        # Otherwise cut the row reductions out (they become a small step of
+        # their own) and the total runs in the flattened-tree mode below.
+        R = element_count(Ts)
+        for t in totals:
+            if t.kind is OpKind.REDUCE and t.op.attrs[0] is ReduceOp.sum and t.dtype.is_float:
+                C = element_count(t.preds[0].shape[len(Ts):]) if len(t.preds[0].shape) >= len(Ts) else 1
+                if not rows_tile_pairwise(R, C):
+                    raise NotFusable(_blame(region, reds[0]),
+                                     f"total over {R}x{C} does not split on row boundaries")
         virtual = None
     else:
         # maps + totals: rows are the subtrees of NumPy's pairwise tree over the
@@ -446,6 +458,27 @@ def thread_space(region: Region):
 def _split(n: int) -> int:
     h = n // 2
     return h - h % 8
+
+
+def rows_tile_pairwise(R: int, C: int) -> bool:
+    """True iff NumPy's pairwise sum over R*C flattened elements is a perfect
+    binary tree whose leaves are the R rows of C elements (oracle/pairwise.py):
+    every multi-row node has > 128 elements (so it splits) and splits at a
+    row boundary into two equal halves."""
+    if R <= 1:
+        return True
+    stack = [R * C]
+    while stack:
+        m = stack.pop()
+        if m == C:
+            continue
+        if m <= 128 or m % C:
+            return False
+        a = _split(m)
+        if a % C or a != m - a:
+            return False
+        stack.append(a)
+    return True
 
 
 def tree_chunks(N: int, cmax: int = 2048):

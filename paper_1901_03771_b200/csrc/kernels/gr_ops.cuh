@@ -111,6 +111,25 @@ template <class T> __device__ __forceinline__ T div_shared(T x, const DivShared<
   const T ax = fabs(x);
   return (ax >= d.xlo && ax <= d.xhi) ? q : div_slow(x, d.s);
 }
+// Two-pass form for kernels that can redo a work item: the FAST pass returns
+// the Markstein quotient and only records (branch-free) whether any dividend
+// fell outside the window; the caller then re-runs the whole item with
+// FAST=false (exact per-element IEEE fallback) when any thread saw one.  No
+// per-element branch or call in the hot pass.
+template <bool FAST, class T>
+__device__ __forceinline__ T div_sh(T x, const DivShared<T>& d, bool& bad) {
+  if constexpr (FAST) {
+    const T q0 = x * d.r;
+    const T e = fma(-q0, d.s, x);
+    const T q = fma(e, d.r, q0);
+    const T ax = fabs(x);
+    bad |= !(ax >= d.xlo && ax <= d.xhi);
+    return q;
+  } else {
+    (void)bad;
+    return div_shared<T>(x, d);
+  }
+}
 
 template <class T> __device__ __forceinline__ T neg(T a) { return -a; }
 template <> __device__ __forceinline__ int neg(int a) { return (int)(0u - (unsigned)a); }

@@ -61,6 +61,16 @@ __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// Per-thread asynchronous 16-byte global->shared copies (LDGSTS).  Each thread
+// stages exactly the elements it will read back, so completion needs only the
+// thread's own wait_group — no CTA barrier — and the copies of the next work
+// item stay in flight while this one computes from registers.
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(sdst)), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 // V consecutive elements (16 bytes) from shared memory into registers
 template <class T, int V> __device__ __forceinline__ void ldsv(T (&d)[V], const T* s) {
   VecU<T, V> u;

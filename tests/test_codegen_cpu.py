@@ -62,6 +62,25 @@ def test_rownorm_coop(sess, C, tmp_path):
     assert ks.source.count("gr::row_sum") == 3   # mean (shared by std via CSE), var, total
 
 
+def test_rows_tile_pairwise():
+    from paper_1901_03771_b200.codegen_rows import rows_tile_pairwise
+    assert rows_tile_pairwise(65536, 4096) and rows_tile_pairwise(64, 256) and rows_tile_pairwise(1, 7)
+    assert not rows_tile_pairwise(58, 4096)      # 29 rows split mid-row
+    assert not rows_tile_pairwise(64, 1)         # 8-accumulator leaves, not a row tree
+    assert not rows_tile_pairwise(4, 16)         # 32-element nodes do not split
+
+
+def test_rownorm_total_non_power_of_two_rows(sess):
+    """58 rows: np.sum's pairwise tree over the flattened y is not a tree of
+    rows, so the total leaves the row region (row stats become their own step
+    and the total runs in flattened-tree mode) instead of a wrong fold."""
+    (x,) = wl.rownorm_inputs(rows=58, cols=4096)
+    ks = kernels(list(wl.rownorm(gp, gp.asarray(x))))
+    assert len(ks) >= 2
+    (x,) = wl.rownorm_inputs(rows=64, cols=4096)
+    assert len(kernels(list(wl.rownorm(gp, gp.asarray(x))))) == 1
+
+
 def test_row_families(sess):
     rng = np.random.default_rng(0)
     z = gp.asarray(rng.standard_normal((100, 10)).astype(np.float32))

@@ -23,6 +23,37 @@ def test_rownorm_exact(sess):
     assert np.asarray(tot) == et
 
 
+@pytest.mark.parametrize("store_y", [False, True])
+def test_rownorm_division_window_redo(sess, store_y):
+    """Rows whose dividends leave the shared-divisor window (exact zeros,
+    denormal-range values, a zero std, inf/nan) take the exact redo pass of
+    the two-pass division; every row must still match NumPy bit for bit."""
+    rng = np.random.default_rng(21)
+    x = (rng.standard_normal((64, 4096)) * 2 + 5).astype(np.float32)
+    x[3, :] = 7.0                        # std 0: 0/0 -> nan everywhere
+    x[5, ::2] = 1.0
+    x[5, 1::2] = -1.0                    # x - mean == ±1 exactly, mean 0
+    x[9, :] = 0.0
+    x[9, 17] = 1e-30                     # tiny dividends
+    x[11, 100] = np.inf                  # inf / nan propagation
+    x[12, 7] = np.nan
+    x[20, :] = rng.standard_normal(4096).astype(np.float32) * np.float32(1e30)
+    with np.errstate(all="ignore"):
+        ey, et = wl.rownorm(np, x)
+        y, tot = wl.rownorm(gp, gp.asarray(x))
+        if store_y:
+            gp.force(y, tot)
+            assert np.array_equal(np.asarray(y), ey, equal_nan=True)
+        got = np.asarray(tot)
+    assert np.array_equal(got, et, equal_nan=True)
+    # and without the pathological rows the fast pass alone is exact
+    xs = np.delete(x, [3, 5, 9, 11, 12, 20], axis=0)
+    ey, et = wl.rownorm(np, xs)
+    y, tot = wl.rownorm(gp, gp.asarray(xs))
+    gp.force(y, tot)
+    assert np.array_equal(np.asarray(y), ey) and np.asarray(tot) == et
+
+
 def test_softmax_argmax(sess):
     rng = np.random.default_rng(3)
     z = rng.standard_normal((1000, 10)).astype(np.float32)
