@@ -401,8 +401,10 @@ def run_grumpy(args, dist):
     h2d = sum(x.nbytes for x in pinned_in)
     d2h = sum(x.nbytes for x in pinned_out)
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    for it in range(1 + e2e_steps):
-        if it == 1:
+    sc0 = sess.stats.streamed_chunks
+    E2E_WARM = 2   # first call compiles the chunk kernels, second reaches the pool's steady state
+    for it in range(E2E_WARM + e2e_steps):
+        if it == E2E_WARM:
             dist.barrier()
             rt.sync()
             t0 = time.perf_counter()
@@ -412,9 +414,9 @@ def run_grumpy(args, dist):
         else:
             arrs = [gp.asarray(x) for x in pinned_in]
         outs = prog(gp, arrs)
-        gp.force(*outs)
-        for o, dst in zip(outs, pinned_out):
-            o.numpy(out=dst)
+        # to_external of every output into page-locked host buffers; regions
+        # reading host inputs row-locally stream (H2D / kernel / D2H overlap)
+        gp.materialize(*outs, out=pinned_out)
     rt.sync()
     e2e_s = dist.max(time.perf_counter() - t0)
     e2e_value = elements * e2e_steps / e2e_s
@@ -428,7 +430,8 @@ def run_grumpy(args, dist):
                    "l2": "inputs %.2f GiB/GPU vs 126 MB L2 (no flush; dominant kernel streams %.2f GiB)"
                          % (sum(x.nbytes for x in host) / 2**30, alg_bytes / 2**30)},
         "e2e": {"value": e2e_value, "unit": "elements/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+                "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                "streamed_chunks_per_step": (sess.stats.streamed_chunks - sc0) / (E2E_WARM + e2e_steps)},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(args.workload),
                      "peak_source": peak_src, "kernel_ms": kmean, "kernel": f"{dom[0][0]}:{dom[0][1]}",
@@ -467,7 +470,7 @@ def main():
     ap.add_argument("--impl", default="grumpy", choices=["grumpy", "reference"])
     ap.add_argument("--workload", default="blackscholes-f32", choices=sorted(WORKLOADS))
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

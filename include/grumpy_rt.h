@@ -100,6 +100,10 @@ int grumpy_rt_compile(const char* src, const char* const* opts, int n_opts,
 int grumpy_rt_compile_cubin(const char* src, const char* const* opts, int n_opts,
                             void* out, size_t cap, size_t* size, double* compile_ms);
 int grumpy_rt_get_function(uint64_t module, const char* name, uint64_t* fn);
+/* Device address and size of a module-scope __constant__/__device__ symbol
+ * (constant-bank staging of small row-invariant leaves; filled with
+ * grumpy_rt_d2d on the runtime stream before each launch). */
+int grumpy_rt_module_global(uint64_t module, const char* name, uint64_t* dptr, size_t* bytes);
 int grumpy_rt_function_info(uint64_t fn, int* num_regs, int* local_bytes,
                             int* static_smem, int* max_threads);
 int grumpy_rt_occupancy(uint64_t fn, int block, size_t dyn_smem, int* blocks_per_sm);
@@ -111,7 +115,21 @@ int grumpy_rt_occupancy(uint64_t fn, int block, size_t dyn_smem, int* blocks_per
 int grumpy_rt_launch(uint64_t fn, unsigned gx, unsigned gy, unsigned gz,
                      unsigned bx, unsigned by, unsigned bz, unsigned dyn_smem,
                      unsigned cluster_x, const void* params, size_t params_size);
+/* Waits for all work of the runtime's context (every stream). */
 int grumpy_rt_sync(void);
+
+/* ---- streams: copy/compute overlap for streamed materialisation ---------
+ * Async work (launch, h2d, d2h_async, d2d, memset, event_record, gemm, NCCL)
+ * goes to the "current" stream: the runtime's own stream unless
+ * grumpy_rt_set_stream selected another (0 selects the runtime's again). */
+int grumpy_rt_stream_create(uint64_t* stream);
+int grumpy_rt_stream_destroy(uint64_t stream);
+int grumpy_rt_set_stream(uint64_t stream);
+/* the current stream waits for `ev` (recorded on any stream) */
+int grumpy_rt_stream_wait_event(uint64_t ev);
+/* asynchronous D2H on the current stream (dst should be page-locked) */
+int grumpy_rt_d2h_async(void* dst, uint64_t src, size_t bytes);
+int grumpy_rt_event_sync(uint64_t ev);
 
 /* ---- events (device timing) ------------------------------------------- */
 int grumpy_rt_event_create(uint64_t* ev);

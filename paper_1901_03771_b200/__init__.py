@@ -17,6 +17,7 @@ Layout of the package (reference module in brackets, /root/reference/SPEC.md):
   runtime.py    C-ABI binding of libgrumpy_rt.so (include/grumpy_rt.h)
   session.py    [session]            ndarray proxy, force, fallback, stats
   distributed.py  leading-axis sharding, NCCL allreduce of partials
+  streaming.py  streamed to_external: H2D / kernels / D2H overlapped in chunks
   errors.py     [errors]             same class names as lazyfuse.errors
 """
 
@@ -35,6 +36,7 @@ from .session import (  # noqa: F401
     force,
     full,
     full_like,
+    materialize,
     ndarray,
     ones,
     ones_like,

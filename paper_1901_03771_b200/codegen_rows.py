@@ -61,8 +61,35 @@ _IDENT = {
 _COMBINE = {ReduceOp.sum: "gr::add", ReduceOp.prod: "gr::mul", ReduceOp.max: "gr::maximum", ReduceOp.min: "gr::minimum"}
 _OPS = {ReduceOp.sum: "gr::OpSum", ReduceOp.prod: "gr::OpProd", ReduceOp.max: "gr::OpMax", ReduceOp.min: "gr::OpMin"}
 
+ARG_UNROLL = 64        # arg-reductions up to this length are fully unrolled
 SMALL_RECOMPUTE = 64   # a reduction re-evaluated per column may reduce at most this many points
 MAX_GRID = 148 * 16    # grid cap for kernels with per-CTA partial slots (keyed sums)
+
+
+class CBankMiss(Exception):
+    """A leaf staged in constant memory is read at a row-dependent offset."""
+
+    def __init__(self, leaf: Node):
+        super().__init__(f"leaf {leaf.id} read per row")
+        self.leaf = leaf
+
+
+CBANK_LEAF_BYTES = 16 * 1024   # per leaf
+CBANK_TOTAL_BYTES = 48 * 1024  # per kernel (the user constant bank is 64 KB)
+CBANK_MIN_ROWS = 4096          # staging pays only when many rows reuse the leaf
+
+
+def cbank_candidates(region: Region, rows: int) -> Dict[int, str]:
+    """Small leaves that may be staged in the constant bank (leaf id -> symbol)."""
+    if rows < CBANK_MIN_ROWS:
+        return {}
+    out, total = {}, 0
+    for i, l in enumerate(region.leaves):
+        nb = element_count(l.shape) * l.dtype.itemsize
+        if 0 < nb <= CBANK_LEAF_BYTES and total + nb <= CBANK_TOTAL_BYTES and l.dtype.itemsize in (4, 8):
+            out[l.id] = f"gr_cin{i}"
+            total += nb
+    return out
 
 
 class Scope:
@@ -108,11 +135,15 @@ def render(scope: Scope, indent: int) -> List[str]:
 class LoopEmitter(ValueEmitter):
     """Scoped emitter: level 0 kernel constants, level 1 the row, 2+ loops."""
 
-    def __init__(self, region: Region, vec_loads=True):
+    def __init__(self, region: Region, vec_loads=True, cbank=None):
         super().__init__(region)
         self.row = Scope(1)
         self.stack: List[Optional[Scope]] = [None, self.row]
         self.vec_loads = vec_loads
+        # leaf id -> __constant__ symbol for small leaves every row reads at
+        # the same (row-independent) offsets, e.g. the k-means centroids
+        self.cbank: Dict[int, str] = dict(cbank or {})
+        self.uniform_vars = set()   # loop indices with row-independent values
 
     # -- scopes ------------------------------------------------------------------
     def emit(self, level, ctype, expr):
@@ -145,6 +176,8 @@ class LoopEmitter(ValueEmitter):
             header = f"for (long long {name} = 0; {name} < {tstr}; ++{name})"
         else:
             header = f"auto f{name} = [&](long long {name}) -> {ret_type}"
+        if kind != "for" or isinstance(trip, int):
+            self.uniform_vars.add(name)
         s = Scope(lvl, kind, header, unroll=unroll, var=var, trip=trip)
         self.stack.append(s)
         return var, s, saved
@@ -195,6 +228,13 @@ class LoopEmitter(ValueEmitter):
         T = leaf.dtype.ctype
         ptr = f"p.in{idx}"
         lvl = off.level
+        sym = self.cbank.get(leaf.id)
+        if sym is not None:
+            if any(v.name not in self.uniform_vars for v, _ in off.terms):
+                raise CBankMiss(leaf)
+            # warp-uniform address: a constant-bank operand (LDCU / c[3][]),
+            # no per-thread load instruction
+            return self.emit(lvl, T, f"{sym}[{off.c()}]"), lvl
         if self.vec_loads and lvl >= 2:
             sc = self.stack[lvl]
             if sc.kind == "for" and sc.unroll and sc.var is not None:
@@ -361,20 +401,43 @@ class LoopEmitter(ValueEmitter):
         T = x.dtype.ctype
         best = self.var_decl(L, T, "0")
         bi = self.var_decl(L, "long long", "0")
-        iv, s, saved = self.open(L, "for", trip=n, unroll=(n <= 16))
-        inner = self._delin(iv, list(axes), [So[a] for a in axes])
-        full = []
-        k = 0
-        for i in range(len(So)):
-            if i in inner:
-                full.append(inner[i])
-            else:
-                full.append(kept[k])
-                k += 1
-        v = self.value(x, full)
-        pred = "gr::arg_better_max" if which == "max" else "gr::arg_better_min"
-        self.stmt(iv.level, f"if ({iv.name} == 0 || {pred}<{T}>({v[0]}, {best})) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
+
+        def operand(iv):
+            inner = self._delin(iv, list(axes), [So[a] for a in axes])
+            full = []
+            k = 0
+            for i in range(len(So)):
+                if i in inner:
+                    full.append(inner[i])
+                else:
+                    full.append(kept[k])
+                    k += 1
+            return self.value(x, full)
+
+        iv, s, saved = self.open(L, "for", trip=n, unroll=(n <= ARG_UNROLL))
+        v = operand(iv)
+        if not x.dtype.is_float:
+            pred = "gr::arg_better_max" if which == "max" else "gr::arg_better_min"
+            self.stmt(iv.level, f"if ({iv.name} == 0 || {pred}<{T}>({v[0]}, {best})) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
+            self.close(s, saved)
+            return bi, L
+        # floats: the scan is a plain ordered compare (first index wins ties)
+        # plus one add whose result is NaN whenever an operand is NaN; only
+        # then is the operand rescanned for np.argmax's answer, its first NaN
+        nacc = self.var_decl(L, T, "0")
+        cmp = ">" if which == "max" else "<"
+        self.stmt(iv.level, f"if ({iv.name} == 0 || {v[0]} {cmp} {best}) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
+        self.stmt(iv.level, f"{nacc} = {nacc} + {v[0]};")
         self.close(s, saved)
+        saved_if = self.stack[L + 1:]
+        del self.stack[L + 1:]
+        sif = Scope(L + 1, "for", header=f"if ({nacc} != {nacc})")
+        self.stack.append(sif)
+        iv2, s2, saved2 = self.open(L + 1, "for", trip=n)
+        v2 = operand(iv2)
+        self.stmt(iv2.level, f"if ({v2[0]} != {v2[0]}) {{ {best} = {v2[0]}; {bi} = {iv2.name}; break; }}")
+        self.close(s2, saved2)
+        self.close(sif, saved_if)
         return bi, L
 
 
@@ -507,10 +570,22 @@ def tree_chunks(N: int, cmax: int = 2048):
 
 
 def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
+    """Thread-per-row kernel; small row-invariant leaves go to the constant
+    bank (retried without a leaf that turns out to be read per row)."""
+    Ts, _totals, virtual = thread_space(region)
+    cbank = cbank_candidates(region, element_count(Ts)) if virtual is None else {}
+    while True:
+        try:
+            return _gen_rows(region, kname, block, cbank)
+        except CBankMiss as e:
+            del cbank[e.leaf.id]
+
+
+def _gen_rows(region: Region, kname, block, cbank) -> KernelSource:
     Ts, totals, virtual = thread_space(region)
     tot_ids = {t.id for t in totals}
     R = element_count(Ts)
-    em = LoopEmitter(region)
+    em = LoopEmitter(region, cbank=cbank)
     rvar = Var("r", 1)
     # row coordinates
     if virtual is None:
@@ -657,15 +732,34 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
             else:
                 em.stmt(1, f"const long long kw{j} = 1LL;")
             wnames.append((j, r))
-        body = [f"for (int src = 0; src < 32; ++src) {{",
-                "  const long long kk = __shfl_sync(0xffffffffu, kkey, src);"]
-        for j, r in wnames:
-            body.append(f"  const {r.dtype.ctype} w{j} = __shfl_sync(0xffffffffu, kw{j}, src);")
-        conds = []
+        # lanes holding the same key form a group (__match_any_sync); the
+        # group's lowest lane sums the group's weights in lane order (one
+        # shuffle round per extra member, rounds = largest group - 1) and
+        # alone updates the bin, so every bin sees a fixed order of adds.
+        # Counts are the group's population count.
+        body = ["const unsigned kpeers = __match_any_sync(0xffffffffu, (unsigned long long)kkey);",
+                "const unsigned klane = threadIdx.x & 31u;",
+                "const bool klead = (kpeers & ((1u << klane) - 1u)) == 0u;",
+                "unsigned krest = klead ? (kpeers & (kpeers - 1u)) : 0u;"]
+        weighted = [(j, r) for j, r in wnames if len(r.preds) == 2]
+        for j, r in weighted:
+            body.append(f"double ks{j} = kw{j};")
+        if weighted:
+            body.append("while (__any_sync(0xffffffffu, krest != 0u)) {")
+            body.append("  const int ksrc = krest ? __ffs(krest) - 1 : (int)klane;")
+            for j, r in weighted:
+                body.append(f"  const double kv{j} = __shfl_sync(0xffffffffu, kw{j}, ksrc);")
+            body.append("  if (krest) {")
+            for j, r in weighted:
+                body.append(f"    ks{j} += kv{j};")
+            body.append("    krest &= krest - 1u;")
+            body.append("  }")
+            body.append("}")
+        body.append("if (klead && kkey >= 0) {")
         for j, r in wnames:
             NBj = r.op.attrs[0]
-            body.append(f"  if (kk >= 0 && kk < {NBj}LL && (int)(kk & 31) == (threadIdx.x & 31)) "
-                        f"khist{j}[(threadIdx.x >> 5) * {NBj} + kk] += w{j};")
+            val = f"ks{j}" if len(r.preds) == 2 else "(long long)__popc(kpeers)"
+            body.append(f"  if (kkey < {NBj}LL) khist{j}[(threadIdx.x >> 5) * {NBj} + kkey] += {val};")
         body.append("}")
         for line in body:
             em.stmt(1, line)
@@ -683,7 +777,14 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
     lines.append("}")
     params = _params_struct(region).replace("    void* __restrict__ scratch;",
                                              "    void* __restrict__ scratch;\n    unsigned int* ticket;")
-    src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params,
+    used_cb = []
+    for i, l in enumerate(region.leaves):
+        sym = cbank.get(l.id)
+        if sym is not None and sym + "[" in "\n".join(lines):
+            used_cb.append((i, sym, element_count(l.shape) * l.dtype.itemsize))
+    cdecl = "".join(f"__constant__ {region.leaves[i].dtype.ctype} {sym}[{nb // region.leaves[i].dtype.itemsize}];\n"
+                    for i, sym, nb in used_cb)
+    src = [HEADER, '#include "gr_reduce.cuh"\n', cdecl, "struct K {", params,
            f"  static constexpr long long NROWS = {R}LL;"]
     src.append("  " + "\n  ".join(lines))
     src.append("};")
@@ -744,7 +845,7 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
                         block=block, groups=R, vec=1, unroll=1, scratch_bytes=scratch_off,
                         meta={"rows": R, "row_shape": Ts, "totals": len(tot_meta), "ticket": bool(tot_meta or kmeta),
                               "virtual": virtual, "block_pow2": True, "keyed": len(kmeta),
-                              "max_grid": MAX_GRID if kmeta else None})
+                              "max_grid": MAX_GRID if kmeta else None, "cbank": used_cb})
 
 
 def _row_partial(em: LoopEmitter, x: Node, rop, T: DType, row_coords, cols):

@@ -53,6 +53,9 @@ int fail(int code, const std::string& msg) {
   X(cuCtxSetCurrent)                 \
   X(cuStreamCreate)                  \
   X(cuStreamSynchronize)             \
+  X(cuStreamDestroy)                 \
+  X(cuStreamWaitEvent)               \
+  X(cuCtxSynchronize)                \
   X(cuMemAlloc)                      \
   X(cuMemFree)                       \
   X(cuMemcpyHtoDAsync)               \
@@ -65,6 +68,7 @@ int fail(int code, const std::string& msg) {
   X(cuMemHostUnregister)             \
   X(cuModuleLoadData)                \
   X(cuModuleGetFunction)             \
+  X(cuModuleGetGlobal)               \
   X(cuFuncGetAttribute)              \
   X(cuFuncSetAttribute)              \
   X(cuOccupancyMaxActiveBlocksPerMultiprocessor) \
@@ -92,6 +96,7 @@ struct State {
   CUdevice dev = 0;
   CUcontext ctx = nullptr;
   CUstream stream = nullptr;
+  CUstream cur = nullptr;   // stream async work goes to (nullptr: `stream`)
   int sm_count = 0;
   cublasHandle_t cublas = nullptr;
   std::mutex mu;
@@ -131,6 +136,8 @@ int load_driver() {
   D.loaded = true;
   return GR_OK;
 }
+
+static inline CUstream CS() { return S.cur ? S.cur : S.stream; }
 
 int need_init() {
   if (!S.init) return fail(GR_ENOINIT, "grumpy_rt_init has not been called");
@@ -362,7 +369,7 @@ int grumpy_rt_alloc(size_t bytes, uint64_t* dptr) {
   CUdeviceptr p = 0;
   CUresult cr = D.p_cuMemAlloc(&p, sz);
   if (cr == CUDA_ERROR_OUT_OF_MEMORY) {
-    D.p_cuStreamSynchronize(S.stream);
+    D.p_cuCtxSynchronize();
     pool_release_cached();
     cr = D.p_cuMemAlloc(&p, sz);
   }
@@ -403,7 +410,7 @@ int grumpy_rt_pool_stats(size_t* in_use, size_t* cached, size_t* peak, size_t* n
 int grumpy_rt_pool_trim(void) {
   int r = need_init();
   if (r) return r;
-  CU_CHECK(D.p_cuStreamSynchronize(S.stream), "cuStreamSynchronize");
+  CU_CHECK(D.p_cuCtxSynchronize(), "cuCtxSynchronize");
   std::lock_guard<std::mutex> lk(S.mu);
   return pool_release_cached();
 }
@@ -413,15 +420,15 @@ int grumpy_rt_h2d(uint64_t dst, const void* src, size_t bytes) {
   int r = need_init();
   if (r) return r;
   if (!bytes) return GR_OK;
-  CU_CHECK(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, S.stream), "cuMemcpyHtoDAsync");
+  CU_CHECK(D.p_cuMemcpyHtoDAsync((CUdeviceptr)dst, src, bytes, CS()), "cuMemcpyHtoDAsync");
   return GR_OK;
 }
 
 int grumpy_rt_d2h(void* dst, uint64_t src, size_t bytes) {
   int r = need_init();
   if (r) return r;
-  if (bytes) CU_CHECK(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, S.stream), "cuMemcpyDtoHAsync");
-  CU_CHECK(D.p_cuStreamSynchronize(S.stream), "cuStreamSynchronize");
+  if (bytes) CU_CHECK(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, CS()), "cuMemcpyDtoHAsync");
+  CU_CHECK(D.p_cuStreamSynchronize(CS()), "cuStreamSynchronize");
   return GR_OK;
 }
 
@@ -429,7 +436,7 @@ int grumpy_rt_d2d(uint64_t dst, uint64_t src, size_t bytes) {
   int r = need_init();
   if (r) return r;
   if (!bytes) return GR_OK;
-  CU_CHECK(D.p_cuMemcpyDtoDAsync((CUdeviceptr)dst, (CUdeviceptr)src, bytes, S.stream), "cuMemcpyDtoDAsync");
+  CU_CHECK(D.p_cuMemcpyDtoDAsync((CUdeviceptr)dst, (CUdeviceptr)src, bytes, CS()), "cuMemcpyDtoDAsync");
   return GR_OK;
 }
 
@@ -437,7 +444,7 @@ int grumpy_rt_memset(uint64_t dst, int byte_value, size_t bytes) {
   int r = need_init();
   if (r) return r;
   if (!bytes) return GR_OK;
-  CU_CHECK(D.p_cuMemsetD8Async((CUdeviceptr)dst, (unsigned char)byte_value, bytes, S.stream), "cuMemsetD8Async");
+  CU_CHECK(D.p_cuMemsetD8Async((CUdeviceptr)dst, (unsigned char)byte_value, bytes, CS()), "cuMemsetD8Async");
   return GR_OK;
 }
 
@@ -541,6 +548,17 @@ int grumpy_rt_get_function(uint64_t module, const char* name, uint64_t* fn) {
   return GR_OK;
 }
 
+int grumpy_rt_module_global(uint64_t module, const char* name, uint64_t* dptr, size_t* bytes) {
+  int r = need_init();
+  if (r) return r;
+  CUdeviceptr p = 0;
+  size_t n = 0;
+  CU_CHECK(D.p_cuModuleGetGlobal(&p, &n, (CUmodule)(uintptr_t)module, name), "cuModuleGetGlobal");
+  *dptr = (uint64_t)p;
+  if (bytes) *bytes = n;
+  return GR_OK;
+}
+
 int grumpy_rt_function_info(uint64_t fn, int* num_regs, int* local_bytes, int* static_smem, int* max_threads) {
   int r = need_init();
   if (r) return r;
@@ -579,7 +597,7 @@ int grumpy_rt_launch(uint64_t fn, unsigned gx, unsigned gy, unsigned gz, unsigne
     cfg.gridDimX = gx; cfg.gridDimY = gy; cfg.gridDimZ = gz;
     cfg.blockDimX = bx; cfg.blockDimY = by; cfg.blockDimZ = bz;
     cfg.sharedMemBytes = dyn_smem;
-    cfg.hStream = S.stream;
+    cfg.hStream = CS();
     CUlaunchAttribute attr;
     memset(&attr, 0, sizeof(attr));
     attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
@@ -591,14 +609,60 @@ int grumpy_rt_launch(uint64_t fn, unsigned gx, unsigned gy, unsigned gz, unsigne
     CU_CHECK(D.p_cuLaunchKernelEx(&cfg, f, nullptr, extra), "cuLaunchKernelEx");
     return GR_OK;
   }
-  CU_CHECK(D.p_cuLaunchKernel(f, gx, gy, gz, bx, by, bz, dyn_smem, S.stream, nullptr, extra), "cuLaunchKernel");
+  CU_CHECK(D.p_cuLaunchKernel(f, gx, gy, gz, bx, by, bz, dyn_smem, CS(), nullptr, extra), "cuLaunchKernel");
   return GR_OK;
 }
 
 int grumpy_rt_sync(void) {
   int r = need_init();
   if (r) return r;
-  CU_CHECK(D.p_cuStreamSynchronize(S.stream), "cuStreamSynchronize");
+  CU_CHECK(D.p_cuCtxSynchronize(), "cuCtxSynchronize");
+  return GR_OK;
+}
+
+// ---- streams (copy/compute overlap of streamed materialisation) --------------
+int grumpy_rt_stream_create(uint64_t* stream) {
+  int r = need_init();
+  if (r) return r;
+  CUstream st;
+  CU_CHECK(D.p_cuStreamCreate(&st, CU_STREAM_NON_BLOCKING), "cuStreamCreate");
+  *stream = (uint64_t)(uintptr_t)st;
+  return GR_OK;
+}
+
+int grumpy_rt_stream_destroy(uint64_t stream) {
+  if (!S.init || !stream) return GR_OK;
+  if (S.cur == (CUstream)(uintptr_t)stream) S.cur = nullptr;
+  CU_CHECK(D.p_cuStreamDestroy((CUstream)(uintptr_t)stream), "cuStreamDestroy");
+  return GR_OK;
+}
+
+int grumpy_rt_set_stream(uint64_t stream) {
+  int r = need_init();
+  if (r) return r;
+  S.cur = (CUstream)(uintptr_t)stream;
+  if (S.cublas) cublasSetStream(S.cublas, CS());
+  return GR_OK;
+}
+
+int grumpy_rt_stream_wait_event(uint64_t ev) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuStreamWaitEvent(CS(), (CUevent)(uintptr_t)ev, 0), "cuStreamWaitEvent");
+  return GR_OK;
+}
+
+int grumpy_rt_d2h_async(void* dst, uint64_t src, size_t bytes) {
+  int r = need_init();
+  if (r) return r;
+  if (bytes) CU_CHECK(D.p_cuMemcpyDtoHAsync(dst, (CUdeviceptr)src, bytes, CS()), "cuMemcpyDtoHAsync");
+  return GR_OK;
+}
+
+int grumpy_rt_event_sync(uint64_t ev) {
+  int r = need_init();
+  if (r) return r;
+  CU_CHECK(D.p_cuEventSynchronize((CUevent)(uintptr_t)ev), "cuEventSynchronize");
   return GR_OK;
 }
 
@@ -615,7 +679,7 @@ int grumpy_rt_event_create(uint64_t* ev) {
 int grumpy_rt_event_record(uint64_t ev) {
   int r = need_init();
   if (r) return r;
-  CU_CHECK(D.p_cuEventRecord((CUevent)(uintptr_t)ev, S.stream), "cuEventRecord");
+  CU_CHECK(D.p_cuEventRecord((CUevent)(uintptr_t)ev, CS()), "cuEventRecord");
   return GR_OK;
 }
 
@@ -639,7 +703,7 @@ static int ensure_cublas() {
   if (S.cublas) return GR_OK;
   cublasStatus_t st = cublasCreate(&S.cublas);
   if (st != CUBLAS_STATUS_SUCCESS) return fail(GR_ECUBLAS, "cublasCreate: status " + std::to_string((int)st));
-  cublasSetStream(S.cublas, S.stream);
+  cublasSetStream(S.cublas, CS());
   // FP32 stays FP32 (no TF32): NumPy/OpenBLAS parity.
   cublasSetMathMode(S.cublas, CUBLAS_DEFAULT_MATH);
   return GR_OK;
@@ -738,7 +802,7 @@ int grumpy_rt_nccl_allreduce(uint64_t send, uint64_t recv, size_t count, int dty
   int nd = nccl_dtype(dtype);
   if (nd < 0 || op < 0 || op > 3) return fail(GR_EINVAL, "bad dtype/op");
   // grumpy op codes match ncclSum=0, ncclProd=1, ncclMax=2, ncclMin=3
-  int rr = N.AllReduce((const void*)send, (void*)recv, count, nd, op, N.comm, S.stream);
+  int rr = N.AllReduce((const void*)send, (void*)recv, count, nd, op, N.comm, CS());
   if (rr) return nccl_fail(rr, "ncclAllReduce");
   return GR_OK;
 }
@@ -750,7 +814,7 @@ int grumpy_rt_nccl_allgather(uint64_t send, uint64_t recv, size_t count_per_rank
   int nd = nccl_dtype(dtype);
   if (nd < 0) return fail(GR_EINVAL, "bad dtype");
   (void)dtype_size;
-  int rr = N.AllGather((const void*)send, (void*)recv, count_per_rank, nd, N.comm, S.stream);
+  int rr = N.AllGather((const void*)send, (void*)recv, count_per_rank, nd, N.comm, CS());
   if (rr) return nccl_fail(rr, "ncclAllGather");
   return GR_OK;
 }

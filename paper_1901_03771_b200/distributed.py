@@ -166,10 +166,13 @@ def shard_of(node: Node):
     return None
 
 
-def classify(roots, memo: Optional[dict] = None) -> Dict[int, str]:
+def classify(roots, memo: Optional[dict] = None, sharded=None) -> Dict[int, str]:
     """Distribution of every unmaterialized node reachable from roots (plus the
-    materialized frontier): "S", "R", "P:<op>", "A:<max|min>"."""
+    materialized frontier): "S", "R", "P:<op>", "A:<max|min>".  ``sharded``
+    (node ids) replaces the registered shard inputs, e.g. the host inputs of a
+    streamed force (streaming.py)."""
     memo = {} if memo is None else memo
+    shards = _SHARDED if sharded is None else sharded
 
     def dist(n: Node) -> str:
         d = memo.get(n.id)
@@ -180,7 +183,7 @@ def classify(roots, memo: Optional[dict] = None) -> Dict[int, str]:
         return d
 
     def _dist(n: Node) -> str:
-        if n.id in _SHARDED:
+        if n.id in shards:
             return "S"
         if n.is_materialized:
             return getattr(n, "dist", None) or "R"

@@ -32,6 +32,7 @@ class Executor:
         self.launch_log = collections.deque(maxlen=4096)  # (family, kernel name) per launch
         self.profile = None           # per-launch CUDA events when enabled
         self._tickets = {}
+        self.out_bind: Dict[int, TensorBuffer] = {}   # root id -> preallocated output (streaming.py)
 
     # -- planner hook ---------------------------------------------------------------
     def row_fusion(self, reduction: Node, consumer: Node) -> bool:
@@ -96,7 +97,7 @@ class Executor:
             empty = all(element_count(r.shape) == 0 for r in region.roots)
             c["ks"] = None if empty else self.kernel_source(region)
         leaves = [st.leaves[i] for i in c["perm"]]
-        outs = [self.new_buffer(r) for r in st.roots]
+        outs = [self.out_bind.pop(r.id, None) or self.new_buffer(r) for r in st.roots]
         ks = c["ks"]
         if ks is None:
             return outs
@@ -111,6 +112,16 @@ class Executor:
             ptrs = [self.device_ptr(l) for l in leaves]
         else:
             ptrs = [self.buffer_ptr(bind[l.id]) for l in leaves]
+        cb = ks.meta.get("cbank")
+        if cb:
+            # small row-invariant leaves live in the module's constant bank:
+            # one stream-ordered device copy per launch (the leaf may change
+            # between launches, e.g. new k-means centroids)
+            dst = c.get("cbank_dst")
+            if dst is None:
+                dst = c["cbank_dst"] = [self.rt.module_global(k, sym)[0] for _i, sym, _nb in cb]
+            for (i, _sym, nb), d in zip(cb, dst):
+                self.rt.d2d_raw(d, ptrs[i], nb)
         ptrs += [b.device.ptr for b in outs]
         scratch = None
         if ks.scratch_bytes:

@@ -61,11 +61,18 @@ SIGNATURES = {
     "grumpy_rt_compile": [_cp, _cpp, _i, _cp, _u64p, _dp, _ip],
     "grumpy_rt_compile_cubin": [_cp, _cpp, _i, _p, _sz, _szp, _dp],
     "grumpy_rt_get_function": [_u64, _cp, _u64p],
+    "grumpy_rt_module_global": [_u64, _cp, _u64p, ctypes.POINTER(ctypes.c_size_t)],
     "grumpy_rt_function_info": [_u64, _ip, _ip, _ip, _ip],
     "grumpy_rt_occupancy": [_u64, _i, _sz, _ip],
     "grumpy_rt_launch": [_u64, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint,
                          ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, _p, _sz],
     "grumpy_rt_sync": [],
+    "grumpy_rt_stream_create": [_u64p],
+    "grumpy_rt_stream_destroy": [_u64],
+    "grumpy_rt_set_stream": [_u64],
+    "grumpy_rt_stream_wait_event": [_u64],
+    "grumpy_rt_d2h_async": [_p, _u64, _sz],
+    "grumpy_rt_event_sync": [_u64],
     "grumpy_rt_event_create": [_u64p],
     "grumpy_rt_event_record": [_u64],
     "grumpy_rt_event_elapsed": [_u64, _u64, _fp],
@@ -180,9 +187,10 @@ class DeviceBuffer:
 class Kernel:
     """A loaded kernel: function handle plus launch geometry policy."""
 
-    __slots__ = ("fn", "name", "block", "blocks_per_sm", "num_regs", "compile_ms", "cache_hit", "source")
+    __slots__ = ("fn", "name", "block", "blocks_per_sm", "num_regs", "compile_ms", "cache_hit", "source", "module")
 
-    def __init__(self, fn, name, block, blocks_per_sm, num_regs, compile_ms, cache_hit, source):
+    def __init__(self, fn, name, block, blocks_per_sm, num_regs, compile_ms, cache_hit, source, module=0):
+        self.module = module
         self.fn = fn
         self.name = name
         self.block = block
@@ -239,6 +247,16 @@ class Runtime:
     def sync(self):
         _check(self.lib.grumpy_rt_sync())
 
+    def module_global(self, k: "Kernel", name: str):
+        """(device address, bytes) of a module-scope symbol of ``k``'s module."""
+        p = ctypes.c_uint64(0)
+        n = ctypes.c_size_t(0)
+        _check(self.lib.grumpy_rt_module_global(k.module, name.encode(), ctypes.byref(p), ctypes.byref(n)))
+        return p.value, n.value
+
+    def d2d_raw(self, dst: int, src: int, nbytes: int):
+        _check(self.lib.grumpy_rt_d2d(dst, src, nbytes))
+
     def pool_stats(self):
         v = [ctypes.c_size_t(0) for _ in range(4)]
         _check(self.lib.grumpy_rt_pool_stats(*[ctypes.byref(x) for x in v]))
@@ -285,7 +303,7 @@ class Runtime:
         regs = ctypes.c_int(0)
         _check(self.lib.grumpy_rt_function_info(fn.value, ctypes.byref(regs), None, None, None))
         self.compile_ms_total += ms.value
-        k = Kernel(fn.value, name, block, max(occ.value, 1), regs.value, ms.value, hit.value, source)
+        k = Kernel(fn.value, name, block, max(occ.value, 1), regs.value, ms.value, hit.value, source, mod.value)
         self._kernels[(source, name)] = k
         return k
 
@@ -294,6 +312,32 @@ class Runtime:
         bx, by, bz = (block, 1, 1) if isinstance(block, int) else block
         _check(self.lib.grumpy_rt_launch(k.fn, gx, gy, gz, bx, by, bz, smem, cluster, params, len(params)))
         self.launches += 1
+
+    # -- streams (streamed materialisation: copies overlap kernels)
+    def stream_create(self) -> int:
+        st = ctypes.c_uint64(0)
+        _check(self.lib.grumpy_rt_stream_create(ctypes.byref(st)))
+        return st.value
+
+    def stream_destroy(self, st: int):
+        _check(self.lib.grumpy_rt_stream_destroy(st))
+
+    def set_stream(self, st: int = 0):
+        """Route async work to stream ``st`` (0: the runtime's own stream)."""
+        _check(self.lib.grumpy_rt_set_stream(st))
+
+    def wait_event(self, ev):
+        """The current stream waits for ``ev``."""
+        _check(self.lib.grumpy_rt_stream_wait_event(ev))
+
+    def h2d_async(self, dst_ptr: int, arr: np.ndarray):
+        _check(self.lib.grumpy_rt_h2d(dst_ptr, arr.ctypes.data, arr.nbytes))
+
+    def d2h_async(self, out: np.ndarray, src_ptr: int):
+        _check(self.lib.grumpy_rt_d2h_async(out.ctypes.data, src_ptr, out.nbytes))
+
+    def event_sync(self, ev):
+        _check(self.lib.grumpy_rt_event_sync(ev))
 
     # -- events
     def event(self):

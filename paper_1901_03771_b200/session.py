@@ -23,6 +23,7 @@ from __future__ import annotations
 import builtins
 import dataclasses
 import numbers
+import os
 import time
 from typing import Any, List, Optional, Sequence
 
@@ -47,6 +48,7 @@ class SessionStats:
     compile_ms: float = 0.0
     h2d_bytes: int = 0
     d2h_bytes: int = 0
+    streamed_chunks: int = 0   # chunks of streamed to_external forces (streaming.py)
 
     def snapshot(self):
         return dataclasses.replace(self)
@@ -1157,6 +1159,39 @@ def force(*arrays: ndarray):
         return
     sess = arrays[0]._session
     sess.force_nodes([a._node for a in arrays])
+
+
+def materialize(*arrays, out=None) -> list:
+    """to_external for several arrays at once: force them
+    together and return host arrays (written into ``out`` when given).
+
+    When the pending region reads host-resident inputs along the roots'
+    leading axis and every root is row-local, the force is streamed
+    (streaming.py): chunks of rows flow H2D -> fused kernel -> D2H on three
+    streams so the PCIe copies overlap each other and the kernels.  Page-
+    locked ``out`` arrays (``Runtime.pinned_empty``) let the D2H run async."""
+    arrays = [a if isinstance(a, ndarray) else asarray(a) for a in arrays]
+    if not arrays:
+        return []
+    outs = list(out) if out is not None else [None] * len(arrays)
+    if len(outs) != len(arrays):
+        raise ShapeMismatch("materialize: one out array per input array")
+    for a, o in zip(arrays, outs):
+        if o is not None and (o.shape != a.shape or o.dtype != a.dtype or not o.flags.c_contiguous):
+            raise ShapeMismatch("out must be a C-contiguous array of the same shape and dtype")
+    sess = arrays[0]._session
+    nodes = [a._node for a in arrays]
+    if (sess.comm is None and os.environ.get("GRUMPY_STREAM", "1") != "0"
+            and len({n.id for n in nodes}) == len(nodes)):
+        from . import streaming
+        p = streaming.plan(nodes)
+        if p is not None:
+            outs = [o if o is not None else np.empty(a.shape, a.dtype) for a, o in zip(arrays, outs)]
+            order = {n.id: i for i, n in enumerate(nodes)}
+            streaming.run(sess, p, [outs[order[r.id]] for r in p.roots])
+            return outs
+    sess.force_nodes(nodes)
+    return [a.numpy(out=o) if o is not None else a.numpy() for a, o in zip(arrays, outs)]
 
 
 def asnumpy(a) -> np.ndarray:

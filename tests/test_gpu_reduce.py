@@ -141,3 +141,46 @@ def test_region_against_eager_oracle(sess):
     r = (x * y - (x * y).mean(1, keepdims=True)).max(1) + x.sum() * 0.0
     expect = eager.evaluate(r.node)
     np.testing.assert_allclose(np.asarray(r), expect, rtol=1e-12)
+
+
+def test_kmeans_nan_inf_ties_exact(sess):
+    """Labels stay np.argmin-exact on the constant-bank / NaN-rescan path:
+    NaN points (first NaN index = 0), a NaN centroid (its index wins for every
+    point), +inf coordinates and duplicate centroids (first index wins)."""
+    P, C = wl.kmeans_inputs(n=8192 + 5, k=64, d=4)
+    P[10, 2] = np.nan
+    P[11] = np.inf
+    P[12, 0] = -np.inf
+    C[7] = C[3]                       # exact ties: index 3 must win
+    P[100:200] = C[3]                 # zero distance to 3 and 7
+    lab = wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C))
+    assert np.array_equal(np.asarray(lab), wl.kmeans_assign(np, P, C))
+    C2 = C.copy()
+    C2[40, 1] = np.nan
+    lab2 = wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C2))
+    assert np.array_equal(np.asarray(lab2), wl.kmeans_assign(np, P, C2))
+
+
+@pytest.mark.parametrize("n", [64, 10])
+def test_row_argmax_nan_rows(sess, n):
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((5000, n)).astype(np.float32)
+    x[::7, n // 2] = np.nan
+    x[::11, n - 1] = np.nan
+    x[3] = np.nan
+    x[4] = 1.0
+    g = gp.asarray(x)
+    for fn in ("argmax", "argmin"):
+        assert np.array_equal(np.asarray(getattr(g * 2.0, fn)(1)), getattr(x * 2.0, fn)(1)), fn
+
+
+@pytest.mark.parametrize("nkeys", [1, 3, 64])
+def test_bincount_collisions(sess, nkeys):
+    """Warp groups of equal keys (__match_any_sync) up to a whole warp."""
+    rng = np.random.default_rng(12)
+    k = rng.integers(0, nkeys, 10007)
+    w = rng.standard_normal(10007)
+    g = gp.bincount(gp.asarray(k), weights=gp.asarray(w), minlength=64)
+    np.testing.assert_allclose(np.asarray(g), np.bincount(k, weights=w, minlength=64), rtol=1e-12, atol=1e-9)
+    c = gp.bincount(gp.asarray(k), minlength=64)
+    assert np.array_equal(np.asarray(c), np.bincount(k, minlength=64))

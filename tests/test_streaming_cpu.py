@@ -1,0 +1,41 @@
+"""Eligibility of streamed materialisation (streaming.py) — DAG analysis only."""
+import numpy as np
+import pytest
+
+import paper_1901_03771_b200 as gp
+from paper_1901_03771_b200 import streaming, workloads as wl
+
+
+@pytest.fixture(autouse=True)
+def small_chunks(monkeypatch):
+    monkeypatch.setattr(streaming, "MIN_BYTES", 1)
+    monkeypatch.setattr(streaming, "CHUNK_BYTES", 64 << 10)
+
+
+def test_blackscholes_streams():
+    S, X, T = wl.blackscholes_inputs(n=1 << 16)
+    call, put = wl.blackscholes(gp, gp.asarray(S), gp.asarray(X), gp.asarray(T))
+    p = streaming.plan([call.node, put.node])
+    assert p is not None and p.N == 1 << 16 and p.rows % streaming.ROW_ALIGN == 0 and p.rows < p.N
+    assert len(p.leaves) == 3
+
+
+def test_row_local_and_library_stream():
+    (x,) = wl.rownorm_inputs(rows=4096, cols=64)
+    y, tot = wl.rownorm(gp, gp.asarray(x))
+    assert streaming.plan([y.node]) is not None            # row statistics are row-local
+    assert streaming.plan([y.node, tot.node]) is None      # the total is a partial over rows
+    X, W1, b1, W2, b2 = wl.mlp_inputs(batch=4096, hidden=32)
+    p, lab = wl.mlp(gp, *[gp.asarray(a) for a in (X, W1, b1, W2, b2)])
+    assert streaming.plan([p.node, lab.node]) is not None  # X@W1 with W1 replicated
+
+
+def test_ineligible():
+    P, C = wl.kmeans_inputs(n=4096, k=8, d=4)
+    lab, sums, counts = wl.kmeans_partials(gp, gp.asarray(P), gp.asarray(C))
+    assert streaming.plan([lab.node] + [s.node for s in sums]) is None   # bincount partials
+    a = gp.asarray(np.arange(4096.0))
+    assert streaming.plan([(a * 2).sum().node]) is None                 # scalar root
+    assert streaming.plan([gp.cumsum(a * 2).node]) is None              # scan along the leading axis
+    small = gp.asarray(np.ones(100))
+    assert streaming.plan([(small + 1).node]) is None                   # too few rows
