@@ -23,9 +23,22 @@ template <class T, int V> union VecU {
 };
 
 // dst[0..V) = src[0..V); src aligned to sizeof(T)*V
+#ifdef GR_LDG_NOALLOC   // experiments: streaming loads that do not allocate in L1
+__device__ __forceinline__ uint4 ldg_na(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+template <class X> __device__ __forceinline__ X ldg_any(const X* p) { return __ldg(p); }
+template <> __device__ __forceinline__ uint4 ldg_any(const uint4* p) { return ldg_na(p); }
+#define GR_LDG ldg_any
+#else
+#define GR_LDG __ldg
+#endif
 template <class T, int V> __device__ __forceinline__ void ldv(T (&dst)[V], const T* __restrict__ src) {
   VecU<T, V> u;
-  u.raw = __ldg(reinterpret_cast<const typename RawVec<sizeof(T) * V>::T*>(src));
+  u.raw = GR_LDG(reinterpret_cast<const typename RawVec<sizeof(T) * V>::T*>(src));
 #pragma unroll
   for (int i = 0; i < V; ++i) dst[i] = u.v[i];
 }

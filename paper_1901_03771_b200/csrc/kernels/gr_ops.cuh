@@ -122,8 +122,10 @@ __device__ __forceinline__ T div_sh(T x, const DivShared<T>& d, bool& bad) {
     const T q0 = x * d.r;
     const T e = fma(-q0, d.s, x);
     const T q = fma(e, d.r, q0);
+#ifndef GR_DIVSH_NOCHECK   // experiments only (tools/variant_bench.py)
     const T ax = fabs(x);
     bad |= !(ax >= d.xlo && ax <= d.xhi);
+#endif
     return q;
   } else {
     (void)bad;

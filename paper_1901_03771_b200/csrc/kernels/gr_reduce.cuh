@@ -305,7 +305,12 @@ template <class Op, class T, int TPR> __device__ __forceinline__ T row_tree(T v,
 }
 
 // Leaf-level combine over the P parts then the row tree (float sums).
-template <class T, int VEC, int P, int TPR> __device__ __forceinline__ T row_sum(const T (&acc)[VEC], T* sh, int ri) {
+// TRAIL: end with a second row barrier so ``sh`` may be rewritten at once;
+// callers that pass another barrier of the row before reusing ``sh`` (a later
+// row reduction with its own ``sh``, or the CTA barrier that ends a row group)
+// skip it.
+template <class T, int VEC, int P, int TPR, bool TRAIL = true>
+__device__ __forceinline__ T row_sum(const T (&acc)[VEC], T* sh, int ri) {
   T s = leaf_local<T, VEC>(acc);
 #pragma unroll
   for (int m = 1; m < P; m <<= 1) s = add<T>(s, shfl_xor<T>(s, m));
@@ -325,7 +330,7 @@ template <class T, int VEC, int P, int TPR> __device__ __forceinline__ T row_sum
     for (int st = 1; st < NW; st <<= 1)
 #pragma unroll
       for (int w = 0; w + st < NW; w += 2 * st) buf[w] = add<T>(buf[w], buf[w + st]);
-    row_bar<TPR>(ri);
+    if constexpr (TRAIL) row_bar<TPR>(ri);
     s = buf[0];
   }
   return s;

@@ -103,7 +103,7 @@ class Executor:
             return outs
         k = c.get("kernel")
         if k is None:
-            k = self.rt.kernel(ks.source, ks.name, ks.block, ks.meta.get("smem", 0))
+            k = self.rt.kernel(ks.source, ks.name, ks.block, ks.meta.get("smem", 0), tune=ks.family == "map")
             if k.cache_hit == 0:
                 self.session.stats.compile_ms += k.compile_ms
             c["kernel"] = k

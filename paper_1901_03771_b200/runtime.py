@@ -285,10 +285,28 @@ class Runtime:
         return arr
 
     # -- compile / launch
-    def kernel(self, source: str, name: str, block: int, smem: int = 0) -> Kernel:
-        k = self._kernels.get((source, name))
+    def kernel(self, source: str, name: str, block: int, smem: int = 0, tune: bool = False) -> Kernel:
+        """Compile + load.  ``tune``: when the kernel sits a few registers above
+        an occupancy cliff, recompile with ``__launch_bounds__(block, occ+1)``
+        and keep that build if ptxas fits it without spilling."""
+        k = self._kernels.get((source, name, tune))
         if k is not None:
             return k
+        k = self._kernel(source, name, block, smem)
+        if tune and smem == 0:
+            want = k.blocks_per_sm + 1
+            cap = (65536 // (want * block)) // 8 * 8
+            tag = f"__launch_bounds__({block})"
+            if want * block <= 2048 and 0 < k.num_regs - cap <= 8 and tag in source:
+                k2 = self._kernel(source.replace(tag, f"__launch_bounds__({block}, {want})"), name, block, smem)
+                local = ctypes.c_int(0)
+                _check(self.lib.grumpy_rt_function_info(k2.fn, None, ctypes.byref(local), None, None))
+                if local.value == 0 and k2.blocks_per_sm > k.blocks_per_sm:
+                    k = k2
+        self._kernels[(source, name, tune)] = k
+        return k
+
+    def _kernel(self, source: str, name: str, block: int, smem: int = 0) -> Kernel:
         opts = nvrtc_options()
         arr = (ctypes.c_char_p * len(opts))(*opts)
         mod = ctypes.c_uint64(0)
@@ -303,9 +321,7 @@ class Runtime:
         regs = ctypes.c_int(0)
         _check(self.lib.grumpy_rt_function_info(fn.value, ctypes.byref(regs), None, None, None))
         self.compile_ms_total += ms.value
-        k = Kernel(fn.value, name, block, max(occ.value, 1), regs.value, ms.value, hit.value, source, mod.value)
-        self._kernels[(source, name)] = k
-        return k
+        return Kernel(fn.value, name, block, max(occ.value, 1), regs.value, ms.value, hit.value, source, mod.value)
 
     def launch(self, k: Kernel, grid, block, params: bytes, smem: int = 0, cluster: int = 1):
         gx, gy, gz = (grid, 1, 1) if isinstance(grid, int) else grid

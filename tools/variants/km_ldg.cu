@@ -1,0 +1,176 @@
+#include "gr_ops.cuh"
+#include "gr_mem.cuh"
+#include "gr_pair.cuh"
+
+#include "gr_reduce.cuh"
+
+__constant__ float __ldg(p.in1 + 256);
+
+struct K {
+  struct Params {
+    const float* __restrict__ in0;
+    const float* __restrict__ in1;
+    long long* __restrict__ out0;
+    double* __restrict__ out1;
+    double* __restrict__ out2;
+    double* __restrict__ out3;
+    double* __restrict__ out4;
+    long long* __restrict__ out5;
+    void* __restrict__ scratch;
+    unsigned int* ticket;
+  };
+  static constexpr long long NROWS = 67108864LL;
+  static __device__ __forceinline__ void row(const Params& p, const long long r, const bool valid, double* khist0, double* khist1, double* khist2, double* khist3, long long* khist4) {
+    (void)valid;
+    float a1 = 0;
+    long long a2 = 0;
+    float L7[4];
+    gr::ldv<float, 4>(L7, p.in0 + (4*r));
+    float a11 = 0;
+  #pragma unroll
+    for (long long i3 = 0; i3 < 64LL; ++i3) {
+      float a4 = gr::f32_bits(0x00000000u);
+      float a5 = gr::f32_bits(0x80000000u);
+  #pragma unroll
+      for (long long i6 = 0; i6 < 4LL; ++i6) {
+        const float t8 = __ldg(p.in1 + (4*i3 + i6));
+        const float t9 = gr::sub<float>(L7[i6], t8);
+        const float t10 = gr::square<float>(t9);
+        a5 = gr::add<float>(a5, t10);
+      }
+      a4 = gr::add<float>(a4, a5);
+      if (i3 == 0 || a4 < a1) { a1 = a4; a2 = i3; }
+      a11 = a11 + a4;
+    }
+    if (a11 != a11) {
+      for (long long i12 = 0; i12 < 64LL; ++i12) {
+        float a13 = gr::f32_bits(0x00000000u);
+        float a14 = gr::f32_bits(0x80000000u);
+  #pragma unroll
+        for (long long i15 = 0; i15 < 4LL; ++i15) {
+          const float t16 = __ldg(p.in1 + (4*i12 + i15));
+          const float t17 = gr::sub<float>(L7[i15], t16);
+          const float t18 = gr::square<float>(t17);
+          a14 = gr::add<float>(a14, t18);
+        }
+        a13 = gr::add<float>(a13, a14);
+        if (a13 != a13) { a1 = a13; a2 = i12; break; }
+      }
+    }
+    gr::st<long long>(p.out0 + r, a2);
+    const long long kkey = valid ? a2 : -1LL;
+    const float t19 = gr::ld<float>(p.in0 + (4*r));
+    const double t20 = gr::cast<double, float>(t19);
+    const double kw0 = t20;
+    const float t21 = gr::ld<float>(p.in0 + (4*r + 1));
+    const double t22 = gr::cast<double, float>(t21);
+    const double kw1 = t22;
+    const float t23 = gr::ld<float>(p.in0 + (4*r + 2));
+    const double t24 = gr::cast<double, float>(t23);
+    const double kw2 = t24;
+    const float t25 = gr::ld<float>(p.in0 + (4*r + 3));
+    const double t26 = gr::cast<double, float>(t25);
+    const double kw3 = t26;
+    const long long kw4 = 1LL;
+    const unsigned kpeers = __match_any_sync(0xffffffffu, (unsigned long long)kkey);
+    const unsigned klane = threadIdx.x & 31u;
+    const bool klead = (kpeers & ((1u << klane) - 1u)) == 0u;
+    unsigned krest = klead ? (kpeers & (kpeers - 1u)) : 0u;
+    double ks0 = kw0;
+    double ks1 = kw1;
+    double ks2 = kw2;
+    double ks3 = kw3;
+    while (__any_sync(0xffffffffu, krest != 0u)) {
+      const int ksrc = krest ? __ffs(krest) - 1 : (int)klane;
+      const double kv0 = __shfl_sync(0xffffffffu, kw0, ksrc);
+      const double kv1 = __shfl_sync(0xffffffffu, kw1, ksrc);
+      const double kv2 = __shfl_sync(0xffffffffu, kw2, ksrc);
+      const double kv3 = __shfl_sync(0xffffffffu, kw3, ksrc);
+      if (krest) {
+        ks0 += kv0;
+        ks1 += kv1;
+        ks2 += kv2;
+        ks3 += kv3;
+        krest &= krest - 1u;
+      }
+    }
+    if (klead && kkey >= 0) {
+      if (kkey < 64LL) khist0[(threadIdx.x >> 5) * 64 + kkey] += ks0;
+      if (kkey < 64LL) khist1[(threadIdx.x >> 5) * 64 + kkey] += ks1;
+      if (kkey < 64LL) khist2[(threadIdx.x >> 5) * 64 + kkey] += ks2;
+      if (kkey < 64LL) khist3[(threadIdx.x >> 5) * 64 + kkey] += ks3;
+      if (kkey < 64LL) khist4[(threadIdx.x >> 5) * 64 + kkey] += (long long)__popc(kpeers);
+    }
+  }
+};
+extern "C" __global__ void __launch_bounds__(128) gr_region(const K::Params p) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  __shared__ double khist0[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) khist0[i] = 0;
+  __shared__ double khist1[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) khist1[i] = 0;
+  __shared__ double khist2[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) khist2[i] = 0;
+  __shared__ double khist3[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) khist3[i] = 0;
+  __shared__ long long khist4[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) khist4[i] = 0;
+  __syncthreads();
+  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < K::NROWS; base += stride) {
+    const long long r = base + (threadIdx.x & 31);
+    K::row(p, r < K::NROWS ? r : K::NROWS - 1, r < K::NROWS, khist0, khist1, khist2, khist3, khist4);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+    double s = khist0[b];
+    for (int w = 1; w < 4; ++w) s += khist0[w * 64 + b];
+    reinterpret_cast<double*>(static_cast<char*>(p.scratch) + 0)[(long long)blockIdx.x * 64 + b] = s;
+  }
+  for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+    double s = khist1[b];
+    for (int w = 1; w < 4; ++w) s += khist1[w * 64 + b];
+    reinterpret_cast<double*>(static_cast<char*>(p.scratch) + 1212416)[(long long)blockIdx.x * 64 + b] = s;
+  }
+  for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+    double s = khist2[b];
+    for (int w = 1; w < 4; ++w) s += khist2[w * 64 + b];
+    reinterpret_cast<double*>(static_cast<char*>(p.scratch) + 2424832)[(long long)blockIdx.x * 64 + b] = s;
+  }
+  for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+    double s = khist3[b];
+    for (int w = 1; w < 4; ++w) s += khist3[w * 64 + b];
+    reinterpret_cast<double*>(static_cast<char*>(p.scratch) + 3637248)[(long long)blockIdx.x * 64 + b] = s;
+  }
+  for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+    long long s = khist4[b];
+    for (int w = 1; w < 4; ++w) s += khist4[w * 64 + b];
+    reinterpret_cast<long long*>(static_cast<char*>(p.scratch) + 4849664)[(long long)blockIdx.x * 64 + b] = s;
+  }
+  if (gr::last_block(p.ticket)) {
+    for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+      double s = 0;
+      for (unsigned c = 0; c < gridDim.x; ++c) s += reinterpret_cast<const double*>(static_cast<const char*>(p.scratch) + 0)[(long long)c * 64 + b];
+      p.out1[b] = s;
+    }
+    for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+      double s = 0;
+      for (unsigned c = 0; c < gridDim.x; ++c) s += reinterpret_cast<const double*>(static_cast<const char*>(p.scratch) + 1212416)[(long long)c * 64 + b];
+      p.out2[b] = s;
+    }
+    for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+      double s = 0;
+      for (unsigned c = 0; c < gridDim.x; ++c) s += reinterpret_cast<const double*>(static_cast<const char*>(p.scratch) + 2424832)[(long long)c * 64 + b];
+      p.out3[b] = s;
+    }
+    for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+      double s = 0;
+      for (unsigned c = 0; c < gridDim.x; ++c) s += reinterpret_cast<const double*>(static_cast<const char*>(p.scratch) + 3637248)[(long long)c * 64 + b];
+      p.out4[b] = s;
+    }
+    for (int b = threadIdx.x; b < 64; b += blockDim.x) {
+      long long s = 0;
+      for (unsigned c = 0; c < gridDim.x; ++c) s += reinterpret_cast<const long long*>(static_cast<const char*>(p.scratch) + 4849664)[(long long)c * 64 + b];
+      p.out5[b] = s;
+    }
+  }
+}
