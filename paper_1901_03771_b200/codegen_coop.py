@@ -99,9 +99,18 @@ class CoopEmitter(LoopEmitter):
             self.stmt(1, f"{T} {name}[16][{self.vec}];")
             if tma_layout is not None and leaf.id in tma_layout:
                 boff, ls, rowb = tma_layout[leaf.id]
+                idx = self.leaf_index[leaf.id]
+                if self.div_fast:
+                    self.stmt(1, "if constexpr (FAST) {")
                 self.stmt(1, f"{{ const {T}* sp = reinterpret_cast<const {T}*>(stage + {boff} + (long long)ri * {rowb}) + "
                              f"(tr / {self.P}) * {ls} + (tr % {self.P}) * {self.vec};")
                 self.stmt(1, f"#pragma unroll\n    for (int mm = 0; mm < 16; ++mm) gr::ldsv<{T}, {self.vec}>({name}[mm], sp + 8 * mm); }}")
+                if self.div_fast:
+                    # redo pass: the stage already holds the next group
+                    self.stmt(1, "} else {")
+                    self.stmt(1, f"#pragma unroll\n    for (int mm = 0; mm < 16; ++mm) "
+                                 f"gr::ldv<{T}, {self.vec}>({name}[mm], p.in{idx} + r * {self.C}LL + cb + 8 * mm);")
+                    self.stmt(1, "}")
             else:
                 idx = self.leaf_index[leaf.id]
                 self.stmt(1, f"#pragma unroll\n    for (int mm = 0; mm < 16; ++mm) "
@@ -340,7 +349,7 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
     rpc = block // tpr
     R = element_count(Ts)
     em = CoopEmitter(region, vec, tpr, rpc, Ts, C)
-    em.div_fast = tma is None and os.environ.get("GRUMPY_DIV_TWO_PASS", "1") != "0"
+    em.div_fast = os.environ.get("GRUMPY_DIV_TWO_PASS", "1") != "0"
     rvar = Var("r", 1)
     if len(Ts) == 1:
         row_coords = [Aff.of(rvar)]
@@ -371,7 +380,7 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
             # the stage is in registers now: release it and start the bulk copy
             # of the next row group, which then overlaps this group's compute
             em.stmt(1, "__syncthreads();")
-            em.stmt(1, "if (threadIdx.x < 32) { gr::fence_proxy_async(); if (gnext < NG) issue(p, stage, bar, gnext, threadIdx.x); }")
+            em.stmt(1, f"if ({'FAST' if em.div_fast else 'true'}) {{ gr::fence_proxy_async(); if (gnext < NG) issue(p, stage, bar, gnext, threadIdx.x); }}")
 
     # totals whose operand is itself a stored root accumulate in the store loop
     # (the value is computed once per element)
@@ -473,6 +482,9 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
     if tma:
         nleaf = C // 128
         total = sum(nleaf * 128 * l.dtype.itemsize for l in prestage)
+        # every thread issues its share of the per-leaf bulk copies: the copy
+        # instruction is uniform-operand, so one warp issuing them all
+        # serialises them (0.328 -> 0.251 ms on rownorm when spread)
         issue = ["static __device__ __forceinline__ void issue(const Params& p, unsigned char* stage, unsigned long long* bar, const long long g, const int lane) {",
                  f"  const long long nvalid = (g * {rpc} + {rpc} <= NROWS) ? {rpc} : (NROWS - g * {rpc});",
                  f"  if (lane == 0) gr::mbar_arrive_expect_tx(bar, (unsigned)(nvalid * {total}));"]
@@ -480,7 +492,7 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
             boff, ls, rowb = tma[l.id]
             lsb = ls * l.dtype.itemsize
             idx = region.leaves.index(l)
-            issue += [f"  for (int c = lane; c < {rpc * nleaf}; c += 32) {{",
+            issue += [f"  for (int c = lane; c < {rpc * nleaf}; c += {block}) {{",
                       f"    const int qq = c / {nleaf}, lf = c % {nleaf};",
                       f"    if (qq < nvalid) gr::bulk_g2s(stage + {boff} + (long long)qq * {rowb} + (long long)lf * {lsb}, "
                       f"p.in{idx} + (g * {rpc} + qq) * {C}LL + (long long)lf * 128, {128 * l.dtype.itemsize}u, bar);",
@@ -496,17 +508,25 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
     src.append("  " + "\n  ".join(lines))
     src.append("};")
     if tma:
-        kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
+        # residency is set by the stage size: cap registers to match it
+        tminb = max(1, min(4, (227 * 1024) // (smem_bytes + 2048)))
+        kern = [f'extern "C" __global__ void __launch_bounds__({block}, {tminb}) {kname}(const K::Params p) {{',
                 "  extern __shared__ __align__(128) unsigned char smem[];",
                 "  __shared__ unsigned long long bar;",
                 "  if (threadIdx.x == 0) { gr::mbar_init(&bar, 1); gr::fence_mbar_init(); }",
                 "  __syncthreads();",
                 "  long long g = blockIdx.x;",
-                "  if (threadIdx.x < 32 && g < K::NG) K::issue(p, smem, &bar, g, threadIdx.x);",
+                "  if (g < K::NG) K::issue(p, smem, &bar, g, threadIdx.x);",
                 "  for (int it = 0; g < K::NG; g += gridDim.x, ++it) {",
-                "    gr::mbar_wait(&bar, (unsigned)(it & 1));",
-                f"    K::rows(p, g * {rpc}, smem, &bar, g + gridDim.x);",
-                "  }"]
+                "    gr::mbar_wait(&bar, (unsigned)(it & 1));"]
+        if two_pass:
+            # the redo pass re-reads its rows from global memory: the stage
+            # already holds (or is receiving) the next row group
+            kern += [f"    if (__syncthreads_or(K::rows<true>(p, g * {rpc}, smem, &bar, g + gridDim.x)))",
+                     f"      K::rows<false>(p, g * {rpc}, smem, &bar, g + gridDim.x);"]
+        else:
+            kern.append(f"    K::rows(p, g * {rpc}, smem, &bar, g + gridDim.x);")
+        kern.append("  }")
     elif async_layout is not None:
         minb = int(os.environ.get("GRUMPY_COOP_MINBLOCKS", "3"))
         kern = [f'extern "C" __global__ void __launch_bounds__({block}, {minb}) {kname}(const K::Params p) {{',

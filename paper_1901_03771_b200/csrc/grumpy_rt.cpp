@@ -570,12 +570,23 @@ int grumpy_rt_function_info(uint64_t fn, int* num_regs, int* local_bytes, int* s
   return GR_OK;
 }
 
+// Kernels that stage through dynamic shared memory (bulk-copy rings) get the
+// whole unified L1/shared array as shared memory; the others keep the default
+// carve-out (maximum L1 for their LDG streams).
+static int smem_attrs(CUfunction f, size_t dyn_smem) {
+  if (dyn_smem > 48 * 1024)
+    CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem), "attr");
+  if (dyn_smem > 0)
+    CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100), "attr");
+  return GR_OK;
+}
+
 int grumpy_rt_occupancy(uint64_t fn, int block, size_t dyn_smem, int* blocks_per_sm) {
   int r = need_init();
   if (r) return r;
   CUfunction f = (CUfunction)(uintptr_t)fn;
-  if (dyn_smem > 48 * 1024)
-    CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem), "attr");
+  r = smem_attrs(f, dyn_smem);
+  if (r) return r;
   CU_CHECK(D.p_cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, f, block, dyn_smem), "occupancy");
   return GR_OK;
 }
@@ -586,8 +597,8 @@ int grumpy_rt_launch(uint64_t fn, unsigned gx, unsigned gy, unsigned gz, unsigne
   int r = need_init();
   if (r) return r;
   CUfunction f = (CUfunction)(uintptr_t)fn;
-  if (dyn_smem > 48 * 1024)
-    CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem), "attr");
+  r = smem_attrs(f, dyn_smem);
+  if (r) return r;
   size_t sz = params_size;
   void* extra[] = {CU_LAUNCH_PARAM_BUFFER_POINTER, const_cast<void*>(params), CU_LAUNCH_PARAM_BUFFER_SIZE, &sz,
                    CU_LAUNCH_PARAM_END};

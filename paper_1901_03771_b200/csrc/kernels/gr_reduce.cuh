@@ -274,9 +274,25 @@ template <class T, int VEC> __device__ __forceinline__ T leaf_local(const T (&a)
 // (>= rows_per_cta * TPR/32 elements).  Every thread of the row gets the result.
 // Barrier over the TPR threads of row slot ri only (named barrier 1 + ri):
 // the warps of one row wait for each other, not for the whole CTA.
+// GR_RPC (rows per CTA, set by the generated source) lets the barrier id be
+// an immediate: a register id makes ptxas reserve all 16 named barriers per
+// CTA, which caps residency at 4 CTAs per SM (ncu "Block Limit Barriers").
+#ifndef GR_RPC
+#define GR_RPC 0
+#endif
 template <int TPR> __device__ __forceinline__ void row_bar(int ri) {
-  if constexpr (TPR >= 1024) {
+  if constexpr (TPR >= 1024 || GR_RPC == 1) {
     __syncthreads();
+  } else if constexpr (GR_RPC == 2) {
+    if (ri == 0) asm volatile("bar.sync 1, %0;" ::"n"(TPR) : "memory");
+    else asm volatile("bar.sync 2, %0;" ::"n"(TPR) : "memory");
+  } else if constexpr (GR_RPC == 4) {
+    switch (ri) {
+      case 0: asm volatile("bar.sync 1, %0;" ::"n"(TPR) : "memory"); break;
+      case 1: asm volatile("bar.sync 2, %0;" ::"n"(TPR) : "memory"); break;
+      case 2: asm volatile("bar.sync 3, %0;" ::"n"(TPR) : "memory"); break;
+      default: asm volatile("bar.sync 4, %0;" ::"n"(TPR) : "memory"); break;
+    }
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(1 + ri), "n"(TPR) : "memory");
   }
