@@ -28,7 +28,7 @@ import os
 import struct
 from typing import Dict, List, Optional, Sequence, Tuple
 
-from .dag import ElemCode, Node, OpKind
+from .dag import ElemCode, Node, OpKind, ReduceOp
 from .errors import UnsupportedNodeInFusedStep
 from .tensor import DType, element_count, row_major_strides
 
@@ -260,6 +260,19 @@ class ValueEmitter:
 
     def cid(self, n: Node) -> int:
         return self.canon.get(n.id, n.id)
+
+    def _feeds_add(self, n: Node) -> bool:
+        """Does a packed add/sub/neg of this region consume ``n``?"""
+        cons = getattr(self, "_cons", None)
+        if cons is None:
+            cons = self._cons = {}
+            for m in self.region.nodes:
+                adds = ((m.op.kind is OpKind.MAP and m.op.code in (ElemCode.add, ElemCode.sub, ElemCode.neg))
+                        or (m.op.kind is OpKind.REDUCE and m.op.attrs[0] is ReduceOp.sum))
+                if adds:
+                    for q in m.preds:
+                        cons[self.cid(q)] = True   # hash-consed twins share the value
+        return cons.get(self.cid(n), False)
 
     def fresh(self, prefix="t"):
         self.counter += 1
@@ -590,17 +603,6 @@ class PairMapEmitter(MapEmitter):
                                                              OpKind.SLICE, OpKind.RESHAPE, OpKind.CAST):
             raise NotPairable(f"{n.op!r}")
         return super()._value(n, coords)
-
-    def _feeds_add(self, n: Node) -> bool:
-        """Does a packed add/sub/neg of this region consume ``n``?"""
-        cons = getattr(self, "_cons", None)
-        if cons is None:
-            cons = self._cons = {}
-            for m in self.region.nodes:
-                if m.op.kind is OpKind.MAP and m.op.code in (ElemCode.add, ElemCode.sub, ElemCode.neg):
-                    for q in m.preds:
-                        cons[self.cid(q)] = True   # hash-consed twins share the value
-        return cons.get(self.cid(n), False)
 
     def derived_var(self, level, expr):
         if level >= LEVEL_LANE:

@@ -25,12 +25,14 @@ registers) lives in ``codegen_coop.py``.
 
 from __future__ import annotations
 
+import os
 from typing import Dict, List, Optional, Sequence, Tuple
 
 from .codegen import (
-    HEADER, Aff, KernelSource, Region, ValueEmitter, Var, _params_struct, bcast_coords, c_literal,
+    _PAIR_BIN, _PAIR_UN, HEADER, Aff, KernelSource, NotPairable, Region, ValueEmitter, Var, _params_struct,
+    bcast_coords, c_literal,
 )
-from .dag import Node, OpKind, ReduceOp
+from .dag import ElemCode, Node, OpKind, ReduceOp
 from .errors import UnsupportedNodeInFusedStep
 from .tensor import DType, element_count, row_major_strides
 
@@ -144,6 +146,12 @@ class LoopEmitter(ValueEmitter):
         # the same (row-independent) offsets, e.g. the k-means centroids
         self.cbank: Dict[int, str] = dict(cbank or {})
         self.uniform_vars = set()   # loop indices with row-independent values
+        # loop pairing: an unrolled f32 arg-reduction loop walks index PAIRS
+        # (2i, 2i+1); values that depend on the logical index (2*iv + half)
+        # are gr::f2 and run as FADD2/FMUL2/FFMA2 (gr_pair.cuh)
+        self.pair_loops = False
+        self.half: Optional[Var] = None
+        self.pairs = set()            # emitted names holding a gr::f2
 
     # -- scopes ------------------------------------------------------------------
     def emit(self, level, ctype, expr):
@@ -229,6 +237,19 @@ class LoopEmitter(ValueEmitter):
         ptr = f"p.in{idx}"
         lvl = off.level
         sym = self.cbank.get(leaf.id)
+        if self.half is not None and off.coef(self.half):
+            # the two logical indices of a paired loop
+            if leaf.dtype is not DType.f32:
+                raise NotPairable("non-f32 leaf in a paired loop")
+            lo = off.without(self.half)
+            hi = lo + off.coef(self.half)
+            if sym is not None:
+                if any(v.name not in self.uniform_vars for v, _ in lo.terms):
+                    raise CBankMiss(leaf)
+                a, b = f"{sym}[{lo.c()}]", f"{sym}[{hi.c()}]"
+            else:
+                a, b = f"gr::ld<{T}>({ptr} + {lo.c()})", f"gr::ld<{T}>({ptr} + {hi.c()})"
+            return self.emit_pair(lvl, f"gr::pk({a}, {b})"), lvl
         if sym is not None:
             if any(v.name not in self.uniform_vars for v, _ in off.terms):
                 raise CBankMiss(leaf)
@@ -263,7 +284,48 @@ class LoopEmitter(ValueEmitter):
                 return self.reduce(n, coords)
             if n.kind is OpKind.ARGREDUCE:
                 return self.argreduce(n, coords)
+            if (self.half is not None and n.kind is OpKind.MAP and n.op.code is not ElemCode.const_splat
+                    and any(c.coef(self.half) for c in coords)):
+                return self._pair_map(n, coords)
         return super()._value(n, coords)
+
+    # -- paired loops ---------------------------------------------------------------
+    def emit_pair(self, level, expr) -> str:
+        name = self.emit(level, "gr::f2", expr)
+        self.pairs.add(name)
+        return name
+
+    def is_pair(self, val) -> bool:
+        return val[0] in self.pairs
+
+    def splat(self, val) -> str:
+        return val[0] if self.is_pair(val) else f"gr::splat({val[0]})"
+
+    def cast(self, val, frm: DType, to: DType):
+        if frm is not to and self.is_pair(val):
+            raise NotPairable("cast of a paired value")
+        return super().cast(val, frm, to)
+
+    def _pair_map(self, n: Node, coords):
+        code = n.op.code
+        args = []
+        for p, lt in zip(n.preds, n.loop):
+            v = self.value(p, bcast_coords(coords, n.shape, p.shape))
+            args.append(self.cast(v, p.dtype, lt))
+        lvl = max(a[1] for a in args)
+        if not any(self.is_pair(a) for a in args):
+            return super()._value(n, coords)
+        if n.dtype is not DType.f32 or any(lt is not DType.f32 for lt in n.loop):
+            raise NotPairable(f"{code} on {n.loop}")
+        names = [self.splat(a) for a in args]
+        if code in (ElemCode.mul, ElemCode.square) and self._feeds_add(n):
+            fn = "gr::p2::mul_nc" if code is ElemCode.mul else "gr::p2::square_nc"
+            return self.emit_pair(lvl, f"{fn}({', '.join(names)})"), lvl
+        if code in (ElemCode.add, ElemCode.sub, ElemCode.mul, ElemCode.div, ElemCode.maximum, ElemCode.minimum):
+            return self.emit_pair(lvl, f"{_PAIR_BIN[code]}({names[0]}, {names[1]})"), lvl
+        if code in _PAIR_UN:
+            return self.emit_pair(lvl, f"{_PAIR_UN[code]}({names[0]})"), lvl
+        raise NotPairable(f"no packed form for {code}")
 
     def _operand_coords(self, r: Node, coords, axes, keepdims):
         x = r.preds[0]
@@ -312,6 +374,8 @@ class LoopEmitter(ValueEmitter):
         if nred == 0:
             return self.const(_IDENT[rop](T), T)
         ident = c_literal(_IDENT[rop](T), T)
+        if self.half is not None and any(c.coef(self.half) for c in kept):
+            return self._reduce_pair(r, x, kept, L)
         acc = self.var_decl(L, ct, ident)
         # coalesce: NumPy merges adjacent reduced axes; the innermost group is
         # pairwise-summed when it contains the last (contiguous) axis.
@@ -371,6 +435,29 @@ class LoopEmitter(ValueEmitter):
         self.close_all(opened)
         return acc, L
 
+    def _reduce_pair(self, r: Node, x: Node, kept, L):
+        """A reduction evaluated for both indices of a paired loop: sums of f32
+        along a short contiguous axis (NumPy's sequential n < 8 fold from -0.0,
+        then the 0.0 identity), as packed adds."""
+        rop, axes, keepdims, odt = r.op.attrs
+        T = r.dtype
+        So = x.shape
+        if (rop is not ReduceOp.sum or T is not DType.f32 or x.dtype is not DType.f32
+                or list(axes) != [len(So) - 1] or So[-1] >= 8):
+            raise NotPairable("paired reduction other than a short f32 sum")
+        n = So[-1]
+        acc = self.fresh("a")
+        self.stmt(L, f"gr::f2 {acc} = gr::splat({c_literal(0, T)});")
+        part = self.fresh("a")
+        self.stmt(L, f"gr::f2 {part} = gr::splat({c_literal(-0.0, T)});")
+        self.pairs.update((acc, part))
+        iv, s, saved = self.open(L, "for", trip=n, unroll=True)
+        v = self.value(x, list(kept) + [Aff.of(iv)])
+        self.stmt(iv.level, f"{part} = gr::p2::add({part}, {self.splat(v)});")
+        self.close(s, saved)
+        self.stmt(L, f"{acc} = gr::p2::add({acc}, {part});")
+        return acc, L
+
     def _delin(self, iv: Var, group, gdims) -> Dict[int, Aff]:
         if len(group) == 1:
             return {group[0]: Aff.of(iv)}
@@ -383,6 +470,12 @@ class LoopEmitter(ValueEmitter):
                 out[a] = Aff.of(self.derived_var(iv.level, f"{rest.c()} % {ext}"))
                 rest = Aff.of(self.derived_var(iv.level, f"{rest.c()} / {ext}"))
         return out
+
+    def _delin_pair(self, iv: Var, group, gdims) -> Dict[int, Aff]:
+        """Coordinates of the logical index 2*iv + half along one axis."""
+        if len(group) != 1:
+            raise NotPairable("paired loop over merged axes")
+        return {group[0]: Aff.of(iv).scale(2) + Aff.of(self.half)}
 
     def argreduce(self, r: Node, coords):
         which, axis, keepdims = r.op.attrs
@@ -424,14 +517,44 @@ class LoopEmitter(ValueEmitter):
         # floats: the scan is a plain ordered compare (first index wins ties)
         # plus one add whose result is NaN whenever an operand is NaN; only
         # then is the operand rescanned for np.argmax's answer, its first NaN
-        nacc = self.var_decl(L, T, "0")
         cmp = ">" if which == "max" else "<"
-        self.stmt(iv.level, f"if ({iv.name} == 0 || {v[0]} {cmp} {best}) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
-        self.stmt(iv.level, f"{nacc} = {nacc} + {v[0]};")
-        self.close(s, saved)
+        if self.pair_loops and n % 2 == 0 and n <= ARG_UNROLL and x.dtype is DType.f32 and self.half is None:
+            # paired scan: drop the scalar loop opened above and walk pairs
+            self.close(s, saved)
+            self.stack[L].lines.pop()
+            nacc = self.fresh("a")
+            self.stmt(L, f"gr::f2 {nacc} = gr::splat(0.0f);")
+            iv, s, saved = self.open(L, "for", trip=n // 2, unroll=True)
+            self.half = Var("gr_half_" + iv.name, iv.level)
+            try:
+                inner = self._delin_pair(iv, list(axes), [So[a] for a in axes])
+                full = []
+                k = 0
+                for i in range(len(So)):
+                    if i in inner:
+                        full.append(inner[i])
+                    else:
+                        full.append(kept[k])
+                        k += 1
+                v = self.value(x, full)
+            finally:
+                self.half = None
+            pv = self.splat(v)
+            self.stmt(iv.level, f"{{ const float vlo = gr::lo({pv}), vhi = gr::hi({pv}); "
+                                f"if ({iv.name} == 0 || vlo {cmp} {best}) {{ {best} = vlo; {bi} = 2 * {iv.name}; }} "
+                                f"if (vhi {cmp} {best}) {{ {best} = vhi; {bi} = 2 * {iv.name} + 1; }} }}")
+            self.stmt(iv.level, f"{nacc} = gr::p2::add({nacc}, {pv});")
+            self.close(s, saved)
+            nan_test = f"gr::lo({nacc}) != gr::lo({nacc}) || gr::hi({nacc}) != gr::hi({nacc})"
+        else:
+            nacc = self.var_decl(L, T, "0")
+            self.stmt(iv.level, f"if ({iv.name} == 0 || {v[0]} {cmp} {best}) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
+            self.stmt(iv.level, f"{nacc} = {nacc} + {v[0]};")
+            self.close(s, saved)
+            nan_test = f"{nacc} != {nacc}"
         saved_if = self.stack[L + 1:]
         del self.stack[L + 1:]
-        sif = Scope(L + 1, "for", header=f"if ({nacc} != {nacc})")
+        sif = Scope(L + 1, "for", header=f"if ({nan_test})")
         self.stack.append(sif)
         iv2, s2, saved2 = self.open(L + 1, "for", trip=n)
         v2 = operand(iv2)
@@ -574,18 +697,31 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
     bank (retried without a leaf that turns out to be read per row)."""
     Ts, _totals, virtual = thread_space(region)
     cbank = cbank_candidates(region, element_count(Ts)) if virtual is None else {}
+    pair = PAIR_LOOPS
     while True:
         try:
-            return _gen_rows(region, kname, block, cbank)
+            return _gen_rows(region, kname, block, cbank, pair)
         except CBankMiss as e:
             del cbank[e.leaf.id]
+        except NotPairable:
+            pair = False
 
 
-def _gen_rows(region: Region, kname, block, cbank) -> KernelSource:
+# Paired arg-reduction loops are exact but off by default: on B200 a packed
+# FADD2/FFMA2 occupies the 32-lane FMA pipe for two cycles, so they only save
+# issue slots, and the paired constant operands need a pair-adjacent layout
+# (measured on k-means 2^26 x 64: scalar 3.25 ms; pairs from the leaf layout
+# 4.14 ms at 254 regs; pairs from a pair-adjacent smem copy 2.99 ms at 44 regs,
+# FMA pipe 65% — profiles/r01s2_kmeans_variants.md).
+PAIR_LOOPS = os.environ.get("GRUMPY_PAIR_LOOPS", "0") == "1"
+
+
+def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
     Ts, totals, virtual = thread_space(region)
     tot_ids = {t.id for t in totals}
     R = element_count(Ts)
     em = LoopEmitter(region, cbank=cbank)
+    em.pair_loops = pair
     rvar = Var("r", 1)
     # row coordinates
     if virtual is None:

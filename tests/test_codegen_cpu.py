@@ -100,6 +100,31 @@ def test_kmeans_keyed(sess):
     assert ks.meta["keyed"] == 5 and "__shfl_sync" in ks.source
 
 
+def test_kmeans_constant_bank_and_match_any(sess):
+    """Centroids (row-invariant, 4 KB) go to the constant bank; the keyed sums
+    use warp groups of equal keys; the 64-way argmin is unrolled."""
+    P, C = (gp.asarray(v) for v in wl.kmeans_inputs(n=8192, k=64, d=4))
+    lab, sums, counts = wl.kmeans_partials(gp, P, C)
+    (ks, _), = kernels([lab, *sums, counts])
+    assert ks.meta["cbank"] and "__constant__ float gr_cin1[256];" in ks.source
+    assert "__match_any_sync" in ks.source and "__popc(kpeers)" in ks.source
+    # a leaf read per row is never staged in the constant bank
+    x = gp.asarray(np.ones((8192, 8), np.float32))
+    (ks2, _), = kernels([(x * 2.0).argmax(1)])
+    assert not ks2.meta["cbank"]
+
+
+def test_paired_argmin_loop_compiles(sess, monkeypatch):
+    from paper_1901_03771_b200 import codegen_rows
+    monkeypatch.setattr(codegen_rows, "PAIR_LOOPS", True)
+    codegen._GEN_CACHE.clear()
+    P, C = (gp.asarray(v) for v in wl.kmeans_inputs(n=8192, k=64, d=4))
+    lab = wl.kmeans_assign(gp, P, C)
+    (ks, cubin), = kernels([lab])
+    assert "gr::p2::square_nc" in ks.source and "2 * i" in ks.source and cubin
+    codegen._GEN_CACHE.clear()
+
+
 def test_views_and_slice_assign(sess):
     rng = np.random.default_rng(1)
     a = gp.asarray(rng.standard_normal((66, 66)))

@@ -184,3 +184,20 @@ def test_bincount_collisions(sess, nkeys):
     np.testing.assert_allclose(np.asarray(g), np.bincount(k, weights=w, minlength=64), rtol=1e-12, atol=1e-9)
     c = gp.bincount(gp.asarray(k), minlength=64)
     assert np.array_equal(np.asarray(c), np.bincount(k, minlength=64))
+
+
+def test_kmeans_paired_loop_exact(sess, monkeypatch):
+    """The (off by default) paired argmin loop keeps np.argmin's answer."""
+    from paper_1901_03771_b200 import codegen, codegen_rows
+    monkeypatch.setattr(codegen_rows, "PAIR_LOOPS", True)
+    codegen._GEN_CACHE.clear()
+    try:
+        P, C = wl.kmeans_inputs(n=8192 + 5, k=64, d=4)
+        P[10, 2] = np.nan
+        C[7] = C[3]
+        lab = wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C))
+        got = np.asarray(lab)
+        assert "gr::p2::" in sess.executor.last_steps[0].cache["ks"].source
+        assert np.array_equal(got, wl.kmeans_assign(np, P, C))
+    finally:
+        codegen._GEN_CACHE.clear()

@@ -4,7 +4,7 @@
 
 #include "gr_reduce.cuh"
 
-__constant__ float gr_cin1[256];
+__shared__ __align__(16) float gr_cin1[256];
 
 struct K {
   struct Params {
@@ -33,7 +33,7 @@ struct K {
       gr::f2 a14 = gr::splat(gr::f32_bits(0x80000000u));
   #pragma unroll
       for (long long i15 = 0; i15 < 4LL; ++i15) {
-        const gr::f2 t16 = gr::pk(gr_cin1[(8*i12 + i15)], gr_cin1[(8*i12 + i15 + 4)]);
+        const gr::f2 t16 = gr::f2{*reinterpret_cast<const unsigned long long*>(&gr_cin1[(i12 * 4 + i15) * 2])};
         const gr::f2 t17 = gr::p2::sub(gr::splat(L7[i15]), t16);
         const gr::f2 t18 = gr::p2::square_nc(t17);
         a14 = gr::p2::add(a14, t18);
@@ -105,6 +105,11 @@ struct K {
 };
 extern "C" __global__ void __launch_bounds__(128) gr_region(const K::Params p) {
   const long long stride = (long long)gridDim.x * blockDim.x;
+  for (int e = threadIdx.x; e < 256; e += blockDim.x) {
+    const int q = e / 8, d = (e / 2) % 4, h = e % 2;
+    gr_cin1[e] = p.in1[(2 * q + h) * 4 + d];
+  }
+  __syncthreads();
   __shared__ double khist0[256];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) khist0[i] = 0;
   __shared__ double khist1[256];

@@ -22,6 +22,7 @@ struct K {
   static constexpr long long NROWS = 67108864LL;
   static __device__ __forceinline__ void row(const Params& p, const long long r, const bool valid, double* khist0, double* khist1, double* khist2, double* khist3, long long* khist4) {
     (void)valid;
+    int gz; asm volatile("mov.u32 %0, 0;" : "=r"(gz));
     float a1 = 0;
     long long a2 = 0;
     float L7[4];
@@ -33,7 +34,7 @@ struct K {
       gr::f2 a14 = gr::splat(gr::f32_bits(0x80000000u));
   #pragma unroll
       for (long long i15 = 0; i15 < 4LL; ++i15) {
-        const gr::f2 t16 = gr::pk(gr_cin1[(8*i12 + i15)], gr_cin1[(8*i12 + i15 + 4)]);
+        const gr::f2 t16 = gr::f2{*reinterpret_cast<const unsigned long long*>(&gr_cin1[(i12 * 4 + i15) * 2 + gz])};
         const gr::f2 t17 = gr::p2::sub(gr::splat(L7[i15]), t16);
         const gr::f2 t18 = gr::p2::square_nc(t17);
         a14 = gr::p2::add(a14, t18);
