@@ -104,6 +104,13 @@ int grumpy_rt_get_function(uint64_t module, const char* name, uint64_t* fn);
  * (constant-bank staging of small row-invariant leaves; filled with
  * grumpy_rt_d2d on the runtime stream before each launch). */
 int grumpy_rt_module_global(uint64_t module, const char* name, uint64_t* dptr, size_t* bytes);
+/* Encode a 2-D tiled TMA descriptor (CUtensorMap, 128 bytes written to
+ * `out128`) for a row-major tensor [dim1][dim0] of `dtype` at `gaddr` whose
+ * rows are `stride1` bytes apart; box = [box1][box0] elements; `swizzle` =
+ * 0, 32, 64 or 128 (bytes).  Passed to kernels inside their by-value
+ * parameter block (__grid_constant__) for cp.async.bulk.tensor loads. */
+int grumpy_rt_tensor_map_2d(uint64_t gaddr, int dtype, uint64_t dim0, uint64_t dim1, uint64_t stride1,
+                            unsigned box0, unsigned box1, int swizzle, void* out128);
 int grumpy_rt_function_info(uint64_t fn, int* num_regs, int* local_bytes,
                             int* static_smem, int* max_threads);
 int grumpy_rt_occupancy(uint64_t fn, int block, size_t dyn_smem, int* blocks_per_sm);

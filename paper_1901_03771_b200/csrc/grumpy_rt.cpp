@@ -69,6 +69,7 @@ int fail(int code, const std::string& msg) {
   X(cuModuleLoadData)                \
   X(cuModuleGetFunction)             \
   X(cuModuleGetGlobal)               \
+  X(cuTensorMapEncodeTiled)          \
   X(cuFuncGetAttribute)              \
   X(cuFuncSetAttribute)              \
   X(cuOccupancyMaxActiveBlocksPerMultiprocessor) \
@@ -556,6 +557,40 @@ int grumpy_rt_module_global(uint64_t module, const char* name, uint64_t* dptr, s
   CU_CHECK(D.p_cuModuleGetGlobal(&p, &n, (CUmodule)(uintptr_t)module, name), "cuModuleGetGlobal");
   *dptr = (uint64_t)p;
   if (bytes) *bytes = n;
+  return GR_OK;
+}
+
+int grumpy_rt_tensor_map_2d(uint64_t gaddr, int dtype, uint64_t dim0, uint64_t dim1, uint64_t stride1,
+                            unsigned box0, unsigned box1, int swizzle, void* out128) {
+  int r = load_driver();
+  if (r) return r;
+  CUtensorMapDataType dt;
+  switch (dtype) {
+    case GR_F32: dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT32; break;
+    case GR_F64: dt = CU_TENSOR_MAP_DATA_TYPE_FLOAT64; break;
+    case GR_I32: dt = CU_TENSOR_MAP_DATA_TYPE_INT32; break;
+    case GR_I64: dt = CU_TENSOR_MAP_DATA_TYPE_INT64; break;
+    case GR_BOOL: dt = CU_TENSOR_MAP_DATA_TYPE_UINT8; break;
+    default: return fail(GR_EINVAL, "tensor map: bad dtype");
+  }
+  CUtensorMapSwizzle sw;
+  switch (swizzle) {
+    case 0: sw = CU_TENSOR_MAP_SWIZZLE_NONE; break;
+    case 32: sw = CU_TENSOR_MAP_SWIZZLE_32B; break;
+    case 64: sw = CU_TENSOR_MAP_SWIZZLE_64B; break;
+    case 128: sw = CU_TENSOR_MAP_SWIZZLE_128B; break;
+    default: return fail(GR_EINVAL, "tensor map: swizzle must be 0, 32, 64 or 128");
+  }
+  const cuuint64_t dims[2] = {dim0, dim1};
+  const cuuint64_t strides[1] = {stride1};
+  const cuuint32_t box[2] = {box0, box1};
+  const cuuint32_t estr[2] = {1, 1};
+  CUtensorMap m;
+  CU_CHECK(D.p_cuTensorMapEncodeTiled(&m, dt, 2, (void*)(uintptr_t)gaddr, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
+           "cuTensorMapEncodeTiled");
+  memcpy(out128, &m, sizeof(m));
   return GR_OK;
 }
 

@@ -55,6 +55,25 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// TMA tensor copies: the 128-byte CUtensorMap built on the host
+// (grumpy_rt_tensor_map_2d) travels in the kernel's __grid_constant__
+// parameter block; one instruction moves a whole box (e.g. a 16 KB row).
+struct alignas(64) TMap {
+  unsigned long long v[16];
+};
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const TMap* map, int x, int y, unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Byte offset of 16-byte chunk `c` (0..7) of 128-byte line `L` inside a box
+// stored with CU_TENSOR_MAP_SWIZZLE_128B (1024-byte aligned atoms).
+__device__ __forceinline__ unsigned sw128(unsigned L, unsigned c) { return L * 128u + ((c ^ (L & 7u)) << 4); }
+
 // Bulk prefetch of [src, src+bytes) into L2 (no shared memory, no completion):
 // later LDGs of that range hit L2 instead of HBM.
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {

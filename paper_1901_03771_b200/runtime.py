@@ -62,6 +62,7 @@ SIGNATURES = {
     "grumpy_rt_compile_cubin": [_cp, _cpp, _i, _p, _sz, _szp, _dp],
     "grumpy_rt_get_function": [_u64, _cp, _u64p],
     "grumpy_rt_module_global": [_u64, _cp, _u64p, ctypes.POINTER(ctypes.c_size_t)],
+    "grumpy_rt_tensor_map_2d": [_u64, _i, _u64, _u64, _u64, ctypes.c_uint, ctypes.c_uint, _i, _p],
     "grumpy_rt_function_info": [_u64, _ip, _ip, _ip, _ip],
     "grumpy_rt_occupancy": [_u64, _i, _sz, _ip],
     "grumpy_rt_launch": [_u64, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint,
@@ -253,6 +254,14 @@ class Runtime:
         n = ctypes.c_size_t(0)
         _check(self.lib.grumpy_rt_module_global(k.module, name.encode(), ctypes.byref(p), ctypes.byref(n)))
         return p.value, n.value
+
+    def tensor_map_2d(self, gaddr: int, dtype: DType, dim0: int, dim1: int, stride1: int,
+                      box0: int, box1: int, swizzle: int = 128) -> bytes:
+        """128-byte CUtensorMap for a row-major [dim1][dim0] tensor (TMA)."""
+        buf = ctypes.create_string_buffer(128)
+        _check(self.lib.grumpy_rt_tensor_map_2d(gaddr, GR_DTYPE[dtype], dim0, dim1, stride1, box0, box1,
+                                                swizzle, buf))
+        return buf.raw
 
     def d2d_raw(self, dst: int, src: int, nbytes: int):
         _check(self.lib.grumpy_rt_d2d(dst, src, nbytes))

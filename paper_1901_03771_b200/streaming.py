@@ -15,8 +15,9 @@ three streams:
 
 so H2D(c+1), kernels(c) and D2H(c-1) overlap.  Eligibility is the sharding
 analysis of distributed.py with the host inputs as the sharded set: every
-forced root must be *sharded* (row-local along the leading axis), nothing
-partial (no reduction over the leading axis, no bincount).  Each chunk re-
+forced root is *sharded* (row-local along the leading axis) or a partial over
+it (a total, a reduction over axis 0, a bincount): partials are combined
+across chunks in a binary tree over chunk order once the last chunk ran.  Each chunk re-
 records the DAG on row slices (same ops, leading extent rewritten), so each
 chunk's region is the same fused kernel as the whole force, and results are
 bit-identical to the unchunked force (rows are independent).  Inputs and
@@ -32,7 +33,7 @@ from typing import Dict, List, Optional, Sequence
 
 import numpy as np
 
-from .dag import Node, Op, OpKind
+from .dag import ElemCode, Node, Op, OpKind
 from .errors import LazyFuseError
 from .tensor import TensorBuffer, element_count
 
@@ -41,7 +42,7 @@ MIN_BYTES = 48 << 20        # smaller forces gain nothing from overlap
 ROW_ALIGN = 256             # chunk row counts: 16-byte aligned views, full vectors
 
 _ALLOWED = {OpKind.MAP, OpKind.CAST, OpKind.BROADCAST, OpKind.TRANSPOSE, OpKind.RESHAPE,
-            OpKind.SLICE, OpKind.REDUCE, OpKind.ARGREDUCE, OpKind.MATMUL, OpKind.MATVEC}
+            OpKind.SLICE, OpKind.REDUCE, OpKind.ARGREDUCE, OpKind.MATMUL, OpKind.MATVEC, OpKind.KEYED_SUM}
 
 
 class DeviceView:
@@ -79,32 +80,47 @@ def _walk(roots: Sequence[Node]):
     return order, list(frontier.values())
 
 
+_COMBINE = {"sum": ElemCode.add, "prod": ElemCode.mul, "max": ElemCode.maximum, "min": ElemCode.minimum}
+
+
 def plan(roots: Sequence[Node], chunk_bytes: Optional[int] = None) -> Optional[StreamPlan]:
-    """A chunked plan for forcing ``roots`` to host, or None if ineligible."""
+    """A chunked plan for forcing ``roots`` to host, or None if ineligible.
+
+    Roots are row-local along the streamed axis ("S": their leading extent is
+    the host inputs') or partials over it ("P:<op>": full/leading-axis
+    reductions and bincounts, combined across chunks after the last chunk)."""
     from . import distributed as D
     chunk_bytes = chunk_bytes or CHUNK_BYTES
     roots = list(dict((r.id, r) for r in roots).values())
-    if not roots or any(r.is_materialized or not r.shape for r in roots):
-        return None
-    N = roots[0].shape[0]
-    if N < 2 * ROW_ALIGN or any(r.shape[0] != N for r in roots):
+    if not roots or any(r.is_materialized for r in roots):
         return None
     nodes, frontier = _walk(roots)
     if any(n.kind not in _ALLOWED for n in nodes if n.preds):
         return None
-    leaves = [f for f in frontier if f.data.device is None and f.data.host is not None
-              and f.shape and f.shape[0] == N]
-    if not leaves:
+    host = [f for f in frontier if f.data.device is None and f.data.host is not None and f.shape]
+    if not host:
+        return None
+    N = max(host, key=lambda f: f.data.nbytes).shape[0]
+    leaves = [f for f in host if f.shape[0] == N]
+    if N < 2 * ROW_ALIGN:
         return None
     try:
         dist = D.classify(roots, sharded={l.id for l in leaves})
     except LazyFuseError:
         return None
-    if any(dist.get(r.id) != "S" for r in roots):
-        return None
-    if any(dist.get(n.id, "R")[0] in "PA" for n in nodes):
-        return None
-    total = sum(l.data.nbytes for l in leaves) + sum(element_count(r.shape) * r.dtype.itemsize for r in roots)
+    root_ids = {r.id for r in roots}
+    for r in roots:
+        d = dist.get(r.id, "R")
+        if d == "S":
+            if not r.shape or r.shape[0] != N:
+                return None
+        elif not (d.startswith("P:") and d[2:] in _COMBINE):
+            return None
+    for n in nodes:
+        if n.id not in root_ids and dist.get(n.id, "R")[0] in "PA":
+            return None                      # a partial consumed inside the region
+    srows = [r for r in roots if dist[r.id] == "S"]
+    total = sum(l.data.nbytes for l in leaves) + sum(element_count(r.shape) * r.dtype.itemsize for r in srows)
     if total < MIN_BYTES:
         return None
     per_row = total / N
@@ -163,9 +179,11 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
     st = _streams(rt)
     g = sess.graph
     N, rows = p.N, p.rows
-    # full-size device buffers: inputs and results (chunks are views)
+    srows = [r for r in p.roots if p.dist[r.id] == "S"]
+    parts = {r.id: [] for r in p.roots if p.dist[r.id] != "S"}   # per-chunk partial nodes
+    # full-size device buffers: inputs and row-local results (chunks are views)
     dev_in = {l.id: rt.alloc(l.data.nbytes) for l in p.leaves}
-    dev_out = {r.id: rt.alloc(element_count(r.shape) * r.dtype.itemsize) for r in p.roots}
+    dev_out = {r.id: rt.alloc(element_count(r.shape) * r.dtype.itemsize) for r in srows}
     for l in p.leaves:
         if not l.data.host.flags.c_contiguous:
             return None
@@ -210,20 +228,23 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
                 buf = TensorBuffer(l.dtype, (c,) + tuple(l.shape[1:]), device=DeviceView(dev_in[l.id], lo * rb, c * rb))
                 memo[l.id] = g.add_input(buf)
             for n in p.nodes:
-                if p.dist.get(n.id, "R") == "S":
+                if p.dist.get(n.id, "R") == "S" or n.id in parts:
                     memo[n.id] = g.add_op(_rewrite(n.op, c), [memo.get(q.id, q) for q in n.preds])
             croots = [memo[r.id] for r in p.roots]
             views = {}
             for r, cr in zip(p.roots, croots):
-                rb = _row_bytes(r)
-                views[cr.id] = TensorBuffer(cr.dtype, cr.shape, device=DeviceView(dev_out[r.id], lo * rb, c * rb))
+                if r.id in dev_out:
+                    rb = _row_bytes(r)
+                    views[cr.id] = TensorBuffer(cr.dtype, cr.shape, device=DeviceView(dev_out[r.id], lo * rb, c * rb))
             ex.out_bind = dict(views)
             try:
                 sess.force_nodes(croots)
             finally:
                 ex.out_bind = {}
             for r, cr in zip(p.roots, croots):
-                if cr.data is not views[cr.id]:
+                if r.id in parts:
+                    parts[r.id].append(cr)
+                elif cr.data is not views[cr.id]:
                     # produced by a library call (cuBLAS output): move it in
                     rb = _row_bytes(r)
                     rt.d2d_raw(dev_out[r.id].ptr + lo * rb, cr.data.device.ptr, c * rb)
@@ -238,6 +259,8 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
             rt.set_stream(st.d2h)
             rt.wait_event(e_k)
             for r, o in zip(p.roots, outs):
+                if r.id not in dev_out:
+                    continue
                 rb = _row_bytes(r)
                 rt.d2h_async(o[lo:lo + c], dev_out[r.id].ptr + lo * rb)
                 sess.stats.d2h_bytes += c * rb
@@ -251,6 +274,22 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
             if ci + 1 < len(chunks):
                 e_in.append(stage_in(ci + 1))
             stage_out(ci, e_k)
+        # partials: combine the chunks' values in a binary tree over chunk
+        # order (one small fused map kernel, on the runtime stream after the
+        # chunk kernels)
+        finals = {}
+        for r in p.roots:
+            if r.id in parts:
+                code = _COMBINE[p.dist[r.id][2:]]
+                level = list(parts[r.id])
+                while len(level) > 1:
+                    nxt = [g.add_op(Op(OpKind.MAP, code), [level[i], level[i + 1]]) for i in range(0, len(level) - 1, 2)]
+                    if len(level) % 2:
+                        nxt.append(level[-1])
+                    level = nxt
+                finals[r.id] = level[0]
+        if finals:
+            sess.force_nodes(list(finals.values()))
         rt.sync()
     finally:
         rt.set_stream(0)
@@ -258,7 +297,16 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
     for l in p.leaves:
         if l.data.device is None:
             l.data.device = dev_in[l.id]
-    for r in p.roots:
-        if not r.is_materialized:
+    for r, o in zip(p.roots, outs):
+        if r.is_materialized:
+            continue
+        if r.id in dev_out:
             g.mark_materialized(r, TensorBuffer(r.dtype, r.shape, device=dev_out[r.id]))
+        else:
+            f = finals[r.id]
+            if f.dtype is not r.dtype or tuple(f.shape) != tuple(r.shape):
+                raise LazyFuseError(f"streamed partial of node {r.id} combined to {f.dtype.value}{f.shape}")
+            g.mark_materialized(r, TensorBuffer(r.dtype, r.shape, device=f.data.device))
+            f.data.device.copy_to_host(o)
+            sess.stats.d2h_bytes += o.nbytes
     return list(outs)

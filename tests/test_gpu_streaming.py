@@ -70,3 +70,30 @@ def test_mlp_streamed_with_library_steps(sess, small_chunks):
     # probabilities within fp32 tolerance, labels exact
     np.testing.assert_allclose(gp_, ep, rtol=1e-5, atol=1e-7)
     assert np.array_equal(glab, elab)
+
+
+def test_partials_streamed(sess, small_chunks):
+    """Partial roots (a total, bincounts) are combined across chunks; row-local
+    roots stay bit-identical."""
+    (x,) = wl.rownorm_inputs(rows=4096, cols=256)
+    y, tot = wl.rownorm(gp, gp.asarray(x))
+    c0 = sess.stats.streamed_chunks
+    gy, gt = gp.materialize(y, tot)
+    assert sess.stats.streamed_chunks - c0 > 4
+    ey, et = wl.rownorm(np, x)
+    assert np.array_equal(gy, np.asarray(_plain(lambda xx: (wl.rownorm(gp, xx)[0],), (x,))[0]))
+    # |total| is rounding noise around 0: bound by eps * sum|y| (SURVEY.md §8(c))
+    assert abs(float(gt) - float(et)) <= 4 * np.finfo(np.float32).eps * float(np.abs(ey).sum())
+    assert np.asarray(tot).shape == () and tot.is_materialized
+
+    P, C = wl.kmeans_inputs(n=1 << 16, k=64, d=4)
+    lab, sums, counts = wl.kmeans_partials(gp, gp.asarray(P), gp.asarray(C))
+    got = gp.materialize(lab, *sums, counts)
+    elab, esums, ecounts = wl.kmeans_partials(np, P, C)
+    assert np.array_equal(got[0], elab)
+    assert np.array_equal(got[-1], ecounts)
+    for g, e in zip(got[1:-1], esums):
+        np.testing.assert_allclose(g, e, rtol=1e-12, atol=1e-9)
+    m = gp.asarray(np.arange(1 << 18, dtype=np.float64))
+    (s,) = gp.materialize((m * 0.5).max(0) + 0 * (m * 0.5).sum())
+    assert float(s) == 0.5 * ((1 << 18) - 1)

@@ -24,18 +24,23 @@ def test_row_local_and_library_stream():
     (x,) = wl.rownorm_inputs(rows=4096, cols=64)
     y, tot = wl.rownorm(gp, gp.asarray(x))
     assert streaming.plan([y.node]) is not None            # row statistics are row-local
-    assert streaming.plan([y.node, tot.node]) is None      # the total is a partial over rows
+    p2 = streaming.plan([y.node, tot.node])                # the total: a partial combined over chunks
+    assert p2 is not None and p2.dist[tot.node.id] == "P:sum"
     X, W1, b1, W2, b2 = wl.mlp_inputs(batch=4096, hidden=32)
     p, lab = wl.mlp(gp, *[gp.asarray(a) for a in (X, W1, b1, W2, b2)])
     assert streaming.plan([p.node, lab.node]) is not None  # X@W1 with W1 replicated
 
 
-def test_ineligible():
+def test_partials_and_ineligible():
     P, C = wl.kmeans_inputs(n=4096, k=8, d=4)
     lab, sums, counts = wl.kmeans_partials(gp, gp.asarray(P), gp.asarray(C))
-    assert streaming.plan([lab.node] + [s.node for s in sums]) is None   # bincount partials
-    a = gp.asarray(np.arange(4096.0))
-    assert streaming.plan([(a * 2).sum().node]) is None                 # scalar root
+    p = streaming.plan([lab.node] + [s.node for s in sums] + [counts.node])   # bincount partials
+    assert p is not None and p.dist[counts.node.id] == "P:sum"
+    a = gp.asarray(np.arange(65536.0))
+    assert streaming.plan([(a * 2).sum().node]) is not None             # a total alone
+    assert streaming.plan([(a * 2).argmax().node]) is None              # arg-reduction over the streamed axis
+    x = gp.asarray(np.ones((4096, 3)))
+    assert streaming.plan([(x - x.mean(0)).node]) is None               # a partial consumed inside
     assert streaming.plan([gp.cumsum(a * 2).node]) is None              # scan along the leading axis
     small = gp.asarray(np.ones(100))
     assert streaming.plan([(small + 1).node]) is None                   # too few rows

@@ -34,7 +34,7 @@ def main():
     for spec in ["base:"] + sys.argv[2:]:
         name, _, pre = spec.partition(":")
         src = ks0.source
-        block, grid_over, smem = ks0.block, None, ks0.meta.get("smem", 0)
+        block, grid_over, smem, tmap = ks0.block, None, ks0.meta.get("smem", 0), False
         if ";" in pre:
             pre, *opts = pre.split(";")
             for o in opts:
@@ -45,6 +45,8 @@ def main():
                     grid_over = int(vv)
                 elif kk == "SMEM":
                     smem = int(vv)
+                elif kk == "TMAP":
+                    tmap = True
         if pre.startswith("FILE="):
             src = open(pre[5:]).read()
         elif pre.startswith("U="):
@@ -67,6 +69,12 @@ def main():
             rt.memset(tk, 0)
             ptrs.append(tk.ptr)
         params = runtime.pack_params(ptrs)
+        if tmap:
+            # leaf 0 as [n/32][32] f32 lines, box 128 lines (one 4096-float row), 128B swizzle
+            l0 = leaves[0]
+            nel = int(np.prod(l0.shape))
+            params = params + bytes(64 - len(params) % 64) if len(params) % 64 else params
+            params += rt.tensor_map_2d(ptrs[0], l0.dtype, 32, nel // 32, 128, 32, 128, 128)
         ts = []
         for i in range(25):
             e0, e1 = rt.event(), rt.event()
