@@ -22,6 +22,7 @@ reduced in several dependent phases (mean → variance → normalised output):
 
 from __future__ import annotations
 
+import os
 from typing import Optional
 
 from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, c_literal
@@ -317,6 +318,8 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
     if best is None:
         return None
     _, W, NS = best
+    if os.environ.get("GRUMPY_WROW_WNS"):       # experiments: "W,NS"
+        W, NS = (int(v) for v in os.environ["GRUMPY_WROW_WNS"].split(","))
     smem = W * NS * slot_bytes
 
     # stage pointers for the staged leaves, per row of this lane

@@ -102,6 +102,8 @@ def plan(roots: Sequence[Node], chunk_bytes: Optional[int] = None) -> Optional[S
         return None
     N = max(host, key=lambda f: f.data.nbytes).shape[0]
     leaves = [f for f in host if f.shape[0] == N]
+    if any(not l.data.host.flags.c_contiguous for l in leaves):
+        return None
     if N < 2 * ROW_ALIGN:
         return None
     try:
@@ -184,9 +186,6 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
     # full-size device buffers: inputs and row-local results (chunks are views)
     dev_in = {l.id: rt.alloc(l.data.nbytes) for l in p.leaves}
     dev_out = {r.id: rt.alloc(element_count(r.shape) * r.dtype.itemsize) for r in srows}
-    for l in p.leaves:
-        if not l.data.host.flags.c_contiguous:
-            return None
     chunks = [(lo, min(rows, N - lo)) for lo in range(0, N, rows)]
     sess.stats.streamed_chunks += len(chunks)
     ev = 0
