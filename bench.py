@@ -170,7 +170,9 @@ WORKLOADS = {
         n=1 << 28, label="f64", desc="Black-Scholes call+put, 2^28 options, fp64 (BASELINE configs[1])",
         inputs=lambda n, s: _wl().blackscholes_inputs(n=n, seed=s, dtype=np.float64),
         program=lambda xp, a: _wl().blackscholes(xp, *a),
-        elements=lambda n: n, bytes=lambda n: 5 * 8 * n, bound="hbm (fp64 pipe limits)"),
+        elements=lambda n: n, bytes=lambda n: 5 * 8 * n, bound="hbm (fp64 pipe limits)",
+        compute=dict(pipe="fp64", ops=171, lanes_per_sm_clk=64,
+                     note="DFMA+DMUL+DADD per option of the libdevice exp/log/erf/div/sqrt code (ncu dynamic count)")),
     "listing1": dict(
         n=1 << 24, label="f64", desc="paper Listing 1 chain (4 mul + 2 add), 2^24 fp64 (BASELINE configs[0])",
         inputs=lambda n, s: _wl().listing1_inputs(n=n, seed=s),
@@ -197,6 +199,10 @@ WORKLOADS = {
         inputs=lambda n, s: _km_inputs(n, s),
         program=lambda xp, a: _km_step(xp, a),
         elements=lambda n: n, bytes=lambda n: n * (KM_D * 4 + 8) + 64 * KM_D * 4, bound="fp32 issue (no FMA, NumPy order)",
+        # NumPy's operation sequence per point: 64 centroids x (D sub + D square
+        # + (D-1) add + the 0.0 identity add of add.reduce)
+        compute=dict(pipe="fp32", ops=64 * (3 * KM_D), lanes_per_sm_clk=128,
+                     note="64 x (4 sub + 4 mul + 3 add + 1 identity add) lane-ops per point"),
         sharded=(0,)),
 }
 WORKLOADS["rownorm"]["sharded"] = (0,)
@@ -436,7 +442,8 @@ def run_grumpy(args, dist):
                      "frac": achieved / peak, "traffic": _traffic(args.workload),
                      "peak_source": peak_src, "kernel_ms": kmean, "kernel": f"{dom[0][0]}:{dom[0][1]}",
                      "kernel_share_of_step": share, "launches_per_step": len(prof) / args.steps,
-                     "algorithmic_bytes_per_launch": alg_bytes, "limiter": w["bound"]},
+                     "algorithmic_bytes_per_launch": alg_bytes, "limiter": w["bound"],
+                     "compute": _compute_roofline(w, n, kmean, clk)},
         "gpu_launches": launches,
         "collectives_per_step": sess.stats.collectives / max(1, args.warmup + args.steps + 1),
         "cuMemAlloc_in_timed_region": allocs_in_timed,
@@ -452,6 +459,20 @@ def run_grumpy(args, dist):
                                 "sample": f"leading extent {sample} (of {w['n']}), eager NumPy (oracle) single thread, best of 2"}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def _compute_roofline(w, n, kernel_ms, clk):
+    """For kernels bound by an arithmetic pipe rather than HBM: lane-ops per
+    second of the dominant kernel against the pipe's peak at the measured SM
+    clock (SMs x lanes per SM per clock)."""
+    c = w.get("compute")
+    if not c:
+        return None
+    mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak = 148 * c["lanes_per_sm_clk"] * mhz * 1e6
+    achieved = w["elements"](n) * c["ops"] / (kernel_ms / 1e3)
+    return {"pipe": c["pipe"], "lane_ops_per_element": c["ops"], "achieved_lane_ops_s": achieved,
+            "peak_lane_ops_s": peak, "frac": achieved / peak, "peak_clock_mhz": mhz, "note": c["note"]}
 
 
 def _traffic(workload):

@@ -97,3 +97,22 @@ def test_partials_streamed(sess, small_chunks):
     m = gp.asarray(np.arange(1 << 18, dtype=np.float64))
     (s,) = gp.materialize((m * 0.5).max(0) + 0 * (m * 0.5).sum())
     assert float(s) == 0.5 * ((1 << 18) - 1)
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_streamed_random_program(sess, monkeypatch, seed):
+    """The randomised programs of test_gpu_programs.py through materialize()
+    with tiny chunks: streamed whenever eligible, same answers as the oracle
+    (row-local results bit-identical to the plain force)."""
+    from oracle import eager
+    from test_gpu_programs import _close, make_program
+    monkeypatch.setattr(streaming, "MIN_BYTES", 1)
+    monkeypatch.setattr(streaming, "ROW_ALIGN", 1)
+    monkeypatch.setattr(streaming, "CHUNK_BYTES", 96)
+    outs, transcendental = make_program(seed)
+    expect = [eager.evaluate(o.node) for o in outs]
+    got = gp.materialize(*outs)
+    for g, e in zip(got, expect):
+        assert g.shape == e.shape and g.dtype == e.dtype
+        assert _close(g, e, e.dtype, transcendental), (seed, g, e)
+

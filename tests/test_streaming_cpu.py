@@ -44,3 +44,23 @@ def test_partials_and_ineligible():
     assert streaming.plan([gp.cumsum(a * 2).node]) is None              # scan along the leading axis
     small = gp.asarray(np.ones(100))
     assert streaming.plan([(small + 1).node]) is None                   # too few rows
+
+
+def test_streamed_random_programs_do_stream(monkeypatch):
+    """Enough of the random programs are streaming-eligible for the test above
+    to exercise the chunked path (not just the fallback)."""
+    from test_gpu_programs import make_program
+    monkeypatch.setattr(streaming, "MIN_BYTES", 1)
+    monkeypatch.setattr(streaming, "ROW_ALIGN", 1)
+    monkeypatch.setattr(streaming, "CHUNK_BYTES", 96)
+    streamed = 0
+    for seed in range(60):
+        s = gp.Session()
+        old = gp.set_default_session(s)
+        try:
+            outs, _ = make_program(seed)
+            if streaming.plan([o.node for o in outs]) is not None:
+                streamed += 1
+        finally:
+            gp.set_default_session(old)
+    assert streamed >= 8, streamed
