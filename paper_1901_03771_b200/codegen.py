@@ -247,6 +247,13 @@ class ValueEmitter:
         # (gr::div_sh<FAST>) and set this before emission
         self.div_fast = False
         self.used_div_fast = False
+        self.ns = ""              # name prefix (two emitters in one function)
+        # fast mode (map family): slice-assigns assume the whole lane group is
+        # inside the assigned region and read the value branch at unclamped,
+        # affine coordinates; each assumption adds a guard the kernel checks
+        # before taking the result (else the clamped, general group runs)
+        self.fast = False
+        self.guards: List[str] = []
         # hash-consing: structurally identical nodes (same op over the same
         # operands) share one value — e.g. the two mean computations of
         # (x - x.mean(1)) / x.std(1).  Evaluation is pure, so this is exact.
@@ -276,7 +283,7 @@ class ValueEmitter:
 
     def fresh(self, prefix="t"):
         self.counter += 1
-        return f"{prefix}{self.counter}"
+        return f"{self.ns}{prefix}{self.counter}"
 
     # -- to implement
     def emit(self, level: int, ctype: str, expr: str) -> str:
@@ -438,6 +445,10 @@ class ValueEmitter:
         """SliceAssign lowers to select(in-region, value-branch, target-branch)
         (SPEC.md:304, 336).  Value-branch coordinates are clamped so the load
         stays in bounds when the predicate is false."""
+        if self.fast:
+            v = self._slice_assign_interior(n, coords)
+            if v is not None:
+                return v
         (region,) = n.op.attrs
         target, val = n.preds
         conds = []
@@ -459,6 +470,32 @@ class ValueEmitter:
         tv = self.value(target, coords)
         lv = max(lvl, vv[1], tv[1])
         return self.emit(lv, n.dtype.ctype, f"gr::select<{n.dtype.ctype}>({pred}, {vv[0]}, {tv[0]})"), lv
+
+
+    def _slice_assign_interior(self, n: Node, coords):
+        """Fast-mode SliceAssign: the lane group lies inside the region, so the
+        result is the value branch at coordinates (c - start) — affine, which
+        keeps its loads vectorised.  The group-level guard is recorded."""
+        (region,) = n.op.attrs
+        target, val = n.preds
+        lane = getattr(self, "lane_var", None)
+        vec = getattr(self, "vec", 1)
+        conds, vcoords = [], []
+        for c, (start, step, length) in zip(coords, region):
+            if step != 1:
+                return None
+            rel = c + (-start)
+            cl = rel.coef(lane) if lane is not None else 0
+            base = rel.without(lane) if lane is not None else rel
+            if cl not in (0, 1) or base.level >= LEVEL_LANE:
+                return None
+            hi = vec - 1 if cl else 0
+            conds.append(f"({base.c()}) >= 0 && ({base.c()}) + {hi} < {length}")
+            vcoords.append(rel)
+        self.guards.extend(conds)
+        vv = self.cast(self.value(val, bcast_coords(vcoords, tuple(r[2] for r in region), val.shape)),
+                       val.dtype, n.dtype)
+        return vv
 
 
 # ---------------------------------------------------------------------------
@@ -497,6 +534,38 @@ class MapEmitter(ValueEmitter):
         name = self.emit(level, "long long", expr)
         return Var(name, level)
 
+    def _addr(self, leaf: Node, off: Aff, width: int = 1) -> str:
+        """Element offset of a load; fast-mode loads run before the group's
+        guard is known, so their addresses are clamped into the leaf."""
+        if not self.fast:
+            return off.c()
+        hi = max(element_count(leaf.shape) - width, 0) // width * width   # keeps vectors aligned
+        return f"gr::clampll({off.c()}, {hi}LL)"
+
+    def group_vector(self, leaf: Node, base: Aff) -> str:
+        """An aligned VEC-element vector of ``leaf`` at ``base`` (group level),
+        shared by every access that needs it."""
+        key = ("gvec", leaf.id, base.key())
+        hit = self.const_memo.get(key)
+        if hit is None:
+            T = leaf.dtype.ctype
+            hit = self.fresh("L")
+            self.group_decls.append(f"{T} {hit}[N][{self.vec}];")
+            self.group_lines.append(f"gr::ldv<{T}, {self.vec}>({hit}[u], p.in{self.leaf_index[leaf.id]} + "
+                                    f"{self._addr(leaf, base, self.vec)});")
+            self.const_memo[key] = hit
+        return hit
+
+    def shifted(self, leaf: Node, rest: Aff):
+        """(V0, V1, s): ``rest`` = aligned base + s (0 < s < VEC), the lanes'
+        elements are window[v + s] of the two aligned vectors V0 ++ V1."""
+        s = rest.const % self.vec
+        base = rest + (-s)
+        if (s == 0 or base.alignment() % self.vec or element_count(leaf.shape) % self.vec
+                or leaf.dtype.itemsize * self.vec != 16):
+            return None
+        return self.group_vector(leaf, base), self.group_vector(leaf, base + self.vec), s
+
     def load_leaf(self, leaf: Node, off: Aff):
         idx = self.leaf_index[leaf.id]
         T = leaf.dtype.ctype
@@ -504,15 +573,18 @@ class MapEmitter(ValueEmitter):
         lvl = off.level
         lane = self.lane_var
         if lvl < LEVEL_LANE:
-            return self.emit(lvl, T, f"gr::ld<{T}>({ptr} + {off.c()})"), lvl
+            return self.emit(lvl, T, f"gr::ld<{T}>({ptr} + {self._addr(leaf, off)})"), lvl
         cv = off.coef(lane)
         rest = off.without(lane)
         if cv == 1 and self.vec > 1 and rest.level < LEVEL_LANE and (rest.alignment() % self.vec == 0):
-            name = self.fresh("L")
-            self.group_decls.append(f"{T} {name}[N][{self.vec}];")
-            self.group_lines.append(f"gr::ldv<{T}, {self.vec}>({name}[u], {ptr} + {rest.c()});")
+            name = self.group_vector(leaf, rest)
             return f"{name}[u][v]", LEVEL_LANE
-        return self.emit(LEVEL_LANE, T, f"gr::ld<{T}>({ptr} + {off.c()})"), LEVEL_LANE
+        if cv == 1 and self.vec > 1 and rest.level < LEVEL_LANE:
+            sh = self.shifted(leaf, rest)
+            if sh is not None:
+                a, b, s_ = sh
+                return f"gr::pick<{T}, {self.vec}>({a}[u], {b}[u], v + {s_})", LEVEL_LANE
+        return self.emit(LEVEL_LANE, T, f"gr::ld<{T}>({ptr} + {self._addr(leaf, off)})"), LEVEL_LANE
 
 
 class NotPairable(Exception):
@@ -599,8 +671,10 @@ class PairMapEmitter(MapEmitter):
             else:
                 raise NotPairable(f"no packed form for {code}")
             return self.emit(LEVEL_LANE, n.dtype.ctype, expr), LEVEL_LANE
-        if n.id not in self.leaf_index and n.op.kind not in (OpKind.MAP, OpKind.TRANSPOSE, OpKind.BROADCAST,
-                                                             OpKind.SLICE, OpKind.RESHAPE, OpKind.CAST):
+        ok = (OpKind.MAP, OpKind.TRANSPOSE, OpKind.BROADCAST, OpKind.SLICE, OpKind.RESHAPE, OpKind.CAST)
+        if self.fast:
+            ok += (OpKind.SLICE_ASSIGN,)    # the interior form is the value branch alone
+        if n.id not in self.leaf_index and n.op.kind not in ok:
             raise NotPairable(f"{n.op!r}")
         return super()._value(n, coords)
 
@@ -621,17 +695,24 @@ class PairMapEmitter(MapEmitter):
         cv = off.coef(lane)
         rest = off.without(lane)
         if cv == 1 and rest.level < LEVEL_LANE and rest.alignment() % self.vec == 0:
-            name = self.fresh("L")
-            self.group_decls.append(f"{T} {name}[N][{self.vec}];")
-            self.group_lines.append(f"gr::ldv<{T}, {self.vec}>({name}[u], p.in{idx} + {rest.c()});")
+            name = self.group_vector(leaf, rest)
             if leaf.dtype is DType.f32:
                 return f"gr::pk({name}[u][2 * v], {name}[u][2 * v + 1])", LEVEL_LANE
             return f"gr::b2{{{name}[u][2 * v], {name}[u][2 * v + 1]}}", LEVEL_LANE
+        if cv == 1 and rest.level < LEVEL_LANE:
+            sh = self.shifted(leaf, rest)
+            if sh is not None:
+                a, b, s_ = sh
+                lo = f"gr::pick<{T}, {self.vec}>({a}[u], {b}[u], 2 * v + {s_})"
+                hi = f"gr::pick<{T}, {self.vec}>({a}[u], {b}[u], 2 * v + {s_ + 1})"
+                if leaf.dtype is DType.f32:
+                    return f"gr::pk({lo}, {hi})", LEVEL_LANE
+                return f"gr::b2{{{lo}, {hi}}}", LEVEL_LANE
         # gather: lane 2v and 2v+1 (the lane variable counts pairs)
         o0 = rest + Aff.of(lane).scale(2 * cv)
         o1 = o0 + cv
-        a = f"gr::ld<{T}>(p.in{idx} + {o0.c()})"
-        b = f"gr::ld<{T}>(p.in{idx} + {o1.c()})"
+        a = f"gr::ld<{T}>(p.in{idx} + {self._addr(leaf, o0)})"
+        b = f"gr::ld<{T}>(p.in{idx} + {self._addr(leaf, o1)})"
         if leaf.dtype is DType.f32:
             return self.emit(LEVEL_LANE, T, f"gr::pk({a}, {b})"), LEVEL_LANE
         return self.emit(LEVEL_LANE, T, f"gr::b2{{{a}, {b}}}"), LEVEL_LANE
@@ -674,10 +755,12 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
         unroll = 1
     rank = len(shape)
 
-    def build(mode, pair=False):
+    def build(mode, pair=False, fast=False):
         lane = Var("v", LEVEL_LANE)
         cls = PairMapEmitter if pair else MapEmitter
         em = cls(region, vec if mode == "group" else 1, None, lane)
+        if fast:
+            em.fast, em.ns = True, "f"
         coords: List[Aff] = []
         if rank == 0:
             lin0 = Aff.of(0)
@@ -724,9 +807,62 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
             pair = False
     if not pair:
         em, outs = build("group")
-    nl = vec // 2 if pair else vec
+    def lane_loop(em, outs, pair, ind):
+        nl = vec // 2 if pair else vec
+        out = []
+        for ri, r in enumerate(region.roots):
+            out.append(f"{ind}{r.dtype.ctype} o{ri}[{vec}];")
+        out.append("#pragma unroll")
+        out.append(f"{ind}for (int v = 0; v < {nl}; ++v) {{")
+        for l in em.lane_lines:
+            out.append(f"{ind}  " + l)
+        for ri, (r, (expr, _lvl)) in enumerate(zip(region.roots, outs)):
+            if not pair:
+                out.append(f"{ind}  o{ri}[v] = {expr};")
+            elif _lvl < LEVEL_LANE:
+                out.append(f"{ind}  o{ri}[2 * v] = {expr}; o{ri}[2 * v + 1] = {expr};")
+            elif r.dtype is DType.f32:
+                out.append(f"{ind}  o{ri}[2 * v] = gr::lo({expr}); o{ri}[2 * v + 1] = gr::hi({expr});")
+            else:
+                out.append(f"{ind}  o{ri}[2 * v] = ({expr}).lo; o{ri}[2 * v + 1] = ({expr}).hi;")
+        out.append(f"{ind}}}")
+        for ri, r in enumerate(region.roots):
+            T = r.dtype.ctype
+            if vec > 1:
+                out.append(f"{ind}gr::stv<{T}, {vec}>(p.out{ri} + lin, o{ri});")
+            else:
+                out.append(f"{ind}gr::st<{T}>(p.out{ri} + lin, o{ri}[0]);")
+        return out
+
+    # ---- fast group (slice-assign regions): the lane group inside every
+    # assigned region, value branches at affine coordinates (vector and
+    # shifted-vector loads); taken when its guard holds, else the general body
+    fast_fn = []
+    if unroll == 1 and vec > 1 and any(n_.kind is OpKind.SLICE_ASSIGN for n_ in region.nodes):
+        fem = fouts = None
+        for fpair in ((True, False) if vec % 2 == 0 and os.environ.get("GRUMPY_PAIR", "1") != "0" else (False,)):
+            try:
+                fem, fouts = build("group", pair=fpair, fast=True)
+                fp = fpair
+                break
+            except NotPairable:
+                continue
+        if fem is not None and fem.guards:
+            fast_fn.append("static __device__ __forceinline__ bool fast_group(const Params& p, long long g0) {")
+            fast_fn += ["  " + c for c in fem.consts]
+            fast_fn.append("  const int u = 0; (void)u;")
+            fast_fn.append(f"  const {ictype} lin = ({ictype})g0 * {vec}; (void)lin;")
+            fast_fn += ["  " + d.replace("[N]", "[1]") for d in fem.group_decls]
+            fast_fn += ["  " + l for l in fem.group_lines]
+            fast_fn.append(f"  if (!({' && '.join('(' + g + ')' for g in dict.fromkeys(fem.guards))})) return false;")
+            fast_fn += lane_loop(fem, fouts, fp, "  ")
+            fast_fn.append("  return true;")
+            fast_fn.append("}")
+
     lines = []
     lines.append("template <int N> static __device__ __forceinline__ void group(const Params& p, long long g0, long long stride) {")
+    if fast_fn:
+        lines.append("  if constexpr (N == 1) { if (fast_group(p, g0)) return; }")
     for d in em.group_decls:
         lines.append("  " + d)
     lines.append("#pragma unroll")
@@ -738,29 +874,7 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
     lines.append("#pragma unroll")
     lines.append("  for (int u = 0; u < N; ++u) {")
     lines.append(f"    const {ictype} lin = ({ictype})(g0 + u * stride) * {vec}; (void)lin;")
-    for ri, r in enumerate(region.roots):
-        lines.append(f"    {r.dtype.ctype} o{ri}[{vec}];")
-    lines.append("#pragma unroll")
-    lines.append(f"    for (int v = 0; v < {nl}; ++v) {{")
-    for l in em.lane_lines:
-        lines.append("      " + l)
-    for ri, (r, (expr, _lvl)) in enumerate(zip(region.roots, outs)):
-        if not pair:
-            lines.append(f"      o{ri}[v] = {expr};")
-            continue
-        if _lvl < LEVEL_LANE:
-            lines.append(f"      o{ri}[2 * v] = {expr}; o{ri}[2 * v + 1] = {expr};")
-        elif r.dtype is DType.f32:
-            lines.append(f"      o{ri}[2 * v] = gr::lo({expr}); o{ri}[2 * v + 1] = gr::hi({expr});")
-        else:
-            lines.append(f"      o{ri}[2 * v] = ({expr}).lo; o{ri}[2 * v + 1] = ({expr}).hi;")
-    lines.append("    }")
-    for ri, r in enumerate(region.roots):
-        T = r.dtype.ctype
-        if vec > 1:
-            lines.append(f"    gr::stv<{T}, {vec}>(p.out{ri} + lin, o{ri});")
-        else:
-            lines.append(f"    gr::st<{T}>(p.out{ri} + lin, o{ri}[0]);")
+    lines += lane_loop(em, outs, pair, "    ")
     lines.append("  }")
     lines.append("}")
     consts = list(em.consts)
@@ -791,6 +905,8 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
            f"  static constexpr long long NGROUPS = {ngroups}LL;",
            f"  static constexpr int U = {unroll};",
            f"  static constexpr bool TAIL = {'true' if tail else 'false'};"]
+    if fast_fn:
+        src.append("  " + "\n  ".join(fast_fn))
     src.append("  " + "\n  ".join(_wrap_consts(lines, consts)))
     src.append("  " + "\n  ".join(tail_lines))
     src.append("};")
@@ -799,7 +915,7 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
                         leaf_slots=list(range(len(region.leaves))),
                         root_slots=list(range(len(region.roots))),
                         block=block, groups=ngroups, vec=vec, unroll=unroll,
-                        meta={"shape": shape, "tail": tail})
+                        meta={"shape": shape, "tail": tail, "fast_group": bool(fast_fn)})
 
 
 def _wrap_consts(fn_lines, consts):

@@ -43,6 +43,13 @@ template <class T, int V> __device__ __forceinline__ void ldv(T (&dst)[V], const
   for (int i = 0; i < V; ++i) dst[i] = u.v[i];
 }
 template <class T> __device__ __forceinline__ T ld(const T* __restrict__ src) { return __ldg(src); }
+
+// Element i (a compile-time constant once the lane loop is unrolled) of the
+// 2V-element window a ++ b: a vector at a constant misalignment (e.g. the
+// x[j-1] and x[j+1] neighbours of a stencil) read as two aligned vectors.
+template <class T, int V> __device__ __forceinline__ T pick(const T (&a)[V], const T (&b)[V], int i) {
+  return i < V ? a[i] : b[i - V];
+}
 template <> __device__ __forceinline__ bool ld(const bool* __restrict__ src) {
   return __ldg(reinterpret_cast<const unsigned char*>(src)) != 0;
 }

@@ -11,6 +11,7 @@ C2 Black-Scholes       (erf normal CDF)
 C3 row-normalise + sum (BASELINE.json configs[2])
 C4 MNIST-style MLP     (np.dot -> library)
 C5 k-means assignment
+Jacobi sweep           (SPEC.md:248 — §8(f) rank 2)
 """
 
 from __future__ import annotations
@@ -134,3 +135,18 @@ def kmeans_centroids(sums, counts, C_old):
     nz = n > 0
     out[nz] = S[nz] / n[nz, None]
     return out.astype(np.float32)
+
+
+# ---- Jacobi -------------------------------------------
+def jacobi_inputs(n=16384, seed=42, dtype=np.float32):
+    rng = np.random.default_rng(seed)
+    return (rng.random((n, n), dtype=np.float32).astype(dtype),)
+
+
+def jacobi(xp, a):
+    """One 5-point Jacobi sweep with fixed boundary: in
+    grumpy the slice-assign lowers to a select over the grid (SPEC.md:304,
+    336), one fused kernel per sweep."""
+    b = a.copy()
+    b[1:-1, 1:-1] = 0.2 * (a[1:-1, 1:-1] + a[1:-1, :-2] + a[1:-1, 2:] + a[:-2, 1:-1] + a[2:, 1:-1])
+    return b

@@ -4,6 +4,7 @@ import numpy as np
 import pytest
 
 import paper_1901_03771_b200 as gp
+from paper_1901_03771_b200 import workloads as wl
 
 pytestmark = pytest.mark.gpu
 
@@ -69,3 +70,33 @@ def test_views_strided(sess):
                           t.transpose(2, 0, 1).reshape(4, 48)[:, ::3])
     assert np.array_equal(np.asarray(gp.asarray(t)[::-1, 0, :].T), t[::-1, 0, :].T)
     np.testing.assert_allclose(np.asarray(g), e, rtol=1e-5, atol=1e-6)
+
+
+@pytest.mark.parametrize("shape,dt", [((256, 256), np.float32), ((258, 300), np.float32), ((6, 10), np.float32),
+                                      ((130, 64), np.float64), ((3, 8), np.float64), ((1024, 12), np.int32)])
+def test_jacobi_fast_interior_groups(sess, shape, dt):
+    """Interior lane groups take the unclamped, vectorised form (shifted-vector
+    neighbours); boundary groups the clamped select form: bit-identical."""
+    from paper_1901_03771_b200 import codegen
+    rng = np.random.default_rng(17)
+    a = (rng.standard_normal(shape) * 8).astype(dt)
+    b = wl.jacobi(gp, gp.asarray(a))
+    got = np.asarray(b)
+    assert np.array_equal(got, wl.jacobi(np, a))
+    ks = sess.executor.last_steps[-1].cache["ks"]
+    assert ks.family == "map" and (ks.meta.get("fast_group") or ks.vec == 1)
+
+
+def test_shifted_vector_slices(sess):
+    """Neighbour differences at constant misalignments read two aligned
+    vectors (gr::pick) instead of per-lane gathers: exact for every shift."""
+    rng = np.random.default_rng(18)
+    x = rng.standard_normal(4096 + 8).astype(np.float32)
+    g = gp.asarray(x)
+    for lo, hi in ((1, 0), (0, 1), (3, 1), (2, 6), (5, 3)):
+        n = 4096
+        got = np.asarray(g[lo:lo + n] - g[hi:hi + n] * 0.5)
+        assert np.array_equal(got, x[lo:lo + n] - x[hi:hi + n] * np.float32(0.5)), (lo, hi)
+    m = rng.standard_normal((64, 72)).astype(np.float64)
+    gm = gp.asarray(m)
+    assert np.array_equal(np.asarray(gm[:, 1:] + gm[:, :-1]), m[:, 1:] + m[:, :-1])
