@@ -247,6 +247,7 @@ class ValueEmitter:
         # (gr::div_sh<FAST>) and set this before emission
         self.div_fast = False
         self.used_div_fast = False
+        self.div_finalize: List[str] = []   # row-end checks of the fast division
         self.ns = ""              # name prefix (two emitters in one function)
         # fast mode (map family): slice-assigns assume the whole lane group is
         # inside the assigned region and read the value branch at unclamped,
@@ -348,7 +349,18 @@ class ValueEmitter:
                     r = self.emit(args[1][1], f"gr::DivShared<{T}>", f"gr::div_prep<{T}>({names[1]})")
                     if args[1][1] == 0:
                         self.const_memo[rk] = r
-                if self.div_fast:
+                if self.div_fast and args[1][1] == 1 and args[0][1] > 1 and hasattr(self, "stmt"):
+                    # row-level divisor, per-element dividends: track the
+                    # dividends' range, test the window once per row
+                    w = self.const_memo.get(("divrange", r))
+                    if w is None:
+                        w = self.fresh("w")
+                        self.stmt(1, f"gr::DivRange<{T}> {w} = gr::div_range_init<{T}>();")
+                        self.const_memo[("divrange", r)] = w
+                        self.div_finalize.append(f"bad |= gr::div_range_bad<{T}>({w}, {r});")
+                    expr = f"gr::div_shr<FAST, {T}>({names[0]}, {r}, {w})"
+                    self.used_div_fast = True
+                elif self.div_fast:
                     expr = f"gr::div_sh<FAST, {T}>({names[0]}, {r}, bad)"
                     self.used_div_fast = True
                 else:

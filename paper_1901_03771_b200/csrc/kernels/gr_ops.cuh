@@ -133,6 +133,35 @@ __device__ __forceinline__ T div_sh(T x, const DivShared<T>& d, bool& bad) {
   }
 }
 
+// Per-row accumulator of the fast pass's dividend range: two FMNMX per
+// element instead of a two-sided window test; the row is flagged once at the
+// end if any |dividend| left [xlo, xhi].  (NaN dividends give NaN quotients
+// either way.)
+template <class T> struct DivRange {
+  T amin, amax;
+};
+template <class T> __device__ __forceinline__ DivRange<T> div_range_init() {
+  return {T(__int_as_float(0x7f800000)), T(0)};
+}
+template <bool FAST, class T>
+__device__ __forceinline__ T div_shr(T x, const DivShared<T>& d, DivRange<T>& w) {
+  if constexpr (FAST) {
+    const T q0 = x * d.r;
+    const T e = fma(-q0, d.s, x);
+    const T q = fma(e, d.r, q0);
+    const T ax = fabs(x);
+    w.amin = fmin(w.amin, ax);
+    w.amax = fmax(w.amax, ax);
+    return q;
+  } else {
+    (void)w;
+    return div_shared<T>(x, d);
+  }
+}
+template <class T> __device__ __forceinline__ bool div_range_bad(const DivRange<T>& w, const DivShared<T>& d) {
+  return !(w.amin >= d.xlo && w.amax <= d.xhi);
+}
+
 template <class T> __device__ __forceinline__ T neg(T a) { return -a; }
 template <> __device__ __forceinline__ int neg(int a) { return (int)(0u - (unsigned)a); }
 template <> __device__ __forceinline__ i64 neg(i64 a) { return (i64)(0ull - (u64)a); }

@@ -140,6 +140,16 @@ class Executor:
                 self.rt.memset(tk, 0)
                 self._tickets[id(ks)] = tk
             ptrs.append(tk.ptr)
+        elif ks.meta.get("redo_words"):
+            ptrs.append(0)
+        if ks.meta.get("redo_words"):
+            # per-row redo flags: zeroed once, cleared by the kernel as it redoes
+            rd = self._tickets.get(("redo", id(ks)))
+            if rd is None:
+                rd = self.rt.alloc(4 * ks.meta["redo_words"])
+                self.rt.memset(rd, 0)
+                self._tickets[("redo", id(ks))] = rd
+            ptrs.append(rd.ptr)
         params = runtime.pack_params(ptrs)
         if self.profile is not None:
             e0, e1 = self._event_pair()

@@ -68,6 +68,10 @@ def main():
             tk = rt.alloc(256)
             rt.memset(tk, 0)
             ptrs.append(tk.ptr)
+        if "REDO" in spec:
+            rd = rt.alloc(1 << 16)
+            rt.memset(rd, 0)
+            ptrs.append(rd.ptr)
         params = runtime.pack_params(ptrs)
         if tmap:
             # leaf 0 as [n/32][32] f32 lines, box 128 lines (one 4096-float row), 128B swizzle
