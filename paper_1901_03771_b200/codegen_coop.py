@@ -192,7 +192,7 @@ class CoopEmitter(LoopEmitter):
         comb = _COMBINE[rop]
         sh = self._sh(T)
         if rop is ReduceOp.sum and T.is_float:
-            tree = self.emit(1, ct, f"gr::row_sum<{ct}, {self.vec}, {self.P}, {self.tpr}>({acc}, {sh}, ri)")
+            tree = self.emit(1, ct, f"gr::row_sum<{ct}, {self.vec}, {self.P}, {self.tpr}, GR_ROWSUM_TRAIL>({acc}, {sh}, ri)")
             if not identity:
                 return tree
             return self.emit(1, ct, f"gr::add<{ct}>({c_literal(0, T)}, {tree})")
@@ -462,6 +462,11 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
         lines.append("  bool bad = false;")
     lines += ["  " + c for c in em.consts]
     lines += render(em.row, 1)
+    # a row sum's trailing barrier protects its smem slots until the next
+    # barrier of the row; with two or more cross-thread combines per row
+    # group another combine's barrier always comes first (0.2377 -> 0.2358 ms)
+    trail = "false" if em.n_sh >= 2 else "true"
+    lines = [l.replace("GR_ROWSUM_TRAIL", trail) for l in lines]
     if templ:
         lines += ["  " + l for l in em.div_finalize]
         lines.append("  return bad;")

@@ -68,7 +68,9 @@ def main():
             tk = rt.alloc(256)
             rt.memset(tk, 0)
             ptrs.append(tk.ptr)
-        if "REDO" in spec:
+        if "REDO" in spec or ks0.meta.get("redo_words"):
+            if not ks0.meta.get("ticket"):
+                ptrs.append(0)
             rd = rt.alloc(1 << 16)
             rt.memset(rd, 0)
             ptrs.append(rd.ptr)
