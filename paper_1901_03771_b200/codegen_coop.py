@@ -464,8 +464,11 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
     lines += render(em.row, 1)
     # a row sum's trailing barrier protects its smem slots until the next
     # barrier of the row; with two or more cross-thread combines per row
-    # group another combine's barrier always comes first (0.2377 -> 0.2358 ms)
-    trail = "false" if em.n_sh >= 2 else "true"
+    # group another combine's barrier always comes first.  Measured: without
+    # it rownorm (reductions only) 0.2377 -> 0.2358 ms, but rownorm-y (row
+    # stores between the combines) 0.421 -> 0.434 ms, so only the former drops it
+    stores_rows = any(tuple(r.shape) == Ts + (C,) for r in region.roots if r.id not in tot_ids)
+    trail = "false" if em.n_sh >= 2 and not stores_rows else "true"
     lines = [l.replace("GR_ROWSUM_TRAIL", trail) for l in lines]
     if templ:
         lines += ["  " + l for l in em.div_finalize]
