@@ -376,7 +376,6 @@ class LoopEmitter(ValueEmitter):
         ident = c_literal(_IDENT[rop](T), T)
         if self.half is not None and any(c.coef(self.half) for c in kept):
             return self._reduce_pair(r, x, kept, L)
-        acc = self.var_decl(L, ct, ident)
         # coalesce: NumPy merges adjacent reduced axes; the innermost group is
         # pairwise-summed when it contains the last (contiguous) axis.
         groups: List[List[int]] = []
@@ -388,6 +387,9 @@ class LoopEmitter(ValueEmitter):
         pairwise = (rop is ReduceOp.sum and T.is_float and groups and groups[-1][-1] == len(So) - 1
                     and element_count([So[a] for a in groups[-1]]) > 1)
         outer_axes = [a for g in (groups[:-1] if pairwise else groups) for a in g]
+        compared_fold = (pairwise and element_count([So[a] for a in groups[-1]]) < 8 and not outer_axes
+                         and self._only_compared(r))
+        acc = None if compared_fold else self.var_decl(L, ct, ident)
         # sequential loops over outer reduced axes (C order)
         ovars, opened = self.loop_coords(L, [So[a] for a in outer_axes])
         loop_lvl = ovars[-1].level if ovars else L
@@ -407,6 +409,21 @@ class LoopEmitter(ValueEmitter):
             return out
 
         comb = _COMBINE[rop]
+        if compared_fold:
+            # consumed only by arg-reductions (ordered compares): NumPy's 0.0
+            # identity add changes nothing but the sign of a zero sum, which no
+            # compare sees — the sequential fold is the value (k-means: one
+            # FADD less per centroid)
+            g = groups[-1]
+            gdims = [So[a] for a in g]
+            Lg = element_count(gdims)
+            part = self.var_decl(loop_lvl, ct, c_literal(-0.0, T))
+            iv, s, saved = self.open(loop_lvl, "for", trip=Lg, unroll=True)
+            inner = self._delin(iv, g, gdims)
+            v = self.cast(self.value(x, full_coords(inner)), x.dtype, T)
+            self.stmt(iv.level, f"{part} = gr::add<{ct}>({part}, {v[0]});")
+            self.close(s, saved)
+            return part, L
         if pairwise and element_count([So[a] for a in groups[-1]]) < 8:
             # NumPy: n < 8 is a sequential fold from -0.0 — an unrolled loop, so
             # contiguous operands become one vector load
@@ -434,6 +451,14 @@ class LoopEmitter(ValueEmitter):
             self.stmt(loop_lvl, f"{acc} = {comb}<{ct}>({acc}, {v[0]});")
         self.close_all(opened)
         return acc, L
+
+    def _only_compared(self, r: Node) -> bool:
+        """Is every consumer of ``r`` in this region an arg-reduction?"""
+        if any(q.id == r.id for q in self.region.roots):
+            return False
+        cid = self.cid(r)
+        users = [n for n in self.region.nodes if any(self.cid(q) == cid for q in n.preds)]
+        return bool(users) and all(n.kind is OpKind.ARGREDUCE for n in users)
 
     def _reduce_pair(self, r: Node, x: Node, kept, L):
         """A reduction evaluated for both indices of a paired loop: sums of f32
