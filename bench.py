@@ -204,6 +204,11 @@ WORKLOADS = {
         compute=dict(pipe="fp32", ops=64 * (3 * KM_D), lanes_per_sm_clk=128,
                      note="64 x (4 sub + 4 mul + 3 add + 1 identity add) lane-ops per point"),
         sharded=(0,)),
+    "cumsum": dict(
+        n=1 << 28, label="f32", desc="map-scan cumsum(x*0.5+1) over 2^28 fp32 (SURVEY.md §8(f))",
+        inputs=lambda n, s: _wl().scan_inputs(n=n, seed=s),
+        program=lambda xp, a: (_wl().scan(xp, *a),),
+        elements=lambda n: n, bytes=lambda n: 2 * 4 * n, bound="hbm"),
     "jacobi": dict(
         n=16384, label="f32", desc="5-point Jacobi sweep (slice-assign), 16384x16384 fp32 (SURVEY.md §8(f))",
         inputs=lambda n, s: _wl().jacobi_inputs(n=n, seed=s),
@@ -240,7 +245,7 @@ def make_program(name):
 def cpu_sample_n(name):
     """Leading extent of the bounded CPU sample (~5-20 s of single-thread NumPy)."""
     return {"blackscholes-f32": 1 << 24, "blackscholes-f64": 1 << 24, "listing1": 1 << 24,
-            "rownorm": 16384, "rownorm-y": 16384, "mlp": 16384, "kmeans": 1 << 20, "jacobi": 4096}[name]
+            "rownorm": 16384, "rownorm-y": 16384, "mlp": 16384, "kmeans": 1 << 20, "jacobi": 4096, "cumsum": 1 << 24}[name]
 
 
 def make_inputs(name, n, seed):

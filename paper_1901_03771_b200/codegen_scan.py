@@ -11,8 +11,9 @@ sequential left fold along the axis (out[k] = out[k-1] ⊕ x[k]).
   decoupled look-back — each CTA scans a 2048-element tile (thread-sequential
   runs, warp-shuffle + shared-memory combine of run totals), publishes its
   aggregate and inclusive prefix, and folds its predecessors' published values
-  (``gr::scan_lookback``); deterministic, float results within tolerance of
-  the sequential fold (reassociation), integers exact.
+  (``gr::tile_lookback``: folds left to right, so the result does not depend
+  on timing — deterministic); float results within tolerance of NumPy's
+  sequential fold (reassociation), integers exact.
 """
 
 from __future__ import annotations
@@ -25,8 +26,7 @@ from .dag import OpKind, ReduceOp
 from .errors import UnsupportedNodeInFusedStep
 from .tensor import DType, element_count, row_major_strides
 
-TILE_THREADS = 256
-ITEMS = 8
+ITEMS = 16
 
 
 def generate(region: Region, kname="gr_region") -> KernelSource:
@@ -99,80 +99,120 @@ def _gen_lines(region, s, x, rop, axis, kname, block=128) -> KernelSource:
 
 
 def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
+    """One pass over a long 1-D scan: 4096-element tiles, coalesced (vector)
+    loads of the map prologue into a padded shared tile, a thread-sequential
+    run per thread, warp and CTA combines, and the deterministic look-back of
+    gr::tile_lookback; results leave through the shared tile as coalesced
+    vector stores."""
     T = s.dtype
     ct = T.ctype
     N = element_count(x.shape)
+    # 8192-element tiles (fewer tiles in flight: shorter look-back walks);
+    # 4096 for 8-byte types so the shared tile stays within 48 KB
+    TILE_THREADS = 512 if T.itemsize <= 4 else 256
     tile = TILE_THREADS * ITEMS
     ntiles = -(-N // tile)
-    em = LoopEmitter(region, vec_loads=False)
-    j, sc, saved = em.open(1, "for", trip=ITEMS, unroll=True)
-    lin_name = em.emit(j.level, "long long", f"base + {j.name}")
-    lin = Var(lin_name, j.level)
-    cl = em.emit(j.level, "long long", f"{lin_name} < {N}LL ? {lin_name} : {N - 1}LL")
-    coords = _flat_coords(em, x.shape, Aff.of(Var(cl, j.level)), j)
-    v = em.cast(em.value(x, coords), x.dtype, T)
-    comb = _COMBINE[rop]
-    em.stmt(j.level, f"vals[{j.name}] = {v[0]};")
-    em.close(sc, saved)
+    vec = max(1, min(4, 16 // max(T.itemsize, x.dtype.itemsize)))
+    chunks = ITEMS // vec
     ident = c_literal(_IDENT[rop](T), T)
-    lines = [f"static __device__ __forceinline__ void load(const Params& p, const long long base, {ct} (&vals)[{ITEMS}]) {{"]
-    lines += ["  " + c for c in em.consts]
-    lines += render(em.row, 1)
-    lines.append("}")
-    params = _params_struct(region)
+    comb = _COMBINE[rop]
     op = _OPS[rop]
+
+    def load_fn(name, full):
+        # element e of the tile = j*(TPB*vec) + vec*tid + v (striped, coalesced)
+        em = LoopEmitter(region, vec_loads=full)
+        tb = Var("tb", 1, align=tile)
+        tt = Var("tt", 1)
+        j, sj, a = em.open(1, "for", trip=chunks, unroll=True)
+        v, sv, b = em.open(j.level, "for", trip=vec, unroll=True)
+        e = Aff.of(j).scale(TILE_THREADS * vec) + Aff.of(tt).scale(vec) + Aff.of(v)
+        if full:
+            lin = Aff.of(tb) + e
+        else:
+            raw = em.emit(v.level, "long long", f"tb + {e.c()}")
+            lin = Aff.of(Var(em.emit(v.level, "long long", f"{raw} < {N}LL ? {raw} : {N - 1}LL"), v.level))
+        coords = _flat_coords(em, x.shape, lin, v)
+        val = em.cast(em.value(x, coords), x.dtype, T)
+        keep = "" if full else f"(tb + {e.c()} < {N}LL) ? "
+        tail = "" if full else f" : {ident}"
+        em.stmt(v.level, f"buf[gr::spad({e.c()})] = {keep}{val[0]}{tail};")
+        em.close(sv, b)
+        em.close(sj, a)
+        out = [f"static __device__ __forceinline__ void {name}(const Params& p, const long long tb, {ct}* buf) {{",
+               "  const long long tt = threadIdx.x;"]
+        out += ["  " + c for c in em.consts]
+        out += render(em.row, 1)
+        out.append("}")
+        return out
+
+    lines = load_fn("load_full", True) + load_fn("load_tail", False)
+    params = _params_struct(region)
     kern = f'''extern "C" __global__ void __launch_bounds__({TILE_THREADS}) {kname}(const K::Params p) {{
-  __shared__ long long tile_id;
+  __shared__ {ct} buf[{tile + tile // 32}];
   __shared__ {ct} wsum[{TILE_THREADS // 32}];
-  __shared__ {ct} tile_prefix;
-  unsigned long long* flags = reinterpret_cast<unsigned long long*>(p.scratch);
-  gr::ScanState<{ct}> st{{flags + 1, reinterpret_cast<{ct}*>(flags + 1 + {ntiles}), reinterpret_cast<{ct}*>(flags + 1 + 2 * {ntiles})}};
+  __shared__ {ct} tile_pre;
+  __shared__ long long tile_id;
+  unsigned long long* counter = reinterpret_cast<unsigned long long*>(p.scratch);
+  unsigned* flags = reinterpret_cast<unsigned*>(counter + 1);
+  {ct}* aggs = reinterpret_cast<{ct}*>(counter + 1 + {(ntiles + 1) // 2});
+  {ct}* incs = aggs + {ntiles};
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (;;) {{
-    if (threadIdx.x == 0) tile_id = (long long)atomicAdd(&flags[0], 1ull);
+    if (threadIdx.x == 0) tile_id = (long long)atomicAdd(counter, 1ull);
     __syncthreads();
     const long long t = tile_id;
-    __syncthreads();
     if (t >= {ntiles}LL) break;
-    const long long base = t * {tile}LL + (long long)threadIdx.x * {ITEMS};
+    const long long tb = t * {tile}LL;
+    if (tb + {tile}LL <= {N}LL) K::load_full(p, tb, buf); else K::load_tail(p, tb, buf);
+    __syncthreads();
     {ct} vals[{ITEMS}];
-    K::load(p, base, vals);
-    // thread-sequential inclusive run
+#pragma unroll
+    for (int i = 0; i < {ITEMS}; ++i) vals[i] = buf[gr::spad({ITEMS} * threadIdx.x + i)];
 #pragma unroll
     for (int i = 1; i < {ITEMS}; ++i) vals[i] = {comb}<{ct}>(vals[i - 1], vals[i]);
-    const int valid = (int)(({N}LL - base) < {ITEMS} ? ({N}LL - base) : {ITEMS});
-    {ct} run = valid > 0 ? vals[valid - 1] : {ident};
-    // warp inclusive scan of run totals (lane order)
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    {ct} inc = run;
+    // warp inclusive scan of the thread runs (lane order)
+    {ct} inc = vals[{ITEMS - 1}];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {{
-      {ct} y = __shfl_up_sync(0xffffffffu, inc, o);
+      const {ct} y = __shfl_up_sync(0xffffffffu, inc, o);
       if (lane >= o) inc = {comb}<{ct}>(y, inc);
     }}
     if (lane == 31) wsum[w] = inc;
     __syncthreads();
-    if (threadIdx.x == 0) {{
+    if (w == 0) {{
       {ct} acc = wsum[0];
-      for (int i = 1; i < {TILE_THREADS // 32}; ++i) {{ acc = {comb}<{ct}>(acc, wsum[i]); wsum[i] = acc; }}
-      tile_prefix = gr::scan_lookback<{op}, {ct}>(st, t, acc);
+      for (int i = 1; i < {TILE_THREADS // 32}; ++i) {{ acc = {comb}<{ct}>(acc, wsum[i]); if (lane == 0) wsum[i] = acc; }}
+      const {ct} pre = gr::tile_lookback<{op}, {ct}>(flags, aggs, incs, t, acc, {ident});
+      if (lane == 0) tile_pre = pre;
     }}
     __syncthreads();
-    // exclusive prefix of this thread = tile prefix (+) warps before (+) lanes before
-    {ct} excl_lane = __shfl_up_sync(0xffffffffu, inc, 1);
-    bool has = false;
-    {ct} pre = {ident};
-    if (t > 0) {{ pre = tile_prefix; has = true; }}
+    // exclusive prefix of this thread: tile prefix, then warps before, then lanes before
+    const {ct} lane_ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    bool has = t > 0;
+    {ct} pre = tile_pre;
     if (w > 0) {{ pre = has ? {comb}<{ct}>(pre, wsum[w - 1]) : wsum[w - 1]; has = true; }}
-    if (lane > 0) {{ pre = has ? {comb}<{ct}>(pre, excl_lane) : excl_lane; has = true; }}
+    if (lane > 0) {{ pre = has ? {comb}<{ct}>(pre, lane_ex) : lane_ex; has = true; }}
 #pragma unroll
-    for (int i = 0; i < {ITEMS}; ++i) {{
-      if (i < valid) p.out0[base + i] = has ? {comb}<{ct}>(pre, vals[i]) : vals[i];
+    for (int i = 0; i < {ITEMS}; ++i) buf[gr::spad({ITEMS} * threadIdx.x + i)] = has ? {comb}<{ct}>(pre, vals[i]) : vals[i];
+    __syncthreads();
+    // coalesced write-back (striped)
+#pragma unroll
+    for (int j = 0; j < {chunks}; ++j) {{
+      const long long e = (long long)j * {TILE_THREADS * vec} + {vec} * threadIdx.x;
+      if (tb + e + {vec} <= {N}LL) {{
+        {ct} o[{vec}];
+#pragma unroll
+        for (int v = 0; v < {vec}; ++v) o[v] = buf[gr::spad(e + v)];
+        gr::stv<{ct}, {vec}>(p.out0 + tb + e, o);
+      }} else {{
+        for (int v = 0; v < {vec}; ++v) if (tb + e + v < {N}LL) p.out0[tb + e + v] = buf[gr::spad(e + v)];
+      }}
     }}
     __syncthreads();
   }}
 }}'''
     src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params, "  " + "\n  ".join(lines), "};", kern]
-    scratch = 8 * (1 + ntiles) + 2 * ntiles * max(T.itemsize, 8) + 256
+    scratch = 8 + 4 * (ntiles + 1) + 2 * ntiles * T.itemsize + 256
     return KernelSource("scan", "\n".join(src) + "\n", kname, list(range(len(region.leaves))), [0],
                         block=TILE_THREADS, groups=ntiles * TILE_THREADS, vec=1, unroll=1, scratch_bytes=scratch,
                         meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,

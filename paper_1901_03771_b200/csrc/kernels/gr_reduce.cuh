@@ -430,6 +430,89 @@ __device__ __forceinline__ T scan_lookback(const ScanState<T>& st, long long til
   return excl;
 }
 
+// Single-pass tile scan with a warp-parallel, order-preserving look-back.
+// Tile t publishes its aggregate (flag 1) and later its inclusive prefix
+// (flag 2) with release stores.  Warp 0 of tile t walks back over windows of
+// 32 predecessors (acquire loads) until a window holds an inclusive prefix,
+// then folds LEFT TO RIGHT: that inclusive prefix, then the aggregates of every
+// later tile up to t-1 (re-read from the aggregate array).  Each inclusive
+// prefix is prefix + aggregate, so any such left fold equals the sequential
+// chain of tile aggregates bit for bit: the result does not depend on timing.
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// padded shared-tile index: one spare word per 32 keeps both the striped
+// (coalesced) and the blocked (per-thread run) accesses bank-conflict free
+__device__ __forceinline__ long long spad(long long e) { return e + (e >> 5); }
+
+template <class Op, class T>
+__device__ __forceinline__ T tile_lookback(unsigned* flags, T* agg, T* inc, long long tile, T tile_agg, T ident) {
+  // warp 0, all lanes; returns the exclusive prefix (ident for tile 0)
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) {
+      inc[0] = tile_agg;
+      st_release_u32(flags, 2u);
+    }
+    return ident;
+  }
+  if (lane == 0) {
+    agg[tile] = tile_agg;
+    st_release_u32(flags + tile, 1u);
+  }
+  long long top = tile - 1;   // nearest tile of the current window (lane 0)
+  int k;
+  T v;
+  for (;;) {
+    const long long q = top - lane;
+    unsigned f = 2u;           // tiles before 0 never matter: tile 0 is inclusive
+    v = ident;
+    if (q >= 0) {
+      do {
+        f = ld_acquire_u32(flags + q);
+      } while (f == 0u);
+      v = (f == 2u) ? __ldcg(inc + q) : __ldcg(agg + q);   // L2: never a stale L1 line
+    }
+    const unsigned m2 = __ballot_sync(0xffffffffu, q >= 0 && f == 2u);
+    if (m2) {
+      k = __ffs(m2) - 1;
+      break;
+    }
+    top -= 32;
+  }
+  // the sequential fold runs in lane 0 over values staged in shared memory
+  // (one dependent add per tile, loads pipelined) — a shuffle per step would
+  // put a shuffle round trip on the critical path of every later tile
+  __shared__ T lb[32];
+  lb[lane] = v;
+  __syncwarp();
+  T pre = ident;
+  if (lane == 0) {
+    pre = lb[k];
+    for (int l = k - 1; l >= 0; --l) pre = Op::template c<T>(pre, lb[l]);
+  }
+  for (long long w = top + 32; w <= tile - 1; w += 32) {
+    __syncwarp();
+    lb[lane] = __ldcg(agg + (w - lane));   // published (flag >= 1) during the walk
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int l = 31; l >= 0; --l) pre = Op::template c<T>(pre, lb[l]);
+    }
+  }
+  if (lane == 0) {
+    inc[tile] = Op::template c<T>(pre, tile_agg);
+    st_release_u32(flags + tile, 2u);
+  }
+  return __shfl_sync(0xffffffffu, pre, 0);
+}
+
 // Grid completion ticket: returns true in exactly one (the last) block, after
 // every block's partials are visible.  The ticket self-resets for the next
 // launch of the same kernel (stream order serialises launches).

@@ -150,3 +150,14 @@ def jacobi(xp, a):
     b = a.copy()
     b[1:-1, 1:-1] = 0.2 * (a[1:-1, 1:-1] + a[1:-1, :-2] + a[1:-1, 2:] + a[:-2, 1:-1] + a[2:, 1:-1])
     return b
+
+
+# ---- map-scan ------------------------------------------
+def scan_inputs(n=1 << 28, seed=42, dtype=np.float32):
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal(n, dtype=np.float32).astype(dtype),)
+
+
+def scan(xp, x):
+    """Map-scan: a fused map prologue feeding one inclusive scan."""
+    return xp.cumsum(x * 0.5 + 1.0)
