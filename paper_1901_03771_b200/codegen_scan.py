@@ -18,6 +18,7 @@ sequential left fold along the axis (out[k] = out[k-1] ⊕ x[k]).
 
 from __future__ import annotations
 
+import os
 from typing import List
 
 from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, c_literal
@@ -109,7 +110,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     N = element_count(x.shape)
     # 8192-element tiles (fewer tiles in flight: shorter look-back walks);
     # 4096 for 8-byte types so the shared tile stays within 48 KB
-    TILE_THREADS = 512 if T.itemsize <= 4 else 256
+    TILE_THREADS = int(os.environ.get("GRUMPY_SCAN_TPB", "512")) if T.itemsize <= 4 else 256
     tile = TILE_THREADS * ITEMS
     ntiles = -(-N // tile)
     vec = max(1, min(4, 16 // max(T.itemsize, x.dtype.itemsize)))
@@ -147,73 +148,120 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
 
     lines = load_fn("load_full", True) + load_fn("load_tail", False)
     params = _params_struct(region)
-    kern = f'''extern "C" __global__ void __launch_bounds__({TILE_THREADS}) {kname}(const K::Params p) {{
-  __shared__ {ct} buf[{tile + tile // 32}];
-  __shared__ {ct} wsum[{TILE_THREADS // 32}];
-  __shared__ {ct} tile_pre;
-  __shared__ long long tile_id;
+    TP = tile + tile // 32          # padded shared tile
+    NTH = TILE_THREADS + 32         # + the look-back warp
+    # residency: two shared tiles per CTA; cap registers so the shared memory,
+    # not the register file, sets the CTAs per SM
+    minb = max(1, min(int(os.environ.get("GRUMPY_SCAN_MINB", "8")), (227 * 1024) // (2 * TP * T.itemsize + 1024)))
+    kern = f'''extern "C" __global__ void __launch_bounds__({NTH}, {minb}) {kname}(const K::Params p) {{
+  // warps 0..{TILE_THREADS // 32 - 1}: data (load, tile-local scan, store) over two shared tiles;
+  // warp {TILE_THREADS // 32}: look-back — tile i's prefix is resolved while the data warps
+  // load and scan tile i+1 (named barriers: 1 data warps, 2 "staged", 3 "prefix ready")
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  {ct}* bufs = reinterpret_cast<{ct}*>(smem_raw);
+  __shared__ {ct} wsum[2][{TILE_THREADS // 32}];
+  __shared__ {ct} tagg[2];
+  __shared__ {ct} tpre[2];
+  __shared__ long long tids[2];
+  __shared__ long long next_id;
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(p.scratch);
   unsigned* flags = reinterpret_cast<unsigned*>(counter + 1);
   {ct}* aggs = reinterpret_cast<{ct}*>(counter + 1 + {(ntiles + 1) // 2});
   {ct}* incs = aggs + {ntiles};
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (;;) {{
-    if (threadIdx.x == 0) tile_id = (long long)atomicAdd(counter, 1ull);
-    __syncthreads();
-    const long long t = tile_id;
-    if (t >= {ntiles}LL) break;
-    const long long tb = t * {tile}LL;
-    if (tb + {tile}LL <= {N}LL) K::load_full(p, tb, buf); else K::load_tail(p, tb, buf);
-    __syncthreads();
-    {ct} vals[{ITEMS}];
-#pragma unroll
-    for (int i = 0; i < {ITEMS}; ++i) vals[i] = buf[gr::spad({ITEMS} * threadIdx.x + i)];
-#pragma unroll
-    for (int i = 1; i < {ITEMS}; ++i) vals[i] = {comb}<{ct}>(vals[i - 1], vals[i]);
-    // warp inclusive scan of the thread runs (lane order)
-    {ct} inc = vals[{ITEMS - 1}];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {{
-      const {ct} y = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc = {comb}<{ct}>(y, inc);
+  if (w == {TILE_THREADS // 32}) {{
+    for (int i = 0;; ++i) {{
+      asm volatile("bar.sync 2, {NTH};" ::: "memory");
+      const long long t = tids[i & 1];
+      if (t < 0) break;
+      const {ct} pre = gr::tile_lookback<{op}, {ct}, false>(flags, aggs, incs, t, tagg[i & 1], {ident});
+      if (lane == 0) tpre[i & 1] = pre;
+      asm volatile("bar.arrive 3, {NTH};" ::: "memory");
     }}
-    if (lane == 31) wsum[w] = inc;
-    __syncthreads();
-    if (w == 0) {{
-      {ct} acc = wsum[0];
-      for (int i = 1; i < {TILE_THREADS // 32}; ++i) {{ acc = {comb}<{ct}>(acc, wsum[i]); if (lane == 0) wsum[i] = acc; }}
-      const {ct} pre = gr::tile_lookback<{op}, {ct}>(flags, aggs, incs, t, acc, {ident});
-      if (lane == 0) tile_pre = pre;
-    }}
-    __syncthreads();
-    // exclusive prefix of this thread: tile prefix, then warps before, then lanes before
-    const {ct} lane_ex = __shfl_up_sync(0xffffffffu, inc, 1);
-    bool has = t > 0;
-    {ct} pre = tile_pre;
-    if (w > 0) {{ pre = has ? {comb}<{ct}>(pre, wsum[w - 1]) : wsum[w - 1]; has = true; }}
-    if (lane > 0) {{ pre = has ? {comb}<{ct}>(pre, lane_ex) : lane_ex; has = true; }}
+    return;
+  }}
+  // ---- data warps
+  long long t;
+  {{
+    if (threadIdx.x == 0) next_id = (long long)atomicAdd(counter, 1ull);
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+    t = next_id < {ntiles}LL ? next_id : -1;
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+  }}
+  int b = 0;
+  if (t >= 0) K::stage(p, t, bufs, wsum[0], &tagg[0], &tids[0], flags, aggs, lane, w);
+  else if (threadIdx.x == 0) tids[0] = -1;
+  asm volatile("bar.arrive 2, {NTH};" ::: "memory");
+  while (t >= 0) {{
+    if (threadIdx.x == 0) next_id = (long long)atomicAdd(counter, 1ull);
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+    const long long tn = next_id < {ntiles}LL ? next_id : -1;
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+    if (tn >= 0) K::stage(p, tn, bufs + (b ^ 1) * {TP}LL, wsum[b ^ 1], &tagg[b ^ 1], &tids[b ^ 1], flags, aggs, lane, w);
+    asm volatile("bar.sync 3, {NTH};" ::: "memory");
+    // tile t: prefix (+) tile-local inclusive scan, coalesced stores
+    {{
+      const {ct}* buf = bufs + b * {TP}LL;
+      const {ct} pre = tpre[b];
+      const long long tb = t * {tile}LL;
 #pragma unroll
-    for (int i = 0; i < {ITEMS}; ++i) buf[gr::spad({ITEMS} * threadIdx.x + i)] = has ? {comb}<{ct}>(pre, vals[i]) : vals[i];
-    __syncthreads();
-    // coalesced write-back (striped)
-#pragma unroll
-    for (int j = 0; j < {chunks}; ++j) {{
-      const long long e = (long long)j * {TILE_THREADS * vec} + {vec} * threadIdx.x;
-      if (tb + e + {vec} <= {N}LL) {{
+      for (int j = 0; j < {chunks}; ++j) {{
+        const long long e = (long long)j * {TILE_THREADS * vec} + {vec} * threadIdx.x;
         {ct} o[{vec}];
 #pragma unroll
-        for (int v = 0; v < {vec}; ++v) o[v] = buf[gr::spad(e + v)];
-        gr::stv<{ct}, {vec}>(p.out0 + tb + e, o);
-      }} else {{
-        for (int v = 0; v < {vec}; ++v) if (tb + e + v < {N}LL) p.out0[tb + e + v] = buf[gr::spad(e + v)];
+        for (int v = 0; v < {vec}; ++v) {{ const {ct} x = buf[gr::spad(e + v)]; o[v] = t > 0 ? {comb}<{ct}>(pre, x) : x; }}
+        if (tb + e + {vec} <= {N}LL) {{
+          gr::stv<{ct}, {vec}>(p.out0 + tb + e, o);
+        }} else {{
+          for (int v = 0; v < {vec}; ++v) if (tb + e + v < {N}LL) p.out0[tb + e + v] = o[v];
+        }}
       }}
     }}
-    __syncthreads();
+    if (tn < 0 && threadIdx.x == 0) tids[b ^ 1] = -1;
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");   // buffer b free, tids visible
+    asm volatile("bar.arrive 2, {NTH};" ::: "memory");
+    t = tn;
+    b ^= 1;
   }}
 }}'''
+    stage = [f"static __device__ __forceinline__ void stage(const Params& p, const long long t, {ct}* buf, {ct}* ws, {ct}* agg_s, long long* tid_s, unsigned* flags, {ct}* aggs, const int lane, const int w) {{",
+             f"  const long long tb = t * {tile}LL;",
+             f"  if (tb + {tile}LL <= {N}LL) load_full(p, tb, buf); else load_tail(p, tb, buf);",
+             f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
+             f"  {ct} vals[{ITEMS}];",
+             "#pragma unroll",
+             f"  for (int i = 0; i < {ITEMS}; ++i) vals[i] = buf[gr::spad({ITEMS} * threadIdx.x + i)];",
+             "#pragma unroll",
+             f"  for (int i = 1; i < {ITEMS}; ++i) vals[i] = {comb}<{ct}>(vals[i - 1], vals[i]);",
+             f"  {ct} inc = vals[{ITEMS - 1}];",
+             "#pragma unroll",
+             "  for (int o = 1; o < 32; o <<= 1) {",
+             f"    const {ct} y = __shfl_up_sync(0xffffffffu, inc, o);",
+             f"    if (lane >= o) inc = {comb}<{ct}>(y, inc);",
+             "  }",
+             "  if (lane == 31) ws[w] = inc;",
+             f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
+             "  if (threadIdx.x == 0) {",
+             f"    {ct} acc = ws[0];",
+             f"    for (int i = 1; i < {TILE_THREADS // 32}; ++i) {{ acc = {comb}<{ct}>(acc, ws[i]); ws[i] = acc; }}",
+             "    *agg_s = acc;",
+             "    *tid_s = t;",
+             f"    gr::tile_publish_agg<{ct}>(flags, aggs, t, acc);",
+             "  }",
+             f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
+             f"  const {ct} lane_ex = __shfl_up_sync(0xffffffffu, inc, 1);",
+             "  bool has = false;",
+             f"  {ct} loc = {ident};",
+             "  if (w > 0) { loc = ws[w - 1]; has = true; }",
+             f"  if (lane > 0) {{ loc = has ? {comb}<{ct}>(loc, lane_ex) : lane_ex; has = true; }}",
+             "#pragma unroll",
+             f"  for (int i = 0; i < {ITEMS}; ++i) buf[gr::spad({ITEMS} * threadIdx.x + i)] = has ? {comb}<{ct}>(loc, vals[i]) : vals[i];",
+             f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
+             "}"]
+    lines = lines + stage
     src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params, "  " + "\n  ".join(lines), "};", kern]
-    scratch = 8 + 4 * (ntiles + 1) + 2 * ntiles * T.itemsize + 256
+    scratch = 8 + 8 * 2 * ntiles + 4 * (ntiles + 1) + 2 * ntiles * T.itemsize + 256
     return KernelSource("scan", "\n".join(src) + "\n", kname, list(range(len(region.leaves))), [0],
-                        block=TILE_THREADS, groups=ntiles * TILE_THREADS, vec=1, unroll=1, scratch_bytes=scratch,
+                        block=NTH, groups=ntiles * NTH, vec=1, unroll=1, scratch_bytes=scratch,
                         meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,
-                              "label": "scan-lookback"})
+                              "label": "scan-lookback", "smem": 2 * TP * T.itemsize})

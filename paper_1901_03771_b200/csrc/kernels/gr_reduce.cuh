@@ -443,6 +443,12 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -451,9 +457,18 @@ __device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
 // (coalesced) and the blocked (per-thread run) accesses bank-conflict free
 __device__ __forceinline__ long long spad(long long e) { return e + (e >> 5); }
 
-template <class Op, class T>
+// Publish a tile's aggregate (flag 1); tile 0 publishes its inclusive prefix
+// from the look-back instead.
+template <class T> __device__ __forceinline__ void tile_publish_agg(unsigned* flags, T* agg, long long tile, T v) {
+  if (tile > 0) {
+    agg[tile] = v;
+    st_release_u32(flags + tile, 1u);
+  }
+}
+
+template <class Op, class T, bool PUBLISH_AGG = true>
 __device__ __forceinline__ T tile_lookback(unsigned* flags, T* agg, T* inc, long long tile, T tile_agg, T ident) {
-  // warp 0, all lanes; returns the exclusive prefix (ident for tile 0)
+  // one full warp; returns the exclusive prefix (ident for tile 0)
   const int lane = threadIdx.x & 31;
   if (tile == 0) {
     if (lane == 0) {
@@ -462,48 +477,50 @@ __device__ __forceinline__ T tile_lookback(unsigned* flags, T* agg, T* inc, long
     }
     return ident;
   }
-  if (lane == 0) {
-    agg[tile] = tile_agg;
-    st_release_u32(flags + tile, 1u);
-  }
-  long long top = tile - 1;   // nearest tile of the current window (lane 0)
-  int k;
-  T v;
+  if (PUBLISH_AGG && lane == 0) tile_publish_agg<T>(flags, agg, tile, tile_agg);
+  // walk back 256 predecessors per round (8 per lane, one L2 round trip),
+  // relaxed flag loads (no L1 invalidation per load); one acquire fence once
+  // an inclusive prefix is in sight
+  constexpr int J = 8;
+  long long top = tile - 1;
+  long long found = -1;
   for (;;) {
-    const long long q = top - lane;
-    unsigned f = 2u;           // tiles before 0 never matter: tile 0 is inclusive
-    v = ident;
-    if (q >= 0) {
-      do {
-        f = ld_acquire_u32(flags + q);
-      } while (f == 0u);
-      v = (f == 2u) ? __ldcg(inc + q) : __ldcg(agg + q);   // L2: never a stale L1 line
+    unsigned f[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {   // J loads in flight
+      const long long q = top - lane - 32 * j;
+      f[j] = q >= 0 ? ld_relaxed_u32(flags + q) : 2u;
     }
-    const unsigned m2 = __ballot_sync(0xffffffffu, q >= 0 && f == 2u);
-    if (m2) {
-      k = __ffs(m2) - 1;
-      break;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {   // rarely taken: a predecessor not yet staged
+      const long long q = top - lane - 32 * j;
+      while (f[j] == 0u) f[j] = ld_relaxed_u32(flags + q);
     }
-    top -= 32;
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const unsigned m2 = __ballot_sync(0xffffffffu, f[j] == 2u && top - lane - 32 * j >= 0);
+      if (found < 0 && m2) found = top - (__ffs(m2) - 1) - 32 * j;
+    }
+    if (found >= 0) break;
+    top -= 32 * J;
   }
-  // the sequential fold runs in lane 0 over values staged in shared memory
-  // (one dependent add per tile, loads pipelined) — a shuffle per step would
-  // put a shuffle round trip on the critical path of every later tile
-  __shared__ T lb[32];
-  lb[lane] = v;
-  __syncwarp();
+  fence_acq_rel_gpu();
+  // left fold from the inclusive prefix of `found` over the aggregates of
+  // found+1 .. tile-1 (increasing tile order), staged 32 at a time in smem
+  __shared__ T lb[32 * J];
   T pre = ident;
-  if (lane == 0) {
-    pre = lb[k];
-    for (int l = k - 1; l >= 0; --l) pre = Op::template c<T>(pre, lb[l]);
-  }
-  for (long long w = top + 32; w <= tile - 1; w += 32) {
+  if (lane == 0) pre = __ldcg(inc + found);
+  for (long long base = found + 1; base <= tile - 1; base += 32 * J) {
     __syncwarp();
-    lb[lane] = __ldcg(agg + (w - lane));   // published (flag >= 1) during the walk
+#pragma unroll
+    for (int j = 0; j < J; ++j) {   // 256 aggregates per round trip
+      const long long q = base + lane + 32 * j;
+      lb[lane + 32 * j] = q <= tile - 1 ? __ldcg(agg + q) : ident;
+    }
     __syncwarp();
     if (lane == 0) {
-#pragma unroll
-      for (int l = 31; l >= 0; --l) pre = Op::template c<T>(pre, lb[l]);
+      const int cnt = (int)((tile - base) < 32 * J ? (tile - base) : 32 * J);
+      for (int l = 0; l < cnt; ++l) pre = Op::template c<T>(pre, lb[l]);
     }
   }
   if (lane == 0) {

@@ -100,3 +100,15 @@ def test_shifted_vector_slices(sess):
     m = rng.standard_normal((64, 72)).astype(np.float64)
     gm = gp.asarray(m)
     assert np.array_equal(np.asarray(gm[:, 1:] + gm[:, :-1]), m[:, 1:] + m[:, :-1])
+
+
+def test_scan_lookback_deterministic(sess):
+    """The tile-tree prefix folds a fixed association of tile aggregates:
+    repeated runs are bit-identical (timing cannot change the result)."""
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((1 << 22) + 1234).astype(np.float32)
+    g = gp.asarray(x)
+    runs = [np.asarray(gp.cumsum(g * 0.5 + 1.0)) for _ in range(3)]
+    assert all(np.array_equal(runs[0], r) for r in runs[1:])
+    ref = np.cumsum((x * np.float32(0.5) + np.float32(1.0)).astype(np.float64))
+    assert np.max(np.abs(runs[0] - ref)) <= 1e-6 * np.max(np.abs(ref)) + 1.0
