@@ -5,11 +5,11 @@
 OUT=gpurun_out/round
 mkdir -p $OUT
 timeout 900 python -m pytest tests -m gpu -q > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
-for w in blackscholes-f32 blackscholes-f64 listing1 rownorm rownorm-y mlp kmeans jacobi; do
+for w in blackscholes-f32 blackscholes-f64 listing1 rownorm rownorm-y mlp kmeans jacobi cumsum; do
   timeout 400 python bench.py --workload $w > $OUT/bench_$w.json 2> $OUT/bench_$w.err
 done
 timeout 300 python bench.py --impl reference > $OUT/bench_reference.json 2> $OUT/bench_reference.err
-for w in blackscholes-f32 blackscholes-f64 listing1 rownorm rownorm-y mlp kmeans jacobi; do
+for w in blackscholes-f32 blackscholes-f64 listing1 rownorm rownorm-y mlp kmeans jacobi cumsum; do
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
     --clock-control none -k regex:gr_ -c 40 --csv --log-file $OUT/launches_$w.csv \
     python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
