@@ -199,10 +199,11 @@ WORKLOADS = {
         inputs=lambda n, s: _km_inputs(n, s),
         program=lambda xp, a: _km_step(xp, a),
         elements=lambda n: n, bytes=lambda n: n * (KM_D * 4 + 8) + 64 * KM_D * 4, bound="fp32 issue (no FMA, NumPy order)",
-        # NumPy's operation sequence per point: 64 centroids x (D sub + D square
-        # + (D-1) add + the 0.0 identity add of add.reduce)
+        # per point: 64 centroids x (D sub + D square + (D-1) add + 1 compare
+        # of the argmin); the seed add of NumPy's fold is an identity and is
+        # not executed
         compute=dict(pipe="fp32", ops=64 * (3 * KM_D), lanes_per_sm_clk=128,
-                     note="64 x (4 sub + 4 mul + 3 add + 1 identity add) lane-ops per point"),
+                     note="64 x (4 sub + 4 mul + 3 add + 1 argmin compare) lane-ops per point"),
         sharded=(0,)),
     "cumsum": dict(
         n=1 << 28, label="f32", desc="map-scan cumsum(x*0.5+1) over 2^28 fp32 (SURVEY.md §8(f))",

@@ -145,6 +145,7 @@ class LoopEmitter(ValueEmitter):
         # leaf id -> __constant__ symbol for small leaves every row reads at
         # the same (row-independent) offsets, e.g. the k-means centroids
         self.cbank: Dict[int, str] = dict(cbank or {})
+        self.cbank_pair: Dict[int, int] = {}   # leaf id -> pair stride of its pair-adjacent copy
         self.uniform_vars = set()   # loop indices with row-independent values
         # loop pairing: an unrolled f32 arg-reduction loop walks index PAIRS
         # (2i, 2i+1); values that depend on the logical index (2*iv + half)
@@ -246,9 +247,21 @@ class LoopEmitter(ValueEmitter):
             if sym is not None:
                 if any(v.name not in self.uniform_vars for v, _ in lo.terms):
                     raise CBankMiss(leaf)
-                a, b = f"{sym}[{lo.c()}]", f"{sym}[{hi.c()}]"
+                B = off.coef(self.half)
+                n = element_count(leaf.shape)
+                if B > 0 and n % (2 * B) == 0 and self.cbank_pair.get(leaf.id, B) == B:
+                    # pair-adjacent copy of the leaf: (x[lo], x[lo+B]) is one
+                    # 64-bit constant -> a uniform-register pair operand
+                    self.cbank_pair[leaf.id] = B
+                    psym = sym + "_p"
+                    expr = (f"((({lo.c()}) / {B}) % 2 == 0 ? gr::f2{{{psym}[(({lo.c()}) / {2 * B}) * {B} + (({lo.c()}) % {B})]}} "
+                            f": gr::pk({sym}[{lo.c()}], {sym}[{hi.c()}]))")
+                    return self.emit_pair(lvl, expr), lvl
+                raise NotPairable("constant-bank leaf without a pair-adjacent copy")
             else:
-                a, b = f"gr::ld<{T}>({ptr} + {lo.c()})", f"gr::ld<{T}>({ptr} + {hi.c()})"
+                # gathered pairs of a row-invariant leaf get hoisted out of the
+                # row loop by ptxas (254 registers, 4.14 vs 3.25 ms for k-means)
+                raise NotPairable("paired operand outside the constant bank")
             return self.emit_pair(lvl, f"gr::pk({a}, {b})"), lvl
         if sym is not None:
             if any(v.name not in self.uniform_vars for v, _ in off.terms):
@@ -421,7 +434,7 @@ class LoopEmitter(ValueEmitter):
             iv, s, saved = self.open(loop_lvl, "for", trip=Lg, unroll=True)
             inner = self._delin(iv, g, gdims)
             v = self.cast(self.value(x, full_coords(inner)), x.dtype, T)
-            self.stmt(iv.level, f"{part} = gr::add<{ct}>({part}, {v[0]});")
+            self.stmt(iv.level, f"{part} = {iv.name} == 0 ? {v[0]} : gr::add<{ct}>({part}, {v[0]});")
             self.close(s, saved)
             return part, L
         if pairwise and element_count([So[a] for a in groups[-1]]) < 8:
@@ -434,7 +447,8 @@ class LoopEmitter(ValueEmitter):
             iv, s, saved = self.open(loop_lvl, "for", trip=Lg, unroll=True)
             inner = self._delin(iv, g, gdims)
             v = self.cast(self.value(x, full_coords(inner)), x.dtype, T)
-            self.stmt(iv.level, f"{part} = gr::add<{ct}>({part}, {v[0]});")
+            # -0.0 + t == t (up to a NaN payload): the first term seeds the fold
+            self.stmt(iv.level, f"{part} = {iv.name} == 0 ? {v[0]} : gr::add<{ct}>({part}, {v[0]});")
             self.close(s, saved)
             self.stmt(loop_lvl, f"{acc} = gr::add<{ct}>({acc}, {part});")
         elif pairwise:
@@ -478,7 +492,9 @@ class LoopEmitter(ValueEmitter):
         self.pairs.update((acc, part))
         iv, s, saved = self.open(L, "for", trip=n, unroll=True)
         v = self.value(x, list(kept) + [Aff.of(iv)])
-        self.stmt(iv.level, f"{part} = gr::p2::add({part}, {self.splat(v)});")
+        # -0.0 + t == t: the first term seeds the fold (the packed add is
+        # inline asm, which ptxas does not fold)
+        self.stmt(iv.level, f"{part} = {iv.name} == 0 ? {self.splat(v)} : gr::p2::add({part}, {self.splat(v)});")
         self.close(s, saved)
         self.stmt(L, f"{acc} = gr::p2::add({acc}, {part});")
         return acc, L
@@ -543,6 +559,7 @@ class LoopEmitter(ValueEmitter):
         # plus one add whose result is NaN whenever an operand is NaN; only
         # then is the operand rescanned for np.argmax's answer, its first NaN
         cmp = ">" if which == "max" else "<"
+        nanop = "gr::max_nan" if which == "max" else "gr::min_nan"
         if self.pair_loops and n % 2 == 0 and n <= ARG_UNROLL and x.dtype is DType.f32 and self.half is None:
             # paired scan: drop the scalar loop opened above and walk pairs
             self.close(s, saved)
@@ -566,11 +583,13 @@ class LoopEmitter(ValueEmitter):
                 self.half = None
             pv = self.splat(v)
             self.stmt(iv.level, f"{{ const float vlo = gr::lo({pv}), vhi = gr::hi({pv}); "
-                                f"if ({iv.name} == 0 || vlo {cmp} {best}) {{ {best} = vlo; {bi} = 2 * {iv.name}; }} "
-                                f"if (vhi {cmp} {best}) {{ {best} = vhi; {bi} = 2 * {iv.name} + 1; }} }}")
-            self.stmt(iv.level, f"{nacc} = gr::p2::add({nacc}, {pv});")
+                                f"if ({iv.name} != 0 && vlo {cmp} {best}) {bi} = 2 * {iv.name}; "
+                                f"{best} = {iv.name} == 0 ? vlo : {nanop}({best}, vlo); "
+                                f"if (vhi {cmp} {best}) {bi} = 2 * {iv.name} + 1; "
+                                f"{best} = {nanop}({best}, vhi); }}")
+            self.stmt(L, f"(void){nacc};")
             self.close(s, saved)
-            nan_test = f"gr::lo({nacc}) != gr::lo({nacc}) || gr::hi({nacc}) != gr::hi({nacc})"
+            nan_test = f"{best} != {best}"
         else:
             nacc = self.var_decl(L, T, "0")
             self.stmt(iv.level, f"if ({iv.name} == 0 || {v[0]} {cmp} {best}) {{ {best} = {v[0]}; {bi} = {iv.name}; }}")
@@ -732,13 +751,15 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
             pair = False
 
 
-# Paired arg-reduction loops are exact but off by default: on B200 a packed
-# FADD2/FFMA2 occupies the 32-lane FMA pipe for two cycles, so they only save
-# issue slots, and the paired constant operands need a pair-adjacent layout
-# (measured on k-means 2^26 x 64: scalar 3.25 ms; pairs from the leaf layout
-# 4.14 ms at 254 regs; pairs from a pair-adjacent smem copy 2.99 ms at 44 regs,
-# FMA pipe 65% — profiles/r01s2_kmeans_variants.md).
-PAIR_LOOPS = os.environ.get("GRUMPY_PAIR_LOOPS", "0") == "1"
+# Paired arg-reduction loops (two candidates per packed FADD2/FFMA2): used when
+# every paired operand is a constant-bank leaf, read from a pair-adjacent copy
+# (one 64-bit constant = one uniform-register pair operand) that a repack
+# kernel of the same module writes before each launch; the running best is
+# kept with min.NaN/max.NaN so a NaN candidate needs no extra add.  Measured on
+# k-means 2^26 x 64: scalar 3.25 ms; pairs gathered from the leaf layout
+# 4.14 ms (254 regs, refused now); pairs from a pair-adjacent smem copy
+# 2.99 ms; pair-adjacent constant bank 2.41 ms (profiles/r01s2_kmeans_variants.md).
+PAIR_LOOPS = os.environ.get("GRUMPY_PAIR_LOOPS", "1") == "1"
 
 
 def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
@@ -945,6 +966,18 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
             used_cb.append((i, sym, element_count(l.shape) * l.dtype.itemsize))
     cdecl = "".join(f"__constant__ {region.leaves[i].dtype.ctype} {sym}[{nb // region.leaves[i].dtype.itemsize}];\n"
                     for i, sym, nb in used_cb)
+    used_pair = []
+    for i, sym, nb in used_cb:
+        B = em.cbank_pair.get(region.leaves[i].id)
+        if B and sym + "_p[" in "\n".join(lines):
+            npairs = nb // region.leaves[i].dtype.itemsize // 2
+            used_pair.append((i, sym + "_p", B, npairs, f"gr_repack{i}"))
+            cdecl += (f"__constant__ unsigned long long {sym}_p[{npairs}];\n"
+                      f'extern "C" __global__ void gr_repack{i}(const float* __restrict__ src, unsigned long long* dst) {{\n'
+                      f"  for (int i = threadIdx.x; i < {npairs}; i += blockDim.x) {{\n"
+                      f"    const int lo = (i / {B}) * {2 * B} + i % {B};\n"
+                      f"    dst[i] = (unsigned long long)__float_as_uint(src[lo]) | ((unsigned long long)__float_as_uint(src[lo + {B}]) << 32);\n"
+                      "  }\n}\n")
     src = [HEADER, '#include "gr_reduce.cuh"\n', cdecl, "struct K {", params,
            f"  static constexpr long long NROWS = {R}LL;"]
     src.append("  " + "\n  ".join(lines))
@@ -1006,7 +1039,7 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
                         block=block, groups=R, vec=1, unroll=1, scratch_bytes=scratch_off,
                         meta={"rows": R, "row_shape": Ts, "totals": len(tot_meta), "ticket": bool(tot_meta or kmeta),
                               "virtual": virtual, "block_pow2": True, "keyed": len(kmeta),
-                              "max_grid": MAX_GRID if kmeta else None, "cbank": used_cb})
+                              "max_grid": MAX_GRID if kmeta else None, "cbank": used_cb, "cbank_pair": used_pair})
 
 
 def _row_partial(em: LoopEmitter, x: Node, rop, T: DType, row_coords, cols):

@@ -79,6 +79,18 @@ __device__ __forceinline__ T pairwise(const F& f, long long off) {
 template <class T> __device__ __forceinline__ bool arg_better_max(T x, T best) {
   return (x > best) || (x != x && best == best);
 }
+// NaN-propagating min/max (PTX min.NaN / max.NaN): arg-reduction scans keep
+// the best value with these so a NaN operand is visible at the end
+__device__ __forceinline__ float min_nan(float a, float b) {
+  float r;
+  asm("min.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
 template <class T> __device__ __forceinline__ bool arg_better_min(T x, T best) {
   return (x < best) || (x != x && best == best);
 }

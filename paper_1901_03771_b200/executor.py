@@ -122,6 +122,14 @@ class Executor:
                 dst = c["cbank_dst"] = [self.rt.module_global(k, sym)[0] for _i, sym, _nb in cb]
             for (i, _sym, nb), d in zip(cb, dst):
                 self.rt.d2d_raw(d, ptrs[i], nb)
+        for i, psym, _b, _npairs, rname in ks.meta.get("cbank_pair") or ():
+            # pair-adjacent copy of a constant-bank leaf (paired arg-reduction
+            # loops): a one-CTA repack kernel of the same module writes it
+            rp = c.setdefault("repack", {})
+            if psym not in rp:
+                rp[psym] = (self.rt.function(k, rname), self.rt.module_global(k, psym)[0])
+            fn, addr = rp[psym]
+            self.rt.launch(fn, 1, 256, runtime.pack_params([ptrs[i], addr]))
         ptrs += [b.device.ptr for b in outs]
         scratch = None
         if ks.scratch_bytes:

@@ -248,6 +248,12 @@ class Runtime:
     def sync(self):
         _check(self.lib.grumpy_rt_sync())
 
+    def function(self, k: "Kernel", name: str) -> "Kernel":
+        """Another kernel of ``k``'s module (e.g. a leaf repack kernel)."""
+        fn = ctypes.c_uint64(0)
+        _check(self.lib.grumpy_rt_get_function(k.module, name.encode(), ctypes.byref(fn)))
+        return Kernel(fn.value, name, 256, 1, 0, 0.0, 1, "", k.module)
+
     def module_global(self, k: "Kernel", name: str):
         """(device address, bytes) of a module-scope symbol of ``k``'s module."""
         p = ctypes.c_uint64(0)

@@ -201,3 +201,18 @@ def test_kmeans_paired_loop_exact(sess, monkeypatch):
         assert np.array_equal(got, wl.kmeans_assign(np, P, C))
     finally:
         codegen._GEN_CACHE.clear()
+
+
+def test_kmeans_lloyd_iterations_exact(sess):
+    """Several Lloyd iterations through one compiled kernel: the centroid
+    leaf (constant bank + its pair-adjacent repacked copy) changes every
+    launch and the labels must track NumPy's every time."""
+    P, C = wl.kmeans_inputs(n=(1 << 14) + 3, k=64, d=4, seed=5)
+    gP = gp.asarray(P)
+    for _ in range(4):
+        lab, sums, counts = wl.kmeans_partials(gp, gP, gp.asarray(C))
+        gp.force(lab, *sums, counts)
+        elab, esums, ecounts = wl.kmeans_partials(np, P, C)
+        assert np.array_equal(np.asarray(lab), elab)
+        assert np.array_equal(np.asarray(counts), ecounts)
+        C = wl.kmeans_centroids(esums, ecounts, C)
