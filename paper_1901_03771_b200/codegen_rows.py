@@ -485,17 +485,24 @@ class LoopEmitter(ValueEmitter):
                 or list(axes) != [len(So) - 1] or So[-1] >= 8):
             raise NotPairable("paired reduction other than a short f32 sum")
         n = So[-1]
-        acc = self.fresh("a")
-        self.stmt(L, f"gr::f2 {acc} = gr::splat({c_literal(0, T)});")
         part = self.fresh("a")
         self.stmt(L, f"gr::f2 {part} = gr::splat({c_literal(-0.0, T)});")
-        self.pairs.update((acc, part))
+        self.pairs.add(part)
+        # consumed only by ordered compares: the 0.0 identity add only
+        # changes the sign of a zero sum, which no compare sees
+        compared = self._only_compared(r)
+        if not compared:
+            acc = self.fresh("a")
+            self.stmt(L, f"gr::f2 {acc} = gr::splat({c_literal(0, T)});")
+            self.pairs.add(acc)
         iv, s, saved = self.open(L, "for", trip=n, unroll=True)
         v = self.value(x, list(kept) + [Aff.of(iv)])
         # -0.0 + t == t: the first term seeds the fold (the packed add is
         # inline asm, which ptxas does not fold)
         self.stmt(iv.level, f"{part} = {iv.name} == 0 ? {self.splat(v)} : gr::p2::add({part}, {self.splat(v)});")
         self.close(s, saved)
+        if compared:
+            return part, L
         self.stmt(L, f"{acc} = gr::p2::add({acc}, {part});")
         return acc, L
 

@@ -35,7 +35,7 @@ def main():
         name, _, pre = spec.partition(":")
         src = ks0.source
         block, grid_over, smem, tmap = ks0.block, None, ks0.meta.get("smem", 0), False
-        if ";" in pre:
+        if ";" in pre and not pre.startswith("REPL="):
             pre, *opts = pre.split(";")
             for o in opts:
                 kk, vv = o.split("=")
@@ -49,6 +49,12 @@ def main():
                     tmap = True
         if pre.startswith("FILE="):
             src = open(pre[5:]).read()
+        elif pre.startswith("REPL="):
+            # REPL=old=>new[@@old2=>new2...]: literal source substitutions
+            for pair in pre[5:].split("@@"):
+                a, b = pair.split("=>")
+                assert a in src, a
+                src = src.replace(a, b)
         elif pre.startswith("U="):
             src = src.replace("static constexpr int U = 1;", f"static constexpr int U = {pre[2:]};")
             src = src.replace("static constexpr int U = 2;", f"static constexpr int U = {pre[2:]};")
@@ -74,6 +80,10 @@ def main():
             rd = rt.alloc(1 << 16)
             rt.memset(rd, 0)
             ptrs.append(rd.ptr)
+        for i, sym, nb in ks0.meta.get("cbank") or ():
+            rt.d2d_raw(rt.module_global(k, sym)[0], ptrs[i], nb)
+        for i, psym, _b, _np, rname in ks0.meta.get("cbank_pair") or ():
+            rt.launch(rt.function(k, rname), 1, 256, runtime.pack_params([ptrs[i], rt.module_global(k, psym)[0]]))
         params = runtime.pack_params(ptrs)
         if tmap:
             # leaf 0 as [n/32][32] f32 lines, box 128 lines (one 4096-float row), 128B swizzle
