@@ -8,12 +8,14 @@ sequential left fold along the axis (out[k] = out[k-1] ⊕ x[k]).
 * scans along an axis with many independent lines: one thread per line, the
   line folded sequentially — exactly NumPy's association (bit-identical);
 * long 1-D scans (axis=None or a single long line): a single-pass scan with
-  decoupled look-back — each CTA scans a 2048-element tile (thread-sequential
-  runs, warp-shuffle + shared-memory combine of run totals), publishes its
-  aggregate and inclusive prefix, and folds its predecessors' published values
-  (``gr::tile_lookback``: folds left to right, so the result does not depend
-  on timing — deterministic); float results within tolerance of NumPy's
-  sequential fold (reassociation), integers exact.
+  decoupled look-back — 8192-element tiles (a warp-specialised CTA: data warps
+  load, scan and store; one warp resolves the tile prefix), each tile
+  publishes its aggregate and then its inclusive prefix inside 64-bit status
+  words (value and flag in one word: no fences), and ``gr::tile_lookback``
+  folds the aggregates above the nearest published inclusive prefix left to
+  right, so the result does not depend on timing — deterministic; float
+  results within tolerance of NumPy's sequential fold (reassociation),
+  integers exact.
 """
 
 from __future__ import annotations
@@ -113,6 +115,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     TILE_THREADS = int(os.environ.get("GRUMPY_SCAN_TPB", "512")) if T.itemsize <= 4 else 256
     tile = TILE_THREADS * ITEMS
     ntiles = -(-N // tile)
+    SW = 1 if T.itemsize <= 4 else 2      # 64-bit status words per published value
     vec = max(1, min(4, 16 // max(T.itemsize, x.dtype.itemsize)))
     chunks = ITEMS // vec
     ident = c_literal(_IDENT[rop](T), T)
@@ -165,16 +168,21 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
   __shared__ long long tids[2];
   __shared__ long long next_id;
   unsigned long long* counter = reinterpret_cast<unsigned long long*>(p.scratch);
-  unsigned* flags = reinterpret_cast<unsigned*>(counter + 1);
-  {ct}* aggs = reinterpret_cast<{ct}*>(counter + 1 + {(ntiles + 1) // 2});
-  {ct}* incs = aggs + {ntiles};
+  unsigned long long* aggs = counter + 1;                       // tile aggregates (status words)
+  unsigned long long* incs = aggs + {ntiles * SW}LL;            // tile inclusive prefixes
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (w == {TILE_THREADS // 32}) {{
     for (int i = 0;; ++i) {{
+#ifdef GR_SCAN_STATS
+      const long long cw = clock64();
+#endif
       asm volatile("bar.sync 2, {NTH};" ::: "memory");
+#ifdef GR_SCAN_STATS
+      if (lane == 0) atomicAdd(&gr::gr_scan_stats[3], (unsigned long long)(clock64() - cw));
+#endif
       const long long t = tids[i & 1];
       if (t < 0) break;
-      const {ct} pre = gr::tile_lookback<{op}, {ct}, false>(flags, aggs, incs, t, tagg[i & 1], {ident});
+      const {ct} pre = gr::tile_lookback<{op}, {ct}>(aggs, incs, t, tagg[i & 1], {ident});
       if (lane == 0) tpre[i & 1] = pre;
       asm volatile("bar.arrive 3, {NTH};" ::: "memory");
     }}
@@ -189,7 +197,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
   }}
   int b = 0;
-  if (t >= 0) K::stage(p, t, bufs, wsum[0], &tagg[0], &tids[0], flags, aggs, lane, w);
+  if (t >= 0) K::stage(p, t, bufs, wsum[0], &tagg[0], &tids[0], aggs, lane, w);
   else if (threadIdx.x == 0) tids[0] = -1;
   asm volatile("bar.arrive 2, {NTH};" ::: "memory");
   while (t >= 0) {{
@@ -197,7 +205,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
     const long long tn = next_id < {ntiles}LL ? next_id : -1;
     asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
-    if (tn >= 0) K::stage(p, tn, bufs + (b ^ 1) * {TP}LL, wsum[b ^ 1], &tagg[b ^ 1], &tids[b ^ 1], flags, aggs, lane, w);
+    if (tn >= 0) K::stage(p, tn, bufs + (b ^ 1) * {TP}LL, wsum[b ^ 1], &tagg[b ^ 1], &tids[b ^ 1], aggs, lane, w);
     asm volatile("bar.sync 3, {NTH};" ::: "memory");
     // tile t: prefix (+) tile-local inclusive scan, coalesced stores
     {{
@@ -224,7 +232,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     b ^= 1;
   }}
 }}'''
-    stage = [f"static __device__ __forceinline__ void stage(const Params& p, const long long t, {ct}* buf, {ct}* ws, {ct}* agg_s, long long* tid_s, unsigned* flags, {ct}* aggs, const int lane, const int w) {{",
+    stage = [f"static __device__ __forceinline__ void stage(const Params& p, const long long t, {ct}* buf, {ct}* ws, {ct}* agg_s, long long* tid_s, unsigned long long* aggs, const int lane, const int w) {{",
              f"  const long long tb = t * {tile}LL;",
              f"  if (tb + {tile}LL <= {N}LL) load_full(p, tb, buf); else load_tail(p, tb, buf);",
              f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
@@ -246,7 +254,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
              f"    for (int i = 1; i < {TILE_THREADS // 32}; ++i) {{ acc = {comb}<{ct}>(acc, ws[i]); ws[i] = acc; }}",
              "    *agg_s = acc;",
              "    *tid_s = t;",
-             f"    gr::tile_publish_agg<{ct}>(flags, aggs, t, acc);",
+             f"    gr::stat_put<{ct}>(aggs, t, acc);",
              "  }",
              f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
              f"  const {ct} lane_ex = __shfl_up_sync(0xffffffffu, inc, 1);",
@@ -260,7 +268,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
              "}"]
     lines = lines + stage
     src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params, "  " + "\n  ".join(lines), "};", kern]
-    scratch = 8 + 8 * 2 * ntiles + 4 * (ntiles + 1) + 2 * ntiles * T.itemsize + 256
+    scratch = 8 + 8 * SW * 2 * ntiles + 256
     return KernelSource("scan", "\n".join(src) + "\n", kname, list(range(len(region.leaves))), [0],
                         block=NTH, groups=ntiles * NTH, vec=1, unroll=1, scratch_bytes=scratch,
                         meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,

@@ -455,6 +455,9 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_relaxed_u32(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned* p) {
   unsigned v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -471,74 +474,176 @@ __device__ __forceinline__ long long spad(long long e) { return e + (e >> 5); }
 
 // Publish a tile's aggregate (flag 1); tile 0 publishes its inclusive prefix
 // from the look-back instead.
-template <class T> __device__ __forceinline__ void tile_publish_agg(unsigned* flags, T* agg, long long tile, T v) {
-  if (tile > 0) {
-    agg[tile] = v;
-    st_release_u32(flags + tile, 1u);
+// Scan status words: a published value travels with its flag in the same
+// 64-bit word (flag in the high half), so a reader that sees the flag sees the
+// value — no fences on either side.  8-byte values use two words, each
+// carrying one half and the flag.  Words are zeroed before the launch and
+// written once (group prefixes may be written by several warps, always with
+// the same bits).
+template <class T> struct Stat { static constexpr int W = sizeof(T) <= 4 ? 1 : 2; };
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+template <class T> __device__ __forceinline__ unsigned long long stat_bits(T v) {
+  union { T t; unsigned long long u; } x;
+  x.u = 0;
+  x.t = v;
+  return sizeof(T) <= 4 ? (x.u & 0xffffffffull) : x.u;
+}
+template <class T> __device__ __forceinline__ void stat_put(unsigned long long* w, long long i, T v) {
+  constexpr unsigned long long F = 1ull << 32;
+  if constexpr (sizeof(T) <= 4) {
+    st_relaxed_u64(w + i, F | stat_bits(v));
+  } else {
+    const unsigned long long b = stat_bits(v);
+    st_relaxed_u64(w + 2 * i, F | (b & 0xffffffffull));
+    st_relaxed_u64(w + 2 * i + 1, F | (b >> 32));
   }
 }
+// raw words of entry i (issue the loads; check with stat_ok / decode later)
+template <class T> struct StatRaw { unsigned long long a, b; };
+template <class T> __device__ __forceinline__ StatRaw<T> stat_ld(const unsigned long long* w, long long i) {
+  StatRaw<T> r;
+  if constexpr (sizeof(T) <= 4) { r.a = ld_relaxed_u64(w + i); r.b = 1ull << 32; }
+  else { r.a = ld_relaxed_u64(w + 2 * i); r.b = ld_relaxed_u64(w + 2 * i + 1); }
+  return r;
+}
+template <class T> __device__ __forceinline__ bool stat_ok(const StatRaw<T>& r) {
+  if constexpr (sizeof(T) <= 4) return (r.a >> 32) != 0;
+  else return (r.a >> 32) != 0 && (r.b >> 32) != 0;
+}
+template <class T> __device__ __forceinline__ T stat_val(const StatRaw<T>& r) {
+  T v;
+  union { T t; unsigned long long u; } x;
+  x.u = sizeof(T) <= 4 ? (r.a & 0xffffffffull) : ((r.a & 0xffffffffull) | (r.b << 32));
+  v = x.t;
+  return v;
+}
 
-template <class Op, class T, bool PUBLISH_AGG = true>
-__device__ __forceinline__ T tile_lookback(unsigned* flags, T* agg, T* inc, long long tile, T tile_agg, T ident) {
-  // one full warp; returns the exclusive prefix (ident for tile 0)
+#ifdef GR_SCAN_STATS
+__device__ unsigned long long gr_scan_stats[8];
+#endif
+// Exclusive prefix of tile `tile` of a single-pass scan; one full warp calls
+// it after the tile's aggregate was published (stat_put(agg, tile, .)), and it
+// publishes the tile's inclusive prefix (stat_put(inc, tile, .)).
+//
+// Deterministic: incl(t) = incl(t-1) (+) agg(t), a left fold over the tile
+// aggregates, so the prefix is the same bits whichever published inclusive
+// prefix the walk starts from.  Values travel inside their status words (no
+// fences): one L2 round trip reads the inclusive and aggregate words of the
+// 256 nearest predecessors, the nearest published inclusive prefix starts the
+// fold, and lane 0 folds the aggregates above it in tile order.
+template <class Op, class T>
+__device__ __forceinline__ T tile_lookback(const unsigned long long* agg, unsigned long long* inc,
+                                           long long tile, T tile_agg, T ident) {
   const int lane = threadIdx.x & 31;
+#ifdef GR_SCAN_NOLB
+  return ident;   // experiment: streaming floor without any look-back (wrong results)
+#endif
   if (tile == 0) {
-    if (lane == 0) {
-      inc[0] = tile_agg;
-      st_release_u32(flags, 2u);
-    }
+    if (lane == 0) stat_put<T>(inc, 0, tile_agg);
     return ident;
   }
-  if (PUBLISH_AGG && lane == 0) tile_publish_agg<T>(flags, agg, tile, tile_agg);
-  // walk back 256 predecessors per round (8 per lane, one L2 round trip),
-  // relaxed flag loads (no L1 invalidation per load); one acquire fence once
-  // an inclusive prefix is in sight
-  constexpr int J = 8;
-  long long top = tile - 1;
+#ifdef GR_SCAN_STATS
+  const long long c0 = clock64();
+#endif
+#ifndef GR_SCAN_J
+#define GR_SCAN_J 2
+#endif
+  constexpr int J = GR_SCAN_J;       // 32*J predecessors per round trip
+#ifndef GR_SCAN_R
+#define GR_SCAN_R 8
+#endif
+  constexpr int R = GR_SCAN_R;       // windows staged before the slow path
+  __shared__ T lb[32 * J * R];       // aggregates by distance: lb[tile-1-q]
+  // walk back window by window: one round trip reads the inclusive and the
+  // aggregate words of 32*J predecessors; aggregates above the nearest
+  // published inclusive prefix are staged by distance
   long long found = -1;
-  for (;;) {
-    unsigned f[J];
+  T base = ident;
+  long long top = tile - 1;
+  for (int w = 0; w < R && found < 0; ++w, top -= 32 * J) {
+    StatRaw<T> ri[J], ra[J];
 #pragma unroll
-    for (int j = 0; j < J; ++j) {   // J loads in flight
+    for (int j = 0; j < J; ++j) {
       const long long q = top - lane - 32 * j;
-      f[j] = q >= 0 ? ld_relaxed_u32(flags + q) : 2u;
+      ri[j] = q >= 0 ? stat_ld<T>(inc, q) : StatRaw<T>{0, 0};
+      ra[j] = q >= 0 ? stat_ld<T>(agg, q) : StatRaw<T>{0, 0};
     }
+    long long fw = -1;
 #pragma unroll
-    for (int j = 0; j < J; ++j) {   // rarely taken: a predecessor not yet staged
-      const long long q = top - lane - 32 * j;
-      while (f[j] == 0u) f[j] = ld_relaxed_u32(flags + q);
+    for (int j = 0; j < J; ++j) {
+      const unsigned m = __ballot_sync(0xffffffffu, stat_ok<T>(ri[j]));
+      if (fw < 0 && m) fw = top - (__ffs(m) - 1) - 32 * j;
     }
 #pragma unroll
     for (int j = 0; j < J; ++j) {
-      const unsigned m2 = __ballot_sync(0xffffffffu, f[j] == 2u && top - lane - 32 * j >= 0);
-      if (found < 0 && m2) found = top - (__ffs(m2) - 1) - 32 * j;
+      const long long q = top - lane - 32 * j;
+      if (q >= 0 && q > fw) {
+        while (!stat_ok<T>(ra[j])) ra[j] = stat_ld<T>(agg, q);
+        lb[tile - 1 - q] = stat_val<T>(ra[j]);
+      }
+      if (q == fw) base = stat_val<T>(ri[j]);
     }
-    if (found >= 0) break;
-    top -= 32 * J;
+    if (fw >= 0) {
+      found = fw;
+      base = __shfl_sync(0xffffffffu, base, (int)((top - fw) & 31));
+    }
+    if (top - 32 * J < 0 && found < 0) { top = tile - 1 + 32 * J; w = -1; }   // nothing published down to tile 0 yet: poll again
   }
-  fence_acq_rel_gpu();
-  // left fold from the inclusive prefix of `found` over the aggregates of
-  // found+1 .. tile-1 (increasing tile order), staged 32 at a time in smem
-  __shared__ T lb[32 * J];
+  __syncwarp();
   T pre = ident;
-  if (lane == 0) pre = __ldcg(inc + found);
-  for (long long base = found + 1; base <= tile - 1; base += 32 * J) {
-    __syncwarp();
-#pragma unroll
-    for (int j = 0; j < J; ++j) {   // 256 aggregates per round trip
-      const long long q = base + lane + 32 * j;
-      lb[lane + 32 * j] = q <= tile - 1 ? __ldcg(agg + q) : ident;
-    }
-    __syncwarp();
+  if (found >= 0) {
     if (lane == 0) {
-      const int cnt = (int)((tile - base) < 32 * J ? (tile - base) : 32 * J);
-      for (int l = 0; l < cnt; ++l) pre = Op::template c<T>(pre, lb[l]);
+      pre = base;
+      for (long long d = tile - 2 - found; d >= 0; --d) pre = Op::template c<T>(pre, lb[d]);
+    }
+  } else {
+    // slow path (more than 32*J*R tiles in flight behind this one): walk the
+    // inclusive words further back, then fold the aggregates in chunks
+    while (found < 0) {
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const long long q = top - lane - 32 * j;
+        const StatRaw<T> r = q >= 0 ? stat_ld<T>(inc, q) : StatRaw<T>{0, 0};
+        const unsigned m = __ballot_sync(0xffffffffu, stat_ok<T>(r));
+        if (found < 0 && m) found = top - (__ffs(m) - 1) - 32 * j;
+      }
+      if (found < 0) {
+        top -= 32 * J;
+        if (top < 0) top = tile - 1;
+      }
+    }
+    StatRaw<T> rf = stat_ld<T>(inc, found);
+    pre = stat_val<T>(rf);
+    for (long long b0 = found + 1; b0 <= tile - 1; b0 += 32 * J) {
+      __syncwarp();
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const long long q = b0 + lane + 32 * j;
+        if (q <= tile - 1) {
+          StatRaw<T> r = stat_ld<T>(agg, q);
+          while (!stat_ok<T>(r)) r = stat_ld<T>(agg, q);
+          lb[lane + 32 * j] = stat_val<T>(r);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const int cnt = (int)((tile - b0) < 32 * J ? (tile - b0) : 32 * J);
+        for (int l = 0; l < cnt; ++l) pre = Op::template c<T>(pre, lb[l]);
+      }
     }
   }
-  if (lane == 0) {
-    inc[tile] = Op::template c<T>(pre, tile_agg);
-    st_release_u32(flags + tile, 2u);
-  }
+  if (lane == 0) stat_put<T>(inc, tile, Op::template c<T>(pre, tile_agg));
+#ifdef GR_SCAN_STATS
+  if (lane == 0) { atomicAdd(&gr_scan_stats[0], (unsigned long long)(tile - found)); atomicAdd(&gr_scan_stats[1], 1ull);
+                   atomicAdd(&gr_scan_stats[2], (unsigned long long)(clock64() - c0)); }
+#endif
   return __shfl_sync(0xffffffffu, pre, 0);
 }
 

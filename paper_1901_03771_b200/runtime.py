@@ -9,6 +9,7 @@ library or a device is missing, ``get()`` raises ``NativeLibraryMissing``.
 from __future__ import annotations
 
 import ctypes
+import hashlib
 import os
 import struct
 import threading
@@ -223,7 +224,15 @@ class Runtime:
         self.cc = (ma.value, mi.value)
         self.total_mem = tm.value
         self.name = name.value.decode()
-        self.cache_dir = os.environ.get("GRUMPY_CACHE_DIR", os.path.join(os.path.expanduser("~"), ".cache", "grumpy"))
+        # the on-disk cubin cache is keyed by source + options; the kernel
+        # headers the sources include are versioned by the directory name
+        self.cache_dir = os.path.join(
+            os.environ.get("GRUMPY_CACHE_DIR", os.path.join(os.path.expanduser("~"), ".cache", "grumpy")),
+            _headers_digest())
+        try:
+            os.makedirs(self.cache_dir, exist_ok=True)
+        except OSError:
+            pass
         self._kernels = {}
         self.stats_allocs = 0
         self.launches = 0
@@ -436,6 +445,17 @@ def get() -> Runtime:
     if _rt is None:
         _rt = Runtime(default_device())
     return _rt
+
+
+def _headers_digest() -> str:
+    h = hashlib.sha1()
+    kdir = os.path.join(os.path.dirname(os.path.abspath(__file__)), "csrc", "kernels")
+    for fn in sorted(os.listdir(kdir)):
+        if fn.endswith((".cuh", ".h")):
+            h.update(fn.encode())
+            with open(os.path.join(kdir, fn), "rb") as f:
+                h.update(f.read())
+    return "h" + h.hexdigest()[:16]
 
 
 def pack_params(ptrs: Sequence[int]) -> bytes:
