@@ -19,6 +19,8 @@ Layout of the package (reference module in brackets, /root/reference/SPEC.md):
   distributed.py  leading-axis sharding, NCCL allreduce of partials
   streaming.py  streamed to_external: H2D / kernels / D2H overlapped in chunks
   errors.py     [errors]             same class names as lazyfuse.errors
+  npyio.py      [tensor-core I/O]    npy v1.0 save/load, DOT dumps of the DAG / plan
+  bench_cli.py  [bench]              `bench run|dot` CLI, BenchReport JSON
 """
 
 from . import errors
@@ -48,6 +50,7 @@ from .session import (  # noqa: F401
 from .session import elementwise as _elementwise
 from .dag import ElemCode as _E
 from .tensor import DType  # noqa: F401
+from .npyio import dump_dot, load, save  # noqa: F401
 
 import numpy as _np
 
