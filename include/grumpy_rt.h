@@ -90,10 +90,17 @@ int grumpy_rt_host_unregister(void* ptr);
  * kernel templates) for sm_100a with `opts`, loads the cubin as a module.
  * A process-wide table and an on-disk cubin cache under `cache_dir` (may be
  * NULL) are keyed by FNV-1a(src, opts).  *compile_ms = NVRTC time, 0 on a
- * cache hit; *cache_hit = 0 (compiled), 1 (memory), 2 (disk). */
+ * cache hit; *cache_hit = 0 (compiled), 1 (memory), 2 (disk), 3 (compiled
+ * ahead by grumpy_rt_precompile). */
 int grumpy_rt_compile(const char* src, const char* const* opts, int n_opts,
                       const char* cache_dir, uint64_t* module,
                       double* compile_ms, int* cache_hit);
+/* JIT/execute pipelining: NVRTC-compile `src` ahead of its
+ * first launch — no CUDA context is touched, so worker threads call it while
+ * the host thread launches earlier steps; the cubin is kept in memory (and in
+ * the disk cache) until grumpy_rt_compile loads it. */
+int grumpy_rt_precompile(const char* src, const char* const* opts, int n_opts,
+                         const char* cache_dir, double* compile_ms);
 /* Compile only (no device needed): writes the sm_100a cubin into `out` when
  * `cap` is large enough; *size is always set.  Used by CPU tests to check
  * every generated kernel builds. */

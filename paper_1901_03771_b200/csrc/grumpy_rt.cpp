@@ -478,12 +478,7 @@ int grumpy_rt_host_unregister(void* ptr) {
 }
 
 // ---- compile ------------------------------------------------------------------
-int grumpy_rt_compile(const char* src, const char* const* opts, int n_opts, const char* cache_dir,
-                      uint64_t* module, double* compile_ms, int* cache_hit) {
-  int r = need_init();
-  if (r) return r;
-  if (compile_ms) *compile_ms = 0.0;
-  if (cache_hit) *cache_hit = 0;
+static uint64_t source_key(const char* src, const char* const* opts, int n_opts) {
   uint64_t h = fnv1a(src, strlen(src));
   for (int i = 0; i < n_opts; ++i) {
     h = fnv1a(opts[i], strlen(opts[i]), h);
@@ -493,6 +488,52 @@ int grumpy_rt_compile(const char* src, const char* const* opts, int n_opts, cons
   nvrtcVersion(&nv_major, &nv_minor);
   h = fnv1a(&nv_major, sizeof(nv_major), h);
   h = fnv1a(&nv_minor, sizeof(nv_minor), h);
+  return h;
+}
+
+// cubins compiled ahead of their first launch (grumpy_rt_precompile), by key
+static std::unordered_map<uint64_t, std::vector<char>> g_cubins;
+static std::mutex g_cubins_mu;
+
+int grumpy_rt_precompile(const char* src, const char* const* opts, int n_opts, const char* cache_dir,
+                         double* compile_ms) {
+  // NVRTC only — no CUDA context needed, safe to call from worker threads
+  if (compile_ms) *compile_ms = 0.0;
+  const uint64_t h = source_key(src, opts, n_opts);
+  {
+    std::lock_guard<std::mutex> lk(S.mu);
+    if (g_modules.count(h)) return GR_OK;
+  }
+  {
+    std::lock_guard<std::mutex> lk(g_cubins_mu);
+    if (g_cubins.count(h)) return GR_OK;
+  }
+  char key[32];
+  snprintf(key, sizeof(key), "%016llx", (unsigned long long)h);
+  std::string path;
+  std::vector<char> cubin;
+  if (cache_dir && cache_dir[0]) {
+    path = std::string(cache_dir) + "/" + key + ".cubin";
+    if (read_file(path, cubin)) return GR_OK;     // the loader reads it from disk
+  }
+  int rc = nvrtc_compile(src, opts, n_opts, cubin, compile_ms);
+  if (rc) return rc;
+  if (!path.empty()) {
+    mkdir(cache_dir, 0755);
+    write_file_atomic(path, cubin);
+  }
+  std::lock_guard<std::mutex> lk(g_cubins_mu);
+  g_cubins[h] = std::move(cubin);
+  return GR_OK;
+}
+
+int grumpy_rt_compile(const char* src, const char* const* opts, int n_opts, const char* cache_dir,
+                      uint64_t* module, double* compile_ms, int* cache_hit) {
+  int r = need_init();
+  if (r) return r;
+  if (compile_ms) *compile_ms = 0.0;
+  if (cache_hit) *cache_hit = 0;
+  const uint64_t h = source_key(src, opts, n_opts);
   {
     std::lock_guard<std::mutex> lk(S.mu);
     auto it = g_modules.find(h);
@@ -507,7 +548,17 @@ int grumpy_rt_compile(const char* src, const char* const* opts, int n_opts, cons
   std::string path;
   std::vector<char> cubin;
   bool have = false;
-  if (cache_dir && cache_dir[0]) {
+  {
+    std::lock_guard<std::mutex> lk(g_cubins_mu);
+    auto it = g_cubins.find(h);
+    if (it != g_cubins.end()) {
+      cubin = std::move(it->second);
+      g_cubins.erase(it);
+      have = true;
+      if (cache_hit) *cache_hit = 3;
+    }
+  }
+  if (!have && cache_dir && cache_dir[0]) {
     path = std::string(cache_dir) + "/" + key + ".cubin";
     have = read_file(path, cubin);
     if (have && cache_hit) *cache_hit = 2;

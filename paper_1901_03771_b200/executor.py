@@ -13,6 +13,7 @@ consecutive forces pipeline on the device.
 from __future__ import annotations
 
 import collections
+import os
 import time
 from typing import Dict, List
 
@@ -21,6 +22,9 @@ from .dag import Node, OpKind
 from .errors import ShapeMismatch, UnsupportedNodeInFusedStep
 from .planner import PlanStep
 from .tensor import DType, TensorBuffer, element_count
+
+
+PRECOMPILE = os.environ.get("GRUMPY_PRECOMPILE", "1") == "1"
 
 
 class Executor:
@@ -54,6 +58,17 @@ class Executor:
     def run(self, steps: List[PlanStep], dist=None, comm=None):
         self.last_steps = steps
         g = self.session.graph
+        cold = [st for st in steps if st.kind == "Fused" and "kernel" not in st.cache]
+        if len(cold) >= 2 and PRECOMPILE:
+            # JIT/execute pipelining: generate every uncompiled step's source
+            # now and compile them on worker threads while the earlier steps
+            # launch (SPEC.md:521 — the paper's JIT bottleneck)
+            srcs = []
+            for st in cold:
+                self._prepare(st)
+                if st.cache["ks"] is not None:
+                    srcs.append(st.cache["ks"].source)
+            self.rt.precompile(srcs)
         for st in steps:
             if st.kind == "Library":
                 outs = [self.run_library(st)]
@@ -85,10 +100,9 @@ class Executor:
             self.session.stats.h2d_bytes += buf.host.nbytes
         return buf.device.ptr
 
-    def run_fused(self, st: PlanStep, bind: Dict[int, TensorBuffer] = None) -> List[TensorBuffer]:
-        """Launch the step's kernel.  ``bind`` (leaf node id → buffer) supplies
-        leaf data explicitly (the reference-style ``run_map(k, leaves, cfg)``
-        entry points); otherwise leaves read their materialized data."""
+    def _prepare(self, st: PlanStep) -> None:
+        """Canonical leaf order and generated kernel source of a fused step
+        (memoized in the step's cache, shared by every plan instantiation)."""
         c = st.cache
         if "perm" not in c:
             region = codegen.canonicalize(codegen.Region(st.roots, st.leaves, st.nodes))
@@ -96,6 +110,13 @@ class Executor:
             c["perm"] = [pos[l.id] for l in region.leaves]
             empty = all(element_count(r.shape) == 0 for r in region.roots)
             c["ks"] = None if empty else self.kernel_source(region)
+
+    def run_fused(self, st: PlanStep, bind: Dict[int, TensorBuffer] = None) -> List[TensorBuffer]:
+        """Launch the step's kernel.  ``bind`` (leaf node id → buffer) supplies
+        leaf data explicitly (the reference-style ``run_map(k, leaves, cfg)``
+        entry points); otherwise leaves read their materialized data."""
+        c = st.cache
+        self._prepare(st)
         leaves = [st.leaves[i] for i in c["perm"]]
         outs = [self.out_bind.pop(r.id, None) or self.new_buffer(r) for r in st.roots]
         ks = c["ks"]

@@ -324,6 +324,15 @@ def _is_view(n: Node) -> bool:
     return n.kind in (OpKind.TRANSPOSE, OpKind.RESHAPE, OpKind.SLICE, OpKind.BROADCAST)
 
 
+_VIEW_KINDS = (OpKind.SLICE, OpKind.RESHAPE, OpKind.TRANSPOSE, OpKind.BROADCAST)
+
+
+def _stencil_read(n: Node, consumers) -> bool:
+    """Is ``n`` read through two or more distinct slices?"""
+    views = {repr(c.op.attrs) for c in consumers.get(n.id, ()) if c.kind is OpKind.SLICE}
+    return len(views) >= 2
+
+
 def plan_regions(roots: Sequence[Node], row_fusion=None, check=None) -> List[PlanStep]:
     """B200 region planner (module docstring).
 
@@ -393,6 +402,12 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=f
         if n.id in extra:
             points[n.id] = n
             continue
+        if n.kind not in _VIEW_KINDS and _stencil_read(n, consumers):
+            # read through two or more different slices (a stencil over a
+            # computed grid: Jacobi sweep k+1 over sweep k): recomputing it
+            # per read multiplies with every chained sweep, so it is
+            # materialized — one kernel per sweep
+            points[n.id] = n
         if n.kind in LIBRARY_KINDS:
             points[n.id] = n
             ops, _, _ = library_operands(n)

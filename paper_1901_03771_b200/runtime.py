@@ -61,6 +61,7 @@ SIGNATURES = {
     "grumpy_rt_host_unregister": [_p],
     "grumpy_rt_compile": [_cp, _cpp, _i, _cp, _u64p, _dp, _ip],
     "grumpy_rt_compile_cubin": [_cp, _cpp, _i, _p, _sz, _szp, _dp],
+    "grumpy_rt_precompile": [_cp, _cpp, _i, _cp, _dp],
     "grumpy_rt_get_function": [_u64, _cp, _u64p],
     "grumpy_rt_module_global": [_u64, _cp, _u64p, ctypes.POINTER(ctypes.c_size_t)],
     "grumpy_rt_tensor_map_2d": [_u64, _i, _u64, _u64, _u64, ctypes.c_uint, ctypes.c_uint, _i, _p],
@@ -234,6 +235,8 @@ class Runtime:
         except OSError:
             pass
         self._kernels = {}
+        self._pending = {}            # source -> Future of a precompile job
+        self._pool = None
         self.stats_allocs = 0
         self.launches = 0
         self.compile_ms_total = 0.0
@@ -330,7 +333,33 @@ class Runtime:
         self._kernels[(source, name, tune)] = k
         return k
 
+    def precompile(self, sources: Sequence[str]) -> None:
+        """Start NVRTC compiles of ``sources`` on worker threads (ctypes drops
+        the GIL in the call); ``_kernel`` waits for its source's job, then
+        loads the cubin it left.  Used when a plan has several uncompiled
+        steps: their compiles overlap each other and the earlier launches."""
+        import concurrent.futures as cf
+        if self._pool is None:
+            self._pool = cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1),
+                                               thread_name_prefix="grumpy-nvrtc")
+        for src in sources:
+            if src in self._pending or any(k[0] == src for k in self._kernels):
+                continue
+            self._pending[src] = self._pool.submit(self._precompile_one, src)
+
+    def _precompile_one(self, source: str) -> float:
+        opts = nvrtc_options()
+        arr = (ctypes.c_char_p * len(opts))(*opts)
+        ms = ctypes.c_double(0)
+        _check(self.lib.grumpy_rt_precompile(source.encode(), arr, len(opts), self.cache_dir.encode(),
+                                             ctypes.byref(ms)))
+        return ms.value
+
     def _kernel(self, source: str, name: str, block: int, smem: int = 0) -> Kernel:
+        pre_ms = 0.0
+        fut = self._pending.pop(source, None)
+        if fut is not None:
+            pre_ms = fut.result()     # raises the compile error here, on the launching thread
         opts = nvrtc_options()
         arr = (ctypes.c_char_p * len(opts))(*opts)
         mod = ctypes.c_uint64(0)
@@ -344,8 +373,11 @@ class Runtime:
         _check(self.lib.grumpy_rt_occupancy(fn.value, block, smem, ctypes.byref(occ)))
         regs = ctypes.c_int(0)
         _check(self.lib.grumpy_rt_function_info(fn.value, ctypes.byref(regs), None, None, None))
-        self.compile_ms_total += ms.value
-        return Kernel(fn.value, name, block, max(occ.value, 1), regs.value, ms.value, hit.value, source, mod.value)
+        cms, h = ms.value, hit.value
+        if h == 3:                    # compiled ahead on a worker thread: still a compile
+            cms, h = pre_ms, 0
+        self.compile_ms_total += cms
+        return Kernel(fn.value, name, block, max(occ.value, 1), regs.value, cms, h, source, mod.value)
 
     def launch(self, k: Kernel, grid, block, params: bytes, smem: int = 0, cluster: int = 1):
         gx, gy, gz = (grid, 1, 1) if isinstance(grid, int) else grid

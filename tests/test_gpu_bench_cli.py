@@ -74,3 +74,15 @@ def test_save_lazy_result_and_reload(tmp_path):
         assert np.array_equal(np.asarray(z.sum(axis=1)), (x * 2.0 + 1.0).sum(axis=1))
     finally:
         gp.set_default_session(old)
+
+
+def test_jit_pipelining_multi_step_cold(tmp_path):
+    """A cold multi-step plan compiles its kernels on worker threads
+    (GRUMPY_PRECOMPILE) and still produces the right results."""
+    env = dict(os.environ, GRUMPY_CACHE_DIR=str(tmp_path / "c"), PYTHONPATH=ROOT)
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "jit_pipeline_probe.py")], env=env,
+                       capture_output=True, text=True, timeout=900)
+    assert p.returncode == 0, p.stderr
+    lines = [json.loads(l.split(" ", 1)[1]) for l in p.stdout.splitlines() if l.startswith("precompile=")]
+    assert len(lines) == 4 and all(l["ok"] for l in lines)
+    assert len({l["kernels"] for l in lines}) == 1 and lines[0]["kernels"] >= 4

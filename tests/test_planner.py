@@ -166,3 +166,17 @@ def test_plan_cache_reuses_structure(sess):
     k2, _ = dag_signature([(a * b + 1).node])
     k3, _ = dag_signature([(a * a + 1).node])
     assert k1 == k2 and k1 != k3
+
+
+def test_chained_jacobi_sweeps_one_step_each(sess):
+    """10 lazily chained sweeps plan as 10 fused maps: a grid
+    read through several slices is materialized, not recomputed per read."""
+    a = gp.asarray(wl.jacobi_inputs(64)[0])
+    for _ in range(10):
+        a = wl.jacobi(gp, a)
+    steps = sess.plan([a.node])
+    assert [s.kernel_kind for s in steps] == ["Map"] * 10
+    # a computed node read through one slice stays fused
+    x = gp.asarray(np.arange(16.0))
+    y = (x * 2.0)[1:] + 1.0
+    assert len(sess.plan([y.node])) == 1
