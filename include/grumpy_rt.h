@@ -154,6 +154,16 @@ int grumpy_rt_event_destroy(uint64_t ev);
 /* ---- run_library: gemm / gemv with transpose flags (
  *      PAPER.md:292-303 cuBLAS).  Row-major semantics:
  *      C[m,n] = op(A)[m,k] * op(B)[k,n];  lda/ldb/ldc are row strides. ---- */
+/* FP32 GEMM arithmetic: 0 = FP32 on the CUDA cores (default), 1 = FP32
+ * emulated with BF16x9 tensor-core products (cuBLAS 12.9, FP32 accuracy). */
+int grumpy_rt_set_gemm_math(int mode);
+/* cuBLASLt f32 GEMM with a fused epilogue: row-major C[m,n] = epi(op(A)op(B)
+ * + bias[n]), epilogue 0 none / 1 bias / 2 relu(bias) — the library-side
+ * alternative to the R1 bias+ReLU region;
+ * emulate = 1 uses BF16x9 emulated FP32. */
+int grumpy_rt_gemm_epilogue(int trans_a, int trans_b, int m, int n, int k, uint64_t a, int lda,
+                            uint64_t b, int ldb, uint64_t c, int ldc, uint64_t bias, int epilogue,
+                            int emulate);
 int grumpy_rt_gemm(int trans_a, int trans_b, int m, int n, int k, int dtype,
                    uint64_t a, int lda, uint64_t b, int ldb, uint64_t c, int ldc);
 /* y[m] = op(A) x, A row-major [rows, cols] (ld = row stride);

@@ -52,6 +52,15 @@ from .dag import ElemCode as _E
 from .tensor import DType  # noqa: F401
 from .npyio import dump_dot, load, save  # noqa: F401
 
+# Load the native shim (and with it cuBLAS 12.9 via its rpath) before anything
+# imports PyTorch, whose wheel carries an older libcublas.so.12 without the
+# BF16x9 FP32 emulation the np.dot boundary uses (session.GEMM_MATH).
+try:
+    from . import runtime as _rt
+    _rt.load_library()
+except Exception:  # noqa: BLE001 — no shim yet (build() not run): fails loudly on first use
+    pass
+
 import numpy as _np
 
 float32 = _np.float32

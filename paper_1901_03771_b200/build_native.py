@@ -42,7 +42,7 @@ def build_shim(force=False) -> str:
         _run([
             "g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-Wall", "-Wno-unused-function",
             f"-I{CUDA}/include", src, "-o", LIB,
-            f"-L{CUDA}/lib64", "-lnvrtc", "-lcublas", "-ldl", f"-Wl,-rpath,{CUDA}/lib64",
+            f"-L{CUDA}/lib64", "-lnvrtc", "-lcublas", "-lcublasLt", "-ldl", f"-Wl,-rpath,{CUDA}/lib64",
         ])
     return LIB
 

@@ -14,6 +14,7 @@
 #include "../../include/grumpy_rt.h"
 
 #include <cuda.h>
+#include <cublasLt.h>
 #include <cublas_v2.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
@@ -100,6 +101,10 @@ struct State {
   CUstream cur = nullptr;   // stream async work goes to (nullptr: `stream`)
   int sm_count = 0;
   cublasHandle_t cublas = nullptr;
+  cublasLtHandle_t lt = nullptr;
+  CUdeviceptr lt_ws = 0;          // cuBLASLt workspace
+  size_t lt_ws_bytes = 0;
+  int gemm_math = 0;              // 0 FP32 (SIMT), 1 FP32 emulated with BF16x9 tensor-core products
   std::mutex mu;
 } S;
 
@@ -796,13 +801,109 @@ int grumpy_rt_event_destroy(uint64_t ev) {
 }
 
 // ---- cuBLAS -------------------------------------------------------------------
+static void apply_gemm_math();
 static int ensure_cublas() {
   if (S.cublas) return GR_OK;
   cublasStatus_t st = cublasCreate(&S.cublas);
   if (st != CUBLAS_STATUS_SUCCESS) return fail(GR_ECUBLAS, "cublasCreate: status " + std::to_string((int)st));
   cublasSetStream(S.cublas, CS());
-  // FP32 stays FP32 (no TF32): NumPy/OpenBLAS parity.
-  cublasSetMathMode(S.cublas, CUBLAS_DEFAULT_MATH);
+  // FP32 stays FP32 (no TF32): NumPy/OpenBLAS parity;
+  // optionally FP32 emulated by BF16x9 products on the tensor cores
+  // (grumpy_rt_set_gemm_math), which keeps FP32 accuracy.
+  apply_gemm_math();
+  return GR_OK;
+}
+
+// BF16x9 emulation needs cuBLAS >= 12.9.  The process may hold an older
+// libcublas.so.12 (e.g. PyTorch's wheel, loaded first), so the 12.9-only
+// entry point is looked up at run time instead of being linked.
+typedef cublasStatus_t (*SetEmulationFn)(cublasHandle_t, cublasEmulationStrategy_t);
+static SetEmulationFn emulation_fn() {
+  static SetEmulationFn fn = (SetEmulationFn)dlsym(RTLD_DEFAULT, "cublasSetEmulationStrategy");
+  return fn;
+}
+static bool emulation_available() {
+  return emulation_fn() != nullptr && cublasLtGetVersion() >= 120900;
+}
+static void apply_gemm_math() {
+  if (!S.cublas) return;
+  cublasSetMathMode(S.cublas, S.gemm_math ? CUBLAS_FP32_EMULATED_BF16X9_MATH : CUBLAS_DEFAULT_MATH);
+  if (emulation_fn())
+    emulation_fn()(S.cublas, S.gemm_math ? CUBLAS_EMULATION_STRATEGY_EAGER : CUBLAS_EMULATION_STRATEGY_DEFAULT);
+}
+
+int grumpy_rt_set_gemm_math(int mode) {
+  if (mode != 0 && mode != 1) return fail(GR_EINVAL, "gemm math mode must be 0 (fp32) or 1 (bf16x9 emulation)");
+  if (mode == 1 && !emulation_available())
+    return fail(GR_EINVAL, "BF16x9 FP32 emulation needs cuBLAS >= 12.9 (an older libcublas.so.12 is loaded)");
+  S.gemm_math = mode;
+  apply_gemm_math();
+  return GR_OK;
+}
+
+// cuBLASLt f32 GEMM with a fused epilogue (none / +bias / relu(+bias)):
+// row-major C[m,n] = epi(op(A) op(B) + bias[n]); bias runs along C's columns.
+int grumpy_rt_gemm_epilogue(int trans_a, int trans_b, int m, int n, int k, uint64_t a, int lda, uint64_t b,
+                            int ldb, uint64_t c, int ldc, uint64_t bias, int epilogue, int emulate) {
+  int r = need_init();
+  if (r) return r;
+  if (!S.lt) {
+    if (cublasLtCreate(&S.lt) != CUBLAS_STATUS_SUCCESS) return fail(GR_ECUBLAS, "cublasLtCreate failed");
+    S.lt_ws_bytes = 32u << 20;
+    CUresult cr = D.p_cuMemAlloc(&S.lt_ws, S.lt_ws_bytes);
+    if (cr != CUDA_SUCCESS) return fail(GR_ECUDA, cu_msg(cr, "cuMemAlloc (cublasLt workspace)"));
+  }
+  if (epilogue < 0 || epilogue > 2) return fail(GR_EINVAL, "epilogue must be 0 (none), 1 (bias), 2 (relu+bias)");
+  // column-major view: C^T[n,m] = op(B)^T[n,k] op(A)^T[k,m]; the bias is per row of C^T
+  cublasOperation_t opa = trans_a ? CUBLAS_OP_T : CUBLAS_OP_N;
+  cublasOperation_t opb = trans_b ? CUBLAS_OP_T : CUBLAS_OP_N;
+  cublasLtMatmulDesc_t desc = nullptr;
+  cublasLtMatrixLayout_t la = nullptr, lb = nullptr, lc = nullptr;
+  cublasLtMatmulPreference_t pref = nullptr;
+  cublasStatus_t st;
+  int out = GR_OK;
+  if (emulate && !emulation_available())
+    return fail(GR_EINVAL, "BF16x9 FP32 emulation needs cuBLAS >= 12.9 (an older libcublas.so.12 is loaded)");
+  const cublasComputeType_t ct = emulate ? CUBLAS_COMPUTE_32F_EMULATED_16BFX9 : CUBLAS_COMPUTE_32F;
+  do {
+    if ((st = cublasLtMatmulDescCreate(&desc, ct, CUDA_R_32F)) != CUBLAS_STATUS_SUCCESS) break;
+    cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_TRANSA, &opb, sizeof(opb));
+    cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_TRANSB, &opa, sizeof(opa));
+    cublasLtEpilogue_t epi = epilogue == 2 ? CUBLASLT_EPILOGUE_RELU_BIAS
+                           : epilogue == 1 ? CUBLASLT_EPILOGUE_BIAS : CUBLASLT_EPILOGUE_DEFAULT;
+    cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_EPILOGUE, &epi, sizeof(epi));
+    if (epilogue) {
+      const void* bp = (const void*)(uintptr_t)bias;
+      cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bp, sizeof(bp));
+      cudaDataType_t bt = CUDA_R_32F;
+      cublasLtMatmulDescSetAttribute(desc, CUBLASLT_MATMUL_DESC_BIAS_DATA_TYPE, &bt, sizeof(bt));
+    }
+    // first operand of the column-major product: B^T (stored as row-major B)
+    const int b_rows = trans_b ? k : n, b_cols = trans_b ? n : k;
+    const int a_rows = trans_a ? m : k, a_cols = trans_a ? k : m;
+    if ((st = cublasLtMatrixLayoutCreate(&la, CUDA_R_32F, b_rows, b_cols, ldb)) != CUBLAS_STATUS_SUCCESS) break;
+    if ((st = cublasLtMatrixLayoutCreate(&lb, CUDA_R_32F, a_rows, a_cols, lda)) != CUBLAS_STATUS_SUCCESS) break;
+    if ((st = cublasLtMatrixLayoutCreate(&lc, CUDA_R_32F, n, m, ldc)) != CUBLAS_STATUS_SUCCESS) break;
+    if ((st = cublasLtMatmulPreferenceCreate(&pref)) != CUBLAS_STATUS_SUCCESS) break;
+    cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &S.lt_ws_bytes,
+                                         sizeof(S.lt_ws_bytes));
+    cublasLtMatmulHeuristicResult_t heur;
+    int found = 0;
+    st = cublasLtMatmulAlgoGetHeuristic(S.lt, desc, la, lb, lc, lc, pref, 1, &heur, &found);
+    if (st != CUBLAS_STATUS_SUCCESS) break;
+    if (!found) { out = fail(GR_ECUBLAS, "cublasLt: no algorithm for this gemm/epilogue"); break; }
+    const float one = 1.f, zero = 0.f;
+    st = cublasLtMatmul(S.lt, desc, &one, (const void*)(uintptr_t)b, la, (const void*)(uintptr_t)a, lb, &zero,
+                        (const void*)(uintptr_t)c, lc, (void*)(uintptr_t)c, lc, &heur.algo,
+                        (void*)(uintptr_t)S.lt_ws, S.lt_ws_bytes, CS());
+  } while (0);
+  if (pref) cublasLtMatmulPreferenceDestroy(pref);
+  if (lc) cublasLtMatrixLayoutDestroy(lc);
+  if (lb) cublasLtMatrixLayoutDestroy(lb);
+  if (la) cublasLtMatrixLayoutDestroy(la);
+  if (desc) cublasLtMatmulDescDestroy(desc);
+  if (out != GR_OK) return out;
+  if (st != CUBLAS_STATUS_SUCCESS) return fail(GR_ECUBLAS, "cublasLt matmul: status " + std::to_string((int)st));
   return GR_OK;
 }
 

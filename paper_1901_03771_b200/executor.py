@@ -71,7 +71,15 @@ class Executor:
             self.rt.precompile(srcs)
         for st in steps:
             if st.kind == "Library":
-                outs = [self.run_library(st)]
+                if self.profile is not None:
+                    e0, e1 = self._event_pair()
+                    self.rt.record(e0)
+                    outs = [self.run_library(st)]
+                    self.rt.record(e1)
+                    label = st.call + (f"+{st.epilogue[0]}" if st.epilogue else "")
+                    self.profile.append(("library", label, e0, e1))
+                else:
+                    outs = [self.run_library(st)]
                 self.session.stats.library_calls += 1
             else:
                 outs = self.run_fused(st)
@@ -214,10 +222,10 @@ class Executor:
 
     def run_library(self, st: PlanStep) -> TensorBuffer:
         """run_library → cuBLAS on the runtime stream."""
-        n = st.root
+        n = st.library_node if st.library_node is not None else st.root
         ops = st.operands
         flags = st.trans_flags
-        out = self.new_buffer(n)
+        out = self.new_buffer(st.root)
         dt = n.dtype
         for o in ops:
             if o.dtype is not dt:
@@ -227,7 +235,14 @@ class Executor:
             ta, tb = flags
             m, nn = n.shape
             k = a.shape[0] if ta else a.shape[1]
-            if m and nn:
+            if m and nn and st.epilogue is not None:
+                # GEMM + bias (+ ReLU) in one cuBLASLt call (the R1 region absorbed)
+                kind, bias = st.epilogue
+                self.rt.gemm_epilogue(ta, tb, m, nn, k, self.device_ptr(a), a.shape[1],
+                                      self.device_ptr(b), b.shape[1], out.device.ptr, nn,
+                                      bias=self.device_ptr(bias), epilogue=kind,
+                                      emulate=self.rt.gemm_math == "bf16x9")
+            elif m and nn:
                 if k == 0:
                     self.rt.memset(out.device, 0)
                 else:

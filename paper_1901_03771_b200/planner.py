@@ -27,6 +27,7 @@ import dataclasses
 from typing import Dict, List, Optional, Sequence, Set, Tuple
 
 from .dag import ElemCode, Node, OpKind, ReduceOp
+from .tensor import DType
 
 LIBRARY_KINDS = (OpKind.MATMUL, OpKind.MATVEC)
 REDUCTION_KINDS = (OpKind.REDUCE, OpKind.ARGREDUCE)
@@ -61,6 +62,10 @@ class PlanStep:
     trans_flags: Tuple[bool, ...] = ()
     operands: List[Node] = dataclasses.field(default_factory=list)
     order_index: int = 0
+    # library steps with a fused cuBLASLt epilogue: the GEMM node (the root is
+    # then its bias-add or ReLU consumer) and ("bias" | "relu_bias", bias node)
+    library_node: Optional[Node] = None
+    epilogue: Optional[Tuple[str, Node]] = None
     # executor-owned memo shared by every instantiation of a cached plan
     # (canonical leaf order, generated kernel source)
     cache: dict = dataclasses.field(default_factory=dict)
@@ -333,7 +338,35 @@ def _stencil_read(n: Node, consumers) -> bool:
     return len(views) >= 2
 
 
-def plan_regions(roots: Sequence[Node], row_fusion=None, check=None) -> List[PlanStep]:
+def _gemm_epilogue(n: Node, consumers, root_ids):
+    """(last node, [chain], bias, kind) when the f32 GEMM ``n`` feeds exactly
+    one ``+ bias[N]`` (optionally then exactly one ``maximum(., 0)``): the
+    pattern a cuBLASLt BIAS / RELU_BIAS epilogue computes in the GEMM."""
+    if (n.kind is not OpKind.MATMUL or n.dtype is not DType.f32 or n.id in root_ids
+            or 0 in n.shape or 0 in n.preds[0].shape):
+        return None
+    cons = consumers.get(n.id, [])
+    if len(cons) != 1:
+        return None
+    a = cons[0]
+    if not (a.kind is OpKind.MAP and a.op.code is ElemCode.add and len(a.preds) == 2 and a.dtype is DType.f32
+            and a.shape == n.shape):
+        return None
+    bias = a.preds[1] if a.preds[0] is n else a.preds[0] if a.preds[1] is n else None
+    N = n.shape[1]
+    if bias is None or bias is n or bias.dtype is not DType.f32 or tuple(bias.shape) not in ((N,), (1, N)):
+        return None
+    cons = consumers.get(a.id, [])
+    if a.id not in root_ids and len(cons) == 1:
+        r = cons[0]
+        z = r.preds[1] if len(r.preds) == 2 and r.preds[0] is a else None
+        if (r.kind is OpKind.MAP and r.op.code is ElemCode.maximum and z is not None and z.shape == ()
+                and z.op.code is ElemCode.const_splat and z.op.attrs and z.op.attrs[0] == 0 and r.dtype is DType.f32):
+            return r, [a, r], bias, "relu_bias"
+    return a, [a], bias, "bias"
+
+
+def plan_regions(roots: Sequence[Node], row_fusion=None, check=None, epilogues: bool = False) -> List[PlanStep]:
     """B200 region planner (module docstring).
 
     ``row_fusion(reduction, consumer)`` proposes keeping a reduction inside its
@@ -344,7 +377,7 @@ def plan_regions(roots: Sequence[Node], row_fusion=None, check=None) -> List[Pla
     extra: Set[int] = set()
     solo: Set[int] = set()
     for _ in range(256):
-        steps = _plan_once(roots, row_fusion, extra, check, solo)
+        steps = _plan_once(roots, row_fusion, extra, check, solo, epilogues)
         if check is None:
             return steps
         bad = None
@@ -373,7 +406,8 @@ def plan_regions(roots: Sequence[Node], row_fusion=None, check=None) -> List[Pla
     raise RuntimeError("region planning did not converge")
 
 
-def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=frozenset()) -> List[PlanStep]:
+def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=frozenset(),
+               epilogues: bool = False) -> List[PlanStep]:
     roots = [r for r in dict((r.id, r) for r in roots).values() if not r.is_materialized]
     if not roots:
         return []
@@ -396,8 +430,28 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=f
 
     # 2. points that must be in memory
     points: Dict[int, Node] = {r.id: r for r in roots}
+    root_ids = set(points)
+    epi: Dict[int, tuple] = {}          # epilogue root id -> (gemm, chain, bias, kind)
+    absorbed: Set[int] = set()
+    if epilogues:
+        for n in demand.values():
+            if not n.is_materialized and n.id not in extra:
+                e = _gemm_epilogue(n, consumers, root_ids)
+                if e is not None and not any(c.id in extra for c in e[1][:-1]):
+                    epi[e[0].id] = (n,) + e[1:]
+                    absorbed.update([n.id] + [c.id for c in e[1][:-1]])
     for n in demand.values():
         if n.is_materialized:
+            continue
+        if n.id in epi:
+            g = epi[n.id][0]
+            points[n.id] = n
+            ops, _, _ = library_operands(g)
+            for p in ops + [epi[n.id][2]]:
+                if not p.is_materialized:
+                    points[p.id] = p
+            continue
+        if n.id in absorbed:
             continue
         if n.id in extra:
             points[n.id] = n
@@ -427,6 +481,15 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=f
     cones = []
     for pid in sorted(points):
         p = points[pid]
+        if pid in epi:
+            g, chain, bias, kind = epi[pid]
+            ops, trans, call = library_operands(g)
+            st = PlanStep("Library", [p], [g] + chain, list(dict((o.id, o) for o in ops + [bias]).values()),
+                          call=call, trans_flags=trans, operands=ops)
+            st.library_node = g
+            st.epilogue = (kind, bias)
+            cones.append(st)
+            continue
         if p.kind in LIBRARY_KINDS:
             ops, trans, call = library_operands(p)
             cones.append(PlanStep("Library", [p], [p], [o for o in ops], call=call, trans_flags=trans, operands=ops))
@@ -635,6 +698,8 @@ def make_template(steps: List[PlanStep], order: List[Node]):
             "nodes": [idx[n.id] for n in st.nodes],
             "leaves": [idx[n.id] for n in st.leaves],
             "operands": [idx[n.id] for n in st.operands],
+            "library_node": idx[st.library_node.id] if st.library_node is not None else None,
+            "epilogue": (st.epilogue[0], idx[st.epilogue[1].id]) if st.epilogue else None,
             "cache": st.cache,
         })
     return tmpl
@@ -646,6 +711,10 @@ def instantiate(tmpl, order: List[Node]) -> List[PlanStep]:
         st = PlanStep(t["kind"], [order[j] for j in t["roots"]], [order[j] for j in t["nodes"]],
                       [order[j] for j in t["leaves"]], kernel_kind=t["kernel_kind"], call=t["call"],
                       trans_flags=t["trans_flags"], operands=[order[j] for j in t["operands"]], order_index=i)
+        if t.get("library_node") is not None:
+            st.library_node = order[t["library_node"]]
+        if t.get("epilogue"):
+            st.epilogue = (t["epilogue"][0], order[t["epilogue"][1]])
         st.cache = t["cache"]
         steps.append(st)
     return steps

@@ -82,6 +82,8 @@ SIGNATURES = {
     "grumpy_rt_event_destroy": [_u64],
     "grumpy_rt_gemm": [_i, _i, _i, _i, _i, _i, _u64, _i, _u64, _i, _u64, _i],
     "grumpy_rt_gemv": [_i, _i, _i, _i, _u64, _i, _u64, _u64],
+    "grumpy_rt_set_gemm_math": [_i],
+    "grumpy_rt_gemm_epilogue": [_i, _i, _i, _i, _i, _u64, _i, _u64, _i, _u64, _i, _u64, _i, _i],
     "grumpy_rt_nccl_load": [_cp],
     "grumpy_rt_nccl_unique_id": [_cp],
     "grumpy_rt_nccl_init": [_i, _i, _cp],
@@ -236,6 +238,13 @@ class Runtime:
             pass
         self._kernels = {}
         self._pending = {}            # source -> Future of a precompile job
+        self.gemm_math = "fp32"
+        want = os.environ.get("GRUMPY_GEMM_MATH", "bf16x9")
+        try:
+            self.set_gemm_math(want)
+        except RuntimeFailure:
+            # an older cuBLAS was loaded first (e.g. PyTorch's wheel): FP32 SIMT
+            self.gemm_math = "fp32"
         self._pool = None
         self.stats_allocs = 0
         self.launches = 0
@@ -429,6 +438,18 @@ class Runtime:
     def gemm(self, trans_a, trans_b, m, n, k, dtype: DType, a, lda, b, ldb, c, ldc):
         _check(self.lib.grumpy_rt_gemm(int(trans_a), int(trans_b), m, n, k, GR_DTYPE[dtype],
                                        a, lda, b, ldb, c, ldc))
+
+    def set_gemm_math(self, mode: str) -> None:
+        """"fp32" (CUDA cores) or "bf16x9" (FP32 emulated on the tensor cores)."""
+        _check(self.lib.grumpy_rt_set_gemm_math({"fp32": 0, "bf16x9": 1}[mode]))
+        self.gemm_math = mode
+
+    def gemm_epilogue(self, trans_a, trans_b, m, n, k, a, lda, b, ldb, c, ldc, bias=0, epilogue="none",
+                      emulate=False):
+        """cuBLASLt f32 GEMM, epilogue "none" | "bias" | "relu_bias" (bias along columns)."""
+        _check(self.lib.grumpy_rt_gemm_epilogue(int(trans_a), int(trans_b), m, n, k, a, lda, b, ldb, c, ldc,
+                                                bias, {"none": 0, "bias": 1, "relu_bias": 2}[epilogue],
+                                                int(emulate)))
 
     def gemv(self, trans, rows, cols, dtype: DType, a, lda, x, y):
         _check(self.lib.grumpy_rt_gemv(int(trans), rows, cols, GR_DTYPE[dtype], a, lda, x, y))

@@ -35,6 +35,15 @@ from .errors import BadAxis, DTypeMismatch, ShapeMismatch, UnsupportedDType
 from .tensor import DType, TensorBuffer, dtype_of, element_count, normalize_axes, normalize_axis
 
 
+# np.dot boundary (tools/gemm_probe.py): f32 GEMMs run
+# as FP32 emulated with BF16x9 tensor-core products (GRUMPY_GEMM_MATH=bf16x9,
+# the default: 2.4x faster than SIMT SGEMM and closer to the float64 product),
+# and a GEMM feeding one `+ bias[N]` (then one `maximum(., 0)`) is planned as a
+# single cuBLASLt call with a BIAS / RELU_BIAS epilogue (GRUMPY_GEMM_EPILOGUE).
+GEMM_MATH = os.environ.get("GRUMPY_GEMM_MATH", "bf16x9")
+GEMM_EPILOGUES = os.environ.get("GRUMPY_GEMM_EPILOGUE", "1") == "1" and GEMM_MATH == "bf16x9"
+
+
 @dataclasses.dataclass
 class SessionStats:
     """Fusion counters plus B200 transfer/compile counters."""
@@ -93,7 +102,8 @@ class Session:
                         done.add(st.root.id)
             return steps
         from . import codegen
-        return _planner.plan_regions(roots, row_fusion=codegen.row_fusable, check=codegen.check_step)
+        return _planner.plan_regions(roots, row_fusion=codegen.row_fusable, check=codegen.check_step,
+                                     epilogues=GEMM_EPILOGUES)
 
     def const(self, value, dtype: DType) -> Node:
         """Interned rank-0 const_splat node (constants are immutable)."""

@@ -1,0 +1,85 @@
+"""np.dot boundary: BF16x9-emulated FP32 GEMMs and
+the cuBLASLt BIAS / RELU_BIAS epilogues that absorb the R1 region."""
+import numpy as np
+import pytest
+
+import paper_1901_03771_b200 as gp
+from paper_1901_03771_b200 import runtime, session as gsession, workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture
+def sess():
+    s = gp.Session()
+    old = gp.set_default_session(s)
+    yield s
+    gp.set_default_session(old)
+
+
+def _scale(X, W, b):
+    return np.abs(X).astype(np.float64) @ np.abs(W).astype(np.float64) + np.abs(b)
+
+
+def test_emulation_active():
+    # this process loaded the shim before any PyTorch import
+    assert runtime.get().gemm_math == gsession.GEMM_MATH == "bf16x9"
+
+
+@pytest.mark.parametrize("shape", [(257, 131, 67), (1024, 784, 256), (5, 3, 1)])
+def test_relu_bias_layer(sess, shape):
+    m, k, n = shape
+    rng = np.random.default_rng(m)
+    X = rng.standard_normal((m, k)).astype(np.float32)
+    W = rng.standard_normal((k, n)).astype(np.float32)
+    b = rng.standard_normal(n).astype(np.float32)
+    h = gp.maximum(gp.asarray(X) @ gp.asarray(W) + gp.asarray(b), 0)
+    steps = sess.plan([h.node])
+    assert len(steps) == 1 and steps[0].kind == "Library" and steps[0].epilogue[0] == "relu_bias"
+    got = np.asarray(h)
+    assert sess.stats.library_calls == 1 and sess.stats.kernels_executed == 0
+    ref = np.maximum(X.astype(np.float64) @ W.astype(np.float64) + b, 0)
+    # FP32-accurate: within a few ulps of the float64 result, relative to sum|x||w|
+    assert np.max(np.abs(got - ref) / _scale(X, W, b)) < 4 * np.finfo(np.float32).eps
+    assert np.array_equal(got == 0, ref == 0) or np.mean((got == 0) != (ref == 0)) < 1e-3
+
+
+def test_bias_only_and_transposed_operand(sess):
+    rng = np.random.default_rng(3)
+    X = rng.standard_normal((300, 96)).astype(np.float32)
+    W = rng.standard_normal((40, 96)).astype(np.float32)
+    b = rng.standard_normal((1, 40)).astype(np.float32)
+    z = gp.asarray(X) @ gp.asarray(W).T + gp.asarray(b)       # transpose absorbed into the op flag
+    t = z.sum()                                                 # z has two consumers: no ReLU absorbed
+    steps = sess.plan([z.node, t.node])
+    lib = [s for s in steps if s.kind == "Library"]
+    assert len(lib) == 1 and lib[0].epilogue[0] == "bias" and lib[0].trans_flags == (False, True)
+    gp.force(z, t)
+    ref = X.astype(np.float64) @ W.T.astype(np.float64) + b
+    assert np.max(np.abs(np.asarray(z) - ref) / _scale(X, W.T, b)) < 4 * np.finfo(np.float32).eps
+
+
+def test_nan_and_signed_zero_follow_numpy(sess):
+    """NaN rows stay NaN through the fused ReLU (np.maximum propagates NaN)."""
+    rng = np.random.default_rng(4)
+    X = rng.standard_normal((64, 32)).astype(np.float32)
+    W = rng.standard_normal((32, 16)).astype(np.float32)
+    b = rng.standard_normal(16).astype(np.float32)
+    X[5, 3] = np.nan
+    X[9] = 0.0
+    b[2] = -1.0
+    got = np.asarray(gp.maximum(gp.asarray(X) @ gp.asarray(W) + gp.asarray(b), 0))
+    exp = np.maximum(X @ W + b, 0)
+    assert np.array_equal(np.isnan(got), np.isnan(exp))
+    fin = ~np.isnan(exp)
+    np.testing.assert_allclose(got[fin], exp[fin], rtol=1e-5, atol=1e-5)
+
+
+def test_mlp_plan_two_library_steps_one_kernel(sess):
+    X, W1, b1, W2, b2 = wl.mlp_inputs(batch=2048, hidden=256)
+    p, lab = wl.mlp(gp, *[gp.asarray(a) for a in (X, W1, b1, W2, b2)])
+    gp.force(p, lab)
+    assert sess.stats.library_calls == 2 and sess.stats.kernels_executed == 1
+    ep, elab = wl.mlp(np, X, W1, b1, W2, b2)
+    np.testing.assert_allclose(np.asarray(p), ep, rtol=1e-4, atol=1e-6)
+    assert np.mean(np.asarray(lab) == elab) >= 0.999
