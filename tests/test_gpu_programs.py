@@ -40,7 +40,7 @@ def make_program(seed):
     transcendental = False   # exp is ulp-accurate, not bit-exact: no branching on it afterwards
     viewed = False
     for _ in range(depth):
-        k = rng.integers(0, 11)
+        k = rng.integers(0, 14)
         other = pool[int(rng.integers(0, len(pool)))]
         try:
             if k == 0:
@@ -73,6 +73,24 @@ def make_program(seed):
                 cur = cur.max(axis=ax) if rng.random() < 0.5 else cur.min(axis=ax)
             elif k == 10 and cur.ndim >= 1:
                 cur = cur.astype(np.float64) / 3
+            elif k == 11 and cur.ndim == 2 and cur.dtype.kind == "f":
+                # np.dot boundary: GEMM, optionally + bias row and ReLU (the
+                # cuBLASLt epilogue pattern); reassociated, so inexact after
+                W = gp.asarray(rng.standard_normal((cur.shape[1], int(rng.integers(1, 17)))).astype(cur.dtype))
+                cur = cur @ W
+                if rng.random() < 0.6:
+                    cur = cur + gp.asarray(rng.standard_normal(cur.shape[1]).astype(cur.dtype))
+                    if rng.random() < 0.5:
+                        cur = gp.maximum(cur, 0)
+                transcendental = True
+            elif k == 12 and cur.ndim >= 1:
+                ax = int(rng.integers(0, cur.ndim))
+                cur = gp.cumsum(cur, axis=ax)
+                transcendental = transcendental or cur.dtype.kind == "f"
+            elif k == 13 and cur.ndim >= 1 and cur.shape[-1] >= 2:
+                nxt = cur.copy()
+                nxt[..., ::2] = cur[..., ::2] * 2 + 1
+                cur = nxt
         except gp.LazyFuseError:
             continue
     finals = [cur]
@@ -88,8 +106,12 @@ def _close(got, exp, dtype, transcendental=False):
         return np.array_equal(got, exp)
     # f32 transcendental ancestry carries f32 ulp error into f64 results
     rtol = 1e-5 if (dtype == np.float32 or transcendental) else 1e-12
-    scale = np.max(np.abs(exp)) if exp.size else 0.0
-    return np.allclose(got, exp, rtol=rtol, atol=rtol * max(1.0, scale) * 64, equal_nan=True)
+    fin = np.isfinite(exp)
+    if not np.array_equal(np.isfinite(got), fin) or not np.array_equal(got[~fin], exp[~fin]) and \
+            not np.array_equal(np.isnan(got[~fin]), np.isnan(exp[~fin])):
+        return False
+    scale = np.max(np.abs(exp[fin])) if fin.any() else 0.0
+    return np.allclose(got[fin], exp[fin], rtol=rtol, atol=rtol * max(1.0, scale) * 64)
 
 
 @pytest.mark.parametrize("seed", range(NPROG))
