@@ -665,7 +665,8 @@ int grumpy_rt_function_info(uint64_t fn, int* num_regs, int* local_bytes, int* s
 // whole unified L1/shared array as shared memory; the others keep the default
 // carve-out (maximum L1 for their LDG streams).
 static int smem_attrs(CUfunction f, size_t dyn_smem) {
-  if (dyn_smem > 48 * 1024)
+  // opt in whenever dynamic + static shared memory may pass the 48 KB default
+  if (dyn_smem > 32 * 1024)
     CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)dyn_smem), "attr");
   if (dyn_smem > 0)
     CU_CHECK(D.p_cuFuncSetAttribute(f, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, 100), "attr");

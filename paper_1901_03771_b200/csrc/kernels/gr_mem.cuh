@@ -33,7 +33,7 @@ __device__ __forceinline__ uint4 ldg_na(const uint4* p) {
 template <class X> __device__ __forceinline__ X ldg_any(const X* p) { return __ldg(p); }
 template <> __device__ __forceinline__ uint4 ldg_any(const uint4* p) { return ldg_na(p); }
 #define GR_LDG ldg_any
-#else
+#elif !defined(GR_LDG)   // a kernel may bring its own (e.g. reads of TMA-staged tiles)
 #define GR_LDG __ldg
 #endif
 template <class T, int V> __device__ __forceinline__ void ldv(T (&dst)[V], const T* __restrict__ src) {
