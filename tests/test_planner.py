@@ -180,3 +180,36 @@ def test_chained_jacobi_sweeps_one_step_each(sess):
     x = gp.asarray(np.arange(16.0))
     y = (x * 2.0)[1:] + 1.0
     assert len(sess.plan([y.node])) == 1
+
+
+def test_gemm_epilogue_absorption(sess):
+    """np.dot boundary: GEMM -> + bias[N] -> maximum(., 0) plans as one
+    Library step with a RELU_BIAS epilogue; a GEMM with another consumer, a
+    non-vector bias or a disabled flag keeps the separate fused map."""
+    X, W1, b1, W2, b2 = wl.mlp_inputs(batch=64, hidden=32)
+    args = [gp.asarray(a) for a in (X, W1, b1, W2, b2)]
+    p, lab = wl.mlp(gp, *args)
+    steps = planner.plan_regions([p.node, lab.node], row_fusion=codegen.row_fusable,
+                                 check=codegen.check_step, epilogues=True)
+    kinds = [(s.kind, s.epilogue[0] if s.epilogue else None) for s in steps]
+    assert kinds == [("Library", "relu_bias"), ("Library", "bias"), ("Fused", None)]
+    assert steps[0].library_node.kind is OpKind.MATMUL and steps[0].root.op.code.name == "maximum"
+    off = planner.plan_regions([p.node, lab.node], row_fusion=codegen.row_fusable,
+                               check=codegen.check_step, epilogues=False)
+    assert [s.kind for s in off] == ["Library", "Fused", "Library", "Fused"]
+    # the GEMM result also consumed elsewhere: no absorption
+    h = args[0] @ args[1]
+    y = gp.maximum(h + args[2], 0)
+    t = h.sum()
+    st = planner.plan_regions([y.node, t.node], row_fusion=codegen.row_fusable,
+                              check=codegen.check_step, epilogues=True)
+    assert all(s.epilogue is None for s in st)
+    # a [M, N] addend is not a bias vector
+    z = args[0] @ args[1] + gp.asarray(np.ones((64, 32), np.float32))
+    st = planner.plan_regions([z.node], row_fusion=codegen.row_fusable, check=codegen.check_step, epilogues=True)
+    assert all(s.epilogue is None for s in st)
+    # plan-cache instantiation carries the epilogue
+    key, order = planner.dag_signature([p.node, lab.node])
+    tmpl = planner.make_template(steps, order)
+    again = planner.instantiate(tmpl, order)
+    assert again[0].epilogue[0] == "relu_bias" and again[0].epilogue[1] is steps[0].epilogue[1]
