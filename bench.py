@@ -393,12 +393,16 @@ def run_grumpy(args, dist):
     launches = sess.stats.kernels_executed - k0
     prof = sess.executor.take_profile()
     sess.executor.profile = None
-    # keep the GPU loaded (untimed) until the sampler has enough points
-    t_load = time.perf_counter()
-    while clocks.since_mark() < 5 and time.perf_counter() - t_load < 3.0:
+    # keep the GPU loaded (untimed) until the sampler has enough points; the
+    # iteration count is agreed over ranks (a step may run a collective, so
+    # every rank must run the same number of them)
+    step_s = rt.elapsed_ms(e_all0, e_all1) / 1e3 / max(args.steps, 1)
+    # (nvidia-smi samples every 100 ms: ~0.8 s of steps covers 5 samples)
+    want = 0 if clocks.since_mark() >= 5 else min(int(0.8 / max(step_s, 1e-6)) + 1, 2000)
+    for _ in range(int(dist.max(float(want)))):
         outs = prog(gp, dev)
         gp.force(*outs)
-        rt.sync()
+    rt.sync()
     clk = clocks.stop()
     dist.barrier()
     total_ms = dist.max(rt.elapsed_ms(e_all0, e_all1))

@@ -97,6 +97,29 @@ class NcclComm(TorchHostComm):
         self.rt.nccl_allreduce(buf.ptr, buf.ptr, count, dtype, GR_OP[op])
 
 
+class HostStagedComm(TorchHostComm):
+    """Device partials combined through host memory over gloo — used when two
+    ranks of the group share one GPU, where NCCL refuses to build a
+    communicator (a single-GPU box running a multi-rank job)."""
+
+    def __init__(self, rt):
+        super().__init__()
+        self.rt = rt
+
+    def allreduce_device(self, buf, count, dtype, op):
+        host = buf.to_numpy(dtype, (count,))
+        buf.copy_from_host(np.ascontiguousarray(self.allreduce_host(host, op).astype(host.dtype)))
+
+
+def _ranks_share_a_device(rt) -> bool:
+    import socket
+    import torch.distributed as td
+    me = (socket.gethostname(), int(getattr(rt, "device", 0)))
+    allv = [None] * td.get_world_size()
+    td.all_gather_object(allv, me)
+    return len(set(allv)) < len(allv)
+
+
 def init(backend: Optional[str] = None, session=None) -> Comm:
     """Join the process group launched by torchrun (RANK/WORLD_SIZE/MASTER_*)."""
     import torch.distributed as td
@@ -112,7 +135,8 @@ def init(backend: Optional[str] = None, session=None) -> Comm:
         comm = TorchHostComm()
     else:
         from . import runtime
-        comm = NcclComm(runtime.get())
+        rt = runtime.get()
+        comm = HostStagedComm(rt) if _ranks_share_a_device(rt) else NcclComm(rt)
     sess.comm = comm
     return comm
 

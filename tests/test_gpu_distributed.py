@@ -64,3 +64,21 @@ def test_sharded_kmeans_partials(dsess):
         np.testing.assert_allclose(np.asarray(s), e, rtol=1e-12, atol=1e-9)
     newC = wl.kmeans_centroids(sums, counts, C)
     np.testing.assert_allclose(newC, wl.kmeans_centroids(esums, ecounts, C), rtol=1e-6)
+
+
+def test_two_ranks_one_gpu_partials():
+    """Two torchrun ranks on the one GPU: shards of k-means and row-normalise
+    inputs, partials combined through host memory (NCCL cannot pair two
+    ranks on one device); every rank checks its results against NumPy."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GRUMPY_DEVICE="0", PYTHONPATH=root)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                        os.path.join(root, "tools", "two_rank_check.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert p.stdout.count(" ok (HostStagedComm)") == 2, p.stdout
