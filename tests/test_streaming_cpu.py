@@ -54,7 +54,7 @@ def test_streamed_random_programs_do_stream(monkeypatch):
     monkeypatch.setattr(streaming, "ROW_ALIGN", 1)
     monkeypatch.setattr(streaming, "CHUNK_BYTES", 96)
     streamed = 0
-    for seed in range(60):
+    for seed in range(200):
         s = gp.Session()
         old = gp.set_default_session(s)
         try:
