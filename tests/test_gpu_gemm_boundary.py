@@ -83,3 +83,22 @@ def test_mlp_plan_two_library_steps_one_kernel(sess):
     ep, elab = wl.mlp(np, X, W1, b1, W2, b2)
     np.testing.assert_allclose(np.asarray(p), ep, rtol=1e-4, atol=1e-6)
     assert np.mean(np.asarray(lab) == elab) >= 0.999
+
+
+def test_emulated_gemm_special_values(sess):
+    """BF16x9-emulated FP32 keeps IEEE special values: +-inf rows, NaN rows,
+    results near the overflow threshold and subnormal results (tools/gemm_special_values.py)."""
+    rng = np.random.default_rng(0)
+    X = rng.random((64, 32)).astype(np.float32)
+    W = rng.random((32, 16)).astype(np.float32)
+    X[3, 5], X[7, 1], X[9, 2], X[11, 0] = np.inf, -np.inf, 3e38, np.nan
+    X[10, :] = 1e-40
+    got = np.asarray(gp.asarray(X) @ gp.asarray(W))
+    with np.errstate(all="ignore"):
+        exp = X.astype(np.float64) @ W.astype(np.float64)
+    assert np.array_equal(np.isnan(got), np.isnan(exp))
+    assert np.array_equal(np.isinf(got), np.isinf(exp)) and np.array_equal(got[np.isinf(exp)], exp[np.isinf(exp)])
+    fin = np.isfinite(exp) & (np.abs(exp) > 1e-37)
+    assert np.max(np.abs(got[fin] - exp[fin]) / np.abs(exp[fin])) < 4 * np.finfo(np.float32).eps
+    sub = np.isfinite(exp) & (np.abs(exp) <= 1e-37)
+    assert np.max(np.abs(got[sub] - exp[sub])) < 1e-44 * 32    # a few subnormal ulps
