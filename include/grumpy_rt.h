@@ -160,7 +160,8 @@ int grumpy_rt_set_gemm_math(int mode);
 /* cuBLASLt f32 GEMM with a fused epilogue: row-major C[m,n] = epi(op(A)op(B)
  * + bias[n]), epilogue 0 none / 1 bias / 2 relu(bias) — the library-side
  * alternative to the R1 bias+ReLU region;
- * emulate = 1 uses BF16x9 emulated FP32. */
+ * emulate = 1 uses BF16x9 emulated FP32, 2 only where it pays (m, n >= 128),
+ * the rule grumpy_rt_gemm applies in emulation mode. */
 int grumpy_rt_gemm_epilogue(int trans_a, int trans_b, int m, int n, int k, uint64_t a, int lda,
                             uint64_t b, int ldb, uint64_t c, int ldc, uint64_t bias, int epilogue,
                             int emulate);

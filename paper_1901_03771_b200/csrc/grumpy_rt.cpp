@@ -830,8 +830,10 @@ static void apply_gemm_math() {
   if (!S.cublas) return;
   cublasSetMathMode(S.cublas, S.gemm_math ? CUBLAS_FP32_EMULATED_BF16X9_MATH : CUBLAS_DEFAULT_MATH);
   if (emulation_fn())
-    emulation_fn()(S.cublas, S.gemm_math ? CUBLAS_EMULATION_STRATEGY_EAGER : CUBLAS_EMULATION_STRATEGY_DEFAULT);
+    emulation_fn()(S.cublas, S.gemm_math ? (getenv("GRUMPY_EMULATION_EAGER") ? CUBLAS_EMULATION_STRATEGY_EAGER : CUBLAS_EMULATION_STRATEGY_PERFORMANT) : CUBLAS_EMULATION_STRATEGY_DEFAULT);
 }
+
+static bool gemm_emulation_pays(int m, int n) { return m >= 128 && n >= 128; }
 
 int grumpy_rt_set_gemm_math(int mode) {
   if (mode != 0 && mode != 1) return fail(GR_EINVAL, "gemm math mode must be 0 (fp32) or 1 (bf16x9 emulation)");
@@ -865,6 +867,7 @@ int grumpy_rt_gemm_epilogue(int trans_a, int trans_b, int m, int n, int k, uint6
   int out = GR_OK;
   if (emulate && !emulation_available())
     return fail(GR_EINVAL, "BF16x9 FP32 emulation needs cuBLAS >= 12.9 (an older libcublas.so.12 is loaded)");
+  if (emulate == 2) emulate = gemm_emulation_pays(m, n);   // 2: emulate where it pays
   const cublasComputeType_t ct = emulate ? CUBLAS_COMPUTE_32F_EMULATED_16BFX9 : CUBLAS_COMPUTE_32F;
   do {
     if ((st = cublasLtMatmulDescCreate(&desc, ct, CUDA_R_32F)) != CUBLAS_STATUS_SUCCESS) break;
@@ -920,6 +923,12 @@ int grumpy_rt_gemm(int trans_a, int trans_b, int m, int n, int k, int dtype, uin
   cublasStatus_t st;
   if (dtype == GR_F32) {
     const float one = 1.f, zero = 0.f;
+    // BF16x9 emulation pays only for GEMMs large in both output dimensions
+    // (tools/skinny_gemm_probe.py: 65536x1024 @ 1024xN — N=16/64 emulated
+    // 245/248 us vs 111/165 us FP32; N=256 319 vs 566 us; N=1024 0.68 vs
+    // 1.67 ms); cuBLAS's own PERFORMANT strategy still emulates the skinny ones
+    const bool emu = S.gemm_math && gemm_emulation_pays(m, n);
+    cublasSetMathMode(S.cublas, emu ? CUBLAS_FP32_EMULATED_BF16X9_MATH : CUBLAS_DEFAULT_MATH);
     st = cublasSgemm(S.cublas, opb, opa, n, m, k, &one, (const float*)b, ldb, (const float*)a, lda, &zero,
                      (float*)c, ldc);
   } else if (dtype == GR_F64) {

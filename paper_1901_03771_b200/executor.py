@@ -241,7 +241,7 @@ class Executor:
                 self.rt.gemm_epilogue(ta, tb, m, nn, k, self.device_ptr(a), a.shape[1],
                                       self.device_ptr(b), b.shape[1], out.device.ptr, nn,
                                       bias=self.device_ptr(bias), epilogue=kind,
-                                      emulate=self.rt.gemm_math == "bf16x9")
+                                      emulate=2 if self.rt.gemm_math == "bf16x9" else 0)
             elif m and nn:
                 if k == 0:
                     self.rt.memset(out.device, 0)

@@ -446,7 +446,8 @@ class Runtime:
 
     def gemm_epilogue(self, trans_a, trans_b, m, n, k, a, lda, b, ldb, c, ldc, bias=0, epilogue="none",
                       emulate=False):
-        """cuBLASLt f32 GEMM, epilogue "none" | "bias" | "relu_bias" (bias along columns)."""
+        """cuBLASLt f32 GEMM, epilogue "none" | "bias" | "relu_bias" (bias along columns);
+        emulate: 0 FP32, 1 BF16x9-emulated FP32, 2 emulated where it pays (both output dims >= 128)."""
         _check(self.lib.grumpy_rt_gemm_epilogue(int(trans_a), int(trans_b), m, n, k, a, lda, b, ldb, c, ldc,
                                                 bias, {"none": 0, "bias": 1, "relu_bias": 2}[epilogue],
                                                 int(emulate)))
