@@ -190,7 +190,7 @@ def shard_of(node: Node):
     return None
 
 
-def classify(roots, memo: Optional[dict] = None, sharded=None) -> Dict[int, str]:
+def classify(roots, memo: Optional[dict] = None, sharded=None, scans: bool = False) -> Dict[int, str]:
     """Distribution of every unmaterialized node reachable from roots (plus the
     materialized frontier): "S", "R", "P:<op>", "A:<max|min>".  ``sharded``
     (node ids) replaces the registered shard inputs, e.g. the host inputs of a
@@ -213,9 +213,9 @@ def classify(roots, memo: Optional[dict] = None, sharded=None) -> Dict[int, str]
             return getattr(n, "dist", None) or "R"
         k = n.kind
         ps = [dist(p) for p in n.preds]
-        if any(p.startswith(("P", "A")) for p in ps):
+        if any(p.startswith(("P", "A", "C")) for p in ps):
             # a partial consumed before its allreduce: planner makes it a root
-            ps = ["R" if p.startswith(("P", "A")) else p for p in ps]
+            ps = ["R" if p.startswith(("P", "A", "C")) else p for p in ps]
         if not any(p == "S" for p in ps):
             return "R"
         if k in (OpKind.MAP, OpKind.CAST, OpKind.BROADCAST, OpKind.SLICE_ASSIGN):
@@ -262,6 +262,14 @@ def classify(roots, memo: Optional[dict] = None, sharded=None) -> Dict[int, str]
                 raise ShapeMismatch("x @ M with M sharded on its rows needs x sharded too")
             raise ShapeMismatch("unsupported sharding of a matrix-vector product")
         if k is OpKind.SCAN:
+            axis = n.op.attrs[1]
+            if axis not in (None, 0):
+                return "S"                       # along a row-local axis
+            if scans and (axis == 0 or len(n.preds[0].shape) == 1):
+                # along the sharded axis: "C:<op>" = carried — each part scans
+                # its rows and continues from the previous part's last value
+                # (streamed to_external, streaming.py)
+                return f"C:{n.op.attrs[0].value}"
             raise ShapeMismatch("cumulative ops along a sharded axis are not supported yet")
         raise ShapeMismatch(f"{n.op!r} on a sharded operand")
 

@@ -42,7 +42,8 @@ MIN_BYTES = 48 << 20        # smaller forces gain nothing from overlap
 ROW_ALIGN = 256             # chunk row counts: 16-byte aligned views, full vectors
 
 _ALLOWED = {OpKind.MAP, OpKind.CAST, OpKind.BROADCAST, OpKind.TRANSPOSE, OpKind.RESHAPE,
-            OpKind.SLICE, OpKind.REDUCE, OpKind.ARGREDUCE, OpKind.MATMUL, OpKind.MATVEC, OpKind.KEYED_SUM}
+            OpKind.SLICE, OpKind.REDUCE, OpKind.ARGREDUCE, OpKind.MATMUL, OpKind.MATVEC, OpKind.KEYED_SUM,
+            OpKind.SCAN}
 
 
 class DeviceView:
@@ -107,21 +108,21 @@ def plan(roots: Sequence[Node], chunk_bytes: Optional[int] = None) -> Optional[S
     if N < 2 * ROW_ALIGN:
         return None
     try:
-        dist = D.classify(roots, sharded={l.id for l in leaves})
+        dist = D.classify(roots, sharded={l.id for l in leaves}, scans=True)
     except LazyFuseError:
         return None
     root_ids = {r.id for r in roots}
     for r in roots:
         d = dist.get(r.id, "R")
-        if d == "S":
-            if not r.shape or r.shape[0] != N:
+        if d == "S" or d.startswith("C:"):
+            if not r.shape or r.shape[0] != N or (d.startswith("C:") and d[2:] not in _COMBINE):
                 return None
         elif not (d.startswith("P:") and d[2:] in _COMBINE):
             return None
     for n in nodes:
-        if n.id not in root_ids and dist.get(n.id, "R")[0] in "PA":
-            return None                      # a partial consumed inside the region
-    srows = [r for r in roots if dist[r.id] == "S"]
+        if n.id not in root_ids and dist.get(n.id, "R")[0] in "PAC":
+            return None                      # a partial or carried scan consumed inside the region
+    srows = [r for r in roots if dist[r.id] == "S" or dist[r.id].startswith("C:")]
     total = sum(l.data.nbytes for l in leaves) + sum(element_count(r.shape) * r.dtype.itemsize for r in srows)
     if total < MIN_BYTES:
         return None
@@ -181,8 +182,10 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
     st = _streams(rt)
     g = sess.graph
     N, rows = p.N, p.rows
-    srows = [r for r in p.roots if p.dist[r.id] == "S"]
-    parts = {r.id: [] for r in p.roots if p.dist[r.id] != "S"}   # per-chunk partial nodes
+    srows = [r for r in p.roots if p.dist[r.id] == "S" or p.dist[r.id].startswith("C:")]
+    carried = {r.id for r in p.roots if p.dist[r.id].startswith("C:")}   # scans along the streamed axis
+    parts = {r.id: [] for r in p.roots if r not in srows}   # per-chunk partial nodes
+    prev_final: Dict[int, Node] = {}
     # full-size device buffers: inputs and row-local results (chunks are views)
     dev_in = {l.id: rt.alloc(l.data.nbytes) for l in p.leaves}
     dev_out = {r.id: rt.alloc(element_count(r.shape) * r.dtype.itemsize) for r in srows}
@@ -227,8 +230,16 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
                 buf = TensorBuffer(l.dtype, (c,) + tuple(l.shape[1:]), device=DeviceView(dev_in[l.id], lo * rb, c * rb))
                 memo[l.id] = g.add_input(buf)
             for n in p.nodes:
-                if p.dist.get(n.id, "R") == "S" or n.id in parts:
+                if p.dist.get(n.id, "R") == "S" or n.id in parts or n.id in carried:
                     memo[n.id] = g.add_op(_rewrite(n.op, c), [memo.get(q.id, q) for q in n.preds])
+            for r in p.roots:
+                if r.id in carried and ci > 0:
+                    # continue from the previous chunk's last row (its scan
+                    # result is already on the device, stream-ordered)
+                    pf = prev_final[r.id]
+                    sl = ((pf.shape[0] - 1, 1, 1),) + tuple((0, 1, e) for e in pf.shape[1:])
+                    carry = g.add_op(Op(OpKind.SLICE, None, (sl,)), [pf])
+                    memo[r.id] = g.add_op(Op(OpKind.MAP, _COMBINE[p.dist[r.id][2:]]), [memo[r.id], carry])
             croots = [memo[r.id] for r in p.roots]
             views = {}
             for r, cr in zip(p.roots, croots):
@@ -247,6 +258,9 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
                     # produced by a library call (cuBLAS output): move it in
                     rb = _row_bytes(r)
                     rt.d2d_raw(dev_out[r.id].ptr + lo * rb, cr.data.device.ptr, c * rb)
+            for r, cr in zip(p.roots, croots):
+                if r.id in carried:
+                    prev_final[r.id] = cr
             keep.append(croots)
             e = st.event(ev)
             ev += 1

@@ -116,3 +116,28 @@ def test_streamed_random_program(sess, monkeypatch, seed):
         assert g.shape == e.shape and g.dtype == e.dtype
         assert _close(g, e, e.dtype, transcendental), (seed, g, e)
 
+
+
+def test_scans_streamed_with_carry(sess, small_chunks):
+    """Scans along the streamed axis ("C" roots): each chunk scans its rows
+    and continues from the previous chunk's last value.  Integers exact;
+    floats no less accurate than NumPy's own sequential fold."""
+    rng = np.random.default_rng(12)
+    xi = rng.integers(-50, 50, 1 << 18)
+    c0 = sess.stats.streamed_chunks
+    (gi,) = gp.materialize(gp.cumsum(gp.asarray(xi) * 3 + 1))
+    assert sess.stats.streamed_chunks - c0 >= 4
+    assert np.array_equal(gi, np.cumsum(xi * 3 + 1))
+    xm = rng.standard_normal((1 << 16, 8))
+    (gm,) = gp.materialize(np.maximum.accumulate(gp.asarray(xm), axis=0))
+    assert np.array_equal(gm, np.maximum.accumulate(xm, axis=0))
+    (g2,) = gp.materialize(gp.cumsum(gp.asarray(xm) * 2, axis=0))
+    assert np.array_equal(np.asarray(g2)[:1], xm[:1] * 2)
+    xf = rng.standard_normal(1 << 18)
+    (gf,) = gp.materialize(gp.cumsum(gp.exp(gp.asarray(xf) * 0.1)))
+    ref = np.cumsum(np.exp(xf * 0.1))
+    exact = np.cumsum(np.exp(xf * 0.1).astype(np.longdouble))
+    assert np.max(np.abs(gf - exact)) <= 2 * np.max(np.abs(ref - exact)) + 2.2e-16 * float(exact[-1])
+    e2 = np.cumsum((xm * 2).astype(np.longdouble), axis=0)
+    r2 = np.cumsum(xm * 2, axis=0)
+    assert np.max(np.abs(g2 - e2)) <= 2 * np.max(np.abs(r2 - e2)) + 2.2e-16 * float(np.abs(e2).max())

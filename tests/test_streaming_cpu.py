@@ -41,7 +41,9 @@ def test_partials_and_ineligible():
     assert streaming.plan([(a * 2).argmax().node]) is None              # arg-reduction over the streamed axis
     x = gp.asarray(np.ones((4096, 3)))
     assert streaming.plan([(x - x.mean(0)).node]) is None               # a partial consumed inside
-    assert streaming.plan([gp.cumsum(a * 2).node]) is None              # scan along the leading axis
+    ps = streaming.plan([gp.cumsum(a * 2).node])                         # scan along the streamed axis: carried
+    assert ps is not None and list(ps.dist.values()).count("C:sum") == 1
+    assert streaming.plan([(gp.cumsum(a * 2) + 1).node]) is None         # a carried scan consumed inside
     small = gp.asarray(np.ones(100))
     assert streaming.plan([(small + 1).node]) is None                   # too few rows
 
