@@ -173,6 +173,13 @@ def shard_info(node: Node):
     return _SHARDED.get(node.id)
 
 
+def leaf_dist(node: Node) -> str:
+    """Distribution tag of a materialized leaf (a plan-cache key part)."""
+    if node.id in _SHARDED:
+        return "S"
+    return getattr(node, "dist", None) or "R"
+
+
 def shard_of(node: Node):
     """(global leading extent, this rank's offset) of the sharded input that
     ``node``'s leading axis comes from, or None."""

@@ -96,7 +96,14 @@ class Executor:
         for r, b in zip(roots, outs):
             d = dist.get(r.id, "R")
             if d.startswith("P:") and element_count(r.shape):
-                comm.allreduce_device(b.device, element_count(r.shape), r.dtype, ReduceOp(d[2:]))
+                if self.profile is not None:
+                    e0, e1 = self._event_pair()
+                    self.rt.record(e0)
+                    comm.allreduce_device(b.device, element_count(r.shape), r.dtype, ReduceOp(d[2:]))
+                    self.rt.record(e1)
+                    self.profile.append(("collective", f"allreduce:{d[2:]}", e0, e1))
+                else:
+                    comm.allreduce_device(b.device, element_count(r.shape), r.dtype, ReduceOp(d[2:]))
                 self.session.stats.collectives += 1
 
     def kernel_source(self, region: codegen.Region) -> codegen.KernelSource:

@@ -486,6 +486,16 @@ class Runtime:
 _rt: Optional[Runtime] = None
 
 
+def device_count() -> int:
+    """CUDA devices visible to this process (0 when there is no driver)."""
+    n = ctypes.c_int(0)
+    try:
+        rc = load_library().grumpy_rt_device_count(ctypes.byref(n))
+    except Exception:  # noqa: BLE001 — no shim: no devices usable
+        return 0
+    return n.value if rc == 0 else 0
+
+
 def default_device() -> int:
     for var in ("GRUMPY_DEVICE", "LOCAL_RANK"):
         if os.environ.get(var):

@@ -81,6 +81,7 @@ class Session:
         self._consts = {}
         self._plan_cache = {}
         self._arg_operand_shape = {}
+        self._shard_cache = {}
         self.comm = None  # distributed.Comm when sharded
 
     @property
@@ -145,23 +146,26 @@ class Session:
     def _force_sharded(self, pending):
         """Leading-axis sharded execution (distributed.py): partial nodes become
         step roots and are allreduced after their kernel; arg-reductions over
-        the sharded axis are combined from (value, global index) pairs."""
+        the sharded axis are combined from (value, global index) pairs.
+
+        Plans are cached like unsharded ones, keyed by the DAG signature plus
+        the distribution of its materialized leaves, so an iterative sharded
+        program pays one classification and one region pass per structure."""
         from . import distributed as D
         t0 = time.perf_counter()
-        dist = D.classify(pending)
-        nodes = {}
-        stack = list(pending)
-        while stack:
-            n = stack.pop()
-            if n.id in nodes:
-                continue
-            nodes[n.id] = n
-            if not n.is_materialized:
-                stack.extend(n.preds)
-        partial = [n for n in nodes.values() if not n.is_materialized and dist.get(n.id, "R")[0] in "PA"]
+        key, order = _planner.dag_signature(pending)
+        leafdist = tuple(D.leaf_dist(n) for n in order if n.is_materialized)
+        ckey = (key, leafdist)
+        hit = self._shard_cache.get(ckey)
+        if hit is None:
+            dist = D.classify(pending)
+            partial = [n for n in order if not n.is_materialized and dist.get(n.id, "R")[0] in "PA"]
+        else:
+            tmpl, partial_idx, tags = hit
+            partial = [order[i] for i in partial_idx]
         aux = {}
         for n in partial:
-            if dist[n.id][0] == "A":
+            if n.op.kind is OpKind.ARGREDUCE:
                 info = D.shard_of(n.preds[0])
                 self._arg_operand_shape[n.id] = (n.preds[0].shape, info[1] if info else 0)
                 which, axis, keepdims = n.op.attrs
@@ -170,13 +174,23 @@ class Session:
                 rop = ReduceOp.max if which == "max" else ReduceOp.min
                 aux[n.id] = self.graph.add_op(Op(OpKind.REDUCE, None, (rop, axes, bool(keepdims), None)), [x])
         roots = list(dict((n.id, n) for n in list(pending) + partial + list(aux.values())).values())
-        steps = self.plan(roots)
+        _k2, order2 = _planner.dag_signature(roots)
+        if hit is None:
+            steps = self.plan(roots)
+            idx = {n.id: i for i, n in enumerate(order)}
+            tags = tuple(dist.get(n.id, "R") for n in order2)
+            if len(self._shard_cache) > 256:
+                self._shard_cache.clear()
+            self._shard_cache[ckey] = (_planner.make_template(steps, order2), [idx[n.id] for n in partial], tags)
+        else:
+            steps = _planner.instantiate(tmpl, order2)
+            dist = {n.id: t for n, t in zip(order2, tags)}
         self.stats.plan_time += time.perf_counter() - t0
         t1 = time.perf_counter()
         self.executor.run(steps, dist=dist, comm=self.comm)
         for n in partial:
-            if dist[n.id][0] == "A":
-                self._combine_arg(n, aux[n.id], dist[n.id][2:])
+            if n.op.kind is OpKind.ARGREDUCE:
+                self._combine_arg(n, aux[n.id], "max" if n.op.attrs[0] == "max" else "min")
             n.dist = "R"
         self.stats.exec_time += time.perf_counter() - t1
 

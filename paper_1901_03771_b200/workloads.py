@@ -161,3 +161,99 @@ def scan_inputs(n=1 << 28, seed=42, dtype=np.float32):
 def scan(xp, x):
     """Map-scan: a fused map prologue feeding one inclusive scan."""
     return xp.cumsum(x * 0.5 + 1.0)
+
+
+# ---- named-shape inputs generated in fixed row blocks ---------------------------
+# The bench shards the named shape along its leading axis (SURVEY.md §8(e)).
+# Generating the global array from fixed row blocks, block b from
+# default_rng([seed, b]), makes rank r's shard identical to rows [lo, hi) of the
+# single-GPU input for any GPU count, and lets the blocks be generated on
+# several host threads.  Replicated operands (weights, centroids) come from
+# default_rng(seed).
+
+def _bs_rows(dtype):
+    def gen(rng, rows):
+        S = rng.uniform(5.0, 30.0, rows).astype(dtype)
+        X = rng.uniform(1.0, 100.0, rows).astype(dtype)
+        T = rng.uniform(0.25, 10.0, rows).astype(dtype)
+        return [S, X, T]
+    return gen
+
+
+def _km_centres(seed, k=64, d=4):
+    rng = np.random.default_rng(seed)
+    centres = rng.uniform(-10, 10, (k, d)).astype(np.float32)
+    C0 = (centres + rng.standard_normal((k, d), dtype=np.float32)).astype(np.float32)
+    return centres, C0
+
+
+def _km_rows(seed):
+    centres, _ = _km_centres(seed)
+
+    def gen(rng, rows):
+        lab = rng.integers(0, centres.shape[0], rows)
+        return [(centres[lab] + rng.standard_normal((rows, centres.shape[1]), dtype=np.float32)).astype(np.float32)]
+    return gen
+
+
+def _mlp_weights(seed, hidden=1024):
+    rng = np.random.default_rng(seed)
+    W1 = (rng.standard_normal((784, hidden), dtype=np.float32) / np.float32(np.sqrt(784))).astype(np.float32)
+    b1 = rng.uniform(-0.1, 0.1, hidden).astype(np.float32)
+    W2 = (rng.standard_normal((hidden, 10), dtype=np.float32) / np.float32(np.sqrt(hidden))).astype(np.float32)
+    b2 = rng.uniform(-0.1, 0.1, 10).astype(np.float32)
+    return [W1, b1, W2, b2]
+
+
+# name -> (global leading extent, rows per block, row generator factory,
+#          replicated-operand factory, input order: "S" sharded / "R" replicated)
+NAMED = {
+    "listing1": (1 << 24, 1 << 20, lambda s: (lambda rng, r: [rng.random(r), rng.random(r), rng.random(r)]),
+                 lambda s: [], "SSS"),
+    "blackscholes-f32": (1 << 28, 1 << 22, lambda s: _bs_rows(np.float32), lambda s: [], "SSS"),
+    "blackscholes-f64": (1 << 28, 1 << 22, lambda s: _bs_rows(np.float64), lambda s: [], "SSS"),
+    "rownorm": (65536, 1024,
+                lambda s: (lambda rng, r: [(rng.standard_normal((r, 4096), dtype=np.float32) * 2 + 5).astype(np.float32)]),
+                lambda s: [], "S"),
+    "mlp": (65536, 1024, lambda s: (lambda rng, r: [rng.random((r, 784), dtype=np.float32)]),
+            lambda s: _mlp_weights(s), "SRRRR"),
+    "kmeans": (1 << 26, 1 << 20, lambda s: _km_rows(s), lambda s: [_km_centres(s)[1]], "SR"),
+    "cumsum": (1 << 28, 1 << 22, lambda s: (lambda rng, r: [rng.standard_normal(r, dtype=np.float32)]),
+               lambda s: [], "S"),
+    "jacobi": (16384, 256, lambda s: (lambda rng, r: [rng.random((r, 16384), dtype=np.float32)]),
+               lambda s: [], "S"),
+}
+NAMED["rownorm-y"] = NAMED["rownorm"]
+
+
+def named_inputs(name, lo=0, hi=None, seed=42, threads=None):
+    """Rows [lo, hi) of the named-shape input of workload ``name`` (block
+    generated, see above), plus its replicated operands, in program order."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os as _os
+
+    n, blk, rows_f, rep_f, order = NAMED[name]
+    hi = n if hi is None else hi
+    gen = rows_f(seed)
+    b0, b1 = lo // blk, (hi + blk - 1) // blk
+    threads = threads or max(1, min(len(_os.sched_getaffinity(0)), 32))
+
+    def block(b):
+        parts = gen(np.random.default_rng([seed, b]), blk)
+        s, e = max(lo, b * blk) - b * blk, min(hi, (b + 1) * blk) - b * blk
+        return [p[s:e] for p in parts]
+
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        blocks = list(ex.map(block, range(b0, b1)))
+    sharded = [np.concatenate([bl[i] for bl in blocks]) if len(blocks) > 1 else np.ascontiguousarray(blocks[0][i])
+               for i in range(len(blocks[0]))]
+    rep = rep_f(seed)
+    out, si, ri = [], 0, 0
+    for c in order:
+        if c == "S":
+            out.append(sharded[si])
+            si += 1
+        else:
+            out.append(rep[ri])
+            ri += 1
+    return out

@@ -82,3 +82,42 @@ def test_two_ranks_one_gpu_partials():
                        env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     assert p.stdout.count(" ok (HostStagedComm)") == 2, p.stdout
+
+
+def test_sharded_plan_cache(dsess):
+    """Repeated sharded forces of one structure reuse the cached plan (one
+    classification + region pass) and stay exact on fresh data."""
+    import paper_1901_03771_b200 as gp
+    import paper_1901_03771_b200.distributed as D
+    rng = np.random.default_rng(12)
+    n0 = len(dsess._shard_cache)
+    for it in range(3):
+        x = rng.standard_normal((256, 64)).astype(np.float32)
+        gx = D.shard_rows(x, session=dsess)
+        y = (gx - gx.mean(1)[:, None])
+        tot, am = y.sum(), gx.argmax()
+        gp.force(tot, am)
+        ey = x - x.mean(1)[:, None]
+        assert np.asarray(tot) == ey.sum()
+        assert np.asarray(am) == x.argmax()
+    assert len(dsess._shard_cache) == n0 + 1
+
+
+def test_two_ranks_two_gpus_nccl():
+    """Two ranks on two distinct GPUs build a real NCCL communicator (never the
+    host-staged fallback); skipped on a one-GPU box."""
+    import subprocess
+    import sys
+    from paper_1901_03771_b200 import runtime
+    if runtime.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PYTHONPATH=root)
+    for k in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT", "GRUMPY_DEVICE"):
+        env.pop(k, None)
+    p = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+                        os.path.join(root, "tools", "two_rank_check.py")],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    assert p.stdout.count(" ok (NcclComm)") == 2, p.stdout
