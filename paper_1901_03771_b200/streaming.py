@@ -58,7 +58,7 @@ class DeviceView:
 
 
 class StreamPlan:
-    __slots__ = ("roots", "nodes", "leaves", "dist", "N", "rows")
+    __slots__ = ("roots", "nodes", "leaves", "dev_leaves", "dist", "N", "rows")
 
 
 def _walk(roots: Sequence[Node]):
@@ -105,10 +105,14 @@ def plan(roots: Sequence[Node], chunk_bytes: Optional[int] = None) -> Optional[S
     leaves = [f for f in host if f.shape[0] == N]
     if any(not l.data.host.flags.c_contiguous for l in leaves):
         return None
+    # device-resident operands with the streamed extent are chunked too (row
+    # views of their buffer, no copy); used at full size inside a chunk they
+    # would not match the chunk's rows
+    dev_leaves = [f for f in frontier if f.data.device is not None and f.shape and f.shape[0] == N]
     if N < 2 * ROW_ALIGN:
         return None
     try:
-        dist = D.classify(roots, sharded={l.id for l in leaves}, scans=True)
+        dist = D.classify(roots, sharded={l.id for l in leaves + dev_leaves}, scans=True)
     except LazyFuseError:
         return None
     root_ids = {r.id for r in roots}
@@ -120,8 +124,14 @@ def plan(roots: Sequence[Node], chunk_bytes: Optional[int] = None) -> Optional[S
         elif not (d.startswith("P:") and d[2:] in _COMBINE):
             return None
     for n in nodes:
-        if n.id not in root_ids and dist.get(n.id, "R")[0] in "PAC":
-            return None                      # a partial or carried scan consumed inside the region
+        if n.id in dist and dist[n.id][0] in "PAC" and n.id not in root_ids:
+            return None                      # a partial or carried scan inside the region
+        for q in n.preds:
+            if dist.get(q.id, "R")[0] in "PAC":
+                # a partial / carried scan (root or not) consumed inside the
+                # region: each chunk would read its chunk-local value, before
+                # the cross-chunk combine or carry
+                return None
     srows = [r for r in roots if dist[r.id] == "S" or dist[r.id].startswith("C:")]
     total = sum(l.data.nbytes for l in leaves) + sum(element_count(r.shape) * r.dtype.itemsize for r in srows)
     if total < MIN_BYTES:
@@ -132,6 +142,7 @@ def plan(roots: Sequence[Node], chunk_bytes: Optional[int] = None) -> Optional[S
         return None
     p = StreamPlan()
     p.roots, p.nodes, p.leaves, p.dist, p.N, p.rows = roots, nodes, leaves, dist, N, rows
+    p.dev_leaves = dev_leaves
     return p
 
 
@@ -228,6 +239,11 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
             for l in p.leaves:
                 rb = _row_bytes(l)
                 buf = TensorBuffer(l.dtype, (c,) + tuple(l.shape[1:]), device=DeviceView(dev_in[l.id], lo * rb, c * rb))
+                memo[l.id] = g.add_input(buf)
+            for l in p.dev_leaves:
+                rb = _row_bytes(l)
+                buf = TensorBuffer(l.dtype, (c,) + tuple(l.shape[1:]),
+                                   device=DeviceView(l.data.device, lo * rb, c * rb))
                 memo[l.id] = g.add_input(buf)
             for n in p.nodes:
                 if p.dist.get(n.id, "R") == "S" or n.id in parts or n.id in carried:

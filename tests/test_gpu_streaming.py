@@ -141,3 +141,34 @@ def test_scans_streamed_with_carry(sess, small_chunks):
     e2 = np.cumsum((xm * 2).astype(np.longdouble), axis=0)
     r2 = np.cumsum(xm * 2, axis=0)
     assert np.max(np.abs(g2 - e2)) <= 2 * np.max(np.abs(r2 - e2)) + 2.2e-16 * float(np.abs(e2).max())
+
+
+def test_streamed_with_device_operand(sess, small_chunks):
+    """x_host + y_device of the same extent: y is chunked as row views of its
+    device buffer; results equal NumPy's."""
+    rng = np.random.default_rng(31)
+    xh = rng.standard_normal((1 << 16, 4))
+    yh = rng.standard_normal((1 << 16, 4))
+    y = gp.asarray(yh)
+    gp.force(y * 1.0)
+    y.node.data.device = runtime.get().upload(yh)
+    k0 = sess.stats.streamed_chunks
+    (got,) = gp.materialize(gp.asarray(xh) * 2 + y)
+    assert sess.stats.streamed_chunks > k0
+    assert np.array_equal(got, xh * 2 + yh)
+
+
+def test_partial_and_carried_roots_read_by_other_roots(sess, small_chunks):
+    """materialize(t, x - t) with t = x.sum(0) and (s, s + a) with s a scan:
+    not streamed (the consumer needs the combined value) and exact."""
+    rng = np.random.default_rng(32)
+    xh = rng.standard_normal((1 << 16, 3))
+    x = gp.asarray(xh)
+    t = x.sum(0)
+    got_t, got_d = gp.materialize(t, x - t)
+    assert np.array_equal(got_t, xh.sum(0)) and np.array_equal(got_d, xh - xh.sum(0))
+    ah = rng.integers(-5, 5, 1 << 16)
+    a = gp.asarray(ah)
+    s = gp.cumsum(a * 2)
+    got_s, got_u = gp.materialize(s, s + a)
+    assert np.array_equal(got_s, np.cumsum(ah * 2)) and np.array_equal(got_u, np.cumsum(ah * 2) + ah)

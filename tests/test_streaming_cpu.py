@@ -66,3 +66,34 @@ def test_streamed_random_programs_do_stream(monkeypatch):
         finally:
             gp.set_default_session(old)
     assert streamed >= 8, streamed
+
+
+def test_partial_or_carried_root_read_by_another_root_is_ineligible():
+    """A partial (total) or carried scan that is itself a root but also read by
+    another root would feed each chunk its chunk-local value."""
+    x = gp.asarray(np.ones((4096, 3)))
+    t = x.sum(0)
+    assert streaming.plan([t.node, (x - t).node]) is None
+    a = gp.asarray(np.arange(65536.0))
+    s = gp.cumsum(a * 2)
+    assert streaming.plan([s.node, (s + a).node]) is None
+    assert streaming.plan([s.node, (a + 1).node]) is not None        # independent roots still stream
+
+
+class _FakeDev:
+    """Stands in for a device allocation (plan() only reads ptr/nbytes)."""
+
+    def __init__(self, nbytes):
+        self.ptr = 1 << 20
+        self.nbytes = nbytes
+
+
+def test_device_operand_with_streamed_extent_is_chunked():
+    """A device-resident operand of the streamed extent is a chunked leaf (a
+    row view of its buffer), not a full-size operand inside every chunk."""
+    xh = np.ones((65536, 4))
+    y = gp.asarray(np.ones((65536, 4)))
+    y.node.data.device = _FakeDev(y.node.data.nbytes)
+    y.node.data.host = None
+    p = streaming.plan([(gp.asarray(xh) + y).node])
+    assert p is not None and [l.id for l in p.dev_leaves] == [y.node.id] and p.dist[y.node.id] == "S"
