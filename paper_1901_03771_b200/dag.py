@@ -50,6 +50,8 @@ from .tensor import (
 
 
 class OpKind(enum.Enum):
+    __hash__ = object.__hash__   # members are singletons: identity hash (recording hot path)
+
     INPUT = "Input"
     MAP = "MapElementwise"
     CAST = "Cast"
@@ -68,6 +70,9 @@ class OpKind(enum.Enum):
 
 class ElemCode(enum.Enum):
     """Elementwise codes (SPEC.md:109-112 plus the NumPy ufuncs the drop-in needs)."""
+
+    __hash__ = object.__hash__   # members are singletons: identity hash (recording hot path)
+
 
     add = "add"
     sub = "sub"
@@ -150,13 +155,16 @@ CODE_OF_UFUNC["erf"] = ElemCode.erf  # scipy.special.erf
 class ReduceOp(enum.Enum):
     """Associative-commutative combine ops with identities."""
 
+    __hash__ = object.__hash__   # members are singletons: identity hash (recording hot path)
+
+
     sum = "sum"
     prod = "prod"
     max = "max"
     min = "min"
 
 
-@dataclasses.dataclass(frozen=True)
+@dataclasses.dataclass(frozen=True, eq=False)
 class Op:
     """An operation: kind plus immutable attributes.
 
@@ -180,6 +188,21 @@ class Op:
     code: Optional[ElemCode] = None
     attrs: Tuple[Any, ...] = ()
 
+    # structural equality with the hash computed once (plan-cache keys hash
+    # every op of a DAG signature on every force)
+    def __post_init__(self):
+        object.__setattr__(self, "_h", hash((self.kind, self.code, self.attrs)))
+
+    def __hash__(self):
+        return self._h
+
+    def __eq__(self, other):
+        if self is other:
+            return True
+        if other.__class__ is not Op:
+            return NotImplemented
+        return self._h == other._h and self.kind is other.kind and self.code is other.code and self.attrs == other.attrs
+
     def __repr__(self):
         if self.kind is OpKind.MAP:
             if self.code is ElemCode.const_splat:
@@ -198,6 +221,7 @@ def const_op(value) -> Op:
 
 
 _ids = itertools.count()
+_MAP_INFER: dict = {}
 
 
 class Node:
@@ -214,7 +238,7 @@ class Node:
         self.id = next(_ids)
         self.op = op
         self.preds: Tuple[Node, ...] = tuple(preds)
-        self.pred_ids = tuple(p.id for p in self.preds)
+        self.pred_ids = tuple([p.id for p in self.preds])
         self.shape = shape
         self.dtype = dtype
         self.loop = loop
@@ -475,8 +499,22 @@ class Graph:
         return self._append(Node(const_op(value), (), tuple(shape), dtype))
 
     def add_op(self, op: Op, preds: Sequence[Node]) -> Node:
-        """Append an unmaterialized node with inferred shape/dtype."""
-        shape, dtype, loop = infer(op, [p.shape for p in preds], [p.dtype for p in preds])
+        """Append an unmaterialized node with inferred shape/dtype.
+
+        Inference is a pure function of (op, operand shapes, operand dtypes),
+        so elementwise results are memoised: re-recording a loop body costs a
+        dictionary hit per op instead of broadcasting and loop resolution."""
+        if op.kind is OpKind.MAP:
+            key = (op, tuple([p.shape for p in preds]), tuple([p.dtype for p in preds]))
+            hit = _MAP_INFER.get(key)
+            if hit is None:
+                hit = infer(op, key[1], key[2])
+                if len(_MAP_INFER) > 65536:
+                    _MAP_INFER.clear()
+                _MAP_INFER[key] = hit
+            shape, dtype, loop = hit
+        else:
+            shape, dtype, loop = infer(op, [p.shape for p in preds], [p.dtype for p in preds])
         return self._append(Node(op, preds, shape, dtype, loop=loop))
 
     @staticmethod

@@ -310,7 +310,8 @@ def elementwise(code: ElemCode, *args, sess: Optional[Session] = None) -> "ndarr
         if t is ndarray:
             preds.append(a._node)
         elif t in _WEAK:
-            _check_int_range(a, lt)
+            if t is int:
+                _check_int_range(a, lt)
             preds.append(sess.const(a, lt))
         else:
             preds.append(_as_node(a, sess))

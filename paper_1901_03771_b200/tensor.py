@@ -31,6 +31,8 @@ Shape = Tuple[int, ...]
 class DType(enum.Enum):
     """Element type tag (SPEC.md:26-30)."""
 
+    __hash__ = object.__hash__   # members are singletons: identity hash (recording hot path)
+
     f32 = "f32"
     f64 = "f64"
     i32 = "i32"
