@@ -576,7 +576,8 @@ def run_grumpy(args, dist):
                      "compute": _compute_roofline(w, rows, kmean, clk)},
         "step_breakdown_ms": {"kernels": kernel_ms_step, "collectives": coll_ms_step,
                               "device_step": my_ms / args.steps,
-                              "host_issue": host_issue_s * 1e3 / args.steps},
+                              "host_issue": host_issue_s * 1e3 / args.steps,
+                              "per_launch": {f"{f}:{l}": statistics.mean(v) for (f, l), v in by_label.items()}},
         "rows_per_gpu": rows,
         "gpu_launches": launches,
         "collectives_in_timed_region": collectives,

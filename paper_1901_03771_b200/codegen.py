@@ -1021,6 +1021,9 @@ def generate(region: Region) -> KernelSource:
     """Pick the kernel family for a region and emit its source."""
     from . import codegen_rows
     kinds = {n.op.kind for n in region.nodes}
+    if OpKind.MATMUL in kinds:
+        # a skinny product as the prologue of its consumers' row kernel
+        return codegen_rows.gen_rows(region)
     if OpKind.SCAN in kinds:
         from . import codegen_scan
         return codegen_scan.generate(region)

@@ -68,6 +68,45 @@ SMALL_RECOMPUTE = 64   # a reduction re-evaluated per column may reduce at most 
 MAX_GRID = 148 * 16    # grid cap for kernels with per-CTA partial slots (keyed sums)
 
 
+# Skinny products z = A @ B (A [R, K] streamed, B [K, N] small) computed as
+# the first stage of their consumers' row kernel (gr_skinny.cuh) instead of a
+# cuBLAS call whose output the consumers read back (C4 layer 2 + softmax).
+SKINNY = os.environ.get("GRUMPY_SKINNY", "1") == "1"
+SKINNY_MAX_N = 16
+SKINNY_MIN_ROWS = 4096
+# "<B placement>,<threads per CTA>,<rows per thread>,<stages>".  MLP layer 2
+# (65536 x 1024 @ 1024 x 10 + softmax + argmax, tools/skinny_sweep.sh):
+# cbank,64,1,3 102 us (LDCU latency: 71% short-scoreboard stalls); cbank
+# 64,2,3 97; smem,64,2,3 78; smem,128,1,3 76; smem,64,4,2 65; smem,128,2,2
+# 58.5 us (256-row boxes, 2 CTAs/SM) — against cuBLAS SIMT 111 + R2 9 us.
+_SK = os.environ.get("GRUMPY_SKINNY_CFG", "smem,128,2,2").split(",")
+SKINNY_B = _SK[0]          # B's k-pairs: "cbank" (64-bit uniform operands) or "smem" (broadcast LDS)
+SKINNY_BLOCK = int(_SK[1])  # threads per CTA
+SKINNY_RT = int(_SK[2])    # rows per thread (each B operand feeds RT rows)
+SKINNY_STAGES = int(_SK[3])  # TMA boxes in flight per CTA
+SKINNY_CBANK_BYTES = 48 * 1024
+
+
+def skinny_ok(n: Node) -> bool:
+    """Planner hook: may the product ``n`` be the in-kernel prologue of its
+    consumers' row region (rather than a library step)?"""
+    if not SKINNY or n.kind is not OpKind.MATMUL or len(n.preds) != 2:
+        return False
+    a, b = n.preds
+    if a.dtype is not DType.f32 or b.dtype is not DType.f32 or len(a.shape) != 2 or len(b.shape) != 2:
+        return False
+    if any(p.kind is OpKind.TRANSPOSE and not p.is_materialized for p in (a, b)):
+        return False                      # transposed operands keep the library's trans flags
+    R, K = a.shape
+    N = b.shape[1]
+    return (R >= SKINNY_MIN_ROWS and K >= 32 and K % 32 == 0 and 0 < N <= SKINNY_MAX_N
+            and K * N * 4 <= SKINNY_CBANK_BYTES and R < 2 ** 31)
+
+
+def _skinny_nodes(region: Region) -> List[Node]:
+    return [n for n in region.nodes if n.kind is OpKind.MATMUL and n.id not in region.leaf_ids]
+
+
 class CBankMiss(Exception):
     """A leaf staged in constant memory is read at a row-dependent offset."""
 
@@ -153,6 +192,8 @@ class LoopEmitter(ValueEmitter):
         self.pair_loops = False
         self.half: Optional[Var] = None
         self.pairs = set()            # emitted names holding a gr::f2
+        # skinny product computed by the tile prologue: (canonical id, row key)
+        self.skinny: Optional[tuple] = None
 
     # -- scopes ------------------------------------------------------------------
     def emit(self, level, ctype, expr):
@@ -293,6 +334,8 @@ class LoopEmitter(ValueEmitter):
     # -- reductions -------------------------------------------------------------------
     def _value(self, n: Node, coords):
         if n.id not in self.leaf_index:
+            if n.kind is OpKind.MATMUL:
+                return self.skinny_value(n, coords)
             if n.kind is OpKind.REDUCE:
                 return self.reduce(n, coords)
             if n.kind is OpKind.ARGREDUCE:
@@ -301,6 +344,18 @@ class LoopEmitter(ValueEmitter):
                     and any(c.coef(self.half) for c in coords)):
                 return self._pair_map(n, coords)
         return super()._value(n, coords)
+
+    def skinny_value(self, n: Node, coords):
+        """z[row, j] of the region's skinny product: register zk[j] filled by
+        the CTA's tile prologue (gr::Skinny) before the row body runs."""
+        if self.skinny is None or self.cid(n) != self.skinny[0]:
+            raise NotFusable(n, "one skinny product per row region")
+        if coords[0].key() != self.skinny[1]:
+            raise NotFusable(n, "skinny product read at another row")
+        col = coords[1]
+        if self.half is not None and col.coef(self.half):
+            raise NotPairable("skinny product read in a paired loop")
+        return f"zk[{col.c()}]", max(col.level, 1)
 
     # -- paired loops ---------------------------------------------------------------
     def emit_pair(self, level, expr) -> str:
@@ -644,9 +699,25 @@ def thread_space(region: Region):
         if n.id not in tot_ids and is_total(n):
             raise NotFusable(n, "a full reduction consumed inside the region")
     keyed = [r for r in region.roots if r.kind is OpKind.KEYED_SUM]
+    mms = _skinny_nodes(region)
+    if mms:
+        for m in mms:
+            if not skinny_ok(m) or any(p.id not in region.leaf_ids for p in m.preds):
+                raise NotFusable(m, "product is not a skinny prologue")
+        if keyed or len({m.preds[0].shape[0] for m in mms}) != 1:
+            raise NotFusable(mms[0], "skinny product with keyed sums / other row spaces")
+        Rm = (mms[0].preds[0].shape[0],)
+        if not reds:
+            for t in totals:
+                if t.kind is OpKind.REDUCE and t.op.attrs[0] is ReduceOp.sum and t.dtype.is_float:
+                    C = element_count(t.preds[0].shape[1:]) if len(t.preds[0].shape) >= 1 else 1
+                    if not rows_tile_pairwise(Rm[0], C):
+                        raise NotFusable(mms[0], "total does not split on row boundaries")
+            return Rm, totals, None
     if keyed and not reds:
         return tuple(keyed[0].preds[0].shape), totals, None
-    if len(reds) == 1 and reds[0] in region.roots and len(region.roots) == 1 + len(totals) and not totals:
+    if (len(reds) == 1 and reds[0] in region.roots and len(region.roots) == 1 + len(totals) and not totals
+            and not mms):
         # a lone reduction root: one thread per output element, loops over the
         # reduced axes in NumPy order (covers sum(axis=0) and middle axes)
         return tuple(reds[0].shape), totals, None
@@ -679,6 +750,8 @@ def thread_space(region: Region):
                     raise NotFusable(_blame(region, reds[0]),
                                      f"total over {R}x{C} does not split on row boundaries")
         virtual = None
+        if mms and tuple(Ts) != Rm:
+            raise NotFusable(mms[0], f"skinny product rows {Rm} differ from the region's rows {Ts}")
     else:
         # maps + totals: rows are the subtrees of NumPy's pairwise tree over the
         # flattened space at depth D, so per-row partials combined by a
@@ -773,6 +846,13 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
     Ts, totals, virtual = thread_space(region)
     tot_ids = {t.id for t in totals}
     R = element_count(Ts)
+    mms = _skinny_nodes(region)
+    if mms:
+        block, RT = SKINNY_BLOCK, SKINNY_RT
+        mm = mms[0]
+        ai, bi = region.leaves.index(mm.preds[0]), region.leaves.index(mm.preds[1])
+        KD, NZ = mm.preds[0].shape[1], mm.preds[1].shape[1]
+        cbank = {k: v for k, v in cbank.items() if k != mm.preds[1].id}
     em = LoopEmitter(region, cbank=cbank)
     em.pair_loops = pair
     rvar = Var("r", 1)
@@ -800,6 +880,11 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
         if D:
             em.stmt(1, f"for (int d = {D - 1}; d >= 0; --d) {{ const long long h = vn / 2, n2 = h - h % 8; "
                        f"if ((r >> d) & 1) {{ vo += n2; vn -= n2; }} else {{ vn = n2; }} }}")
+
+    if mms:
+        if virtual is not None or len(Ts) != 1:
+            raise NotFusable(mms[0], "skinny product outside a 1-D row space")
+        em.skinny = (em.cid(mms[0]), row_coords[0].key())
 
     def full_root_coords(shape):
         """Open loops over the columns of a root of ``shape`` (shape[:len(Ts)] == Ts)."""
@@ -958,8 +1043,11 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
             scratch_off += ((MAX_GRID * NBj * 8 + 255) // 256) * 256
             kmeta.append((j, r, NBj, off))
 
+    if mms and kmeta:
+        raise NotFusable(mms[0], "skinny product with keyed sums")
     lines = ["static __device__ __forceinline__ void row(const Params& p, const long long r, const bool valid"
-             + "".join(f", {r.dtype.ctype}* khist{j}" for j, r, _, _ in kmeta) + ") {",
+             + "".join(f", {r.dtype.ctype}* khist{j}" for j, r, _, _ in kmeta)
+             + (f", const float (&zk)[{NZ}]" if mms else "") + ") {",
              "  (void)valid;"]
     lines += ["  " + c for c in em.consts]
     lines += render(em.row, 1)
@@ -985,13 +1073,57 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
                       f"    const int lo = (i / {B}) * {2 * B} + i % {B};\n"
                       f"    dst[i] = (unsigned long long)__float_as_uint(src[lo]) | ((unsigned long long)__float_as_uint(src[lo + {B}]) << 32);\n"
                       "  }\n}\n")
-    src = [HEADER, '#include "gr_reduce.cuh"\n', cdecl, "struct K {", params,
+    inc = '#include "gr_reduce.cuh"\n'
+    if mms:
+        # A by TMA (tensor map first in the parameter block), B as k-pairs in
+        # the constant bank written by a one-CTA repack kernel of the module
+        params = params.replace("  struct Params {\n", "  struct Params {\n    gr::TMap tmap0;\n", 1)
+        inc += '#include "gr_tma.cuh"\n#include "gr_skinny.cuh"\n'
+        psym, npairs = f"gr_skb{bi}_p", KD * NZ // 2
+        cdecl += (f"__constant__ unsigned long long {psym}[{npairs}];\n"
+                  f'extern "C" __global__ void gr_repack{bi}(const float* __restrict__ src, unsigned long long* dst) {{\n'
+                  f"  for (int i = threadIdx.x; i < {npairs}; i += blockDim.x) {{\n"
+                  f"    const int lo = (i / {NZ}) * {2 * NZ} + i % {NZ};\n"
+                  f"    dst[i] = (unsigned long long)__float_as_uint(src[lo]) | ((unsigned long long)__float_as_uint(src[lo + {NZ}]) << 32);\n"
+                  "  }\n}\n")
+        if SKINNY_B == "cbank":
+            used_pair.append((bi, psym, NZ, npairs, f"gr_repack{bi}"))
+    src = [HEADER, inc, cdecl, "struct K {", params,
            f"  static constexpr long long NROWS = {R}LL;"]
     src.append("  " + "\n  ".join(lines))
     src.append("};")
     kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
             "  const long long stride = (long long)gridDim.x * blockDim.x;"]
-    if kmeta:
+    skinny_smem = 0
+    if mms:
+        S_ = SKINNY_STAGES
+        kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const __grid_constant__ K::Params p) {{',
+                "  const long long stride = (long long)gridDim.x * blockDim.x;"]
+        if SKINNY_B == "smem" or S_ * block * RT * 128 > 40 * 1024:
+            skinny_smem = S_ * block * RT * 128 + (KD * NZ * 4 if SKINNY_B == "smem" else 0) + 1024 + 64
+            kern += ["  extern __shared__ unsigned char gr_dyn[];",
+                     "  float* gr_ring = reinterpret_cast<float*>(gr_dyn + ((1024u - (gr::smem_u32(gr_dyn) & 1023u)) & 1023u));",
+                     f"  unsigned long long* gr_bs = reinterpret_cast<unsigned long long*>(gr_ring + {S_ * block * RT * 32});",
+                     f"  unsigned long long* gr_full = gr_bs + {KD * NZ // 2 if SKINNY_B == 'smem' else 0};"]
+            if SKINNY_B == "smem":
+                kern.append(f"  gr::Skinny<{block}, {KD}, {NZ}, {S_}, {RT}>::load_pairs(gr_bs, p.in{bi});")
+            bsrc = "gr_bs" if SKINNY_B == "smem" else psym
+        else:
+            kern += [f"  __shared__ __align__(1024) float gr_ring[{S_ * block * RT * 32}];",
+                     f"  __shared__ __align__(8) unsigned long long gr_full[{S_}];"]
+            bsrc = psym
+        kern += [f"  gr::Skinny<{block}, {KD}, {NZ}, {S_}, {RT}> sk;",
+                 "  sk.init(gr_ring, gr_full, &p.tmap0, K::NROWS);",
+                 f"  for (long long base = (long long)blockIdx.x * {block * RT}; base < K::NROWS; base += stride * {RT}) {{",
+                 f"    float zk[{RT}][{NZ}];",
+                 f"    sk.tile(zk, {bsrc});",
+                 "#pragma unroll",
+                 f"    for (int j = 0; j < {RT}; ++j) {{",
+                 f"      const long long r = base + threadIdx.x + j * {block};",
+                 "      if (r < K::NROWS) K::row(p, r, true, zk[j]);",
+                 "    }",
+                 "  }"]
+    elif kmeta:
         for j, r, NBj, off in kmeta:
             kern.append(f"  __shared__ {r.dtype.ctype} khist{j}[{warps * NBj}];")
             kern.append(f"  for (int i = threadIdx.x; i < {warps * NBj}; i += blockDim.x) khist{j}[i] = 0;")
@@ -1043,10 +1175,13 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
     return KernelSource("rows", "\n".join(src) + "\n", kname,
                         leaf_slots=list(range(len(region.leaves))),
                         root_slots=list(range(len(region.roots))),
-                        block=block, groups=R, vec=1, unroll=1, scratch_bytes=scratch_off,
+                        block=block, groups=R, vec=1, unroll=RT if mms else 1, scratch_bytes=scratch_off,
                         meta={"rows": R, "row_shape": Ts, "totals": len(tot_meta), "ticket": bool(tot_meta or kmeta),
                               "virtual": virtual, "block_pow2": True, "keyed": len(kmeta),
-                              "max_grid": MAX_GRID if kmeta else None, "cbank": used_cb, "cbank_pair": used_pair})
+                              "max_grid": MAX_GRID if kmeta else None, "cbank": used_cb, "cbank_pair": used_pair,
+                              "tmaps": [(ai, KD, R, 32, block * RT, 128)] if mms else [],
+                              "skinny": (KD, NZ, SKINNY_B, block, RT, SKINNY_STAGES) if mms else None,
+                              **({"smem": skinny_smem} if skinny_smem else {})})
 
 
 def _row_partial(em: LoopEmitter, x: Node, rop, T: DType, row_coords, cols):

@@ -36,6 +36,7 @@ class Executor:
         self.launch_log = collections.deque(maxlen=4096)  # (family, kernel name) per launch
         self.profile = None           # per-launch CUDA events when enabled
         self._tickets = {}
+        self._tmaps = {}
         self.out_bind: Dict[int, TensorBuffer] = {}   # root id -> preallocated output (streaming.py)
 
     # -- planner hook ---------------------------------------------------------------
@@ -195,6 +196,15 @@ class Executor:
                 self._tickets[("redo", id(ks))] = rd
             ptrs.append(rd.ptr)
         params = runtime.pack_params(ptrs)
+        tm = ks.meta.get("tmaps")
+        if tm:
+            # TMA tensor maps lead the parameter block (alignas(64) gr::TMap
+            # members first in K::Params); the block is padded to the struct's
+            # 64-byte alignment
+            maps = b"".join(self._tensor_map(ptrs[i], leaves[i].dtype, d0, d1, b0, b1, sw)
+                            for i, d0, d1, b0, b1, sw in tm)
+            params = maps + params
+            params += b"\0" * (-len(params) % 64)
         if self.profile is not None:
             e0, e1 = self._event_pair()
             self.rt.record(e0)
@@ -209,6 +219,16 @@ class Executor:
         # later launches on the same stream
         del scratch
         return outs
+
+    def _tensor_map(self, ptr, dtype, d0, d1, b0, b1, sw) -> bytes:
+        """128-byte CUtensorMap of a row-major [d1][d0] leaf (cached per buffer)."""
+        key = (ptr, dtype, d0, d1, b0, b1, sw)
+        m = self._tmaps.get(key)
+        if m is None:
+            if len(self._tmaps) > 256:
+                self._tmaps.clear()
+            m = self._tmaps[key] = self.rt.tensor_map_2d(ptr, dtype, d0, d1, d0 * dtype.itemsize, b0, b1, sw)
+        return m
 
     # -- optional per-launch device timing (bench.py) ----------------------------------
     def enable_profile(self):

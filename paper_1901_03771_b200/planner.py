@@ -139,7 +139,7 @@ def library_operands(n: Node):
 def _kernel_kind(root: Node) -> str:
     if root.kind is OpKind.SCAN:
         return "MapScan"
-    if root.kind in REDUCTION_KINDS or root.kind is OpKind.KEYED_SUM:
+    if root.kind in REDUCTION_KINDS or root.kind in (OpKind.KEYED_SUM, OpKind.MATMUL):
         return "MapReduce"
     return "Map"
 
@@ -366,18 +366,21 @@ def _gemm_epilogue(n: Node, consumers, root_ids):
     return a, [a], bias, "bias"
 
 
-def plan_regions(roots: Sequence[Node], row_fusion=None, check=None, epilogues: bool = False) -> List[PlanStep]:
+def plan_regions(roots: Sequence[Node], row_fusion=None, check=None, epilogues: bool = False,
+                 skinny=None) -> List[PlanStep]:
     """B200 region planner (module docstring).
 
     ``row_fusion(reduction, consumer)`` proposes keeping a reduction inside its
-    consumer's kernel (None: every reduction is its own step).  ``check(step)``
+    consumer's kernel (None: every reduction is its own step).  ``skinny(n)``
+    proposes computing a small-N product inside its consumers' row kernel
+    instead of a library step (the code generator may still refuse it).  ``check(step)``
     is the code generator's verdict; when it raises an exception carrying
     ``.node`` that node becomes a materialization point and planning repeats.
     """
     extra: Set[int] = set()
     solo: Set[int] = set()
     for _ in range(256):
-        steps = _plan_once(roots, row_fusion, extra, check, solo, epilogues)
+        steps = _plan_once(roots, row_fusion, extra, check, solo, epilogues, skinny)
         if check is None:
             return steps
         bad = None
@@ -407,7 +410,7 @@ def plan_regions(roots: Sequence[Node], row_fusion=None, check=None, epilogues: 
 
 
 def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=frozenset(),
-               epilogues: bool = False) -> List[PlanStep]:
+               epilogues: bool = False, skinny=None) -> List[PlanStep]:
     roots = [r for r in dict((r.id, r) for r in roots).values() if not r.is_materialized]
     if not roots:
         return []
@@ -433,9 +436,12 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=f
     root_ids = set(points)
     epi: Dict[int, tuple] = {}          # epilogue root id -> (gemm, chain, bias, kind)
     absorbed: Set[int] = set()
+    def is_skinny(n):
+        return skinny is not None and n.id not in extra and not n.is_materialized and skinny(n)
+
     if epilogues:
         for n in demand.values():
-            if not n.is_materialized and n.id not in extra:
+            if not n.is_materialized and n.id not in extra and not is_skinny(n):
                 e = _gemm_epilogue(n, consumers, root_ids)
                 if e is not None and not any(c.id in extra for c in e[1][:-1]):
                     epi[e[0].id] = (n,) + e[1:]
@@ -453,6 +459,12 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=f
             continue
         if n.id in absorbed:
             continue
+        if n.kind in LIBRARY_KINDS:
+            # operands of a product are in memory (library call or TMA stream)
+            ops, _, _ = library_operands(n) if not is_skinny(n) else (list(n.preds), None, None)
+            for p in ops:
+                if not p.is_materialized:
+                    points[p.id] = p
         if n.id in extra:
             points[n.id] = n
             continue
@@ -463,11 +475,8 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=f
             # materialized — one kernel per sweep
             points[n.id] = n
         if n.kind in LIBRARY_KINDS:
-            points[n.id] = n
-            ops, _, _ = library_operands(n)
-            for p in ops:
-                if not p.is_materialized:
-                    points[p.id] = p
+            if not is_skinny(n):
+                points[n.id] = n
         elif n.kind in (OpKind.SCAN, OpKind.KEYED_SUM):
             points[n.id] = n
         elif n.kind in REDUCTION_KINDS:
@@ -490,7 +499,7 @@ def _plan_once(roots: Sequence[Node], row_fusion, extra: Set[int], check, solo=f
             st.epilogue = (kind, bias)
             cones.append(st)
             continue
-        if p.kind in LIBRARY_KINDS:
+        if p.kind in LIBRARY_KINDS and not is_skinny(p):
             ops, trans, call = library_operands(p)
             cones.append(PlanStep("Library", [p], [p], [o for o in ops], call=call, trans_flags=trans, operands=ops))
             continue

@@ -102,9 +102,9 @@ class Session:
                         steps.append(st)
                         done.add(st.root.id)
             return steps
-        from . import codegen
+        from . import codegen, codegen_rows
         return _planner.plan_regions(roots, row_fusion=codegen.row_fusable, check=codegen.check_step,
-                                     epilogues=GEMM_EPILOGUES)
+                                     epilogues=GEMM_EPILOGUES, skinny=codegen_rows.skinny_ok)
 
     def const(self, value, dtype: DType) -> Node:
         """Interned rank-0 const_splat node (constants are immutable)."""

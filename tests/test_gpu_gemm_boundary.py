@@ -102,3 +102,71 @@ def test_emulated_gemm_special_values(sess):
     assert np.max(np.abs(got[fin] - exp[fin]) / np.abs(exp[fin])) < 4 * np.finfo(np.float32).eps
     sub = np.isfinite(exp) & (np.abs(exp) <= 1e-37)
     assert np.max(np.abs(got[sub] - exp[sub])) < 1e-44 * 32    # a few subnormal ulps
+
+
+def _skinny_ref(A, B):
+    """float64 product and its |A||B| scale (the tolerance's sum of |terms|)."""
+    return A.astype(np.float64) @ B.astype(np.float64), np.abs(A).astype(np.float64) @ np.abs(B).astype(np.float64)
+
+
+@pytest.mark.parametrize("R,K,N", [(8192, 256, 10), (4096 + 37, 32, 16), (5000, 1024, 1), (65536, 1024, 10)])
+def test_skinny_product_forced(sess, R, K, N):
+    """z = A @ B with B small: one row kernel (TMA-streamed A, constant-bank
+    B), no library call; |z - z64| <= 2K eps32 sum|a||b| (fp32 FMA chains)."""
+    rng = np.random.default_rng(R + K + N)
+    A = rng.standard_normal((R, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    z = gp.asarray(A) @ gp.asarray(B)
+    got = np.asarray(z)
+    assert sess.stats.library_calls == 0 and sess.stats.kernels_executed == 1
+    e, sc = _skinny_ref(A, B)
+    assert np.all(np.abs(got - e) <= 2 * K * 6e-8 * sc)
+
+
+def test_skinny_product_with_row_consumers(sess):
+    rng = np.random.default_rng(5)
+    A = rng.standard_normal((8192, 128)).astype(np.float32)
+    B = rng.standard_normal((128, 7)).astype(np.float32)
+    b = rng.standard_normal(7).astype(np.float32)
+    ga = gp.asarray(A)
+    z = ga @ gp.asarray(B) + gp.asarray(b)
+    m = z.max(1)
+    y = gp.maximum(z, 0) * 2.0
+    am = z.argmax(1)
+    gp.force(m, y, am)
+    assert sess.stats.library_calls == 0
+    e = A.astype(np.float64) @ B.astype(np.float64) + b
+    _, sc = _skinny_ref(A, B)
+    tol = 2 * 128 * 6e-8 * (sc + np.abs(b))
+    assert np.all(np.abs(np.asarray(m) - e.max(1)) <= tol.max(1))
+    assert np.all(np.abs(np.asarray(y) - np.maximum(e, 0) * 2) <= 2 * tol)
+    lab = np.asarray(am)
+    srt = np.sort(e, axis=1)
+    clear = (srt[:, -1] - srt[:, -2]) > 2 * tol.max(1)
+    assert np.array_equal(lab[clear], e.argmax(1)[clear])
+
+
+def test_mlp_layer2_fused(sess):
+    """C4 at batch 8192: layer 1 = one cuBLASLt GEMM with the RELU_BIAS
+    epilogue, layer 2 + b2 + softmax + argmax = one hand-written row kernel."""
+    X, W1, b1, W2, b2 = wl.mlp_inputs(batch=8192, hidden=1024)
+    p, lab = wl.mlp(gp, *[gp.asarray(a) for a in (X, W1, b1, W2, b2)])
+    gp.force(p, lab)
+    assert sess.stats.library_calls == 1 and sess.stats.kernels_executed == 1
+    ep, elab = wl.mlp(np, X, W1, b1, W2, b2)
+    assert np.max(np.abs(np.asarray(p) - ep)) <= 1e-5
+    assert np.array_equal(np.asarray(lab), elab)
+
+
+def test_skinny_disabled_matches(sess, monkeypatch):
+    from paper_1901_03771_b200 import codegen_rows
+    rng = np.random.default_rng(9)
+    A = rng.standard_normal((8192, 64)).astype(np.float32)
+    B = rng.standard_normal((64, 3)).astype(np.float32)
+    z1 = np.asarray(gp.asarray(A) @ gp.asarray(B))
+    monkeypatch.setattr(codegen_rows, "SKINNY", False)
+    s2 = gp.Session()
+    z2 = np.asarray(gp.asarray(A, session=s2) @ gp.asarray(B, session=s2))
+    assert s2.stats.library_calls == 1
+    e, sc = _skinny_ref(A, B)
+    assert np.all(np.abs(z1 - e) <= 2 * 64 * 6e-8 * sc) and np.all(np.abs(z2 - e) <= 2 * 64 * 6e-8 * sc)

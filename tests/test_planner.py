@@ -213,3 +213,41 @@ def test_gemm_epilogue_absorption(sess):
     tmpl = planner.make_template(steps, order)
     again = planner.instantiate(tmpl, order)
     assert again[0].epilogue[0] == "relu_bias" and again[0].epilogue[1] is steps[0].epilogue[1]
+
+
+def test_skinny_product_plans_inside_the_row_region(sess):
+    """C4 layer 2 at the config batch: h @ W2 (N = 10) + b2 + softmax + argmax
+    is ONE fused row step after the layer-1 library call (gr_skinny.cuh
+    prologue); below the row threshold it stays a library step."""
+    from paper_1901_03771_b200 import codegen_rows
+    X, W1, b1, W2, b2 = wl.mlp_inputs(batch=8192, hidden=256)
+    args = [gp.asarray(a) for a in (X, W1, b1, W2, b2)]
+    p, lab = wl.mlp(gp, *args)
+    steps = planner.plan_regions([p.node, lab.node], row_fusion=codegen.row_fusable, check=codegen.check_step,
+                                 epilogues=True, skinny=codegen_rows.skinny_ok)
+    assert [(s.kind, s.epilogue[0] if s.epilogue else None) for s in steps] == [("Library", "relu_bias"),
+                                                                                 ("Fused", None)]
+    fused = steps[1]
+    assert any(n.kind is OpKind.MATMUL for n in fused.nodes)
+    region = codegen.canonicalize(codegen.Region(fused.roots, fused.leaves, fused.nodes))
+    ks = codegen.generate(region)
+    assert ks.meta["skinny"][:2] == (256, 10) and ks.meta["tmaps"] and ks.block == codegen_rows.SKINNY_BLOCK
+    assert "gr::Skinny<" in ks.source and "__grid_constant__" in ks.source
+    small = [gp.asarray(a) for a in wl.mlp_inputs(batch=1024, hidden=256)]
+    p2, lab2 = wl.mlp(gp, *small)
+    st2 = planner.plan_regions([p2.node, lab2.node], row_fusion=codegen.row_fusable, check=codegen.check_step,
+                               epilogues=True, skinny=codegen_rows.skinny_ok)
+    assert [s.kind for s in st2] == ["Library", "Library", "Fused"]
+
+
+def test_skinny_ineligible_shapes(sess):
+    from paper_1901_03771_b200 import codegen_rows
+    A = gp.asarray(np.ones((8192, 100), np.float32))      # K not a multiple of 32
+    B = gp.asarray(np.ones((100, 4), np.float32))
+    assert not codegen_rows.skinny_ok((A @ B).node)
+    A2 = gp.asarray(np.ones((8192, 64), np.float32))
+    B2 = gp.asarray(np.ones((64, 17), np.float32))        # N > 16
+    assert not codegen_rows.skinny_ok((A2 @ B2).node)
+    B3 = gp.asarray(np.ones((64, 16), np.float64))        # f64
+    assert not codegen_rows.skinny_ok((A2 @ B3).node)
+    assert codegen_rows.skinny_ok((A2 @ gp.asarray(np.ones((64, 16), np.float32))).node)
