@@ -13,119 +13,68 @@ import pytest
 import paper_1901_03771_b200 as gp
 from paper_1901_03771_b200 import workloads as wl
 from oracle import eager
+from random_programs import GP, Numpy, make_program
 
 pytestmark = pytest.mark.gpu
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 NPROG = int(os.environ.get("GRUMPY_RANDOM_PROGRAMS", "120"))
 
 
-def _rand_shape(rng, rank):
-    return tuple(int(rng.integers(1, 17)) for _ in range(rank))
-
-
-def make_program(seed):
-    rng = np.random.default_rng(seed)
-    rank = int(rng.integers(1, 4))
-    shape = _rand_shape(rng, rank)
-    dt = rng.choice([np.float32, np.float64, np.int32, np.int64])
-    pool = []
-    for _ in range(int(rng.integers(1, 4))):
-        s = list(shape)
-        if rng.random() < 0.3:          # broadcastable operand
-            s[int(rng.integers(0, rank))] = 1
-        a = rng.standard_normal(s) * 4 if np.dtype(dt).kind == "f" else rng.integers(-20, 20, s)
-        pool.append(gp.asarray(np.asarray(a, dtype=dt)))
-    depth = int(rng.integers(1, 13))
-    cur = pool[0]
-    transcendental = False   # exp is ulp-accurate, not bit-exact: no branching on it afterwards
-    viewed = False
-    for _ in range(depth):
-        k = rng.integers(0, 14)
-        other = pool[int(rng.integers(0, len(pool)))]
-        try:
-            if k == 0:
-                cur = cur + other
-            elif k == 1:
-                cur = cur * other - 1
-            elif k == 2:
-                cur = gp.maximum(cur, other)
-            elif k == 3 and cur.dtype.kind == "f":
-                cur = gp.exp(cur * 0.1) + gp.sqrt(gp.abs(cur))
-                transcendental = True
-            elif k == 4 and not transcendental:
-                cur = gp.where(cur > other, cur, other * 2)
-            elif k == 5 and cur.ndim >= 2:
-                cur = cur.transpose()
-                viewed = True
-            elif k == 6 and cur.ndim >= 1 and cur.shape[-1] > 2:
-                cur = cur[..., 1:] if rng.random() < 0.5 else cur[..., ::2]
-                viewed = True
-            elif k == 7 and cur.ndim >= 2:
-                cur = cur.reshape(-1, cur.shape[-1])
-            elif k == 8 and cur.ndim >= 2:
-                ax = int(rng.integers(0, cur.ndim))
-                cur = cur.sum(axis=ax, keepdims=bool(rng.random() < 0.5))
-                # NumPy reduces a strided view in memory order, the kernel in C
-                # order: same value up to reassociation, so not bit-exact
-                transcendental = transcendental or (viewed and cur.dtype.kind == "f")
-            elif k == 9 and cur.ndim >= 1:
-                ax = int(rng.integers(0, cur.ndim))
-                cur = cur.max(axis=ax) if rng.random() < 0.5 else cur.min(axis=ax)
-            elif k == 10 and cur.ndim >= 1:
-                cur = cur.astype(np.float64) / 3
-            elif k == 11 and cur.ndim == 2 and cur.dtype.kind == "f":
-                # np.dot boundary: GEMM, optionally + bias row and ReLU (the
-                # cuBLASLt epilogue pattern); reassociated, so inexact after
-                W = gp.asarray(rng.standard_normal((cur.shape[1], int(rng.integers(1, 17)))).astype(cur.dtype))
-                cur = cur @ W
-                if rng.random() < 0.6:
-                    cur = cur + gp.asarray(rng.standard_normal(cur.shape[1]).astype(cur.dtype))
-                    if rng.random() < 0.5:
-                        cur = gp.maximum(cur, 0)
-                transcendental = True
-            elif k == 12 and cur.ndim >= 1:
-                ax = int(rng.integers(0, cur.ndim))
-                cur = gp.cumsum(cur, axis=ax)
-                transcendental = transcendental or cur.dtype.kind == "f"
-            elif k == 13 and cur.ndim >= 1 and cur.shape[-1] >= 2:
-                nxt = cur.copy()
-                nxt[..., ::2] = cur[..., ::2] * 2 + 1
-                cur = nxt
-        except gp.LazyFuseError:
-            continue
-    finals = [cur]
-    if cur.ndim >= 1 and rng.random() < 0.5 and not transcendental:
-        finals.append(cur.argmax(axis=int(rng.integers(0, cur.ndim))))
-    if rng.random() < 0.5:
-        finals.append(cur.sum())
-    return finals, transcendental
-
-
-def _close(got, exp, dtype, transcendental=False):
-    if dtype.kind in "biu":
-        return np.array_equal(got, exp)
-    # f32 transcendental ancestry carries f32 ulp error into f64 results
-    rtol = 1e-5 if (dtype == np.float32 or transcendental) else 1e-12
-    fin = np.isfinite(exp)
-    if not np.array_equal(np.isfinite(got), fin) or not np.array_equal(got[~fin], exp[~fin]) and \
-            not np.array_equal(np.isnan(got[~fin]), np.isnan(exp[~fin])):
-        return False
-    scale = np.max(np.abs(exp[fin])) if fin.any() else 0.0
-    return np.allclose(got[fin], exp[fin], rtol=rtol, atol=rtol * max(1.0, scale) * 64)
+def _within(got, wide, native, mag, eps, depth):
+    """Per element: the device's error against an extended-precision run of
+    the same program is at most 4x NumPy's own error plus
+    64*(depth+2)*eps times the element's magnitude run (sum of |terms|)."""
+    got = np.asarray(got)
+    fin = np.isfinite(wide.astype(np.float64)) & np.isfinite(native)
+    if not np.array_equal(np.isnan(got[~fin]), np.isnan(native[~fin])):
+        return False, "nan positions"
+    nn = ~fin & ~np.isnan(native)
+    if not np.array_equal(got[nn], native[nn]):
+        return False, "inf values"
+    g = got[fin].astype(np.longdouble)
+    w = wide[fin].astype(np.longdouble)
+    n = native[fin].astype(np.longdouble)
+    m = np.abs(mag[fin].astype(np.longdouble))
+    bound = 4 * np.abs(n - w) + 64 * (depth + 2) * eps * m + np.longdouble(1e-300)
+    err = np.abs(g - w)
+    bad = int(np.count_nonzero(~(err <= bound)))
+    return bad == 0, f"{bad} elements over the bound; worst err/bound {float(np.max(err / bound)) if err.size else 0:.3g}"
 
 
 @pytest.mark.parametrize("seed", range(NPROG))
 def test_random_program(sess, seed):
-    outs, transcendental = make_program(seed)
+    outs, transcendental, depth = make_program(seed, GP())
     expect = [eager.evaluate(o.node) for o in outs]
+    native, _t, _d = make_program(seed, Numpy())
+    wide, _t, _d = make_program(seed, Numpy(wide=True))
+    mag, _t, _d = make_program(seed, Numpy(absolute=True))
+    f32_ancestry = any(getattr(n, "dtype", None) is not None and np.dtype(n.dtype.np) == np.float32
+                       for n in _ancestry([o.node for o in outs]))
     gp.force(*outs)
-    for o, e in zip(outs, expect):
+    for o, e, nv, wv, mv in zip(outs, expect, native, wide, mag):
         got = np.asarray(o)
-        assert got.shape == e.shape and got.dtype == e.dtype
-        assert _close(got, e, e.dtype, transcendental), (seed, o.node, got, e)
-        if not transcendental and e.dtype.kind == "f" and o.node.kind.value == "MapElementwise":
+        nv = np.asarray(nv)
+        assert got.shape == e.shape == nv.shape and got.dtype == e.dtype == nv.dtype
+        if e.dtype.kind in "biu":
+            assert np.array_equal(got, e) and np.array_equal(got, nv), (seed, o.node)
+            continue
+        eps = 2.0 ** -24 if (e.dtype == np.float32 or f32_ancestry) else 2.0 ** -53
+        ok, why = _within(got, np.asarray(wv), nv, np.asarray(mv), eps, depth)
+        assert ok, (seed, o.node, why)
+        if not transcendental and o.node.kind.value == "MapElementwise":
             # +,-,*,/,sqrt,max and casts are IEEE-exact: bit-identical to NumPy
             assert np.array_equal(got, e, equal_nan=True), (seed, "not bit-exact", o.node)
+
+
+def _ancestry(roots):
+    seen, stack = {}, list(roots)
+    while stack:
+        n = stack.pop()
+        if n.id in seen:
+            continue
+        seen[n.id] = n
+        stack.extend(n.preds)
+    return seen.values()
 
 
 def test_config_fixtures(sess):

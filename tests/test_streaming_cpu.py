@@ -51,7 +51,7 @@ def test_partials_and_ineligible():
 def test_streamed_random_programs_do_stream(monkeypatch):
     """Enough of the random programs are streaming-eligible for the test above
     to exercise the chunked path (not just the fallback)."""
-    from test_gpu_programs import make_program
+    from random_programs import make_program
     monkeypatch.setattr(streaming, "MIN_BYTES", 1)
     monkeypatch.setattr(streaming, "ROW_ALIGN", 1)
     monkeypatch.setattr(streaming, "CHUNK_BYTES", 96)
@@ -60,7 +60,7 @@ def test_streamed_random_programs_do_stream(monkeypatch):
         s = gp.Session()
         old = gp.set_default_session(s)
         try:
-            outs, _ = make_program(seed)
+            outs, _t, _d = make_program(seed)
             if streaming.plan([o.node for o in outs]) is not None:
                 streamed += 1
         finally:
