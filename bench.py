@@ -266,6 +266,11 @@ WORKLOADS = {
         desc="map-scan cumsum(x*0.5+1) over 2^28 fp32 (SURVEY.md §8(f))",
         program=lambda xp, a: (_programs().scan(xp, *a),),
         elements=lambda n: n, bytes=lambda n: 2 * 4 * n, bound="hbm", shardable=False),
+    "transpose": dict(
+        label="f32", shape="[16384, 16384]",
+        desc="x.T + y, 16384x16384 fp32: transposed leaf staged through shared-memory tiles (north_star K1 staging)",
+        program=lambda xp, a: (_programs().transpose_add(xp, *a),),
+        elements=lambda n: n * 16384, bytes=lambda n: 3 * 4 * n * 16384, bound="hbm", shardable=False),
     "jacobi": dict(
         label="f32", shape="[16384, 16384]",
         desc="5-point Jacobi sweep (slice-assign), 16384x16384 fp32 (SURVEY.md §8(f))",
@@ -322,7 +327,7 @@ def host_inputs(name, lo, hi):
 def cpu_sample_n(name):
     """Leading extent of the bounded single-thread CPU sample (~5-20 s)."""
     return {"blackscholes-f32": 1 << 24, "blackscholes-f64": 1 << 24, "listing1": 1 << 24,
-            "rownorm": 16384, "rownorm-y": 16384, "mlp": 16384, "kmeans": 1 << 20, "jacobi": 4096,
+            "rownorm": 16384, "rownorm-y": 16384, "mlp": 16384, "kmeans": 1 << 20, "jacobi": 4096, "transpose": 4096,
             "cumsum": 1 << 24}[name]
 
 
@@ -357,6 +362,10 @@ class BlockedNumpy:
                 s, e = max(lo - 1, 0), min(hi + 1, self.rows)
                 return self.prog(np, [self.inputs[0][s:e]])[0][lo - s:lo - s + (hi - lo)]
             return list(self.pool.map(f, self.blocks))
+        if name == "transpose":
+            x, y = self.inputs
+            return list(self.pool.map(lambda b: _programs().transpose_add(np, x[:, b[0]:b[1]], y[b[0]:b[1]]),
+                                      self.blocks))
         if name == "cumsum":
             parts = list(self.pool.map(lambda b: self.prog(np, self._part(*b))[0], self.blocks))
             offs = np.cumsum([np.float32(0)] + [p[-1] for p in parts[:-1]]).astype(np.float32)

@@ -7,7 +7,8 @@ At 2^28 elements the eager program is evaluated on row blocks over host
 threads (SURVEY.md §7 hard part 8: chunked oracle, exact for row-local results,
 bounded for reductions).  Tolerances:
 
-  listing1, jacobi      bit-exact (only + and * in NumPy order, no contraction)
+  listing1, jacobi,     bit-exact (only + and * in NumPy order, no contraction)
+  transpose
   blackscholes f32/f64  |Δ| <= 1e-5 / 1e-12 · max(S, X)   (prices cancel)
   rownorm y             |Δ| <= 1e-5 · (1 + |y|); bit-exact mismatches reported
   rownorm total         |Δ| <= 4·log2(n)·eps32·Σ|y|; single shard of a power-
@@ -242,3 +243,16 @@ def _check_jacobi(wl, name, inp, out, threads, comm_sum, world):
     e = wl.jacobi(np, a)
     mm = int(np.count_nonzero(e.view(np.uint32) != got.view(np.uint32)))
     return _result(mm == 0, e.size, mm, float(np.max(np.abs(e - got))), "bit-exact")
+
+
+def _check_transpose(wl, name, inp, out, threads, comm_sum, world):
+    x, y = inp
+    got = out[0]
+
+    def f(blk):
+        lo, hi = blk
+        e = wl.transpose_add(np, x[:, lo:hi], y[lo:hi])
+        return int(np.count_nonzero(e.view(np.uint32) != got[lo:hi].view(np.uint32)))
+
+    mm = sum(_map_blocks(threads, y.shape[0], f))
+    return _result(mm == 0, got.size, mm, 0.0 if mm == 0 else float("nan"), "bit-exact")

@@ -1038,6 +1038,10 @@ def generate(region: Region) -> KernelSource:
         if ks is not None:
             return ks
         return codegen_rows.gen_rows(region)
+    from . import codegen_tile
+    ks = codegen_tile.try_generate(region)
+    if ks is not None:
+        return ks
     return gen_map(region)
 
 

@@ -152,6 +152,13 @@ def jacobi(xp, a):
     return b
 
 
+# ---- transposed operand (north_star: shared-memory staging of strided operands)
+def transpose_add(xp, x, y):
+    """x.T + y: the transposed leaf is staged through shared memory tiles
+    (codegen_tile.py), the output and y move row-wise."""
+    return x.T + y
+
+
 # ---- map-scan (SURVEY.md §8(f) rank 1) ------------------------------------------
 def scan_inputs(n=1 << 28, seed=42, dtype=np.float32):
     rng = np.random.default_rng(seed)
@@ -224,6 +231,9 @@ NAMED = {
                lambda s: [], "S"),
 }
 NAMED["rownorm-y"] = NAMED["rownorm"]
+NAMED["transpose"] = (16384, 256, lambda s: (lambda rng, r: [rng.random((r, 16384), dtype=np.float32),
+                                                             rng.random((r, 16384), dtype=np.float32)]),
+                      lambda s: [], "SS")
 
 
 def named_inputs(name, lo=0, hi=None, seed=42, threads=None):

@@ -92,3 +92,13 @@ def test_programs_loader_does_not_map_the_shim():
     out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
                          cwd=fullsize.__file__.rsplit("/oracle/", 1)[0])
     assert out.stdout.strip() == "ok", out.stderr
+
+
+def test_transpose_checker():
+    rng = np.random.default_rng(1)
+    x = rng.random((300, 300), dtype=np.float32)
+    y = rng.random((300, 300), dtype=np.float32)
+    out = x.T + y
+    assert fullsize.check("transpose", [x, y], [out], threads=4)["ok"]
+    out[5, 7] += 1
+    assert not fullsize.check("transpose", [x, y], [out], threads=4)["ok"]
