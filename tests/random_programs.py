@@ -103,14 +103,75 @@ def _rand_shape(rng, rank):
     return tuple(int(rng.integers(1, 17)) for _ in range(rank))
 
 
+def _header(rng):
+    rank = int(rng.integers(1, 4))
+    shape = _rand_shape(rng, rank)
+    dt = rng.choice([np.float32, np.float64, np.int32, np.int64])
+    return rank, shape, dt
+
+
+def input_dtype(seed):
+    return np.dtype(_header(np.random.default_rng(seed))[2])
+
+
+def within(got, wide, native, mag, eps, depth):
+    """Per element: the device's error against an extended-precision run of
+    the same program is at most 4x NumPy's own error plus
+    64*(depth+2)*eps times the element's magnitude run (sum of |terms|);
+    non-finite values must match NumPy's exactly (NaN positions, inf signs)."""
+    got = np.asarray(got)
+    fin = np.isfinite(wide.astype(np.float64)) & np.isfinite(native)
+    if not np.array_equal(np.isnan(got[~fin]), np.isnan(native[~fin])):
+        return False, "nan positions"
+    nn = ~fin & ~np.isnan(native)
+    if not np.array_equal(got[nn], native[nn]):
+        return False, "inf values"
+    g = got[fin].astype(np.longdouble)
+    w = wide[fin].astype(np.longdouble)
+    n = native[fin].astype(np.longdouble)
+    m = np.abs(mag[fin].astype(np.longdouble))
+    bound = 4 * np.abs(n - w) + 64 * (depth + 2) * eps * m + np.longdouble(1e-300)
+    err = np.abs(g - w)
+    bad = int(np.count_nonzero(~(err <= bound)))
+    return bad == 0, f"{bad} elements over the bound; worst err/bound {float(np.max(err / bound)) if err.size else 0:.3g}"
+
+
+def check_outputs(seed, got, eager_expect=None):
+    """Check a run's outputs (host arrays, program order) for ``seed``:
+    integers/bools exact against NumPy (and the eager oracle), floats within
+    the per-element bound.  Returns a list of failures."""
+    native, transcendental, depth = make_program(seed, Numpy())
+    wide, _t, _d = make_program(seed, Numpy(wide=True))
+    mag, _t, _d = make_program(seed, Numpy(absolute=True))
+    f32 = input_dtype(seed) == np.float32
+    bad = []
+    for k, (g, nv, wv, mv) in enumerate(zip(got, native, wide, mag)):
+        g, nv = np.asarray(g), np.asarray(nv)
+        if g.shape != nv.shape or g.dtype != nv.dtype:
+            bad.append((k, "shape/dtype", g.shape, nv.shape, g.dtype, nv.dtype))
+            continue
+        if eager_expect is not None:
+            e = eager_expect[k]
+            if e.shape != g.shape or e.dtype != g.dtype:
+                bad.append((k, "eager shape/dtype"))
+                continue
+        if g.dtype.kind in "biu":
+            if not np.array_equal(g, nv) or (eager_expect is not None and not np.array_equal(g, eager_expect[k])):
+                bad.append((k, "integer mismatch"))
+            continue
+        eps = 2.0 ** -24 if (g.dtype == np.float32 or f32) else 2.0 ** -53
+        ok, why = within(g, np.asarray(wv), nv, np.asarray(mv), eps, depth)
+        if not ok:
+            bad.append((k, why))
+    return bad
+
+
 def make_program(seed, xp=None):
     """(outputs, transcendental, depth): ``transcendental`` marks programs whose
     float results carry libm (ulp-accurate, not correctly rounded) error."""
     xp = xp or GP()
     rng = np.random.default_rng(seed)
-    rank = int(rng.integers(1, 4))
-    shape = _rand_shape(rng, rank)
-    dt = rng.choice([np.float32, np.float64, np.int32, np.int64])
+    rank, shape, dt = _header(rng)
     fdt = np.dtype(dt).kind == "f"
     pool = []
     for _ in range(int(rng.integers(1, 4))):

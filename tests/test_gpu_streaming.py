@@ -105,16 +105,15 @@ def test_streamed_random_program(sess, monkeypatch, seed):
     with tiny chunks: streamed whenever eligible, same answers as the oracle
     (row-local results bit-identical to the plain force)."""
     from oracle import eager
-    from test_gpu_programs import _close, make_program
+    from random_programs import check_outputs, make_program
     monkeypatch.setattr(streaming, "MIN_BYTES", 1)
     monkeypatch.setattr(streaming, "ROW_ALIGN", 1)
     monkeypatch.setattr(streaming, "CHUNK_BYTES", 96)
-    outs, transcendental = make_program(seed)
+    outs, transcendental, _depth = make_program(seed)
     expect = [eager.evaluate(o.node) for o in outs]
     got = gp.materialize(*outs)
-    for g, e in zip(got, expect):
-        assert g.shape == e.shape and g.dtype == e.dtype
-        assert _close(g, e, e.dtype, transcendental), (seed, g, e)
+    bad = check_outputs(seed, got, expect)
+    assert not bad, (seed, bad)
 
 
 
