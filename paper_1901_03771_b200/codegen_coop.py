@@ -24,7 +24,7 @@ import os
 
 from typing import List, Optional
 
-from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, c_literal
+from .codegen import HEADER, Aff, KernelSource, NotPairable, Region, Var, _params_struct, bcast_coords, c_literal
 from .codegen_rows import (
     _COMBINE, _IDENT, _OPS, LoopEmitter, NotFusable, is_total, render, thread_space,
 )
@@ -53,14 +53,22 @@ class CoopEmitter(LoopEmitter):
         self.staged = {}
         self.discovered = []
         self.n_sh = 0
+        # paired element loops: (v, v+1) of a thread's VEC elements as one
+        # gr::f2 — sums, differences, products and the shared-divisor
+        # division issue once per pair (FADD2/FMUL2/FFMA2)
+        self.coop_pair = False
 
     # col coordinate of the current coop loops
     def coop_col(self, m: Var, v: Var) -> Aff:
+        if self.half is not None and v.name == self.half.name[len("gr_half_"):]:
+            return Aff.of(self.cb) + Aff.of(m).scale(8) + Aff.of(v).scale(2) + Aff.of(self.half)
         return Aff.of(self.cb) + Aff.of(m).scale(8) + Aff.of(v)
 
     def close_coop(self, mm, vv):
         self.close(vv[1], vv[2])
         self.close(mm[1], mm[2])
+        if self.half is not None and self.half.name == "gr_half_" + vv[0].name:
+            self.half = None
 
     def prestage(self, leaves, tma_layout=None, async_layout=None, block=256):
         """Load whole row segments of ``leaves`` into registers up front: from
@@ -118,6 +126,17 @@ class CoopEmitter(LoopEmitter):
             self.staged[(leaf.id, rowkey)] = name
 
     def load_leaf(self, leaf: Node, off: Aff):
+        if self.half is not None and off.coef(self.half):
+            # paired loop: elements (2*vp, 2*vp + 1) of the staged segment
+            for m, v in self._coop_pairs():
+                if (off.coef(self.half) == 1 and off.coef(v) == 2 and off.coef(m) == 8
+                        and off.coef(self.cb) == 1 and leaf.dtype is DType.f32):
+                    rest = off.without(v).without(m).without(self.cb).without(self.half)
+                    name = self.staged.get((leaf.id, rest.key()))
+                    if name is not None and rest.level <= 1:
+                        return self.emit_pair(v.level, f"gr::pk({name}[{m.name}][2 * {v.name}], "
+                                                        f"{name}[{m.name}][2 * {v.name} + 1])"), v.level
+            raise NotPairable("paired leaf outside the staged row segment")
         # staged row segment: offset = rest + cb + 8*m + v with m, v the coop loop vars
         for m, v in self._coop_pairs():
             if off.coef(v) == 1 and off.coef(m) == 8 and off.coef(self.cb) == 1:
@@ -142,16 +161,59 @@ class CoopEmitter(LoopEmitter):
         for i in range(2, len(self.stack) - 1):
             a, b = self.stack[i], self.stack[i + 1]
             if (a is not None and b is not None and a.kind == "for" and b.kind == "for" and a.trip == 16
-                    and b.trip == self.vec and getattr(a, "coop", False)):
+                    and b.trip in (self.vec, self.vec // 2) and getattr(a, "coop", False)):
                 out.append((a.var, b.var))
         return out
 
-    def open_coop(self, level):
-        """Open the (m < 16, v < VEC) loops over this thread's row elements."""
+    def open_coop(self, level, paired=False):
+        """Open the (m < 16, v < VEC) loops over this thread's row elements;
+        ``paired``: v walks element pairs (v < VEC/2) with the pair's half as
+        the symbolic ``self.half`` (values become gr::f2)."""
         m, sm, savm = self.open(level, "for", trip=16, unroll=True)
         sm.coop = True
-        v, sv, savv = self.open(m.level, "for", trip=self.vec, unroll=True)
+        v, sv, savv = self.open(m.level, "for", trip=self.vec // 2 if paired else self.vec, unroll=True)
+        if paired:
+            self.half = Var("gr_half_" + v.name, v.level)
         return (m, sm, savm), (v, sv, savv)
+
+    def pairable_sum(self, x: Node, rop, T: DType) -> bool:
+        return (self.coop_pair and rop is ReduceOp.sum and T is DType.f32 and x.dtype is DType.f32
+                and self.vec % 2 == 0)
+
+    def _pair_map(self, n: Node, coords):
+        """Packed element ops; a division by a row-level divisor keeps the
+        shared-reciprocal Markstein form (two FFMA2 per pair) instead of the
+        per-lane IEEE division."""
+        from .dag import ElemCode
+        if n.op.code is ElemCode.div and n.loop[0] is DType.f32 and n.dtype is DType.f32:
+            a = self.cast(self.value(n.preds[0], bcast_coords(coords, n.shape, n.preds[0].shape)),
+                          n.preds[0].dtype, n.loop[0])
+            b = self.cast(self.value(n.preds[1], bcast_coords(coords, n.shape, n.preds[1].shape)),
+                          n.preds[1].dtype, n.loop[1])
+            if self.is_pair(a) and not self.is_pair(b) and b[1] < a[1]:
+                rk = ("rcp", b[0])
+                r = self.const_memo.get(rk)
+                if r is None or b[1] > 0:
+                    r = self.emit(b[1], "gr::DivShared<float>", f"gr::div_prep<float>({b[0]})")
+                    if b[1] == 0:
+                        self.const_memo[rk] = r
+                r2 = self.const_memo.get(("rcp2", r))
+                if r2 is None:
+                    r2 = self.emit(max(b[1], 0), "gr::p2::DivShared2", f"gr::p2::div_prep2({r})")
+                    self.const_memo[("rcp2", r)] = r2
+                if self.div_fast and b[1] == 1:
+                    w = self.const_memo.get(("divrange", r))
+                    if w is None:
+                        w = self.fresh("w")
+                        self.stmt(1, f"gr::DivRange<float> {w} = gr::div_range_init<float>();")
+                        self.const_memo[("divrange", r)] = w
+                        self.div_finalize.append(f"bad |= gr::div_range_bad<float>({w}, {r});")
+                    self.used_div_fast = True
+                    return self.emit_pair(a[1], f"gr::p2::div_shr<FAST>({a[0]}, {r2}, {w})"), a[1]
+                if not self.div_fast:
+                    return self.emit_pair(a[1], f"gr::p2::div_shared({a[0]}, {r2})"), a[1]
+                raise NotPairable("paired division outside the row-divisor form")
+        return super()._pair_map(n, coords)
 
     # -- row-complete reductions ---------------------------------------------------
     def _row_complete(self, r: Node, axes) -> bool:
@@ -178,6 +240,20 @@ class CoopEmitter(LoopEmitter):
         ct = T.ctype
         acc = self.fresh("acc")
         self.stmt(1, f"{ct} {acc}[{self.vec}];")
+        if self.pairable_sum(x, rop, T):
+            # the thread's VEC accumulators as VEC/2 packed pairs: lane v of
+            # pair vp is accumulator 2*vp + v, same adds in the same order
+            acc2 = self.fresh("acc")
+            self.stmt(1, f"gr::f2 {acc2}[{self.vec // 2}];")
+            mm, vv = self.open_coop(1, paired=True)
+            m, v = mm[0], vv[0]
+            val = self.value(x, list(row_coords) + [self.coop_col(m, v)])
+            pv = self.splat(val)
+            self.stmt(v.level, f"{acc2}[{v.name}] = ({m.name} == 0) ? {pv} : gr::p2::add({acc2}[{v.name}], {pv});")
+            self.close_coop(mm, vv)
+            for k in range(self.vec // 2):
+                self.stmt(1, f"{acc}[{2 * k}] = gr::lo({acc2}[{k}]); {acc}[{2 * k + 1}] = gr::hi({acc2}[{k}]);")
+            return self.finish_coop(acc, rop, T, identity)
         mm, vv = self.open_coop(1)
         m, v = mm[0], vv[0]
         val = self.cast(self.value(x, list(row_coords) + [self.coop_col(m, v)]), x.dtype, T)
@@ -311,7 +387,7 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
             leaves.append(leaf)
     if not leaves:
         return ks
-    block = max(256, tpr)
+    block = max(COOP_BLOCK, tpr)
     rpc = block // tpr
     P = 8 // vec
     layout = {}
@@ -342,13 +418,30 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
     return second[0] if second is not None else ks
 
 
+COOP_PAIR = os.environ.get("GRUMPY_COOP_PAIR", "1") == "1"
+COOP_BLOCK = int(os.environ.get("GRUMPY_COOP_BLOCK", "256"))
+
+
 def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch=False, async_layout=None):
+    """Generate with packed element pairs when every paired value has a packed
+    form (f32), else with scalar element loops."""
+    if COOP_PAIR and q[3] % 2 == 0:
+        try:
+            return _generate1(region, q, kname, prestage, tma, smem_bytes, l2_prefetch, async_layout, pair=True)
+        except NotPairable:
+            pass
+    return _generate1(region, q, kname, prestage, tma, smem_bytes, l2_prefetch, async_layout, pair=False)
+
+
+def _generate1(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch=False, async_layout=None,
+               pair=False):
     Ts, totals, C, vec, tpr = q
     tot_ids = {t.id for t in totals}
-    block = max(256, tpr)
+    block = max(COOP_BLOCK, tpr)
     rpc = block // tpr
     R = element_count(Ts)
     em = CoopEmitter(region, vec, tpr, rpc, Ts, C)
+    em.coop_pair = pair
     em.div_fast = os.environ.get("GRUMPY_DIV_TWO_PASS", "1") != "0"
     rvar = Var("r", 1)
     if len(Ts) == 1:
@@ -402,19 +495,41 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
                 a = em.fresh("acc")
                 em.stmt(1, f"{t.dtype.ctype} {a}[{vec}];")
                 accs.append((t, a))
+            paired = (em.coop_pair and r.dtype is DType.f32 and vec % 2 == 0
+                      and all(em.pairable_sum(r, t.op.attrs[0], t.dtype) for t, _a in accs))
             m, sm, savm = em.open(1, "for", trip=16, unroll=True)
             sm.coop = True
             em.stmt(m.level, f"{T} {o}[{vec}];")
-            v, sv, savv = em.open(m.level, "for", trip=vec, unroll=True)
-            val = em.value(r, row_coords + [em.coop_col(m, v)])
-            em.stmt(v.level, f"{o}[{v.name}] = {val[0]};")
-            for t, a in accs:
-                tv = em.cast(val, r.dtype, t.dtype)
-                comb = _COMBINE[t.op.attrs[0]]
-                em.stmt(v.level, f"{a}[{v.name}] = ({m.name} == 0) ? {tv[0]} : {comb}<{t.dtype.ctype}>({a}[{v.name}], {tv[0]});")
-            em.close(sv, savv)
+            if paired:
+                pacc = []
+                for t, a in accs:
+                    a2 = em.fresh("acc")
+                    em.stmt(1, f"gr::f2 {a2}[{vec // 2}];")
+                    pacc.append(a2)
+                v, sv, savv = em.open(m.level, "for", trip=vec // 2, unroll=True)
+                em.half = Var("gr_half_" + v.name, v.level)
+                val = em.value(r, row_coords + [em.coop_col(m, v)])
+                pv = em.splat(val)
+                em.stmt(v.level, f"{o}[2 * {v.name}] = gr::lo({pv}); {o}[2 * {v.name} + 1] = gr::hi({pv});")
+                for a2 in pacc:
+                    em.stmt(v.level, f"{a2}[{v.name}] = ({m.name} == 0) ? {pv} : gr::p2::add({a2}[{v.name}], {pv});")
+                em.close(sv, savv)
+                em.half = None
+            else:
+                v, sv, savv = em.open(m.level, "for", trip=vec, unroll=True)
+                val = em.value(r, row_coords + [em.coop_col(m, v)])
+                em.stmt(v.level, f"{o}[{v.name}] = {val[0]};")
+                for t, a in accs:
+                    tv = em.cast(val, r.dtype, t.dtype)
+                    comb = _COMBINE[t.op.attrs[0]]
+                    em.stmt(v.level, f"{a}[{v.name}] = ({m.name} == 0) ? {tv[0]} : {comb}<{t.dtype.ctype}>({a}[{v.name}], {tv[0]});")
+                em.close(sv, savv)
             em.stmt(m.level, f"if (valid) gr::stv<{T}, {vec}>(p.out{ri} + r * {C}LL + cb + 8 * {m.name}, {o});")
             em.close(sm, savm)
+            if paired:
+                for (t, a), a2 in zip(accs, pacc):
+                    for k in range(vec // 2):
+                        em.stmt(1, f"{a}[{2 * k}] = gr::lo({a2}[{k}]); {a}[{2 * k + 1}] = gr::hi({a2}[{k}]);")
             for t, a in accs:
                 tot_partials[t.id] = em.finish_coop(a, t.op.attrs[0], t.dtype, identity=False)
         else:
@@ -574,7 +689,7 @@ def _generate(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetch
         # leaf (64 registers) capping the kernel at 80 registers fits three
         # CTAs per SM: 0.270 ms vs 0.307 ms at two (profiles/r01_rownorm_modes.md)
         data_regs = sum(16 * vec * l.dtype.itemsize // 4 for l in (prestage or []))
-        minb = int(os.environ.get("GRUMPY_COOP_MINBLOCKS", "3" if 0 < data_regs <= 64 else "0"))
+        minb = int(os.environ.get("GRUMPY_COOP_MINBLOCKS", str(768 // block) if 0 < data_regs <= 64 else "0"))
         lb = f"{block}, {minb}" if minb else f"{block}"
         kern = [f'extern "C" __global__ void __launch_bounds__({lb}) {kname}(const K::Params p) {{',
                 f"  for (long long g = blockIdx.x; g < K::NG; g += gridDim.x) {{"]
