@@ -16,8 +16,10 @@ layer (single process, worker pool — SPEC.md:412-413), so this module is new:
   of sharded keys, a matmul contracting a sharded axis) or ``A:<max|min>``
   (first-index arg-reduction over the sharded axis).  Partial nodes are forced
   to be step roots; after their kernel the executor allreduces them in place
-  (sum/prod/max/min → ncclAllReduce).  Arg partials are combined from an
-  allgather of (value, global index) pairs with NumPy's first-index rule.
+  (sum/prod/max/min → ncclAllReduce).  Arg partials are combined on the
+  device: ncclAllGather of every rank's (best value, global index), then an
+  arg-reduction over the rank axis (lower ranks hold lower global indices, so
+  NumPy's first-index and NaN rules carry over) selects the index.
 
 Elementwise regions need no communication at all (weak or strong scaling is
 the caller's choice of shard size).
@@ -51,6 +53,11 @@ class Comm:
         raise NotImplementedError
 
     def allreduce_device(self, buf, count: int, dtype, op: ReduceOp):
+        raise NotImplementedError
+
+    def allgather_device(self, rt, buf, count: int, dtype):
+        """Rank-ordered concatenation of every rank's ``count`` elements of
+        ``buf`` into a new device buffer of world * count elements."""
         raise NotImplementedError
 
 
@@ -96,6 +103,11 @@ class NcclComm(TorchHostComm):
     def allreduce_device(self, buf, count, dtype, op):
         self.rt.nccl_allreduce(buf.ptr, buf.ptr, count, dtype, GR_OP[op])
 
+    def allgather_device(self, rt, buf, count, dtype):
+        out = rt.alloc(max(1, self.world * count * dtype.itemsize))
+        self.rt.nccl_allgather(buf.ptr, out.ptr, count, dtype)
+        return out
+
 
 class HostStagedComm(TorchHostComm):
     """Device partials combined through host memory over gloo — used when two
@@ -109,6 +121,10 @@ class HostStagedComm(TorchHostComm):
     def allreduce_device(self, buf, count, dtype, op):
         host = buf.to_numpy(dtype, (count,))
         buf.copy_from_host(np.ascontiguousarray(self.allreduce_host(host, op).astype(host.dtype)))
+
+    def allgather_device(self, rt, buf, count, dtype):
+        host = buf.to_numpy(dtype, (count,))
+        return rt.upload(np.ascontiguousarray(self.allgather_host(host).reshape(-1).astype(host.dtype)))
 
 
 def _ranks_share_a_device(rt) -> bool:

@@ -674,26 +674,28 @@ def dag_signature(roots: Sequence[Node]):
     for r in roots:
         if r.id in local:
             continue
-        stack = [(r, False)]
+        stack = [r]
         while stack:
-            n, expanded = stack.pop()
-            if n.id in local:
+            n = stack[-1]
+            nid = n.id
+            if nid in local:
+                stack.pop()
                 continue
-            if n.is_materialized:
-                local[n.id] = len(order)
+            if n.data is not None:
+                stack.pop()
+                local[nid] = len(order)
                 order.append(n)
                 items.append(("L", n.shape, n.dtype))
                 continue
-            if not expanded:
-                stack.append((n, True))
-                for p in reversed(n.preds):
-                    if p.id not in local:
-                        stack.append((p, False))
+            pending = [p for p in n.preds if p.id not in local]
+            if pending:
+                stack.extend(reversed(pending))
                 continue
-            local[n.id] = len(order)
+            stack.pop()
+            local[nid] = len(order)
             order.append(n)
-            items.append((n.op, n.shape, n.dtype, tuple(local[p.id] for p in n.preds)))
-    return (tuple(items), tuple(local[r.id] for r in roots)), order
+            items.append((n.op, n.shape, n.dtype, tuple([local[p.id] for p in n.preds])))
+    return (tuple(items), tuple([local[r.id] for r in roots])), order
 
 
 def make_template(steps: List[PlanStep], order: List[Node]):

@@ -195,19 +195,33 @@ class Session:
         self.stats.exec_time += time.perf_counter() - t1
 
     def _combine_arg(self, n, aux, which):
-        from . import distributed as D
-        local_idx = self.to_numpy(n)
-        local_val = self.to_numpy(aux)
+        """Global first-index arg-reduction from every rank's (best value,
+        local index), on the device: the local index is offset to a global
+        one, both are gathered over the ranks (ncclAllGather), and an
+        arg-reduction over the rank axis picks the winning rank per element —
+        ranks hold consecutive rows, so the lowest rank among equal values
+        (and the first NaN) is NumPy's first index."""
+        from .tensor import TensorBuffer as _TB
         src_shape, off_rows = self._arg_operand_shape[n.id]
-        if n.op.attrs[1] is None:
-            # flat index over the local [n_local, ...] block -> global
-            offset = off_rows * int(np.prod(src_shape[1:]))
-        else:
-            offset = off_rows
-        g = D.combine_arg(which, local_idx, local_val, offset, self.comm)
-        g = np.ascontiguousarray(g.astype(np.int64).reshape(n.shape))
-        n.data.host = g
-        n.data.device.copy_from_host(g)
+        offset = off_rows * int(np.prod(src_shape[1:])) if n.op.attrs[1] is None else off_rows
+        comm = self.comm
+        world = comm.world
+        count = int(np.prod(n.shape)) if n.shape else 1
+        gidx = ndarray(n, self) + np.int64(offset)
+        self.force_nodes([gidx._node])
+        rt = self.executor.rt
+        gv = comm.allgather_device(rt, aux.data.device, count, aux.dtype)
+        gi = comm.allgather_device(rt, gidx._node.data.device, count, DType.i64)
+        self.stats.collectives += 2
+        V = ndarray(self.graph.add_input(_TB(aux.dtype, (world,) + tuple(n.shape), device=gv)), self)
+        I = ndarray(self.graph.add_input(_TB(DType.i64, (world,) + tuple(n.shape), device=gi)), self)
+        win = V.argmax(axis=0) if which == "max" else V.argmin(axis=0)
+        res = I[0] * (win == 0)
+        for k in range(1, world):
+            res = res + I[k] * (win == k)
+        self.force_nodes([res._node])
+        n.data.device = res._node.data.device
+        n.data.host = None
 
     def to_numpy(self, node: Node) -> np.ndarray:
         self.force_nodes([node])
@@ -331,7 +345,20 @@ def _session_of(args) -> Session:
 
 
 def _binop(code, swap=False):
+    op = _MAP_OPS[code]
+
     def f(self, other):
+        t = type(other)
+        if t is ndarray and other._session is self._session:
+            # hot path: two lazy arrays of one session
+            a, b = (other._node, self._node) if swap else (self._node, other._node)
+            return ndarray(self._session.graph.add_op(op, (a, b)), self._session)
+        if t is float and self._node.dtype.is_float:
+            # float scalar with a float array: NEP 50 keeps the array's dtype
+            sess = self._session
+            c = sess.const(other, self._node.dtype)
+            a, b = (c, self._node) if swap else (self._node, c)
+            return ndarray(sess.graph.add_op(op, (a, b)), sess)
         if isinstance(other, (list, tuple)):
             other = np.asarray(other)
         if not isinstance(other, (ndarray, np.ndarray, np.generic, numbers.Number)):

@@ -32,4 +32,23 @@ gp.force(y, tot)
 ey, etot = wl.rownorm(np, x)
 np.testing.assert_allclose(np.asarray(y), ey[off:off + ln], rtol=1e-5, atol=1e-5)
 assert abs(float(np.asarray(tot)) - float(etot)) < 1e-2
+# full-array and axis-0 arg-reductions over the sharded axis: device combine
+# (allgather of (value, global index), arg-reduction over the rank axis)
+z = np.random.default_rng(5).standard_normal((1000, 37))
+z[700, 3] = z.max() + 1.0               # global max on the last rank
+off, ln = D.split(z.shape[0], world, rank)
+gz = D.local_input(z[off:off + ln], z.shape[0], off)
+am, amin0 = gz.argmax(), gz.argmin(axis=0)
+gp.force(am, amin0)
+assert int(np.asarray(am)) == z.argmax(), (int(np.asarray(am)), z.argmax())
+assert np.array_equal(np.asarray(amin0), z.argmin(axis=0))
+zt = z.copy()
+zt[10, :] = zt.max()                      # ties: the first (lowest-rank) index wins
+zt[990, :] = zt.max()
+gt = D.local_input(zt[off:off + ln], zt.shape[0], off)
+assert np.array_equal(np.asarray(gt.argmax(axis=0)), zt.argmax(axis=0))
+zn = z.copy()
+zn[600, 5] = np.nan                       # NaN is the extreme value (np.argmax)
+gn = D.local_input(zn[off:off + ln], zn.shape[0], off)
+assert int(np.asarray(gn.argmax())) == zn.argmax()
 print(f"rank {rank}/{world} ok ({type(comm).__name__})", flush=True)
