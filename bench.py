@@ -249,6 +249,11 @@ WORKLOADS = {
         # emulated with BF16x9 tensor-core products + the bias/ReLU epilogue
         # (the R1 region absorbed)
         library_flops={"Gemm+relu_bias": lambda n: 2.0 * n * 784 * MLP_H, "Gemm": lambda n: 2.0 * n * 784 * MLP_H},
+        # the repo's own kernels of the step (HBM rooflines): layer 2 + b2 +
+        # softmax + argmax as the skinny-product row kernel, and the R1
+        # bias+ReLU map when the cuBLASLt epilogue is off (GRUMPY_GEMM_EPILOGUE=0)
+        repo_bytes={"rows:gr_region": lambda n: n * MLP_H * 4 + n * 10 * 4 + n * 8 + MLP_H * 10 * 4 + 40,
+                    "map:gr_region": lambda n: 2 * n * MLP_H * 4 + MLP_H * 4},
         bound="tensor (cuBLASLt BF16x9-emulated FP32 GEMM + fused bias/ReLU epilogue)"),
     "kmeans": dict(
         label="f32", shape=f"[2^26, {KM_D}] points x 64 centroids",
@@ -587,6 +592,12 @@ def run_grumpy(args, dist):
                               "device_step": my_ms / args.steps,
                               "host_issue": host_issue_s * 1e3 / args.steps,
                               "per_launch": {f"{f}:{l}": statistics.mean(v) for (f, l), v in by_label.items()}},
+        "repo_kernel_rooflines": [
+            {"kernel": k, "kernel_ms": statistics.mean(by_label[tuple(k.split(":", 1))]),
+             "algorithmic_bytes": fb(rows),
+             "achieved_gbs": fb(rows) / (statistics.mean(by_label[tuple(k.split(":", 1))]) / 1e3) / 1e9,
+             "frac": fb(rows) / (statistics.mean(by_label[tuple(k.split(":", 1))]) / 1e3) / 1e9 / peak}
+            for k, fb in w.get("repo_bytes", {}).items() if tuple(k.split(":", 1)) in by_label],
         "rows_per_gpu": rows,
         "gpu_launches": launches,
         "collectives_in_timed_region": collectives,
