@@ -22,11 +22,11 @@ from __future__ import annotations
 
 import os
 
-from typing import List, Optional
+from typing import Optional
 
 from .codegen import HEADER, Aff, KernelSource, NotPairable, Region, Var, _params_struct, bcast_coords, c_literal
 from .codegen_rows import (
-    _COMBINE, _IDENT, _OPS, LoopEmitter, NotFusable, is_total, render, thread_space,
+    _COMBINE, _IDENT, _OPS, LoopEmitter, NotFusable, render, thread_space,
 )
 from .dag import Node, OpKind, ReduceOp
 from .tensor import DType, element_count

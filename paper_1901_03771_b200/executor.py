@@ -14,12 +14,11 @@ from __future__ import annotations
 
 import collections
 import os
-import time
 from typing import Dict, List
 
 from . import codegen, runtime
 from .dag import Node, OpKind
-from .errors import ShapeMismatch, UnsupportedNodeInFusedStep
+from .errors import ShapeMismatch
 from .planner import PlanStep
 from .tensor import DType, TensorBuffer, element_count
 

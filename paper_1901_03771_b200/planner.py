@@ -26,7 +26,7 @@ from __future__ import annotations
 import dataclasses
 from typing import Dict, List, Optional, Sequence, Set, Tuple
 
-from .dag import ElemCode, Node, OpKind, ReduceOp
+from .dag import ElemCode, Node, OpKind
 from .tensor import DType
 
 LIBRARY_KINDS = (OpKind.MATMUL, OpKind.MATVEC)
