@@ -178,6 +178,9 @@ int grumpy_rt_nccl_unique_id(char* id128);
 int grumpy_rt_nccl_init(int rank, int nranks, const char* id128);
 int grumpy_rt_nccl_allreduce(uint64_t send, uint64_t recv, size_t count, int dtype, int op);
 int grumpy_rt_nccl_allgather(uint64_t send, uint64_t recv, size_t count_per_rank, int dtype);
+/* ncclGroupStart/End around the collectives of one plan step (one launch) */
+int grumpy_rt_nccl_group_start(void);
+int grumpy_rt_nccl_group_end(void);
 int grumpy_rt_nccl_destroy(void);
 
 #ifdef __cplusplus

@@ -259,6 +259,8 @@ struct Nccl {
   int (*AllReduce)(const void*, void*, size_t, int, int, NcclComm, CUstream) = nullptr;
   int (*AllGather)(const void*, void*, size_t, int, NcclComm, CUstream) = nullptr;
   int (*CommDestroy)(NcclComm) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(int) = nullptr;
   NcclComm comm = nullptr;
 } N;
@@ -978,6 +980,8 @@ int grumpy_rt_nccl_load(const char* path) {
   GR_NSYM(AllReduce, "ncclAllReduce")
   GR_NSYM(AllGather, "ncclAllGather")
   GR_NSYM(CommDestroy, "ncclCommDestroy")
+  GR_NSYM(GroupStart, "ncclGroupStart")
+  GR_NSYM(GroupEnd, "ncclGroupEnd")
   GR_NSYM(GetErrorString, "ncclGetErrorString")
 #undef GR_NSYM
   return GR_OK;
@@ -1024,6 +1028,22 @@ int grumpy_rt_nccl_allgather(uint64_t send, uint64_t recv, size_t count_per_rank
   (void)dtype_size;
   int rr = N.AllGather((const void*)send, (void*)recv, count_per_rank, nd, N.comm, CS());
   if (rr) return nccl_fail(rr, "ncclAllGather");
+  return GR_OK;
+}
+
+// Several collectives of one plan step issued as ONE NCCL launch (the
+// k-means step allreduces four f64 partial sums and the counts)
+int grumpy_rt_nccl_group_start(void) {
+  if (!N.handle) return fail(GR_ENOINIT, "grumpy_rt_nccl_load first");
+  int rr = N.GroupStart();
+  if (rr) return nccl_fail(rr, "ncclGroupStart");
+  return GR_OK;
+}
+
+int grumpy_rt_nccl_group_end(void) {
+  if (!N.handle) return fail(GR_ENOINIT, "grumpy_rt_nccl_load first");
+  int rr = N.GroupEnd();
+  if (rr) return nccl_fail(rr, "ncclGroupEnd");
   return GR_OK;
 }
 

@@ -60,6 +60,11 @@ class Comm:
         ``buf`` into a new device buffer of world * count elements."""
         raise NotImplementedError
 
+    def group(self):
+        """Context manager batching the collectives issued inside it."""
+        import contextlib
+        return contextlib.nullcontext()
+
 
 class TorchHostComm(Comm):
     """torch.distributed (gloo) on host arrays: CPU tests and host-side combines."""
@@ -107,6 +112,19 @@ class NcclComm(TorchHostComm):
         out = rt.alloc(max(1, self.world * count * dtype.itemsize))
         self.rt.nccl_allgather(buf.ptr, out.ptr, count, dtype)
         return out
+
+    def group(self):
+        """ncclGroupStart/End: the step's allreduces go out as one launch."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def cm():
+            self.rt.nccl_group_start()
+            try:
+                yield
+            finally:
+                self.rt.nccl_group_end()
+        return cm()
 
 
 class HostStagedComm(TorchHostComm):

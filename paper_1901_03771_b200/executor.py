@@ -93,18 +93,21 @@ class Executor:
         """Allreduce partial roots in place on the runtime stream (NCCL), right
         after the kernel that produced them (distributed.py)."""
         from .dag import ReduceOp
-        for r, b in zip(roots, outs):
-            d = dist.get(r.id, "R")
-            if d.startswith("P:") and element_count(r.shape):
-                if self.profile is not None:
-                    e0, e1 = self._event_pair()
-                    self.rt.record(e0)
-                    comm.allreduce_device(b.device, element_count(r.shape), r.dtype, ReduceOp(d[2:]))
-                    self.rt.record(e1)
-                    self.profile.append(("collective", f"allreduce:{d[2:]}", e0, e1))
-                else:
-                    comm.allreduce_device(b.device, element_count(r.shape), r.dtype, ReduceOp(d[2:]))
+        parts = [(r, b, dist.get(r.id, "R")) for r, b in zip(roots, outs)]
+        parts = [(r, b, d) for r, b, d in parts if d.startswith("P:") and element_count(r.shape)]
+        if not parts:
+            return
+        if self.profile is not None:
+            e0, e1 = self._event_pair()
+            self.rt.record(e0)
+        # every partial of the step in one NCCL group: one launch, one latency
+        with comm.group():
+            for r, b, d in parts:
+                comm.allreduce_device(b.device, element_count(r.shape), r.dtype, ReduceOp(d[2:]))
                 self.session.stats.collectives += 1
+        if self.profile is not None:
+            self.rt.record(e1)
+            self.profile.append(("collective", "allreduce:" + ",".join(sorted({d[2:] for _r, _b, d in parts})), e0, e1))
 
     def kernel_source(self, region: codegen.Region) -> codegen.KernelSource:
         return codegen.cached_generate(region)

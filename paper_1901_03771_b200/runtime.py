@@ -89,6 +89,8 @@ SIGNATURES = {
     "grumpy_rt_nccl_init": [_i, _i, _cp],
     "grumpy_rt_nccl_allreduce": [_u64, _u64, _sz, _i, _i],
     "grumpy_rt_nccl_allgather": [_u64, _u64, _sz, _i],
+    "grumpy_rt_nccl_group_start": [],
+    "grumpy_rt_nccl_group_end": [],
     "grumpy_rt_nccl_destroy": [],
 }
 
@@ -481,6 +483,12 @@ class Runtime:
 
     def nccl_allgather(self, send: int, recv: int, count: int, dtype: DType):
         _check(self.lib.grumpy_rt_nccl_allgather(send, recv, count, GR_DTYPE[dtype]))
+
+    def nccl_group_start(self):
+        _check(self.lib.grumpy_rt_nccl_group_start())
+
+    def nccl_group_end(self):
+        _check(self.lib.grumpy_rt_nccl_group_end())
 
 
 _rt: Optional[Runtime] = None
