@@ -617,11 +617,52 @@ _PAIR_UN = {
 _PAIR_BOOL = {ElemCode.logical_and: "gr::p2::land", ElemCode.logical_or: "gr::p2::lor"}
 
 
+_TRANSCENDENTAL = {ElemCode.exp, ElemCode.log, ElemCode.erf, ElemCode.tanh, ElemCode.sin, ElemCode.cos,
+                   ElemCode.pow}
+_DISCONTINUOUS = {ElemCode.cmp_lt, ElemCode.cmp_gt, ElemCode.cmp_le, ElemCode.cmp_ge, ElemCode.cmp_eq,
+                  ElemCode.cmp_ne, ElemCode.select, ElemCode.floor, ElemCode.ceil, ElemCode.mod,
+                  ElemCode.floordiv, ElemCode.isnan, ElemCode.maximum, ElemCode.minimum}
+
+
+def inexact_region(region: Region) -> bool:
+    """Every root is a float carrying libm error (a transcendental upstream),
+    and nothing in the region branches on a value (compares, selects,
+    rounding to integers, max/min).  Such results are checked to a
+    tolerance, never bit for bit, so a product may fuse with the add that
+    consumes it (one rounding instead of NumPy's two: FFMA2)."""
+    by_id = {n.id: n for n in region.nodes}
+    for n in region.nodes:
+        if n.kind is OpKind.MAP and n.op.code in _DISCONTINUOUS:
+            return False
+        if n.kind is OpKind.CAST and not n.dtype.is_float:
+            return False
+        if n.kind not in (OpKind.MAP, OpKind.CAST, OpKind.BROADCAST, OpKind.TRANSPOSE, OpKind.SLICE, OpKind.RESHAPE):
+            return False
+    memo = {}
+
+    def trans(n):
+        if n.id not in by_id:
+            return False
+        if n.id not in memo:
+            memo[n.id] = (n.kind is OpKind.MAP and n.op.code in _TRANSCENDENTAL) or any(trans(p) for p in n.preds)
+        return memo[n.id]
+    return all(r.dtype.is_float and trans(r) for r in region.roots)
+
+
+CONTRACT = os.environ.get("GRUMPY_CONTRACT", "1") == "1"
+
+
 class PairMapEmitter(MapEmitter):
     """Map emitter whose lane loop walks lane PAIRS (v = 0 .. VEC/2-1) and
     evaluates f32 lane values as packed ``gr::f2`` (FADD2/FMUL2/FFMA2), bools
     as ``gr::b2``.  Values hoisted out of the lane loop stay scalar and are
-    splatted once where a lane pair consumes them."""
+    splatted once where a lane pair consumes them.  In an inexact region
+    (``inexact_region``) products feeding adds are left to ptxas's FFMA2
+    contraction."""
+
+    def __init__(self, *a, **k):
+        super().__init__(*a, **k)
+        self.contract = CONTRACT and inexact_region(self.region)
 
     def emit(self, level, ctype, expr):
         if level >= LEVEL_LANE:
@@ -666,7 +707,7 @@ class PairMapEmitter(MapEmitter):
             if any(lt not in (DType.f32, DType.bool8) for _, lt in args) or n.dtype not in (DType.f32, DType.bool8):
                 raise NotPairable(f"{code} on {n.loop}")
             names = [self.splat(a, lt)[0] for a, lt in args]
-            if code in (ElemCode.mul, ElemCode.square) and self._feeds_add(n):
+            if code in (ElemCode.mul, ElemCode.square) and self._feeds_add(n) and not self.contract:
                 # keep ptxas from contracting the product into its add (gr_pair.cuh)
                 fn = "gr::p2::mul_nc" if code is ElemCode.mul else "gr::p2::square_nc"
                 return self.emit(LEVEL_LANE, n.dtype.ctype, f"{fn}({', '.join(names)})"), LEVEL_LANE
