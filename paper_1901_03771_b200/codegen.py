@@ -330,6 +330,9 @@ class ValueEmitter:
             code = n.op.code
             if code is ElemCode.const_splat:
                 return self.const(n.op.attrs[0], n.dtype)
+            fused = self._fma(n, coords) if getattr(self, "fma_ok", False) else None
+            if fused is not None:
+                return fused
             args = []
             for p, lt in zip(n.preds, n.loop):
                 v = self.value(p, bcast_coords(coords, n.shape, p.shape))
@@ -396,6 +399,42 @@ class ValueEmitter:
         if k is OpKind.SLICE_ASSIGN:
             return self.slice_assign(n, coords)
         raise UnsupportedNodeInFusedStep(f"{n.op!r} cannot appear inside this fused step")
+
+    def _fma(self, n: Node, coords):
+        """add/sub with a single-use product operand as one fused multiply-add
+        (inexact regions only: ``fma_ok``, set by the map family)."""
+        code = n.op.code
+        if code not in (ElemCode.add, ElemCode.sub) or not n.dtype.is_float or n.loop[0] is not n.dtype:
+            return None
+        uses = getattr(self, "_uses", None)
+        if uses is None:
+            uses = self._uses = {}
+            for m in self.region.nodes:
+                for q in m.preds:
+                    uses[q.id] = uses.get(q.id, 0) + 1
+            for r in self.region.roots:
+                uses[r.id] = uses.get(r.id, 0) + 2
+        for k, prod in enumerate(n.preds):
+            if (prod.kind is OpKind.MAP and prod.op.code is ElemCode.mul and prod.id not in self.leaf_index
+                    and uses.get(prod.id, 0) == 1 and prod.dtype is n.dtype and prod.loop[0] is n.dtype
+                    and prod.loop[1] is n.dtype):
+                other = n.preds[1 - k]
+                pc = bcast_coords(coords, n.shape, prod.shape)
+                a = self.cast(self.value(prod.preds[0], bcast_coords(pc, prod.shape, prod.preds[0].shape)),
+                              prod.preds[0].dtype, n.dtype)
+                b = self.cast(self.value(prod.preds[1], bcast_coords(pc, prod.shape, prod.preds[1].shape)),
+                              prod.preds[1].dtype, n.dtype)
+                c = self.cast(self.value(other, bcast_coords(coords, n.shape, other.shape)), other.dtype, n.dtype)
+                T = n.dtype.ctype
+                lvl = max(a[1], b[1], c[1])
+                if code is ElemCode.add:
+                    expr = f"gr::fma_({a[0]}, {b[0]}, {c[0]})"
+                elif k == 0:            # a*b - c
+                    expr = f"gr::fma_({a[0]}, {b[0]}, gr::neg<{T}>({c[0]}))"
+                else:                   # c - a*b
+                    expr = f"gr::fma_(gr::neg<{T}>({a[0]}), {b[0]}, {c[0]})"
+                return self.emit(lvl, T, expr), lvl
+        return None
 
     def reshape_coords(self, coords, out_shape, in_shape) -> List[Aff]:
         """Index map through Reshape: linearize over the
@@ -812,6 +851,7 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
         lane = Var("v", LEVEL_LANE)
         cls = PairMapEmitter if pair else MapEmitter
         em = cls(region, vec if mode == "group" else 1, None, lane)
+        em.fma_ok = CONTRACT and inexact_region(region)
         if fast:
             em.fast, em.ns = True, "f"
         coords: List[Aff] = []

@@ -162,6 +162,11 @@ template <class T> __device__ __forceinline__ bool div_range_bad(const DivRange<
   return !(w.amin >= d.xlo && w.amax <= d.xhi);
 }
 
+// fused multiply-add for inexact regions (codegen.inexact_region): one
+// rounding of a*b+c where NumPy rounds the product and the sum separately
+__device__ __forceinline__ float fma_(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_(double a, double b, double c) { return fma(a, b, c); }
+
 template <class T> __device__ __forceinline__ T neg(T a) { return -a; }
 template <> __device__ __forceinline__ int neg(int a) { return (int)(0u - (unsigned)a); }
 template <> __device__ __forceinline__ i64 neg(i64 a) { return (i64)(0ull - (u64)a); }
