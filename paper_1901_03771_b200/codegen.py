@@ -844,7 +844,7 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
     # one 16-byte group per leaf per thread per trip: measured best for f32 and
     # f64 (BS f64 U=2: 80 regs, 4.13 ms; U=1: 46 regs, 4.02 ms)
     if unroll is None:
-        unroll = 1
+        unroll = int(os.environ.get("GRUMPY_MAP_UNROLL", "1"))
     rank = len(shape)
 
     def build(mode, pair=False, fast=False):
