@@ -473,20 +473,37 @@ def _matmul_dtype(dts):
 class Graph:
     """Append-only DAG with a weak node store (see module docstring)."""
 
+    # The store maps id -> weakref.ref(node) in a plain dict (a
+    # WeakValueDictionary's per-insert callback costs as much as building the
+    # node); dead entries are swept every _SWEEP appends.
+    _SWEEP = 4096
+
     def __init__(self):
-        self._nodes: "weakref.WeakValueDictionary[int, Node]" = weakref.WeakValueDictionary()
+        self._nodes: Dict[int, "weakref.ref[Node]"] = {}
+        self._since_sweep = 0
+
+    def _sweep(self):
+        self._nodes = {k: r for k, r in self._nodes.items() if r() is not None}
+        self._since_sweep = 0
 
     def __len__(self):
+        self._sweep()
         return len(self._nodes)
 
     def get(self, nid: int) -> Optional[Node]:
-        return self._nodes.get(nid)
+        r = self._nodes.get(nid)
+        return r() if r is not None else None
 
     def live_nodes(self) -> List[Node]:
-        return [self._nodes[k] for k in sorted(self._nodes.keys()) if k in self._nodes]
+        self._sweep()
+        out = [self._nodes[k]() for k in sorted(self._nodes)]
+        return [n for n in out if n is not None]
 
     def _append(self, n: Node) -> Node:
-        self._nodes[n.id] = n
+        self._nodes[n.id] = weakref.ref(n)
+        self._since_sweep += 1
+        if self._since_sweep >= self._SWEEP:
+            self._sweep()
         return n
 
     def add_input(self, buf: TensorBuffer) -> Node:
@@ -505,10 +522,14 @@ class Graph:
         so elementwise results are memoised: re-recording a loop body costs a
         dictionary hit per op instead of broadcasting and loop resolution."""
         if op.kind is OpKind.MAP:
-            key = (op, tuple([p.shape for p in preds]), tuple([p.dtype for p in preds]))
+            if len(preds) == 2:
+                a, b = preds
+                key = (op, a.shape, a.dtype, b.shape, b.dtype)
+            else:
+                key = (op,) + tuple([x for p in preds for x in (p.shape, p.dtype)])
             hit = _MAP_INFER.get(key)
             if hit is None:
-                hit = infer(op, key[1], key[2])
+                hit = infer(op, [p.shape for p in preds], [p.dtype for p in preds])
                 if len(_MAP_INFER) > 65536:
                     _MAP_INFER.clear()
                 _MAP_INFER[key] = hit
