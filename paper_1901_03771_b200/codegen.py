@@ -425,16 +425,19 @@ class ValueEmitter:
                 b = self.cast(self.value(prod.preds[1], bcast_coords(pc, prod.shape, prod.preds[1].shape)),
                               prod.preds[1].dtype, n.dtype)
                 c = self.cast(self.value(other, bcast_coords(coords, n.shape, other.shape)), other.dtype, n.dtype)
-                T = n.dtype.ctype
-                lvl = max(a[1], b[1], c[1])
-                if code is ElemCode.add:
-                    expr = f"gr::fma_({a[0]}, {b[0]}, {c[0]})"
-                elif k == 0:            # a*b - c
-                    expr = f"gr::fma_({a[0]}, {b[0]}, gr::neg<{T}>({c[0]}))"
-                else:                   # c - a*b
-                    expr = f"gr::fma_(gr::neg<{T}>({a[0]}), {b[0]}, {c[0]})"
-                return self.emit(lvl, T, expr), lvl
+                return self._fma_emit(n, a, b, c, k)
         return None
+
+    def _fma_emit(self, n: Node, a, b, c, k):
+        T = n.dtype.ctype
+        lvl = max(a[1], b[1], c[1])
+        if n.op.code is ElemCode.add:
+            expr = f"gr::fma_({a[0]}, {b[0]}, {c[0]})"
+        elif k == 0:            # a*b - c
+            expr = f"gr::fma_({a[0]}, {b[0]}, gr::neg<{T}>({c[0]}))"
+        else:                   # c - a*b
+            expr = f"gr::fma_(gr::neg<{T}>({a[0]}), {b[0]}, {c[0]})"
+        return self.emit(lvl, T, expr), lvl
 
     def reshape_coords(self, coords, out_shape, in_shape) -> List[Aff]:
         """Index map through Reshape: linearize over the
@@ -696,8 +699,9 @@ class PairMapEmitter(MapEmitter):
     evaluates f32 lane values as packed ``gr::f2`` (FADD2/FMUL2/FFMA2), bools
     as ``gr::b2``.  Values hoisted out of the lane loop stay scalar and are
     splatted once where a lane pair consumes them.  In an inexact region
-    (``inexact_region``) products feeding adds are left to ptxas's FFMA2
-    contraction."""
+    (``inexact_region``) a single-use product feeding an add/sub becomes an
+    explicit FFMA2 (the same products the scalar tail fuses); every other
+    product stays uncontractable (``mul_nc``)."""
 
     def __init__(self, *a, **k):
         super().__init__(*a, **k)
@@ -733,8 +737,33 @@ class PairMapEmitter(MapEmitter):
             raise NotPairable("cast inside the lane loop")
         return super().cast(val, frm, to)
 
+    def _fma_emit(self, n: Node, a, b, c, k):
+        """The packed form of ``ValueEmitter._fma``: exactly the products the
+        scalar (tail) body fuses are fused here, so a lane's result does not
+        depend on whether it ran packed or scalar (chunking, sharding)."""
+        if max(a[1], b[1], c[1]) < LEVEL_LANE:
+            return super()._fma_emit(n, a, b, c, k)
+        if n.dtype is not DType.f32:
+            raise NotPairable("fused multiply-add on non-f32 lanes")
+        if n.op.code is ElemCode.sub:
+            # negate the operand that is hoisted out of the lane loop when there
+            # is one (free), else per lane
+            tgt = 2 if k == 0 else 0
+            v = (a, b, c)[tgt]
+            if v[1] < LEVEL_LANE:
+                v = (MapEmitter.emit(self, v[1], "float", f"gr::neg<float>({v[0]})"), v[1])
+            else:
+                v = (self.emit(LEVEL_LANE, "float", f"gr::p2::neg({v[0]})"), LEVEL_LANE)
+            a, b, c = [v if i == tgt else x for i, x in enumerate((a, b, c))]
+        names = [self.splat(x, DType.f32)[0] for x in (a, b, c)]
+        return self.emit(LEVEL_LANE, "float", f"gr::p2::fma({names[0]}, {names[1]}, {names[2]})"), LEVEL_LANE
+
     def _value(self, n: Node, coords):
         if n.id not in self.leaf_index and n.op.kind is OpKind.MAP and n.op.code is not ElemCode.const_splat:
+            if self.contract:
+                fused = self._fma(n, coords)
+                if fused is not None:
+                    return fused
             code = n.op.code
             args = []
             for p, lt in zip(n.preds, n.loop):
@@ -746,7 +775,7 @@ class PairMapEmitter(MapEmitter):
             if any(lt not in (DType.f32, DType.bool8) for _, lt in args) or n.dtype not in (DType.f32, DType.bool8):
                 raise NotPairable(f"{code} on {n.loop}")
             names = [self.splat(a, lt)[0] for a, lt in args]
-            if code in (ElemCode.mul, ElemCode.square) and self._feeds_add(n) and not self.contract:
+            if code in (ElemCode.mul, ElemCode.square) and self._feeds_add(n):
                 # keep ptxas from contracting the product into its add (gr_pair.cuh)
                 fn = "gr::p2::mul_nc" if code is ElemCode.mul else "gr::p2::square_nc"
                 return self.emit(LEVEL_LANE, n.dtype.ctype, f"{fn}({', '.join(names)})"), LEVEL_LANE

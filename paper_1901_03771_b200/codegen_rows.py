@@ -45,6 +45,55 @@ class NotFusable(UnsupportedNodeInFusedStep):
         self.node = node
 
 
+# Certified nearest-centre argmin (gr_nearest.cuh): argmin_j sum_k (u_k - C[j,k])^2
+# over a constant-bank centre table ranks the centres by an expanded key (four
+# FFMA2 per centre pair instead of 4 sub + 4 mul + 3 add per centre) and runs
+# the exact NumPy-order scan only for rows whose label the key's error bound
+# cannot certify.  Labels are np.argmin's in every case.
+NEAREST = os.environ.get("GRUMPY_NEAREST", "1") == "1"
+NEAREST_MAX_D = 8
+# CTAs per SM asked of ptxas (__launch_bounds__ min blocks) for row kernels
+# with a nearest-centre search: the search itself needs few registers, the
+# rare exact fallback scan many; capping lets the fallback spill instead of
+# starving the hot loop of warps
+NEAREST_MIN_BLOCKS = int(os.environ.get("GRUMPY_NEAREST_MINB", "10"))
+NEAREST_MAX_K = 256
+
+
+def match_nearest(x: Node, axes):
+    """(u, centre leaf, K, D) when ``x`` is ((u - c) ** 2).sum(-1) with u of
+    shape (N, 1, D) and c a (1, K, D) / (K, D) view of an f32 leaf, reduced
+    over axis 1 of x's (N, K); else None."""
+    if (x.kind is not OpKind.REDUCE or x.dtype is not DType.f32 or len(x.shape) != 2 or tuple(axes) != (1,)):
+        return None
+    rop, raxes, keepdims, _odt = x.op.attrs
+    s = x.preds[0]
+    if rop is not ReduceOp.sum or keepdims or tuple(raxes) != (2,) or len(s.shape) != 3:
+        return None
+    N, K, D = s.shape
+    if not (2 <= K <= NEAREST_MAX_K and K % 2 == 0 and 1 <= D <= NEAREST_MAX_D):
+        return None
+    if s.kind is not OpKind.MAP or s.dtype is not DType.f32 or s.loop[0] is not DType.f32:
+        return None
+    if s.op.code is ElemCode.square:
+        d = s.preds[0]
+    elif s.op.code is ElemCode.mul and s.preds[0].id == s.preds[1].id:
+        d = s.preds[0]
+    else:
+        return None
+    if (d.kind is not OpKind.MAP or d.op.code is not ElemCode.sub or d.dtype is not DType.f32
+            or tuple(d.loop) != (DType.f32, DType.f32)):
+        return None
+    for u, c in (d.preds, d.preds[::-1]):
+        if tuple(u.shape) != (N, 1, D) or tuple(c.shape) not in ((1, K, D), (K, D)):
+            continue
+        while c.kind is OpKind.RESHAPE and not c.is_materialized:
+            c = c.preds[0]
+        if c.dtype is DType.f32 and tuple(c.shape) in ((K, D), (1, K, D)) and c.is_materialized:
+            return u, c, K, D
+    return None
+
+
 def is_total(n: Node) -> bool:
     """A reduction to a single value (all axes), e.g. y.sum() or argmax(axis=None)."""
     if n.kind is OpKind.REDUCE:
@@ -194,6 +243,8 @@ class LoopEmitter(ValueEmitter):
         self.pairs = set()            # emitted names holding a gr::f2
         # skinny product computed by the tile prologue: (canonical id, row key)
         self.skinny: Optional[tuple] = None
+        # centre leaf id -> (K, D, table symbol) of certified nearest-centre searches
+        self.nearest: Dict[int, tuple] = {}
 
     # -- scopes ------------------------------------------------------------------
     def emit(self, level, ctype, expr):
@@ -594,6 +645,47 @@ class LoopEmitter(ValueEmitter):
         n = element_count([So[a] for a in axes])
         if L >= 2 and n > SMALL_RECOMPUTE:
             raise NotFusable(r, f"arg-reduction over {n} points would be recomputed per column")
+        if NEAREST and which == "min" and self.half is None:
+            nn = self._nearest(x, axes, kept, L)
+            if nn is not None:
+                return nn
+        return self._argreduce_exact(x, which, axes, kept, L, n)
+
+    def _nearest(self, x: Node, axes, kept, L):
+        """argmin over ((u - C) ** 2).sum(-1) with C a constant-bank centre
+        table: the certified expanded-key search of gr_nearest.cuh, the exact
+        NumPy-order scan only for rows it cannot certify."""
+        m = match_nearest(x, axes)
+        if m is None:
+            return None
+        u, leaf, K, D = m
+        sym = self.cbank.get(leaf.id)
+        if sym is None or len(kept) != 1 or kept[0].level != L:
+            return None
+        tsym = sym + "_nn"
+        self.nearest[leaf.id] = (K, D, tsym)
+        pv = self.fresh("P")
+        self.stmt(L, f"float {pv}[{D}];")
+        iv, s, saved = self.open(L, "for", trip=D, unroll=True)
+        v = self.cast(self.value(u, [kept[0], Aff.of(0), Aff.of(iv)]), u.dtype, DType.f32)
+        self.stmt(iv.level, f"{pv}[{iv.name}] = {v[0]};")
+        self.close(s, saved)
+        lab = self.fresh("a")
+        self.stmt(L, f"int {lab}; const bool {lab}ok = gr::nearest_centre<{K}, {D}>({pv}, {tsym}, {lab});")
+        bi = self.var_decl(L, "long long", lab)
+        saved_if = self.stack[L + 1:]
+        del self.stack[L + 1:]
+        sif = Scope(L + 1, "for", header=f"if (!{lab}ok)")
+        self.stack.append(sif)
+        ebi, _ = self._argreduce_exact(x, "min", axes, kept, L + 1, K)
+        self.stmt(L + 1, f"{bi} = {ebi};")
+        self.close(sif, saved_if)
+        return bi, L
+
+    def _argreduce_exact(self, x: Node, which, axes, kept, L, n):
+        """First-index arg-reduction in NumPy's order (the value compared is
+        the operand exactly as NumPy computes it)."""
+        So = x.shape
         T = x.dtype.ctype
         best = self.var_decl(L, T, "0")
         bi = self.var_decl(L, "long long", "0")
@@ -1074,6 +1166,17 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
                       f"    dst[i] = (unsigned long long)__float_as_uint(src[lo]) | ((unsigned long long)__float_as_uint(src[lo + {B}]) << 32);\n"
                       "  }\n}\n")
     inc = '#include "gr_reduce.cuh"\n'
+    for lid, (K_, D_, tsym) in em.nearest.items():
+        # certified nearest-centre table (gr_nearest.cuh), packed per launch
+        i = next(j for j, l in enumerate(region.leaves) if l.id == lid)
+        H_ = (D_ + 3) // 2 + ((D_ + 3) // 2) % 2
+        words = H_ + K_ // 2 * ((D_ + 2) + (D_ + 2) % 2)
+        cdecl += (f"__constant__ float2 {tsym}[{words}];\n"
+                  f'extern "C" __global__ void gr_nnpack{i}(const float* __restrict__ src, float2* dst) {{\n'
+                  f"  gr::nearest_pack<{K_}, {D_}>(src, dst);\n}}\n")
+        used_pair.append((i, tsym, 0, words, f"gr_nnpack{i}"))
+    if em.nearest:
+        inc += '#include "gr_nearest.cuh"\n'
     if mms:
         # A by TMA (tensor map first in the parameter block), B as k-pairs in
         # the constant bank written by a one-CTA repack kernel of the module
@@ -1092,7 +1195,8 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
            f"  static constexpr long long NROWS = {R}LL;"]
     src.append("  " + "\n  ".join(lines))
     src.append("};")
-    kern = [f'extern "C" __global__ void __launch_bounds__({block}) {kname}(const K::Params p) {{',
+    lb = f"{block}, {NEAREST_MIN_BLOCKS}" if em.nearest and NEAREST_MIN_BLOCKS > 0 else f"{block}"
+    kern = [f'extern "C" __global__ void __launch_bounds__({lb}) {kname}(const K::Params p) {{',
             "  const long long stride = (long long)gridDim.x * blockDim.x;"]
     skinny_smem = 0
     if mms:

@@ -1,0 +1,144 @@
+// gr_nearest.cuh — certified nearest-centre search for argmin over squared
+// distances to a small constant set of centres (k-means assignment, C5).
+//
+// The user program is NumPy's
+//     d = ((P[:, None, :] - C[None]) ** 2).sum(-1);  lab = d.argmin(1)
+// whose labels must match np.argmin over NumPy's float32 distances exactly
+// (first index on ties, NaN extreme).  Evaluating d as written costs 4 sub,
+// 4 mul and 3 add per centre plus the ordered compare.  Here each row instead
+// ranks the centres by the expanded distance
+//     key_j = (||c'_j||^2 + ||p'||^2) - 2 p'.c'_j     (p' = p - o, c' = c - o)
+// one FADD2 and four FFMA2 per centre PAIR, with the centre index written into
+// the key's low mantissa bits so that one FMNMX keeps both the best key and
+// its index.  The two smallest keys are tracked (m1 < m2, FMNMX3); the label
+// is certified when
+//     m2 - m1 > 2.1 Dc + e (|m1| + |m2|) + 8e-7 max(m1 + e |m1| + Dc, 0) + 1e-35
+// with Dc = 24 u (||p'||^2 + 2 max_j ||c'_j||^2) bounding the chain's error
+// against the exact distance D_j (origin shift 4.06u, ||c'||^2 and ||p'||^2
+// roundings 5u, five roundings of terms <= 2R 10u; u = 2^-24), e = 1.01 *
+// 2^(BITS-23) the index bits' relative perturbation (x - e|x| is increasing,
+// so every key >= m2 bounds its distance below by m2 - e|m2| - Dc), and
+// 8e-7 > 2.01 gamma_6 NumPy's own rounding of the distances (six roundings of
+// non-negative terms: |D^_j - D_j| <= gamma_6 D_j).  Then D^_label < D^_j for
+// every other centre: the label IS np.argmin.  A row that fails (near-ties,
+// NaN or inf anywhere, magnitudes above 1e37 where the chain could overflow)
+// returns false and the caller runs the exact NumPy-order scan for it.
+//
+// Table layout (written per launch by the region's one-CTA pack kernel from
+// the centre leaf, in the constant bank): float2 tab[H + K/2 * S], records
+// 16-byte aligned (H, S even) so each is whole LDCU.128 loads,
+//   header (H float2): o[0..D-1] (origin, the centres' mean),
+//   o[D] = CC = max_j ||c'_j||^2 rounded up (NaN when any centre is not
+//   finite: every row then takes the exact scan), o[D+1] = ~MASK (bits);
+//   pair jp: tab[H + jp*S + k] = (c'_{2jp,k}, c'_{2jp+1,k}), k < D, and
+//   tab[H + jp*S + D] = (||c'_{2jp}||^2, ||c'_{2jp+1}||^2) (double, rounded),
+//   tab[H + jp*S + D + 1] = the index pair (2jp, 2jp+1) as integer bits (a
+//   uniform operand of the embedding LOP3 instead of a per-key immediate move).
+#pragma once
+
+namespace gr {
+
+template <int K, int D>
+struct Nearest {
+  static_assert(K >= 2 && K % 2 == 0 && K <= 256, "centre count");
+  static constexpr int H = (D + 3) / 2 + ((D + 3) / 2) % 2;   // 16-byte aligned records
+  static constexpr int S = (D + 2) + (D + 2) % 2;              // float2 per centre pair (even)
+  static constexpr int BITS = K <= 2 ? 1 : K <= 4 ? 2 : K <= 8 ? 3 : K <= 16 ? 4 : K <= 32 ? 5 : K <= 64 ? 6 : K <= 128 ? 7 : 8;
+  static constexpr unsigned MASK = (1u << BITS) - 1u;
+  static constexpr int WORDS = H + K / 2 * S;
+};
+
+__device__ __forceinline__ unsigned nn_embed(float v, unsigned keep, unsigned idx) {
+  unsigned r;
+  // (bits & keep) | idx in one LOP3 (keep held in a register)
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(__float_as_uint(v)), "r"(keep), "r"(idx));
+  return r;
+}
+__device__ __forceinline__ float nn_min3(float a, float b, float c) {
+  float r;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+template <int K, int D>
+__device__ __forceinline__ bool nearest_centre(const float (&p)[D], const float2* __restrict__ tab, int& label) {
+  using N = Nearest<K, D>;
+  const float* hdr = reinterpret_cast<const float*>(tab);
+  float q[D];
+  float pp = 0.0f;
+#pragma unroll
+  for (int k = 0; k < D; ++k) {
+    const float pk = __fsub_rn(p[k], hdr[k]);
+    q[k] = -2.0f * pk;
+    pp = __fmaf_rn(pk, pk, pp);
+  }
+  // the mask as a register operand (a volatile read of the header word the
+  // pack kernel wrote): the LOP3 then takes the index pair as its uniform
+  // operand, no per-key index move or LDC
+  const unsigned keep = *reinterpret_cast<const volatile unsigned*>(hdr + D + 1);
+  const float inf = __int_as_float(0x7f800000);
+  float m1 = inf, m2 = inf;
+#pragma unroll
+  for (int jp = 0; jp < K / 2; ++jp) {
+    const float2* c = tab + N::H + jp * N::S;
+    float2 acc = __fadd2_rn(make_float2(pp, pp), c[D]);
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc = __ffma2_rn(make_float2(q[k], q[k]), c[k], acc);
+    // the record's index pair (2jp, 2jp+1) arrives with its centre words
+    const float2 ix = c[D + 1];
+    const float k0 = __uint_as_float(nn_embed(acc.x, keep, __float_as_uint(ix.x)));
+    const float k1 = __uint_as_float(nn_embed(acc.y, keep, __float_as_uint(ix.y)));
+    const float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
+    m2 = nn_min3(m2, fmaxf(m1, lo), hi);
+    m1 = fminf(m1, lo);
+  }
+  label = (int)(__float_as_uint(m1) & N::MASK);
+  constexpr float E = 1.01f * (float)(1u << N::BITS) * 1.1920928955078125e-07f;
+  const float R = pp + 2.0f * hdr[D];
+  const float dc = 24.0f * 5.9604644775390625e-08f * R;
+  const float a1 = fabsf(m1), a2 = fabsf(m2);
+  const float thr = 2.1f * dc + E * (a1 + a2) + 8e-7f * fmaxf(m1 + E * a1 + dc, 0.0f) + 1e-35f;
+  // NaN anywhere (p, centres, keys) makes a comparison false: exact scan
+  return R < 1e37f && m2 - m1 > thr;
+}
+
+// Pack kernel body (one CTA): origin, CC and the pair table from the row-major
+// [K][D] centre leaf.
+template <int K, int D>
+__device__ __forceinline__ void nearest_pack(const float* __restrict__ src, float2* __restrict__ tab) {
+  using N = Nearest<K, D>;
+  __shared__ double o[D];
+  __shared__ double cc[K];
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  if (threadIdx.x < D) {
+    double s = 0.0;
+    for (int j = 0; j < K; ++j) s += (double)src[j * D + threadIdx.x];
+    o[threadIdx.x] = (double)(float)(s / K);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < D; ++k) {
+      const float v = src[j * D + k];
+      if (!isfinite(v)) bad = 1;
+      const float cp = __fsub_rn(v, (float)o[k]);
+      s += (double)cp * (double)cp;
+      reinterpret_cast<float*>(tab + N::H + (j / 2) * N::S + k)[j & 1] = cp;
+    }
+    cc[j] = s;
+    reinterpret_cast<float*>(tab + N::H + (j / 2) * N::S + D)[j & 1] = (float)s;
+    reinterpret_cast<unsigned*>(tab + N::H + (j / 2) * N::S + D + 1)[j & 1] = (unsigned)j;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int j = 0; j < K; ++j) m = cc[j] > m ? cc[j] : m;
+    float* hdr = reinterpret_cast<float*>(tab);
+    for (int k = 0; k < D; ++k) hdr[k] = (float)o[k];
+    hdr[D] = bad ? __int_as_float(0x7fffffff) : __double2float_ru(m * (1.0 + 1e-6));
+    reinterpret_cast<unsigned*>(hdr)[D + 1] = ~N::MASK;
+  }
+}
+
+}  // namespace gr

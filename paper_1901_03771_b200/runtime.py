@@ -21,6 +21,10 @@ import numpy as np
 from .errors import NativeLibraryMissing, RuntimeFailure
 from .tensor import DType
 
+# bytes of per-thread local memory (spill) a register-capped rebuild of a map
+# kernel may use and still be kept for its extra resident CTAs
+TUNE_MAX_LOCAL = int(os.environ.get("GRUMPY_TUNE_MAX_LOCAL", "0"))
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgrumpy_rt.so")
 KERNEL_DIR = os.path.join(HERE, "csrc", "kernels")
@@ -339,7 +343,7 @@ class Runtime:
                 k2 = self._kernel(source.replace(tag, f"__launch_bounds__({block}, {want})"), name, block, smem)
                 local = ctypes.c_int(0)
                 _check(self.lib.grumpy_rt_function_info(k2.fn, None, ctypes.byref(local), None, None))
-                if local.value == 0 and k2.blocks_per_sm > k.blocks_per_sm:
+                if local.value <= TUNE_MAX_LOCAL and k2.blocks_per_sm > k.blocks_per_sm:
                     k = k2
         self._kernels[(source, name, tune)] = k
         return k

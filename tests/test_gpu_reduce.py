@@ -216,3 +216,51 @@ def test_kmeans_lloyd_iterations_exact(sess):
         assert np.array_equal(np.asarray(lab), elab)
         assert np.array_equal(np.asarray(counts), ecounts)
         C = wl.kmeans_centroids(esums, ecounts, C)
+
+
+@pytest.mark.parametrize("K,D,scale", [(64, 4, 1.0), (2, 1, 1e-3), (8, 3, 50.0), (256, 8, 1e4), (16, 2, 1e-20),
+                                       (64, 4, 1e3)])
+def test_nearest_centre_certified_exact(sess, K, D, scale):
+    """The certified expanded-key search (gr_nearest.cuh) with its exact
+    fallback: labels equal np.argmin on adversarial inputs — points on
+    bisectors (exact ties), a few ulps off them, on centres, duplicated
+    centres, far points, non-finite coordinates — and bincount partials of
+    the same region stay right."""
+    rng = np.random.default_rng([K, D])
+    C = (rng.standard_normal((K, D)) * scale).astype(np.float32)
+    if K >= 4:
+        C[K // 2] = C[1]
+    n = 40000
+    P = (C[rng.integers(0, K, n)] + rng.standard_normal((n, D)).astype(np.float32) * np.float32(scale * 0.5)).astype(np.float32)
+    i, j = rng.integers(0, K, 3000), rng.integers(0, K, 3000)
+    P[:3000] = ((C[i].astype(np.float64) + C[j]) / 2).astype(np.float32)
+    P[3000:6000] = (P[:3000] * (1 + rng.integers(-4, 5, (3000, 1)) * np.float32(2 ** -23))).astype(np.float32)
+    P[6000:6100] = C[rng.integers(0, K, 100)]
+    P[6100] *= np.float32(1e3)
+    P[6101, 0] = np.nan
+    P[6102] = np.inf
+    P[6103, -1] = np.float32(3e19)
+    lab = wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C))
+    got = np.asarray(lab)
+    assert "gr::nearest_centre" in sess.executor.last_steps[0].cache["ks"].source
+    assert np.array_equal(got, wl.kmeans_assign(np, P, C))
+    C2 = C.copy()
+    C2[K - 1, 0] = np.nan                  # a NaN centre: every row takes the exact scan
+    assert np.array_equal(np.asarray(wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C2))), wl.kmeans_assign(np, P, C2))
+
+
+def test_nearest_centre_off_matches(sess, monkeypatch):
+    """GRUMPY_NEAREST=0 (the NumPy-order scan alone) gives the same labels."""
+    from paper_1901_03771_b200 import codegen, codegen_rows
+    P, C = wl.kmeans_inputs(n=(1 << 15) + 3, k=64, d=4)
+    on = np.asarray(wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C)))
+    monkeypatch.setattr(codegen_rows, "NEAREST", False)
+    codegen._GEN_CACHE.clear()
+    sess._plan_cache.clear()
+    try:
+        off = wl.kmeans_assign(gp, gp.asarray(P), gp.asarray(C))
+        got = np.asarray(off)
+        assert "gr::nearest_centre" not in sess.executor.last_steps[0].cache["ks"].source
+    finally:
+        codegen._GEN_CACHE.clear()
+    assert np.array_equal(on, got) and np.array_equal(on, wl.kmeans_assign(np, P, C))
