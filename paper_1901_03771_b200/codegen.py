@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import math
 import os
+import re
 import struct
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -406,24 +407,37 @@ class ValueEmitter:
         code = n.op.code
         if code not in (ElemCode.add, ElemCode.sub) or not n.dtype.is_float or n.loop[0] is not n.dtype:
             return None
-        uses = getattr(self, "_uses", None)
-        if uses is None:
-            uses = self._uses = {}
+        fusable = getattr(self, "_fusable", None)
+        if fusable is None:
+            # products every consumer of which is an add/sub of the same type
+            # (and that are not roots): each consumer fuses its own copy
+            users = {}
             for m in self.region.nodes:
                 for q in m.preds:
-                    uses[q.id] = uses.get(q.id, 0) + 1
-            for r in self.region.roots:
-                uses[r.id] = uses.get(r.id, 0) + 2
-        for k, prod in enumerate(n.preds):
-            if (prod.kind is OpKind.MAP and prod.op.code is ElemCode.mul and prod.id not in self.leaf_index
-                    and uses.get(prod.id, 0) == 1 and prod.dtype is n.dtype and prod.loop[0] is n.dtype
-                    and prod.loop[1] is n.dtype):
+                    users.setdefault(q.id, []).append(m)
+            roots = {r.id for r in self.region.roots}
+            fusable = self._fusable = set()
+            for m in self.region.nodes:
+                if (m.kind is OpKind.MAP and m.op.code in (ElemCode.mul, ElemCode.square) and m.id not in roots
+                        and m.id not in self.leaf_index and all(lt is m.dtype for lt in m.loop)):
+                    us = users.get(m.id, [])
+                    adds = [u.kind is OpKind.MAP and u.op.code in (ElemCode.add, ElemCode.sub) and u.dtype is m.dtype
+                            for u in us]
+                    if us and ((FMA_MULTI == "any" and any(adds)) or (FMA_MULTI == "all" and all(adds))
+                               or (len(us) == 1 and all(adds))):
+                        fusable.add(m.id)
+        order = list(enumerate(n.preds))
+        if FMA_PICK == "last":
+            order.reverse()
+        for k, prod in order:
+            if prod.id in fusable and prod.dtype is n.dtype:
                 other = n.preds[1 - k]
                 pc = bcast_coords(coords, n.shape, prod.shape)
                 a = self.cast(self.value(prod.preds[0], bcast_coords(pc, prod.shape, prod.preds[0].shape)),
                               prod.preds[0].dtype, n.dtype)
-                b = self.cast(self.value(prod.preds[1], bcast_coords(pc, prod.shape, prod.preds[1].shape)),
-                              prod.preds[1].dtype, n.dtype)
+                b = a if prod.op.code is ElemCode.square else self.cast(
+                    self.value(prod.preds[1], bcast_coords(pc, prod.shape, prod.preds[1].shape)),
+                    prod.preds[1].dtype, n.dtype)
                 c = self.cast(self.value(other, bcast_coords(coords, n.shape, other.shape)), other.dtype, n.dtype)
                 return self._fma_emit(n, a, b, c, k)
         return None
@@ -692,6 +706,22 @@ def inexact_region(region: Region) -> bool:
 
 
 CONTRACT = os.environ.get("GRUMPY_CONTRACT", "1") == "1"
+# fuse a product into every add/sub that consumes it (the product itself is
+# then never formed) rather than only into a sole consumer
+# ptxas's own FFMA2 contraction of the packed body (with the tail run through
+# the same body): measured 1.054 vs 1.078 ms on Black-Scholes f32, but which
+# product ptxas fuses in a*b - c*d follows the emission order, which differs
+# between recordings of the same program (streamed chunks vs a plain force
+# disagreed in the last bit) — off; explicit, DAG-determined fusion instead
+PTXAS_CONTRACT = os.environ.get("GRUMPY_PTXAS_CONTRACT", "0") == "1"
+# "one": only a product with a single (add/sub) consumer; "all": a product all
+# of whose consumers are adds/subs; "any": every add/sub consumer fuses its own
+# copy of the product (the product is still formed for other consumers) — the
+# choice ptxas makes when it contracts
+FMA_MULTI = os.environ.get("GRUMPY_FMA_MULTI", "one")
+# which product an add/sub of two fusable products fuses: its "first" or
+# "last" operand (fixed by the DAG, never by emission order)
+FMA_PICK = os.environ.get("GRUMPY_FMA_PICK", "last")
 
 
 class PairMapEmitter(MapEmitter):
@@ -706,6 +736,11 @@ class PairMapEmitter(MapEmitter):
     def __init__(self, *a, **k):
         super().__init__(*a, **k)
         self.contract = CONTRACT and inexact_region(self.region)
+        # "explicit": the single-use products fused as explicit FFMA2 (the
+        # same ones the scalar tail fuses); "ptxas": products feeding adds
+        # are plain FMUL2 that ptxas contracts itself — used only when every
+        # point of the space runs this packed body (no scalar tail)
+        self.contract_mode = "explicit"
 
     def emit(self, level, ctype, expr):
         if level >= LEVEL_LANE:
@@ -760,7 +795,7 @@ class PairMapEmitter(MapEmitter):
 
     def _value(self, n: Node, coords):
         if n.id not in self.leaf_index and n.op.kind is OpKind.MAP and n.op.code is not ElemCode.const_splat:
-            if self.contract:
+            if self.contract and self.contract_mode == "explicit":
                 fused = self._fma(n, coords)
                 if fused is not None:
                     return fused
@@ -775,7 +810,8 @@ class PairMapEmitter(MapEmitter):
             if any(lt not in (DType.f32, DType.bool8) for _, lt in args) or n.dtype not in (DType.f32, DType.bool8):
                 raise NotPairable(f"{code} on {n.loop}")
             names = [self.splat(a, lt)[0] for a, lt in args]
-            if code in (ElemCode.mul, ElemCode.square) and self._feeds_add(n):
+            if code in (ElemCode.mul, ElemCode.square) and self._feeds_add(n) and not (
+                    self.contract and self.contract_mode == "ptxas"):
                 # keep ptxas from contracting the product into its add (gr_pair.cuh)
                 fn = "gr::p2::mul_nc" if code is ElemCode.mul else "gr::p2::square_nc"
                 return self.emit(LEVEL_LANE, n.dtype.ctype, f"{fn}({', '.join(names)})"), LEVEL_LANE
@@ -876,11 +912,13 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
         unroll = int(os.environ.get("GRUMPY_MAP_UNROLL", "1"))
     rank = len(shape)
 
-    def build(mode, pair=False, fast=False):
+    def build(mode, pair=False, fast=False, contract_mode="explicit"):
         lane = Var("v", LEVEL_LANE)
         cls = PairMapEmitter if pair else MapEmitter
         em = cls(region, vec if mode == "group" else 1, None, lane)
-        em.fma_ok = CONTRACT and inexact_region(region)
+        em.fma_ok = CONTRACT and inexact_region(region) and contract_mode == "explicit"
+        if pair:
+            em.contract_mode = contract_mode
         if fast:
             em.fast, em.ns = True, "f"
         coords: List[Aff] = []
@@ -921,9 +959,18 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
 
     # ---- group body (vectorised); f32 regions evaluate lane pairs packed
     pair = False
+    packed_tail = False
     if vec % 2 == 0 and os.environ.get("GRUMPY_PAIR", "1") != "0":
         try:
-            em, outs = build("group", pair=True)
+            if PTXAS_CONTRACT and CONTRACT and inexact_region(region) and (tail == 0 or rank == 1):
+                # ptxas contraction, provided the tail (if any) can run this
+                # same packed body (every point then gets the same contractions)
+                em, outs = build("group", pair=True, contract_mode="ptxas")
+                packed_tail = tail == 0 or _packable_tail(em)
+                if not packed_tail:
+                    em, outs = build("group", pair=True)
+            else:
+                em, outs = build("group", pair=True)
             pair = True
         except NotPairable:
             pair = False
@@ -1003,7 +1050,20 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
 
     # ---- scalar tail (rank-1 spaces whose length is not a multiple of VEC)
     tail_lines = ["static __device__ __forceinline__ void tail(const Params& p) {"]
-    if tail:
+    if tail and packed_tail and pair:
+        # the last partial group through the packed body: masked vector loads
+        # and stores, lanes beyond the end computed on a copy of element 0
+        tail_lines.append("  const int u = 0; (void)u;")
+        tail_lines.append(f"  const {ictype} lin = ({ictype}){ngroups * vec}; (void)lin;")
+        for l in consts:
+            tail_lines.append("  " + l)
+        for d in em.group_decls:
+            tail_lines.append("  " + d.replace("[N]", "[1]"))
+        for l in em.group_lines:
+            tail_lines.append("  " + _TAIL_LD.sub(rf"gr::ldv_part<\1, \2>(\3, \4 + (lin), {tail});", l))
+        for l in lane_loop(em, outs, pair, "  "):
+            tail_lines.append(_TAIL_ST.sub(rf"gr::stv_part<\1, \2>(\3 + lin, \4, {tail});", l))
+    elif tail:
         em2, outs2 = build("tail")
         consts2 = em2.consts
         tail_lines.append(f"  for (int v = 0; v < {tail}; ++v) {{")
@@ -1038,6 +1098,20 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
                         root_slots=list(range(len(region.roots))),
                         block=block, groups=ngroups, vec=vec, unroll=unroll,
                         meta={"shape": shape, "tail": tail, "fast_group": bool(fast_fn)})
+
+
+_TAIL_LD = re.compile(r"gr::ldv<([^,]+), (\d+)>\(([^,]+), (p\.in\d+) \+ \(lin\)\);")
+_TAIL_ST = re.compile(r"gr::stv<([^,]+), (\d+)>\((p\.out\d+) \+ lin, (o\d+)\);")
+
+
+def _packable_tail(em) -> bool:
+    """Every global access of the packed group body is a whole vector at the
+    group's start (rank-1 contiguous leaves), so the last partial group can
+    run the same body with masked loads and stores."""
+    for l in em.group_lines:
+        if "p.in" in l and not _TAIL_LD.fullmatch(l.strip()):
+            return False
+    return not any("p.in" in l for l in em.lane_lines)
 
 
 def _wrap_consts(fn_lines, consts):
@@ -1141,12 +1215,11 @@ def generate(region: Region) -> KernelSource:
         return codegen_rows.gen_rows(region)
     if kinds & {OpKind.REDUCE, OpKind.ARGREDUCE}:
         from . import codegen_coop, codegen_wrow
-        ks = codegen_coop.try_generate(region)
-        if ks is not None:
-            return ks
-        ks = codegen_wrow.try_generate(region)
-        if ks is not None:
-            return ks
+        order = (codegen_wrow, codegen_coop) if ROW_FAMILY == "wrow" else (codegen_coop, codegen_wrow)
+        for fam in order:
+            ks = fam.try_generate(region)
+            if ks is not None:
+                return ks
         return codegen_rows.gen_rows(region)
     from . import codegen_tile
     ks = codegen_tile.try_generate(region)
@@ -1154,6 +1227,10 @@ def generate(region: Region) -> KernelSource:
         return ks
     return gen_map(region)
 
+
+# long-row reduction regions: the cooperative register-staged family first
+# ("coop", default) or the warp-per-row shared-memory ring ("wrow")
+ROW_FAMILY = os.environ.get("GRUMPY_ROW_FAMILY", "coop")
 
 _GEN_CACHE: Dict[tuple, KernelSource] = {}
 

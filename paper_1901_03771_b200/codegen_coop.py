@@ -184,36 +184,8 @@ class CoopEmitter(LoopEmitter):
         """Packed element ops; a division by a row-level divisor keeps the
         shared-reciprocal Markstein form (two FFMA2 per pair) instead of the
         per-lane IEEE division."""
-        from .dag import ElemCode
-        if n.op.code is ElemCode.div and n.loop[0] is DType.f32 and n.dtype is DType.f32:
-            a = self.cast(self.value(n.preds[0], bcast_coords(coords, n.shape, n.preds[0].shape)),
-                          n.preds[0].dtype, n.loop[0])
-            b = self.cast(self.value(n.preds[1], bcast_coords(coords, n.shape, n.preds[1].shape)),
-                          n.preds[1].dtype, n.loop[1])
-            if self.is_pair(a) and not self.is_pair(b) and b[1] < a[1]:
-                rk = ("rcp", b[0])
-                r = self.const_memo.get(rk)
-                if r is None or b[1] > 0:
-                    r = self.emit(b[1], "gr::DivShared<float>", f"gr::div_prep<float>({b[0]})")
-                    if b[1] == 0:
-                        self.const_memo[rk] = r
-                r2 = self.const_memo.get(("rcp2", r))
-                if r2 is None:
-                    r2 = self.emit(max(b[1], 0), "gr::p2::DivShared2", f"gr::p2::div_prep2({r})")
-                    self.const_memo[("rcp2", r)] = r2
-                if self.div_fast and b[1] == 1:
-                    w = self.const_memo.get(("divrange", r))
-                    if w is None:
-                        w = self.fresh("w")
-                        self.stmt(1, f"gr::DivRange<float> {w} = gr::div_range_init<float>();")
-                        self.const_memo[("divrange", r)] = w
-                        self.div_finalize.append(f"bad |= gr::div_range_bad<float>({w}, {r});")
-                    self.used_div_fast = True
-                    return self.emit_pair(a[1], f"gr::p2::div_shr<FAST>({a[0]}, {r2}, {w})"), a[1]
-                if not self.div_fast:
-                    return self.emit_pair(a[1], f"gr::p2::div_shared({a[0]}, {r2})"), a[1]
-                raise NotPairable("paired division outside the row-divisor form")
-        return super()._pair_map(n, coords)
+        v = shared_div_pair(self, n, coords)
+        return v if v is not None else super()._pair_map(n, coords)
 
     # -- row-complete reductions ---------------------------------------------------
     def _row_complete(self, r: Node, axes) -> bool:
@@ -725,3 +697,40 @@ def _generate1(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetc
                             "bulk_copy": bool(tma), "cp_async": async_layout is not None,
                             "label": "coop-tma" if tma else ("coop-async" if async_layout is not None else "coop")})
     return ks, em
+
+
+def shared_div_pair(em, n: Node, coords):
+    """A packed division by a row-level (shared) divisor: one reciprocal per
+    row, the Markstein correction as two FFMA2 per pair; with the emitter's
+    two-pass division (``div_fast``) the dividends' range is tracked and the
+    row is redone exactly when any left the window.  None when ``n`` is not
+    such a division."""
+    from .dag import ElemCode
+    if not (n.op.code is ElemCode.div and n.loop[0] is DType.f32 and n.dtype is DType.f32):
+        return None
+    a = em.cast(em.value(n.preds[0], bcast_coords(coords, n.shape, n.preds[0].shape)), n.preds[0].dtype, n.loop[0])
+    b = em.cast(em.value(n.preds[1], bcast_coords(coords, n.shape, n.preds[1].shape)), n.preds[1].dtype, n.loop[1])
+    if not (em.is_pair(a) and not em.is_pair(b) and b[1] < a[1]):
+        return None
+    rk = ("rcp", b[0])
+    r = em.const_memo.get(rk)
+    if r is None or b[1] > 0:
+        r = em.emit(b[1], "gr::DivShared<float>", f"gr::div_prep<float>({b[0]})")
+        if b[1] == 0:
+            em.const_memo[rk] = r
+    r2 = em.const_memo.get(("rcp2", r))
+    if r2 is None:
+        r2 = em.emit(max(b[1], 0), "gr::p2::DivShared2", f"gr::p2::div_prep2({r})")
+        em.const_memo[("rcp2", r)] = r2
+    if em.div_fast and b[1] == 1:
+        w = em.const_memo.get(("divrange", r))
+        if w is None:
+            w = em.fresh("w")
+            em.stmt(1, f"gr::DivRange<float> {w} = gr::div_range_init<float>();")
+            em.const_memo[("divrange", r)] = w
+            em.div_finalize.append(f"bad |= gr::div_range_bad<float>({w}, {r});")
+        em.used_div_fast = True
+        return em.emit_pair(a[1], f"gr::p2::div_shr<FAST>({a[0]}, {r2}, {w})"), a[1]
+    if not em.div_fast:
+        return em.emit_pair(a[1], f"gr::p2::div_shared({a[0]}, {r2})"), a[1]
+    raise NotPairable("paired division outside the row-divisor form")

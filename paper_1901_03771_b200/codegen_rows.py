@@ -164,6 +164,15 @@ class CBankMiss(Exception):
         self.leaf = leaf
 
 
+# Row kernels whose rows are short contiguous slices of a leaf prefetch the
+# next grid-stride row of that leaf into L1 before evaluating the current one
+# (hides the load latency at the low occupancy of register-heavy row bodies)
+ROW_PREFETCH = os.environ.get("GRUMPY_ROW_PREFETCH", "1") == "1"
+ROW_PREFETCH_MAX_BYTES = 128
+# bincount keys are matched as 32-bit words (keys outside every histogram map
+# to one ignored word): MATCH.ANY on 32 bits instead of 64
+MATCH32 = os.environ.get("GRUMPY_MATCH32", "1") == "1"
+
 CBANK_LEAF_BYTES = 16 * 1024   # per leaf
 CBANK_TOTAL_BYTES = 48 * 1024  # per kernel (the user constant bank is 64 KB)
 CBANK_MIN_ROWS = 4096          # staging pays only when many rows reuse the leaf
@@ -380,6 +389,16 @@ class LoopEmitter(ValueEmitter):
                     self.stmt(plvl, f"gr::ldv<{T}, {trip}>({name}, {ptr} + {rest.c()});")
                     self.memo[key] = (name, plvl, self.stack[plvl] if plvl > 0 else None)
                     return f"{name}[{sc.var.name}]", lvl
+        # a scalar read covered by a vector load already issued in scope
+        # (k-means: the bincount weights P[r, d] after the row's P[r, :] load)
+        for trip in (16, 8, 4, 2):
+            for j in range(trip):
+                rest = off + Aff.of(-j)
+                if rest.const % trip or rest.alignment() % trip:
+                    continue
+                hit = self.memo.get(("vec", leaf.id, rest.key(), trip))
+                if hit is not None and (hit[1] == 0 or (hit[1] < len(self.stack) and self.stack[hit[1]] is hit[2])):
+                    return f"{hit[0]}[{j}]", max(lvl, hit[1])
         return self.emit(lvl, T, f"gr::ld<{T}>({ptr} + {off.c()})"), lvl
 
     # -- reductions -------------------------------------------------------------------
@@ -1092,7 +1111,15 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
         for j, (ri, r) in enumerate(keyed):
             if r.preds[0] is not key_node and r.preds[0].id != key_node.id:
                 raise NotFusable(r, "bincounts of one region must share their keys")
-            if len(r.preds) == 2:
+            w_ = r.preds[1] if len(r.preds) == 2 else None
+            if (w_ is not None and w_.kind is OpKind.CAST and w_.dtype is DType.f64
+                    and w_.preds[0].dtype in (DType.f32, DType.i32)):
+                w_ = w_.preds[0]
+            if w_ is not None and w_.dtype in (DType.f32, DType.i32):
+                # exactly representable in f64: shuffled at 4 bytes, widened on add
+                wv = em.value(w_, row_coords)
+                em.stmt(1, f"const {w_.dtype.ctype} kw{j} = {wv[0]};")
+            elif len(r.preds) == 2:
                 wv = em.cast(em.value(r.preds[1], row_coords), r.preds[1].dtype, DType.f64)
                 em.stmt(1, f"const double kw{j} = {wv[0]};")
             else:
@@ -1103,21 +1130,24 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
         # shuffle round per extra member, rounds = largest group - 1) and
         # alone updates the bin, so every bin sees a fixed order of adds.
         # Counts are the group's population count.
-        body = ["const unsigned kpeers = __match_any_sync(0xffffffffu, (unsigned long long)kkey);",
+        NBmax = max(r.op.attrs[0] for _j, r in wnames)
+        mkey = (f"(kkey >= 0 && kkey < {NBmax}LL) ? (unsigned)kkey : 0xffffffffu" if MATCH32 and NBmax < 2 ** 31
+                else "(unsigned long long)kkey")
+        body = [f"const unsigned kpeers = __match_any_sync(0xffffffffu, {mkey});",
                 "const unsigned klane = threadIdx.x & 31u;",
                 "const bool klead = (kpeers & ((1u << klane) - 1u)) == 0u;",
                 "unsigned krest = klead ? (kpeers & (kpeers - 1u)) : 0u;"]
         weighted = [(j, r) for j, r in wnames if len(r.preds) == 2]
         for j, r in weighted:
-            body.append(f"double ks{j} = kw{j};")
+            body.append(f"double ks{j} = (double)kw{j};")
         if weighted:
             body.append("while (__any_sync(0xffffffffu, krest != 0u)) {")
             body.append("  const int ksrc = krest ? __ffs(krest) - 1 : (int)klane;")
             for j, r in weighted:
-                body.append(f"  const double kv{j} = __shfl_sync(0xffffffffu, kw{j}, ksrc);")
+                body.append(f"  const auto kv{j} = __shfl_sync(0xffffffffu, kw{j}, ksrc);")
             body.append("  if (krest) {")
             for j, r in weighted:
-                body.append(f"    ks{j} += kv{j};")
+                body.append(f"    ks{j} += (double)kv{j};")
             body.append("    krest &= krest - 1u;")
             body.append("  }")
             body.append("}")
@@ -1137,6 +1167,19 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
 
     if mms and kmeta:
         raise NotFusable(mms[0], "skinny product with keyed sums")
+    # leaves read as short contiguous row slices: prefetched a row ahead
+    pref = []
+    if ROW_PREFETCH and virtual is None and len(Ts) == 1 and not mms:
+        body_txt = "\n".join(render(em.row, 1))
+        for i, l in enumerate(region.leaves):
+            if len(l.shape) < 1 or l.shape[0] != R or l.id in cbank:
+                continue
+            W = element_count(l.shape[1:])
+            if W * l.dtype.itemsize > ROW_PREFETCH_MAX_BYTES:
+                continue
+            pat = f"p.in{i} + ({W}*r" if W > 1 else f"p.in{i} + (r"
+            if pat in body_txt:
+                pref.append((i, W))
     lines = ["static __device__ __forceinline__ void row(const Params& p, const long long r, const bool valid"
              + "".join(f", {r.dtype.ctype}* khist{j}" for j, r, _, _ in kmeta)
              + (f", const float (&zk)[{NZ}]" if mms else "") + ") {",
@@ -1234,8 +1277,9 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
         kern.append("  __syncthreads();")
         hargs = "".join(f", khist{j}" for j, _, _, _ in kmeta)
         kern += ["  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < K::NROWS; base += stride) {",
-                 "    const long long r = base + (threadIdx.x & 31);",
-                 f"    K::row(p, r < K::NROWS ? r : K::NROWS - 1, r < K::NROWS{hargs});",
+                 "    const long long r = base + (threadIdx.x & 31);"]
+        kern += [f"    if (r + stride < K::NROWS) gr::prefetch_l1(p.in{i} + (r + stride) * {W}LL);" for i, W in pref]
+        kern += [f"    K::row(p, r < K::NROWS ? r : K::NROWS - 1, r < K::NROWS{hargs});",
                  "  }",
                  "  __syncthreads();"]
         for j, r, NBj, off in kmeta:
@@ -1246,8 +1290,13 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
                      f"    reinterpret_cast<{ct}*>(static_cast<char*>(p.scratch) + {off})[(long long)blockIdx.x * {NBj} + b] = s;",
                      "  }"]
     else:
-        kern += ["  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride)",
-                 "    K::row(p, r, true);"]
+        if pref:
+            kern += ["  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride) {"]
+            kern += [f"    if (r + stride < K::NROWS) gr::prefetch_l1(p.in{i} + (r + stride) * {W}LL);" for i, W in pref]
+            kern += ["    K::row(p, r, true);", "  }"]
+        else:
+            kern += ["  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride)",
+                     "    K::row(p, r, true);"]
     if tot_meta or kmeta:
         kern.append("  if (gr::last_block(p.ticket)) {")
         for j, r, NBj, off in kmeta:

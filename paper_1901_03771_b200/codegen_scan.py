@@ -31,6 +31,15 @@ from .tensor import DType, element_count, row_major_strides
 
 ITEMS = 16
 
+# Long 1-D scans whose inputs are contiguous arrays of the scan's length: TMA
+# tile ring (see _gen_lookback_tma)
+SCAN_TMA = os.environ.get("GRUMPY_SCAN_TMA", "0") == "1"
+SCAN_TMA_MIN = 1 << 20
+SCAN_TMA_SMEM = 200 * 1024
+SCAN_TMA_STAGES = int(os.environ.get("GRUMPY_SCAN_STAGES", "6"))
+SCAN_TMA_LAG = int(os.environ.get("GRUMPY_SCAN_LAG", "3"))
+SCAN_TMA_LBW = int(os.environ.get("GRUMPY_SCAN_LBW", "1"))
+
 
 def generate(region: Region, kname="gr_region") -> KernelSource:
     scans = [r for r in region.roots if r.kind is OpKind.SCAN]
@@ -44,6 +53,13 @@ def generate(region: Region, kname="gr_region") -> KernelSource:
             raise NotFusable(n, "reductions before a scan run as their own step")
     if axis is None or len(x.shape) == 1:
         n = element_count(x.shape)
+        if SCAN_TMA and len(x.shape) == 1 and n >= SCAN_TMA_MIN:
+            try:
+                ks = _gen_lookback_tma(region, s, x, rop, kname)
+                if ks is not None:
+                    return ks
+            except NotFusable:
+                pass
         if n > 8192:
             return _gen_lookback(region, s, x, rop, kname)
         return _gen_lines(region, s, x, rop, None, kname)
@@ -273,3 +289,264 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
                         block=NTH, groups=ntiles * NTH, vec=1, unroll=1, scratch_bytes=scratch,
                         meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,
                               "label": "scan-lookback", "smem": 2 * TP * T.itemsize})
+
+
+class _StagedEmitter(LoopEmitter):
+    """Loop emitter whose staged leaves are read from a swizzled shared-memory
+    tile (16-byte chunks, gr::lds_sw) instead of global memory."""
+
+    def __init__(self, region, staged, tb):
+        super().__init__(region, vec_loads=True)
+        self.staged = staged      # leaf id -> name of the tile's base pointer
+        self.tb = tb
+
+    def load_leaf(self, leaf, off):
+        sym = self.staged.get(leaf.id)
+        if sym is None:
+            if off.level >= 2:
+                raise NotFusable(leaf, "unstaged leaf read per element")
+            return super().load_leaf(leaf, off)
+        lvl = off.level
+        sc = self.stack[lvl] if lvl >= 2 else None
+        if sc is None or sc.kind != "for" or not sc.unroll or sc.var is None or off.coef(sc.var) != 1:
+            raise NotFusable(leaf, "staged leaf not read along the item loop")
+        rest = off.without(sc.var)
+        if rest.coef(self.tb) != 1 or sc.trip * leaf.dtype.itemsize != 16:
+            raise NotFusable(leaf, "staged leaf read off the tile")
+        rel = rest.without(self.tb)
+        key = ("svec", leaf.id, rel.key())
+        hit = self.memo.get(key)
+        if hit is not None and (hit[1] == 0 or (hit[1] < len(self.stack) and self.stack[hit[1]] is hit[2])):
+            return f"{hit[0]}[{sc.var.name}]", lvl
+        T = leaf.dtype.ctype
+        name = self.fresh("L")
+        plvl = max(rel.level, 1)
+        self.stmt(plvl, f"{T} {name}[{sc.trip}];")
+        self.stmt(plvl, f"gr::lds_sw<{T}, {sc.trip}>({name}, {sym}, (unsigned){rel.c()});")
+        self.memo[key] = (name, plvl, self.stack[plvl] if plvl > 0 else None)
+        return f"{name}[{sc.var.name}]", lvl
+
+
+def _gen_lookback_tma(region, s, x, rop, kname):
+    """Single-pass look-back scan fed by TMA (sm_100a).
+
+    A producer warp streams each input leaf's 32 KB tile into a ring of
+    shared-memory stages with cp.async.bulk.tensor (128-byte swizzle,
+    mbarrier completion) as far ahead as the ring allows, so the loads of
+    the next tiles are always in flight; 16 data warps read their 16
+    consecutive elements per thread straight from the swizzled tile
+    (conflict-free 16-byte chunks), evaluate the map prologue in registers and
+    scan (thread run, warp, CTA), and one look-back warp resolves the tile
+    prefix (gr::tile_lookback) while the data warps scan the next tile.  The
+    finished tile is written back into its stage and leaves with one TMA
+    tensor store.  Association is the same as the register-staged kernel
+    (_gen_lookback): the results are bit-identical to it."""
+    T = s.dtype
+    ct = T.ctype
+    N = element_count(x.shape)
+    isz = T.itemsize
+    if isz not in (4, 8):
+        return None
+    staged = [l for l in region.leaves if tuple(l.shape) == (N,)]
+    if not staged or any(l.dtype.itemsize != isz for l in staged):
+        return None
+    W = 128 // isz                       # elements per 128-byte line
+    if N % W:
+        return None
+    TPB = 512 if isz == 4 else 256
+    tile = TPB * ITEMS
+    tile_b = tile * isz                  # 32 KB
+    rows = tile // W                     # 256 lines per box
+    ntiles = -(-N // tile)
+    NL = len(staged)
+    S_ = min(SCAN_TMA_STAGES, SCAN_TMA_SMEM // (NL * tile_b))
+    if S_ < 3:
+        return None
+    vec = 16 // isz
+    NW = TPB // 32
+    ident = c_literal(_IDENT[rop](T), T)
+    comb = _COMBINE[rop]
+    op = _OPS[rop]
+
+    # ---- per-thread items: the map prologue on 16 consecutive elements
+    tb = Var("tb", 1, align=tile)
+    tt = Var("tt", 1)
+    em = _StagedEmitter(region, {l.id: f"sg{k}" for k, l in enumerate(staged)}, tb)
+    j, sj, a = em.open(1, "for", trip=ITEMS // vec, unroll=True)
+    v, sv, b = em.open(j.level, "for", trip=vec, unroll=True)
+    e = Aff.of(tt).scale(ITEMS) + Aff.of(j).scale(vec) + Aff.of(v)
+    val = em.cast(em.value(x, [Aff.of(tb) + e]), x.dtype, T)
+    em.stmt(v.level, f"vals[{vec} * {j.name} + {v.name}] = {val[0]};")
+    em.close(sv, b)
+    em.close(sj, a)
+    args = "".join(f", const unsigned char* sg{k}" for k in range(NL))
+    items = [f"static __device__ __forceinline__ void items(const Params& p, const long long tb{args}, {ct} (&vals)[{ITEMS}]) {{",
+             "  const long long tt = threadIdx.x; (void)tb;"]
+    items += ["  " + c for c in em.consts]
+    items += render(em.row, 1)
+    items.append("}")
+    body = "\n".join(items)
+    for i, l in enumerate(region.leaves):
+        if l in staged and f"p.in{i}" in body:
+            raise NotFusable(l, "staged leaf also read from global memory")
+
+    params = _params_struct(region)
+    maps = "".join(f"    gr::TMap tmap{k};\n" for k in range(NL + 1))
+    params = params.replace("  struct Params {\n", "  struct Params {\n" + maps, 1)
+    LAG = min(SCAN_TMA_LAG, S_ - 2)       # tiles waiting for their prefix
+    NLW = SCAN_TMA_LBW                    # look-back warps
+    M = LAG + NLW                         # mailbox slots
+    NTH = TPB + 32 * NLW + 32
+    sgs = ", ".join(f"ring + ((long long)s * {NL} + {k}) * {tile_b}" for k in range(NL))
+    loads = "\n".join(f"        gr::tma_load_2d(ring + ((long long)s * {NL} + {k}) * {tile_b}, &p.tmap{k}, 0, (int)(t * {rows}), &full[s]);"
+                      for k in range(NL))
+    kern = f"""extern "C" __global__ void __launch_bounds__({NTH}, 1) {kname}(const __grid_constant__ K::Params p) {{
+  // warps 0..{NW - 1}: data (scan); warps {NW}..{NW + NLW - 1}: look-back (iteration i
+  // goes to warp NW + i % {NLW}); warp {NW + NLW}: TMA producer.  A tile's
+  // locally scanned values wait in its stage for {LAG} iterations while its
+  // prefix resolves; mailboxes in shared memory hand tiles to the look-back
+  // warps and prefixes back (sequence-numbered, volatile + block fences).
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* ring = smem_raw + ((1024u - (gr::smem_u32(smem_raw) & 1023u)) & 1023u);
+  __shared__ unsigned long long full[{S_}], empty[{S_}];
+  __shared__ long long stid[{S_}];
+  __shared__ {ct} wsum[2][{NW}];
+  __shared__ long long mb_tid[{M}];
+  __shared__ {ct} mb_agg[{M}], mb_pre[{M}];
+  __shared__ volatile int mb_pub[{M}], mb_done[{M}];
+  __shared__ gr::LookbackBuf<{ct}> lbw[{NLW}];
+  unsigned long long* aggs = reinterpret_cast<unsigned long long*>(p.scratch) + 1;
+  unsigned long long* incs = aggs + {ntiles * (1 if isz <= 4 else 2)}LL;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {{
+    for (int i = 0; i < {S_}; ++i) {{ gr::mbar_init(&full[i], 1); gr::mbar_init(&empty[i], 1); }}
+    for (int i = 0; i < {M}; ++i) {{ mb_pub[i] = 0; mb_done[i] = 0; }}
+    gr::fence_mbar_init();
+  }}
+  __syncthreads();
+  if (w == {NW + NLW}) {{
+    if (lane == 0) {{
+      for (int i = 0;; ++i) {{
+        const int s = i % {S_};
+        if (i >= {S_}) gr::mbar_wait(&empty[s], ((i / {S_}) - 1) & 1);
+        // static round-robin tiles: the grid is persistent (one CTA per SM, all
+        // resident), so tiles are processed in rounds of gridDim.x and a tile's
+        // look-back reaches back about one round, however deep the ring
+        const long long t = (long long)blockIdx.x + (long long)i * gridDim.x;
+        if (t >= {ntiles}LL) {{ stid[s] = -1; gr::mbar_arrive(&full[s]); break; }}
+        stid[s] = t;
+        gr::mbar_arrive_expect_tx(&full[s], {NL * tile_b}u);
+{loads}
+      }}
+    }}
+    return;
+  }}
+  if (w >= {NW}) {{
+    const int k = w - {NW};
+    for (int i = k;; i += {NLW}) {{
+      const int m = i % {M};
+      while (mb_pub[m] != i + 1) {{ }}
+      __threadfence_block();
+      const long long t = mb_tid[m];
+      if (t < 0) break;
+      const {ct} pre = gr::tile_lookback_buf<{op}, {ct}>(aggs, incs, t, mb_agg[m], {ident}, lbw[k].v);
+      if (lane == 0) {{ mb_pre[m] = pre; __threadfence_block(); mb_done[m] = i + 1; }}
+      __syncwarp();
+    }}
+    return;
+  }}
+  // ---- data warps
+  long long ptid[{LAG + 1}];
+  int srel = -1;
+  auto finalize = [&](const int j, const long long tj) {{
+    // tile of iteration j: prefix (+) its tile-local scan (waiting in its
+    // stage), back into the stage, one TMA store
+    const int m = j % {M};
+    if (threadIdx.x == 0) {{ while (mb_done[m] != j + 1) {{ }} __threadfence_block(); }}
+    asm volatile("bar.sync 1, {TPB};" ::: "memory");
+    const {ct} pre = mb_pre[m];
+    unsigned char* ob = ring + (long long)(j % {S_}) * {NL * tile_b};
+#pragma unroll
+    for (int q = 0; q < {ITEMS // vec}; ++q) {{
+      {ct} o[{vec}];
+      gr::lds_sw<{ct}, {vec}>(o, ob, {ITEMS} * threadIdx.x + {vec} * q);
+      if (tj > 0) {{
+#pragma unroll
+        for (int k2 = 0; k2 < {vec}; ++k2) o[k2] = {comb}<{ct}>(pre, o[k2]);
+        gr::sts_sw<{ct}, {vec}>(ob, {ITEMS} * threadIdx.x + {vec} * q, o);
+      }}
+    }}
+    gr::fence_proxy_async();
+    asm volatile("bar.sync 1, {TPB};" ::: "memory");
+    if (threadIdx.x == 0) {{
+      gr::tma_store_2d(&p.tmap{NL}, 0, (int)(tj * {rows}), ob);
+      gr::bulk_commit();
+      gr::bulk_wait_read<1>();
+      if (srel >= 0) gr::mbar_arrive(&empty[srel]);
+    }}
+    srel = j % {S_};
+  }};
+  for (int i = 0;; ++i) {{
+    const int s = i % {S_};
+    gr::mbar_wait(&full[s], (i / {S_}) & 1);
+    const long long t = stid[s];
+    if (t < 0) {{
+      if (threadIdx.x == 0) {{
+        for (int e = 0; e < {NLW}; ++e) {{ mb_tid[(i + e) % {M}] = -1; __threadfence_block(); mb_pub[(i + e) % {M}] = i + e + 1; }}
+      }}
+      for (int j = (i > {LAG} ? i - {LAG} : 0); j < i; ++j) finalize(j, ptid[j % {LAG + 1}]);
+      break;
+    }}
+    {ct} vals[{ITEMS}];
+    unsigned char* sb = ring + (long long)s * {NL * tile_b};
+    K::items(p, t * {tile}LL, {sgs}, vals);
+#pragma unroll
+    for (int k2 = 1; k2 < {ITEMS}; ++k2) vals[k2] = {comb}<{ct}>(vals[k2 - 1], vals[k2]);
+    {ct} inc = vals[{ITEMS - 1}];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {{
+      const {ct} y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc = {comb}<{ct}>(y, inc);
+    }}
+    {ct}* ws = wsum[i & 1];
+    if (lane == 31) ws[w] = inc;
+    asm volatile("bar.sync 1, {TPB};" ::: "memory");
+    if (threadIdx.x == 0) {{
+      {ct} acc = ws[0];
+      for (int k2 = 1; k2 < {NW}; ++k2) {{ acc = {comb}<{ct}>(acc, ws[k2]); ws[k2] = acc; }}
+      gr::stat_put<{ct}>(aggs, t, acc);
+      const int m = i % {M};
+      mb_tid[m] = t;
+      mb_agg[m] = acc;
+      __threadfence_block();
+      mb_pub[m] = i + 1;
+    }}
+    asm volatile("bar.sync 1, {TPB};" ::: "memory");
+    const {ct} lane_ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    bool has = false;
+    {ct} loc = {ident};
+    if (w > 0) {{ loc = ws[w - 1]; has = true; }}
+    if (lane > 0) {{ loc = has ? {comb}<{ct}>(loc, lane_ex) : lane_ex; has = true; }}
+    // tile-local inclusive scan back into the stage (this thread's own chunks)
+#pragma unroll
+    for (int q = 0; q < {ITEMS // vec}; ++q) {{
+      {ct} o[{vec}];
+#pragma unroll
+      for (int k2 = 0; k2 < {vec}; ++k2) o[k2] = has ? {comb}<{ct}>(loc, vals[{vec} * q + k2]) : vals[{vec} * q + k2];
+      gr::sts_sw<{ct}, {vec}>(sb, {ITEMS} * threadIdx.x + {vec} * q, o);
+    }}
+    ptid[i % {LAG + 1}] = t;
+    if (i >= {LAG}) finalize(i - {LAG}, ptid[(i - {LAG}) % {LAG + 1}]);
+  }}
+  if (threadIdx.x == 0) gr::bulk_wait<0>();
+}}"""
+    pre = "".join(f"#define {d.replace('=', ' ', 1)}\n" for d in os.environ.get("GRUMPY_SCAN_DEFINES", "").split(",") if d)  # experiments
+    src = [pre + HEADER, '#include "gr_reduce.cuh"\n#include "gr_tma.cuh"\n', "struct K {", params, "  " + body.replace("\n", "\n  "), "};", kern]
+    scratch = 8 + 8 * (1 if isz <= 4 else 2) * 2 * ntiles + 256
+    slots = [region.leaves.index(l) for l in staged]
+    tmaps = [(i, W, N // W, W, rows, 128) for i in slots] + [(len(region.leaves), W, N // W, W, rows, 128)]
+    return KernelSource("scan", "\n".join(src) + "\n", kname, list(range(len(region.leaves))), [0],
+                        block=NTH, groups=ntiles * NTH, vec=1, unroll=1, scratch_bytes=scratch,
+                        meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,
+                              "label": "scan-tma", "smem": S_ * NL * tile_b + 1024, "tmaps": tmaps,
+                              "stages": S_})

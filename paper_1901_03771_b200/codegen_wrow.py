@@ -25,12 +25,13 @@ from __future__ import annotations
 import os
 from typing import Optional
 
-from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, c_literal
+from .codegen import HEADER, Aff, KernelSource, NotPairable, Region, Var, _params_struct, c_literal
 from .codegen_rows import _COMBINE, _IDENT, _OPS, LoopEmitter, NotFusable, render, thread_space
 from .dag import Node, OpKind, ReduceOp
 from .tensor import DType, element_count
 
 SMEM_BUDGET = 200 * 1024
+WROW_DIV_TWO_PASS = os.environ.get("GRUMPY_WROW_TWO_PASS", "1") == "1"
 
 
 def _regular(c: int) -> bool:
@@ -48,6 +49,7 @@ class WrowEmitter(LoopEmitter):
         self.lfb = Var("lfb", 1, align=128)   # first column of this lane's leaves
         self.staged = []        # leaf nodes streamed through shared memory
         self.staged_ptr = {}
+        self.pair = False       # float row sums over element pairs (f32x2)
 
     # -- the (li, m, j) loops over a lane's elements --------------------------------
     def open_elem(self, level=1):
@@ -75,28 +77,47 @@ class WrowEmitter(LoopEmitter):
 
     def load_leaf(self, leaf: Node, off: Aff):
         roles = self._roles()
+        if {"li", "m", "jp"} <= set(roles) and self.half is not None:
+            li, m, jp = roles["li"].var, roles["m"].var, roles["jp"].var
+            if (off.coef(jp) == 2 and off.coef(self.half) == 1 and off.coef(m) == 8 and off.coef(li) == 128
+                    and off.coef(self.lfb) == 1 and tuple(leaf.shape) == self.Ts + (self.C,)
+                    and leaf.dtype is DType.f32):
+                rest = off.without(jp).without(self.half).without(m).without(li).without(self.lfb)
+                if rest.key() == Aff.of(Var("r", 1)).scale(self.C).key():
+                    name = self._lds(leaf, li, m)
+                    return self.emit_pair(jp.level, f"gr::pk({name}[2 * {jp.name}], {name}[2 * {jp.name} + 1])"), jp.level
+            raise NotPairable("paired row element off the staged leaf")
         if {"li", "m", "j"} <= set(roles):
             li, m, j = roles["li"].var, roles["m"].var, roles["j"].var
             if (off.coef(j) == 1 and off.coef(m) == 8 and off.coef(li) == 128 and off.coef(self.lfb) == 1
                     and tuple(leaf.shape) == self.Ts + (self.C,) and leaf.dtype.itemsize in (4, 8)):
                 rest = off.without(j).without(m).without(li).without(self.lfb)
                 if rest.key() == Aff.of(Var("r", 1)).scale(self.C).key():
-                    if leaf.id not in self.staged_ptr:
-                        self.staged_ptr[leaf.id] = len(self.staged)
-                        self.staged.append(leaf)
-                    k = self.staged_ptr[leaf.id]
-                    T = leaf.dtype.ctype
-                    key = ("lds", leaf.id, m.name, li.name)
-                    hit = self.memo_get(key)
-                    if hit is None:
-                        name = self.fresh("L")
-                        ls = 128 + 16 // leaf.dtype.itemsize
-                        self.stmt(m.level, f"{T} {name}[8];")
-                        self.stmt(m.level, f"gr::lds8<{T}>({name}, reinterpret_cast<const {T}*>(sst{k}) + "
-                                           f"(lf0 + {li.name}) * {ls} + 8 * {m.name});")
-                        hit = self.memo_put(key, (name, m.level))
-                    return f"{hit[0]}[{j.name}]", j.level
+                    return f"{self._lds(leaf, li, m)}[{j.name}]", j.level
         return super().load_leaf(leaf, off)
+
+    def _lds(self, leaf: Node, li: Var, m: Var) -> str:
+        """The 8 staged elements (li, m, 0..7) of ``leaf`` in registers."""
+        if leaf.id not in self.staged_ptr:
+            self.staged_ptr[leaf.id] = len(self.staged)
+            self.staged.append(leaf)
+        k = self.staged_ptr[leaf.id]
+        T = leaf.dtype.ctype
+        key = ("lds", leaf.id, m.name, li.name)
+        hit = self.memo_get(key)
+        if hit is None:
+            name = self.fresh("L")
+            ls = 128 + 16 // leaf.dtype.itemsize
+            self.stmt(m.level, f"{T} {name}[8];")
+            self.stmt(m.level, f"gr::lds8<{T}>({name}, reinterpret_cast<const {T}*>(sst{k}) + "
+                               f"(lf0 + {li.name}) * {ls} + 8 * {m.name});")
+            hit = self.memo_put(key, (name, m.level))
+        return hit[0]
+
+    def _pair_map(self, n: Node, coords):
+        from .codegen_coop import shared_div_pair
+        v = shared_div_pair(self, n, coords)
+        return v if v is not None else super()._pair_map(n, coords)
 
     # -- row-complete reductions -------------------------------------------------------
     def _row_complete(self, x: Node, axes) -> bool:
@@ -118,6 +139,8 @@ class WrowEmitter(LoopEmitter):
 
     def row_reduce(self, x: Node, rop, T: DType, row_coords, identity=True, value_fn=None):
         """Reduce x over the row (NumPy order for float sums)."""
+        if self.pair and rop is ReduceOp.sum and T is DType.f32 and x.dtype is DType.f32:
+            return self._row_reduce_pair(x, T, row_coords, identity)
         ct = T.ctype
         lsum = self.fresh("ls")
         self.stmt(1, f"{ct} {lsum}[{self.lpl}];")
@@ -141,6 +164,38 @@ class WrowEmitter(LoopEmitter):
         s = self.emit(1, ct, f"gr::warp_tree<{op}, {ct}>({s}, {self.lpr})")
         if identity and rop is ReduceOp.sum and T.is_float:
             s = self.emit(1, ct, f"gr::add<{ct}>({c_literal(0, T)}, {s})")
+        return s
+
+    def _row_reduce_pair(self, x: Node, T: DType, row_coords, identity):
+        """Float row sum with element pairs: NumPy's eight leaf accumulators
+        as four gr::f2 (FADD2), unpacked for the leaf combine."""
+        lsum = self.fresh("ls")
+        self.stmt(1, f"float {lsum}[{self.lpl}];")
+        acc = self.fresh("acc")
+        li, sli, a = self.open(1, "for", trip=self.lpl, unroll=True)
+        sli.coop = "li"
+        m, sm, b = self.open(li.level, "for", trip=16, unroll=True)
+        sm.coop = "m"
+        jp, sj, c = self.open(m.level, "for", trip=4, unroll=True)
+        sj.coop = "jp"
+        self.stmt(li.level, f"gr::f2 {acc}[4];")
+        self.half = Var("gr_half_" + jp.name, jp.level)
+        try:
+            col = Aff.of(self.lfb) + Aff.of(li).scale(128) + Aff.of(m).scale(8) + Aff.of(jp).scale(2) + Aff.of(self.half)
+            val = self.value(x, list(row_coords) + [col])
+            pv = self.splat(val)
+            self.stmt(jp.level, f"{acc}[{jp.name}] = ({m.name} == 0) ? {pv} : gr::p2::add({acc}[{jp.name}], {pv});")
+        finally:
+            self.half = None
+        self.close(sj, c)
+        self.close(sm, b)
+        self.stmt(li.level, f"{{ float a8[8]; for (int q = 0; q < 4; ++q) {{ a8[2 * q] = gr::lo({acc}[q]); "
+                            f"a8[2 * q + 1] = gr::hi({acc}[q]); }} {lsum}[{li.name}] = gr::leaf_local<float, 8>(a8); }}")
+        self.close(sli, a)
+        s = self.emit(1, "float", f"gr::lane_tree<gr::OpSum, float, {self.lpl}>({lsum})")
+        s = self.emit(1, "float", f"gr::warp_tree<gr::OpSum, float>({s}, {self.lpr})")
+        if identity:
+            s = self.emit(1, "float", f"gr::add<float>({c_literal(0, T)}, {s})")
         return s
 
     def argreduce(self, r: Node, coords):
@@ -203,7 +258,19 @@ def _params_with(region):
                                           "    void* __restrict__ scratch;\n    unsigned int* ticket;")
 
 
+WROW_PAIR = os.environ.get("GRUMPY_WROW_PAIR", "1") == "1"
+
+
 def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
+    if WROW_PAIR:
+        try:
+            return _try_generate(region, kname, pair=True)
+        except NotPairable:
+            pass
+    return _try_generate(region, kname, pair=False)
+
+
+def _try_generate(region: Region, kname="gr_region", pair=False) -> Optional[KernelSource]:
     q = _qualifies(region)
     if q is None:
         return None
@@ -215,6 +282,11 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
     rpw = 32 // lpr
     R = element_count(Ts)
     em = WrowEmitter(region, Ts, C, lpr, lpl, rpw)
+    # two-pass division by row-level divisors: the fast pass tracks the
+    # dividends' range; a warp whose rows left the exact window redoes its
+    # rows from the stage it still holds (no flags, no second launch)
+    em.div_fast = WROW_DIV_TWO_PASS and lpr == 32
+    em.pair = pair and lpr == 32
     rvar = Var("r", 1)
     if len(Ts) == 1:
         row_coords = [Aff.of(rvar)]
@@ -329,7 +401,10 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
         ptr_lines.append(f"  const unsigned char* sst{k} = stage + {off} + (long long)q * {nleaf * leaf_bytes[k]};")
         off += rpw * nleaf * leaf_bytes[k]
 
-    lines = ["static __device__ __forceinline__ void rows(const Params& p, const unsigned char* stage, const long long g, const int lane) {",
+    two_pass = em.used_div_fast
+    lines = [("template <bool FAST> static __device__ __forceinline__ bool" if two_pass else
+              "static __device__ __forceinline__ void") +
+             " rows(const Params& p, const unsigned char* stage, const long long g, const int lane) {",
              f"  const int q = lane / {lpr};",
              f"  const int lr = lane % {lpr};",
              f"  const long long r0 = g * {rpw} + q;",
@@ -338,8 +413,13 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
              f"  const int lf0 = lr * {lpl};",
              "  const long long lfb = (long long)lf0 * 128;"]
     lines += ptr_lines
+    if two_pass:
+        lines.append("  bool bad = false;")
     lines += ["  " + c for c in em.consts]
     lines += render(em.row, 1)
+    if two_pass:
+        lines += ["  " + l for l in em.div_finalize]
+        lines.append("  return bad;")
     lines.append("}")
 
     # bulk-copy issue for one row group: copies spread over the 32 lanes
@@ -386,7 +466,9 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
             f"      if (gn < NG) K::issue(p, wbase + sn * {slot_bytes}, &bars[warp * {NS} + sn], gn, lane);",
             "    }",
             f"    gr::mbar_wait(&bars[warp * {NS} + s], (unsigned)((it / {NS}) & 1));",
-            f"    K::rows(p, wbase + s * {slot_bytes}, g, lane);",
+            (f"    if (__any_sync(0xffffffffu, K::rows<true>(p, wbase + s * {slot_bytes}, g, lane))) "
+             f"K::rows<false>(p, wbase + s * {slot_bytes}, g, lane);" if two_pass else
+             f"    K::rows(p, wbase + s * {slot_bytes}, g, lane);"),
             "  }"]
     if tot_meta:
         kern.append("  if (gr::last_block(p.ticket)) {")

@@ -62,4 +62,22 @@ template <class T, int V> __device__ __forceinline__ void stv(T* __restrict__ ds
 }
 template <class T> __device__ __forceinline__ void st(T* __restrict__ dst, T x) { *dst = x; }
 
+// the first n of V elements (the last partial group of a packed map body);
+// lanes past n read element 0 and are never stored
+template <class T, int V> __device__ __forceinline__ void ldv_part(T (&dst)[V], const T* __restrict__ src, int n) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) dst[i] = src[i < n ? i : 0];
+}
+template <class T, int V> __device__ __forceinline__ void stv_part(T* __restrict__ dst, const T (&src)[V], int n) {
+#pragma unroll
+  for (int i = 0; i < V; ++i)
+    if (i < n) dst[i] = src[i];
+}
+
+// L1 prefetch of the next grid-stride row's leaf data (row family): no
+// register or scoreboard dependency, the row's own loads then hit L1
+template <class T> __device__ __forceinline__ void prefetch_l1(const T* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 }  // namespace gr

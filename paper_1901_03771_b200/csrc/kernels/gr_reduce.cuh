@@ -538,9 +538,28 @@ __device__ unsigned long long gr_scan_stats[8];
 // fences): one L2 round trip reads the inclusive and aggregate words of the
 // 256 nearest predecessors, the nearest published inclusive prefix starts the
 // fold, and lane 0 folds the aggregates above it in tile order.
+#ifndef GR_SCAN_J
+#define GR_SCAN_J 2
+#endif
+#ifndef GR_SCAN_R
+#define GR_SCAN_R 8
+#endif
+template <class T> struct LookbackBuf { T v[32 * GR_SCAN_J * GR_SCAN_R]; };
+
+template <class Op, class T>
+__device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, unsigned long long* inc,
+                                               long long tile, T tile_agg, T ident, T* lb);
 template <class Op, class T>
 __device__ __forceinline__ T tile_lookback(const unsigned long long* agg, unsigned long long* inc,
                                            long long tile, T tile_agg, T ident) {
+  __shared__ LookbackBuf<T> lbs;
+  return tile_lookback_buf<Op, T>(agg, inc, tile, tile_agg, ident, lbs.v);
+}
+// lb: the calling warp's own staging array (32 * J * R values); several
+// look-back warps of one CTA each pass their own
+template <class Op, class T>
+__device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, unsigned long long* inc,
+                                               long long tile, T tile_agg, T ident, T* lb) {
   const int lane = threadIdx.x & 31;
 #ifdef GR_SCAN_NOLB
   return ident;   // experiment: streaming floor without any look-back (wrong results)
@@ -552,15 +571,9 @@ __device__ __forceinline__ T tile_lookback(const unsigned long long* agg, unsign
 #ifdef GR_SCAN_STATS
   const long long c0 = clock64();
 #endif
-#ifndef GR_SCAN_J
-#define GR_SCAN_J 2
-#endif
   constexpr int J = GR_SCAN_J;       // 32*J predecessors per round trip
-#ifndef GR_SCAN_R
-#define GR_SCAN_R 8
-#endif
   constexpr int R = GR_SCAN_R;       // windows staged before the slow path
-  __shared__ T lb[32 * J * R];       // aggregates by distance: lb[tile-1-q]
+  // lb: aggregates by distance, lb[tile-1-q]
   // walk back window by window: one round trip reads the inclusive and the
   // aggregate words of 32*J predecessors; aggregates above the nearest
   // published inclusive prefix are staged by distance

@@ -70,6 +70,47 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const TMap* map, int x, i
       : "memory");
 }
 
+// shared -> global tensor store of a whole box (bulk-group completion):
+// commit, then wait_group.read before the smem is overwritten, wait_group
+// before the kernel may exit
+__device__ __forceinline__ void tma_store_2d(const TMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                   reinterpret_cast<unsigned long long>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N> __device__ __forceinline__ void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Element offset -> byte offset inside a [rows][128 B] box stored with the
+// 128-byte swizzle: element e of an S-byte type sits in line e*S/128, 16-byte
+// chunk (e*S%128)/16 xor (line % 8).
+template <int S> __device__ __forceinline__ unsigned sw128_elem(unsigned e) {
+  const unsigned b = e * S;
+  return (b & ~127u) | ((((b >> 4) & 7u) ^ ((b >> 7) & 7u)) << 4) | (b & 15u);
+}
+// V consecutive elements (one 16-byte chunk) of a swizzled box <-> registers
+template <class T, int V> __device__ __forceinline__ void lds_sw(T (&d)[V], const unsigned char* base, unsigned e) {
+  static_assert(sizeof(T) * V == 16, "one 16-byte chunk");
+  VecU<T, V> u;
+  u.raw = *reinterpret_cast<const uint4*>(base + sw128_elem<sizeof(T)>(e));
+#pragma unroll
+  for (int i = 0; i < V; ++i) d[i] = u.v[i];
+}
+template <class T, int V> __device__ __forceinline__ void sts_sw(unsigned char* base, unsigned e, const T (&s)[V]) {
+  static_assert(sizeof(T) * V == 16, "one 16-byte chunk");
+  VecU<T, V> u;
+#pragma unroll
+  for (int i = 0; i < V; ++i) u.v[i] = s[i];
+  *reinterpret_cast<uint4*>(base + sw128_elem<sizeof(T)>(e)) = u.raw;
+}
+
 // Byte offset of 16-byte chunk `c` (0..7) of 128-byte line `L` inside a box
 // stored with CU_TENSOR_MAP_SWIZZLE_128B (1024-byte aligned atoms).
 __device__ __forceinline__ unsigned sw128(unsigned L, unsigned c) { return L * 128u + ((c ^ (L & 7u)) << 4); }

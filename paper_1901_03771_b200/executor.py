@@ -203,7 +203,9 @@ class Executor:
             # TMA tensor maps lead the parameter block (alignas(64) gr::TMap
             # members first in K::Params); the block is padded to the struct's
             # 64-byte alignment
-            maps = b"".join(self._tensor_map(ptrs[i], leaves[i].dtype, d0, d1, b0, b1, sw)
+            # slots past the leaves are the step's outputs (TMA stores)
+            dts = [l.dtype for l in leaves] + [r.dtype for r in st.roots]
+            maps = b"".join(self._tensor_map(ptrs[i], dts[i], d0, d1, b0, b1, sw)
                             for i, d0, d1, b0, b1, sw in tm)
             params = maps + params
             params += b"\0" * (-len(params) % 64)

@@ -23,7 +23,7 @@ from .tensor import DType
 
 # bytes of per-thread local memory (spill) a register-capped rebuild of a map
 # kernel may use and still be kept for its extra resident CTAs
-TUNE_MAX_LOCAL = int(os.environ.get("GRUMPY_TUNE_MAX_LOCAL", "0"))
+TUNE_MAX_LOCAL = int(os.environ.get("GRUMPY_TUNE_MAX_LOCAL", "8"))
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgrumpy_rt.so")

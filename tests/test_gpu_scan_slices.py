@@ -112,3 +112,47 @@ def test_scan_lookback_deterministic(sess):
     assert all(np.array_equal(runs[0], r) for r in runs[1:])
     ref = np.cumsum((x * np.float32(0.5) + np.float32(1.0)).astype(np.float64))
     assert np.max(np.abs(runs[0] - ref)) <= 1e-6 * np.max(np.abs(ref)) + 1.0
+
+
+@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 32, 3 << 20, (1 << 21) + 7])
+@pytest.mark.parametrize("kind", ["f32", "f64", "i64", "f32x2", "max"])
+def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
+    """The TMA-fed look-back scan (codegen_scan._gen_lookback_tma) has the
+    register-staged kernel's association: results bit-identical to it, for
+    one- and two-leaf map prologues, 4- and 8-byte types, sums and max; lengths
+    that are not a multiple of the tile (zero-filled last box) or of the
+    128-byte line (register-staged fallback)."""
+    from paper_1901_03771_b200 import codegen, codegen_scan
+    rng = np.random.default_rng([n, len(kind)])
+    if kind == "i64":
+        xs = [rng.integers(-1000, 1000, n)]
+    elif kind == "f64":
+        xs = [rng.standard_normal(n)]
+    else:
+        xs = [rng.standard_normal(n).astype(np.float32) for _ in range(2 if kind == "f32x2" else 1)]
+
+    def prog():
+        g = [gp.asarray(v) for v in xs]
+        if kind == "max":
+            return np.maximum.accumulate(g[0] * 2.0)
+        if kind == "f32x2":
+            return gp.cumsum(g[0] * g[1] + 1.0)
+        return gp.cumsum(g[0] * 3 + 1)
+
+    outs, labels = [], []
+    for tma in (True, False):
+        monkeypatch.setattr(codegen_scan, "SCAN_TMA", tma)
+        codegen._GEN_CACHE.clear()
+        sess._plan_cache.clear()
+        r = prog()
+        outs.append(np.asarray(r))
+        labels.append(sess.executor.last_steps[-1].cache["ks"].meta.get("label"))
+    codegen._GEN_CACHE.clear()
+    sess._plan_cache.clear()
+    assert labels[1] == "scan-lookback"
+    assert labels[0] == ("scan-tma" if n % 32 == 0 else "scan-lookback")
+    assert np.array_equal(outs[0], outs[1])
+    if kind in ("i64",):
+        assert np.array_equal(outs[0], np.cumsum(xs[0] * 3 + 1))
+    if kind == "max":
+        assert np.array_equal(outs[0], np.maximum.accumulate(xs[0] * np.float32(2.0)))
