@@ -1,0 +1,104 @@
+"""Code-generation choices of round 2, checked on CPU (sources and NVRTC
+builds, no GPU): DAG-determined product fusion in inexact regions, the
+nearest-centre pattern, row prefetch and 32-bit bincount keys, the TMA scan
+and warp-per-row generators."""
+import numpy as np
+import pytest
+
+import paper_1901_03771_b200 as gp
+from paper_1901_03771_b200 import codegen, codegen_rows, codegen_scan, runtime, workloads as wl
+
+
+def _source(roots):
+    sess = gp.session.default_session()
+    st = sess.plan([r.node for r in roots])[0]
+    return codegen.generate(codegen.canonicalize(codegen.Region(st.roots, st.leaves, st.nodes)))
+
+
+def test_fusion_same_in_packed_body_and_tail():
+    """An inexact f32 region with a tail: the packed body fuses with explicit
+    FFMA2 and the scalar tail with FMA — never ptxas's own contraction (whose
+    choice follows the emission order)."""
+    S, X, T = wl.blackscholes_inputs(n=(1 << 12) + 3)
+    ks = _source(list(wl.blackscholes(gp, *map(gp.asarray, (S, X, T)))))
+    body, tail = ks.source.split("void tail(")
+    assert "gr::p2::fma(" in body and "gr::fma_(" in tail
+    assert "ldv_part" not in ks.source                # the ptxas-contraction experiment is off
+    assert "gr::p2::mul_nc" in body                  # unfused products stay uncontractable
+
+
+def test_fusion_picks_by_operand_position():
+    """a*b - c*d: the product fused is fixed by the DAG (the last operand by
+    default), the other is formed uncontractably."""
+    rng = np.random.default_rng(1)
+    a, b, c, d = (gp.asarray(rng.standard_normal(4096).astype(np.float32)) for _ in range(4))
+    ks = _source([a * b - gp.exp(c) * d])
+    assert "gr::p2::fma(" in ks.source and "gr::p2::mul_nc(" in ks.source
+    assert codegen.FMA_PICK in ("first", "last")
+
+
+def test_exact_regions_never_fuse():
+    rng = np.random.default_rng(2)
+    a, b = (gp.asarray(rng.standard_normal(4096).astype(np.float32)) for _ in range(2))
+    ks = _source([a * b + 1.0])
+    assert "fma(" not in ks.source.replace("mul_nc", "")
+
+
+@pytest.mark.parametrize("form", ["square", "mul", "reversed"])
+def test_nearest_pattern_forms(form):
+    P, C = wl.kmeans_inputs(n=4096, k=16, d=3)
+    gP, gC = gp.asarray(P), gp.asarray(C)
+    if form == "square":
+        d = ((gP[:, None, :] - gC[None]) ** 2).sum(-1)
+    elif form == "mul":
+        t = gP[:, None, :] - gC[None]
+        d = (t * t).sum(-1)
+    else:
+        d = ((gC[None] - gP[:, None, :]) ** 2).sum(-1)
+    assert codegen_rows.match_nearest(d.node, (1,)) is not None
+    ks = _source([d.argmin(1)])
+    assert "gr::nearest_centre<16, 3>" in ks.source and "gr_nnpack" in ks.source
+    assert ks.meta["cbank_pair"]
+    runtime.compile_cubin(ks.source)
+
+
+def test_nearest_not_for_other_programs():
+    P, C = wl.kmeans_inputs(n=4096, k=15, d=3)            # odd centre count
+    gP, gC = gp.asarray(P), gp.asarray(C)
+    d = ((gP[:, None, :] - gC[None]) ** 2).sum(-1)
+    assert codegen_rows.match_nearest(d.node, (1,)) is None
+    P2, C2 = wl.kmeans_inputs(n=4096, k=16, d=3)
+    d2 = ((gp.asarray(P2)[:, None, :] - gp.asarray(C2)[None]) ** 2).sum(-1)
+    assert "nearest_centre" not in _source([d2.argmax(1)]).source      # argmax: the plain scan
+
+
+def test_kmeans_row_prefetch_and_match32():
+    P, C = wl.kmeans_inputs(n=1 << 14)
+    lab, sums, counts = wl.kmeans_partials(gp, gp.asarray(P), gp.asarray(C))
+    ks = _source([lab] + sums + [counts])
+    assert "gr::prefetch_l1(p.in0 + (r + stride) * 4LL)" in ks.source
+    assert "(unsigned)kkey : 0xffffffffu" in ks.source
+    assert "const float kw0 = L" in ks.source                  # weights reuse the row's vector load
+    assert f"__launch_bounds__(128, {codegen_rows.NEAREST_MIN_BLOCKS})" in ks.source
+    runtime.compile_cubin(ks.source)
+
+
+def test_scan_tma_generator_builds(monkeypatch):
+    monkeypatch.setattr(codegen_scan, "SCAN_TMA", True)
+    x = gp.asarray(np.arange(1 << 20, dtype=np.float32))
+    ks = _source([gp.cumsum(x * 0.5 + 1.0)])
+    assert ks.meta["label"] == "scan-tma"
+    assert len(ks.meta["tmaps"]) == 2 and ks.meta["tmaps"][-1][0] == 1     # leaf map + output map
+    runtime.compile_cubin(ks.source)
+    odd = gp.asarray(np.arange((1 << 20) + 7, dtype=np.float32))
+    assert _source([gp.cumsum(odd)]).meta["label"] == "scan-lookback"    # not a multiple of a line
+
+
+def test_wrow_generator_paired_two_pass(monkeypatch):
+    monkeypatch.setattr(codegen, "ROW_FAMILY", "wrow")
+    (x,) = wl.rownorm_inputs(rows=256, cols=4096)
+    y, t = wl.rownorm(gp, gp.asarray(x))
+    ks = _source([t])
+    assert ks.family == "wrow"
+    assert "gr::p2::div_shr<FAST>" in ks.source and "K::rows<false>" in ks.source
+    runtime.compile_cubin(ks.source)

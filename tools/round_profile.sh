@@ -18,7 +18,7 @@ for w in $WL; do
     --clock-control none -c 60 --csv --log-file $OUT/launches_$w.csv \
     python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 done
-for w in blackscholes-f32 mlp transpose rownorm; do
+for w in blackscholes-f32 mlp transpose rownorm kmeans cumsum; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gr_region -s 3 -c 1 \
     -o $OUT/full_$w python bench.py --workload $w --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 done
