@@ -258,12 +258,15 @@ WORKLOADS = {
         label="f32", shape=f"[2^26, {KM_D}] points x 64 centroids",
         desc=f"k-means assignment, 2^26 points x 64 centroids, D={KM_D} (BASELINE configs[4])",
         program=lambda xp, a: _km_step(xp, a),
-        elements=lambda n: n, bytes=lambda n: n * (KM_D * 4 + 8) + 64 * KM_D * 4, bound="fp32 issue (no FMA, NumPy order)",
-        # per point: 64 centroids x (D sub + D square + (D-1) add + 1 compare
-        # of the argmin); the seed add of NumPy's fold is an identity and is
-        # not executed
+        elements=lambda n: n, bytes=lambda n: n * (KM_D * 4 + 8) + 64 * KM_D * 4,
+        bound="issue (certified nearest-centre search: FFMA2 keys + FMNMX top-2, NumPy-order scan for uncertified rows)",
+        # per point, the program as NumPy states it: 64 centroids x (D sub +
+        # D square + (D-1) add + 1 compare of the argmin) — algorithmic
+        # lane-ops; the kernel's expanded-key search executes fewer
         compute=dict(pipe="fp32", ops=64 * (3 * KM_D), lanes_per_sm_clk=128,
-                     note="64 x (4 sub + 4 mul + 3 add + 1 argmin compare) lane-ops per point"),
+                     note="algorithmic: 64 x (4 sub + 4 mul + 3 add + 1 argmin compare) lane-ops per point "
+                          "(the NumPy formulation; the certified key search executes 64 x ~2.5 FP32-pipe "
+                          "instructions + ~3.5 ALU instructions per point)"),
         collective=True),
     "cumsum": dict(
         label="f32", shape="[2^28]",

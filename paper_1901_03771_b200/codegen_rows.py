@@ -26,6 +26,7 @@ registers) lives in ``codegen_coop.py``.
 from __future__ import annotations
 
 import os
+import re
 from typing import Dict, List, Optional, Sequence, Tuple
 
 from .codegen import (
@@ -53,10 +54,10 @@ class NotFusable(UnsupportedNodeInFusedStep):
 NEAREST = os.environ.get("GRUMPY_NEAREST", "1") == "1"
 NEAREST_MAX_D = 8
 # CTAs per SM asked of ptxas (__launch_bounds__ min blocks) for row kernels
-# with a nearest-centre search: the search itself needs few registers, the
-# rare exact fallback scan many; capping lets the fallback spill instead of
-# starving the hot loop of warps
-NEAREST_MIN_BLOCKS = int(os.environ.get("GRUMPY_NEAREST_MINB", "10"))
+# with a nearest-centre search (0: none).  With the exact fallback scan out
+# of line (gr::nearest_exact, __noinline__) the k-means kernel needs 32
+# registers and runs at full occupancy uncapped.
+NEAREST_MIN_BLOCKS = int(os.environ.get("GRUMPY_NEAREST_MINB", "0"))
 NEAREST_MAX_K = 256
 
 
@@ -114,7 +115,8 @@ _OPS = {ReduceOp.sum: "gr::OpSum", ReduceOp.prod: "gr::OpProd", ReduceOp.max: "g
 
 ARG_UNROLL = 64        # arg-reductions up to this length are fully unrolled
 SMALL_RECOMPUTE = 64   # a reduction re-evaluated per column may reduce at most this many points
-MAX_GRID = 148 * 16    # grid cap for kernels with per-CTA partial slots (keyed sums)
+MAX_GRID = int(os.environ.get("GRUMPY_KEYED_MAX_GRID", str(148 * 16)))  # grid cap for kernels with per-CTA partial slots (keyed sums)
+KEYED_GROUP = 32       # CTAs per first-level fold of the keyed-sum partials (tickets: 1 + MAX_GRID / 32 words)
 
 
 # Skinny products z = A @ B (A [R, K] streamed, B [K, N] small) computed as
@@ -691,15 +693,9 @@ class LoopEmitter(ValueEmitter):
         self.close(s, saved)
         lab = self.fresh("a")
         self.stmt(L, f"int {lab}; const bool {lab}ok = gr::nearest_centre<{K}, {D}>({pv}, {tsym}, {lab});")
-        bi = self.var_decl(L, "long long", lab)
-        saved_if = self.stack[L + 1:]
-        del self.stack[L + 1:]
-        sif = Scope(L + 1, "for", header=f"if (!{lab}ok)")
-        self.stack.append(sif)
-        ebi, _ = self._argreduce_exact(x, "min", axes, kept, L + 1, K)
-        self.stmt(L + 1, f"{bi} = {ebi};")
-        self.close(sif, saved_if)
-        return bi, L
+        # uncertified rows: the exact NumPy-order scan, out of line
+        self.stmt(L, f"if (!{lab}ok) {lab} = gr::nearest_exact<{K}, {D}>({pv}, {sym});")
+        return self.emit(L, "long long", lab), L
 
     def _argreduce_exact(self, x: Node, which, axes, kept, L, n):
         """First-index arg-reduction in NumPy's order (the value compared is
@@ -1192,7 +1188,7 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
     used_cb = []
     for i, l in enumerate(region.leaves):
         sym = cbank.get(l.id)
-        if sym is not None and sym + "[" in "\n".join(lines):
+        if sym is not None and re.search(rf"\b{sym}\b(?!_)", "\n".join(lines)):
             used_cb.append((i, sym, element_count(l.shape) * l.dtype.itemsize))
     cdecl = "".join(f"__constant__ {region.leaves[i].dtype.ctype} {sym}[{nb // region.leaves[i].dtype.itemsize}];\n"
                     for i, sym, nb in used_cb)
@@ -1297,16 +1293,38 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
         else:
             kern += ["  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride)",
                      "    K::row(p, r, true);"]
-    if tot_meta or kmeta:
-        kern.append("  if (gr::last_block(p.ticket)) {")
+    if kmeta:
+        # two-level fold of the per-CTA histograms: the last CTA of each group
+        # of KEYED_GROUP folds its group's partials (in CTA order), the last
+        # group to finish folds the group partials (in group order) — a fixed
+        # association whose serial tail is two short folds, not one over the grid
+        gscr = []
         for j, r, NBj, off in kmeta:
+            gscr.append(scratch_off)
+            scratch_off += ((-(-MAX_GRID // KEYED_GROUP)) * NBj * 8 + 255) // 256 * 256
+        kern += [f"  const unsigned kgid = blockIdx.x / {KEYED_GROUP}u;",
+                 f"  const unsigned kgn = min({KEYED_GROUP}u, gridDim.x - kgid * {KEYED_GROUP}u);",
+                 f"  const unsigned kng = (gridDim.x + {KEYED_GROUP - 1}u) / {KEYED_GROUP}u;",
+                 "  if (!gr::last_arrival(p.ticket + 1 + kgid, kgn)) return;"]
+        for (j, r, NBj, off), goff in zip(kmeta, gscr):
+            ct = r.dtype.ctype
+            kern += [f"  for (int b = threadIdx.x; b < {NBj}; b += blockDim.x) {{",
+                     f"    {ct} s = 0;",
+                     f"    s = gr::seq_fold<{ct}>(s, reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {off}) + (long long)kgid * {KEYED_GROUP * NBj} + b, kgn, {NBj});",
+                     f"    reinterpret_cast<{ct}*>(static_cast<char*>(p.scratch) + {goff})[(long long)kgid * {NBj} + b] = s;",
+                     "  }"]
+        kern.append("  if (gr::last_arrival(p.ticket, kng)) {")
+        for (j, r, NBj, off), goff in zip(kmeta, gscr):
             ri = region.roots.index(r)
             ct = r.dtype.ctype
             kern += [f"    for (int b = threadIdx.x; b < {NBj}; b += blockDim.x) {{",
                      f"      {ct} s = 0;",
-                     f"      for (unsigned c = 0; c < gridDim.x; ++c) s += reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {off})[(long long)c * {NBj} + b];",
+                     f"      s = gr::seq_fold<{ct}>(s, reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {goff}) + b, kng, {NBj});",
                      f"      p.out{ri}[b] = s;",
                      "    }"]
+    elif tot_meta:
+        kern.append("  if (gr::last_block(p.ticket)) {")
+    if tot_meta or kmeta:
         for ri, rop, T, off in tot_meta:
             ct = T.ctype
             if isinstance(rop, tuple):

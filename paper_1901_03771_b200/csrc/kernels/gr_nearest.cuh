@@ -12,14 +12,14 @@
 // the key's low mantissa bits so that one FMNMX keeps both the best key and
 // its index.  The two smallest keys are tracked (m1 < m2, FMNMX3); the label
 // is certified when
-//     m2 - m1 > 2.1 Dc + e (|m1| + |m2|) + 8e-7 max(m1 + e |m1| + Dc, 0) + 1e-35
+//     m2 - m1 > 2.1 Dc + e (|m1| + |m2|) + g max(m1 + e |m1| + Dc, 0) + 1e-35
 // with Dc = 24 u (||p'||^2 + 2 max_j ||c'_j||^2) bounding the chain's error
 // against the exact distance D_j (origin shift 4.06u, ||c'||^2 and ||p'||^2
 // roundings 5u, five roundings of terms <= 2R 10u; u = 2^-24), e = 1.01 *
 // 2^(BITS-23) the index bits' relative perturbation (x - e|x| is increasing,
 // so every key >= m2 bounds its distance below by m2 - e|m2| - Dc), and
-// 8e-7 > 2.01 gamma_6 NumPy's own rounding of the distances (six roundings of
-// non-negative terms: |D^_j - D_j| <= gamma_6 D_j).  Then D^_label < D^_j for
+// g = 2.1 (D + 2) u > 2.01 gamma_(D+1) NumPy's own rounding of the distances
+// (at most D + 1 roundings of non-negative terms: |D^_j - D_j| <= gamma D_j).  Then D^_label < D^_j for
 // every other centre: the label IS np.argmin.  A row that fails (near-ties,
 // NaN or inf anywhere, magnitudes above 1e37 where the chain could overflow)
 // returns false and the caller runs the exact NumPy-order scan for it.
@@ -97,9 +97,58 @@ __device__ __forceinline__ bool nearest_centre(const float (&p)[D], const float2
   const float R = pp + 2.0f * hdr[D];
   const float dc = 24.0f * 5.9604644775390625e-08f * R;
   const float a1 = fabsf(m1), a2 = fabsf(m2);
-  const float thr = 2.1f * dc + E * (a1 + a2) + 8e-7f * fmaxf(m1 + E * a1 + dc, 0.0f) + 1e-35f;
+  // NumPy's own rounding: a term passes through at most D + 1 roundings (sub,
+  // square, the D - 1 adds of the sequential fold; 5 for the n == 8 tree),
+  // |D^_j - D_j| <= gamma_(D+1) D_j; 2.1 (D + 2) u covers 2.01 gamma_(D+1)
+  constexpr float NP = 2.1f * (D + 2) * 5.9604644775390625e-08f;
+  const float thr = 2.1f * dc + E * (a1 + a2) + NP * fmaxf(m1 + E * a1 + dc, 0.0f) + 1e-35f;
   // NaN anywhere (p, centres, keys) makes a comparison false: exact scan
   return R < 1e37f && m2 - m1 > thr;
+}
+
+// np.argmin over NumPy's float32 distances, exactly: d_j = ((p0-c0)^2 +
+// (p1-c1)^2) + ... (sub, square, then a left fold over the D < 8 terms —
+// NumPy's pairwise sum is sequential below 8 elements; its 0.0 start changes
+// only the sign of a zero sum, which no compare sees), first index on ties,
+// the first NaN wins.  Out of line: the rows that need it are rare, and its
+// registers stay out of the hot loop's allocation.
+template <int D> struct Point { float v[D]; };   // passed by value: registers, no stack copy
+
+template <int K, int D>
+__device__ __noinline__ int nearest_exact_v(const Point<D> pt, const float* __restrict__ c) {
+  const float* p = pt.v;
+  static_assert(D <= 8, "NumPy's 8-accumulator block for 8 <= n <= 128 is written out for n == 8 only");
+  float best = 0.0f;
+  int bi = 0;
+  for (int j = 0; j < K; ++j) {
+    float sq[D];
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float t = __fsub_rn(p[k], c[j * D + k]);
+      sq[k] = __fmul_rn(t, t);
+    }
+    float d;
+    if constexpr (D == 8) {
+      // n == 8: eight accumulators, combined as a fixed tree
+      d = __fadd_rn(__fadd_rn(__fadd_rn(sq[0], sq[1]), __fadd_rn(sq[2], sq[3])),
+                    __fadd_rn(__fadd_rn(sq[4], sq[5]), __fadd_rn(sq[6], sq[7])));
+    } else {
+      d = sq[0];
+#pragma unroll
+      for (int k = 1; k < D; ++k) d = __fadd_rn(d, sq[k]);
+    }
+    if (d != d) return j;
+    if (j == 0 || d < best) { best = d; bi = j; }
+  }
+  return bi;
+}
+
+template <int K, int D>
+__device__ __forceinline__ int nearest_exact(const float (&p)[D], const float* __restrict__ c) {
+  Point<D> pt;
+#pragma unroll
+  for (int k = 0; k < D; ++k) pt.v[k] = p[k];
+  return nearest_exact_v<K, D>(pt, c);
 }
 
 // Pack kernel body (one CTA): origin, CC and the pair table from the row-major

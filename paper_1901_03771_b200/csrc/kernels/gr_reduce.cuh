@@ -192,6 +192,23 @@ template <class Op, class T> __device__ __forceinline__ T warp_tree(T v, int wid
 // chunk as a perfect binary tree (binary-counter stack), then warp and CTA
 // trees: for power-of-two n this is exactly the perfect binary tree over p,
 // i.e. NumPy's pairwise split above row granularity.
+// s = (((s + p[0]) + p[stride]) + ...) over n terms, in that order, with the
+// loads of each batch of 8 issued before its adds: the fold of per-CTA
+// partials by the last CTA waits on L2 once per batch instead of once per
+// term (same association as the plain loop, bit for bit)
+template <class T> __device__ __forceinline__ T seq_fold(T s, const T* p, unsigned n, long long stride) {
+  unsigned c = 0;
+  for (; c + 8 <= n; c += 8) {
+    T v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __ldcg(p + (long long)(c + k) * stride);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += v[k];
+  }
+  for (; c < n; ++c) s += __ldcg(p + (long long)c * stride);
+  return s;
+}
+
 template <class Op, class T> __device__ T block_tree(const T* p, long long n, T ident) {
   __shared__ T sh[32];
   const int t = threadIdx.x, nt = blockDim.x;
@@ -658,6 +675,25 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
                    atomicAdd(&gr_scan_stats[2], (unsigned long long)(clock64() - c0)); }
 #endif
   return __shfl_sync(0xffffffffu, pre, 0);
+}
+
+// Ticket of a group of `expected` blocks: true in exactly the last of them to
+// arrive, after every earlier arrival's writes are visible; self-resetting.
+// Called by whole blocks (uniformly).
+__device__ __forceinline__ bool last_arrival(unsigned int* ticket, unsigned int expected) {
+  __shared__ bool am_last_a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(ticket, 1u);
+    am_last_a = (prev == expected - 1);
+  }
+  __syncthreads();
+  if (am_last_a) {
+    __threadfence();
+    if (threadIdx.x == 0) *ticket = 0u;
+  }
+  return am_last_a;
 }
 
 // Grid completion ticket: returns true in exactly one (the last) block, after

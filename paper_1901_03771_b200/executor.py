@@ -183,7 +183,7 @@ class Executor:
             # every launch (launches of one kernel are stream-ordered)
             tk = self._tickets.get(id(ks))
             if tk is None:
-                tk = self.rt.alloc(256)
+                tk = self.rt.alloc(4096)      # [0]: grid ticket, [1..]: keyed-sum group tickets
                 self.rt.memset(tk, 0)
                 self._tickets[id(ks)] = tk
             ptrs.append(tk.ptr)

@@ -117,6 +117,7 @@ def test_kmeans_constant_bank_and_match_any(sess):
 def test_paired_argmin_loop_compiles(sess, monkeypatch):
     from paper_1901_03771_b200 import codegen_rows
     monkeypatch.setattr(codegen_rows, "PAIR_LOOPS", True)
+    monkeypatch.setattr(codegen_rows, "NEAREST", False)     # the exact paired scan itself
     codegen._GEN_CACHE.clear()
     P, C = (gp.asarray(v) for v in wl.kmeans_inputs(n=8192, k=64, d=4))
     lab = wl.kmeans_assign(gp, P, C)

@@ -79,7 +79,7 @@ def test_kmeans_row_prefetch_and_match32():
     assert "gr::prefetch_l1(p.in0 + (r + stride) * 4LL)" in ks.source
     assert "(unsigned)kkey : 0xffffffffu" in ks.source
     assert "const float kw0 = L" in ks.source                  # weights reuse the row's vector load
-    assert f"__launch_bounds__(128, {codegen_rows.NEAREST_MIN_BLOCKS})" in ks.source
+    assert "gr::nearest_exact<64, 4>(" in ks.source             # the exact scan out of line
     runtime.compile_cubin(ks.source)
 
 

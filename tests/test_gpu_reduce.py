@@ -187,10 +187,13 @@ def test_bincount_collisions(sess, nkeys):
 
 
 def test_kmeans_paired_loop_exact(sess, monkeypatch):
-    """The (off by default) paired argmin loop keeps np.argmin's answer."""
+    """The paired argmin loop (the NumPy-order scan, here without the
+    nearest-centre search in front of it) keeps np.argmin's answer."""
     from paper_1901_03771_b200 import codegen, codegen_rows
     monkeypatch.setattr(codegen_rows, "PAIR_LOOPS", True)
+    monkeypatch.setattr(codegen_rows, "NEAREST", False)
     codegen._GEN_CACHE.clear()
+    sess._plan_cache.clear()
     try:
         P, C = wl.kmeans_inputs(n=8192 + 5, k=64, d=4)
         P[10, 2] = np.nan

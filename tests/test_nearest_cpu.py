@@ -50,7 +50,8 @@ def emulate(P, C):
         R = (pp + F(2) * CC).astype(F)
         dc = (F(24 * 2.0 ** -24) * R).astype(F)
         a1, a2 = np.abs(m1), np.abs(m2)
-        thr = (F(2.1) * dc + E * (a1 + a2) + F(8e-7) * np.maximum((m1 + E * a1 + dc).astype(F), F(0))
+        NP = F(2.1 * (D + 2) * 2.0 ** -24)
+        thr = (F(2.1) * dc + E * (a1 + a2) + NP * np.maximum((m1 + E * a1 + dc).astype(F), F(0))
                + F(1e-35)).astype(F)
         ok = (R < F(1e37)) & ((m2 - m1).astype(F) > thr)
     return lab, ok

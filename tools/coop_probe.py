@@ -64,7 +64,13 @@ def rotate_fenced(src):
         BARRIER = False
 
 
-VARIANTS = {"base": lambda s: s, "rotate": rotate, "rotate_fenced": rotate_fenced,
+def no_final_fold(src):
+    """timing only: the last CTA's fold of the row partials skipped"""
+    import re as _re
+    return _re.sub(r"gr::block_tree<[^;]*;", "0.0f;", src)
+
+
+VARIANTS = {"base": lambda s: s, "rotate": rotate, "rotate_fenced": rotate_fenced, "nofold": no_final_fold,
             "rotate_fenced_mb2": lambda s: rotate_fenced(s).replace("__launch_bounds__(256, 3)", "__launch_bounds__(256, 2)"),
             "rotate_mb2": lambda s: rotate(s).replace("__launch_bounds__(256, 3)", "__launch_bounds__(256, 2)"),
             "rotate_mb4": lambda s: rotate(s).replace("__launch_bounds__(256, 3)", "__launch_bounds__(256, 4)")}
