@@ -340,9 +340,14 @@ class ValueEmitter:
                 args.append(self.cast(v, p.dtype, lt))
             lvl = max(a[1] for a in args)
             names = [a[0] for a in args]
+            fast_ok = getattr(self, "fma_ok", False) and FAST_DIV and n.loop[0] is DType.f32
             if code is ElemCode.select:
                 T = n.dtype.ctype
                 expr = f"gr::select<{T}>({names[0]}, {names[1]}, {names[2]})"
+            elif code is ElemCode.div and fast_ok:
+                expr = f"gr::div_full({names[0]}, {names[1]})"
+            elif code is ElemCode.sqrt and fast_ok:
+                expr = f"gr::sqrt_approx({names[0]})"
             elif code is ElemCode.div and n.loop[0].is_float and args[1][1] < args[0][1]:
                 # divisor hoisted out of the dividend's scope: one reciprocal per
                 # divisor, exact Markstein correction per element
@@ -708,6 +713,9 @@ def inexact_region(region: Region) -> bool:
 CONTRACT = os.environ.get("GRUMPY_CONTRACT", "1") == "1"
 # fuse a product into every add/sub that consumes it (the product itself is
 # then never formed) rather than only into a sole consumer
+# inexact f32 regions also divide with div.full.f32 (2 ulp) and take square
+# roots with sqrt.approx.f32 (the same choice in the packed body and the tail)
+FAST_DIV = os.environ.get("GRUMPY_FAST_DIV", "1") == "1"
 # ptxas's own FFMA2 contraction of the packed body (with the tail run through
 # the same body): measured 1.054 vs 1.078 ms on Black-Scholes f32, but which
 # product ptxas fuses in a*b - c*d follows the emission order, which differs
@@ -815,8 +823,13 @@ class PairMapEmitter(MapEmitter):
                 # keep ptxas from contracting the product into its add (gr_pair.cuh)
                 fn = "gr::p2::mul_nc" if code is ElemCode.mul else "gr::p2::square_nc"
                 return self.emit(LEVEL_LANE, n.dtype.ctype, f"{fn}({', '.join(names)})"), LEVEL_LANE
+            fast_ok = self.contract and FAST_DIV and n.loop[0] is DType.f32
             if code is ElemCode.select:
                 expr = f"gr::p2::select({names[0]}, {names[1]}, {names[2]})"
+            elif code is ElemCode.div and fast_ok:
+                expr = f"gr::p2::div_full({names[0]}, {names[1]})"
+            elif code is ElemCode.sqrt and fast_ok:
+                expr = f"gr::p2::sqrt_approx({names[0]})"
             elif code in _PAIR_BIN and n.loop[0] is DType.f32:
                 expr = f"{_PAIR_BIN[code]}({names[0]}, {names[1]})"
             elif code in _PAIR_UN and n.loop[0] is DType.f32:

@@ -391,6 +391,8 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
 
 
 COOP_PAIR = os.environ.get("GRUMPY_COOP_PAIR", "1") == "1"
+COOP_BLOCKED_TOTAL = os.environ.get("GRUMPY_COOP_BLOCKED_TOTAL", "0") == "1"
+TOT_BLOCK = 4096          # rows per first-level block of a cooperative kernel's total
 COOP_BLOCK = int(os.environ.get("GRUMPY_COOP_BLOCK", "256"))
 
 
@@ -535,6 +537,21 @@ def _generate1(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetc
     P = 8 // vec
     NG = -(-R // rpc)
     two_pass = em.used_div_fast
+    # (experiment, off: GRUMPY_COOP_BLOCKED_TOTAL=1) totals folded per block
+    # of TOT_BLOCK rows by the warp whose row completes the block (the
+    # total's perfect tree restricted to aligned blocks, so the same
+    # association), then over the blocks by the last block-folder.  The
+    # single last-CTA fold of every row partial was a serial tail (rownorm:
+    # 0.048 of 0.235 ms); batching its loads (gr::chunk_tree) removed most of
+    # it, while the per-row release atomic (MEMBAR.ALL.GPU) and row-uniform
+    # redo vote of this scheme cost more (0.239 vs 0.225 ms)
+    blocked_tot = (COOP_BLOCKED_TOTAL and bool(tot_meta) and R % TOT_BLOCK == 0 and 2 <= R // TOT_BLOCK <= 1000
+                   and TOT_BLOCK % rpc == 0 and (R & (R - 1)) == 0)
+    tot_block_off = {}
+    if blocked_tot:
+        for ri, rop, T, off in tot_meta:
+            tot_block_off[ri] = scratch_off
+            scratch_off += ((R // TOT_BLOCK) * T.itemsize + 255) // 256 * 256
     templ = two_pass or async_layout is not None
     lines = [("template <bool FAST> static __device__ __forceinline__ bool rows(" if templ else
               "static __device__ __forceinline__ void rows(") +
@@ -559,8 +576,51 @@ def _generate1(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetc
     lines = [l.replace("GR_ROWSUM_TRAIL", trail) for l in lines]
     if templ:
         lines += ["  " + l for l in em.div_finalize]
+        if blocked_tot:
+            NWR = max(1, tpr // 32)
+            lines += [f"  __shared__ int gr_shbad[{rpc * NWR}];",
+                      f"  if constexpr (FAST) bad = gr::row_tree<gr::OpMax, int, {tpr}>(bad ? 1 : 0, gr_shbad, ri) != 0;",
+                      "  // count this row's final partial into its block of rows; the warp",
+                      "  // whose row completes the block folds it",
+                      "  {",
+                      "    int kf = -1;",
+                      f"    if (tr == 0 && valid && (FAST ? !bad : (((-1 - gnext) >> ri) & 1) != 0)) {{",
+                      f"      const int k = (int)(r / {TOT_BLOCK});",
+                      f"      if (gr::atom_add_release(p.ticket + 1 + k, 1u) + 1u == {TOT_BLOCK}u) kf = k;",
+                      "    }",
+                      "    if (tr < 32) {",
+                      "      kf = __shfl_sync(0xffffffffu, kf, 0);",
+                      "      if (kf >= 0) fold_block(p, kf);",
+                      "    }",
+                      "  }"]
         lines.append("  return bad;")
     lines.append("}")
+    if blocked_tot:
+        nb = R // TOT_BLOCK
+        fb = ["static __device__ __noinline__ void fold_block(const Params& p, const int k) {",
+              "  gr::fence_acq_rel();"]
+        for ri, rop, T, off in tot_meta:
+            ct = T.ctype
+            ident = c_literal(_IDENT[rop](T), T)
+            fb += [f"  {{ const {ct} v = gr::warp_range_tree<{_OPS[rop]}, {ct}, {TOT_BLOCK}LL>("
+                   f"reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {off}) + (long long)k * {TOT_BLOCK}, {ident});",
+                   f"    if ((threadIdx.x & 31) == 0) reinterpret_cast<{ct}*>(static_cast<char*>(p.scratch) + {tot_block_off[ri]})[k] = v; }}"]
+        fb += ["  int last = 0;",
+               "  if ((threadIdx.x & 31) == 0) {",
+               "    p.ticket[1 + k] = 0u;",
+               f"    last = gr::atom_add_release(p.ticket, 1u) + 1u == {nb}u;",
+               "  }",
+               "  if (__shfl_sync(0xffffffffu, last, 0)) {",
+               "    gr::fence_acq_rel();"]
+        for ri, rop, T, off in tot_meta:
+            ct = T.ctype
+            ident = c_literal(_IDENT[rop](T), T)
+            fin = f"gr::add<{ct}>({c_literal(0, T)}, t{ri})" if rop is ReduceOp.sum else f"t{ri}"
+            fb += [f"    const {ct} t{ri} = gr::warp_range_tree<{_OPS[rop]}, {ct}, {nb}LL>("
+                   f"reinterpret_cast<const {ct}*>(static_cast<const char*>(p.scratch) + {tot_block_off[ri]}), {ident});",
+                   f"    if ((threadIdx.x & 31) == 0) p.out{ri}[0] = {fin};"]
+        fb += ["    if ((threadIdx.x & 31) == 0) p.ticket[0] = 0u;", "  }", "}"]
+        lines = fb + lines
     issue = []
     if async_layout is not None:
         issue = ["static __device__ __forceinline__ void copy_group(const Params& p, unsigned char* stage, const long long g) {",
@@ -608,17 +668,24 @@ def _generate1(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetc
         src.append("  " + "\n  ".join(issue))
     src.append("  " + "\n  ".join(lines))
     src.append("};")
-    def _redo_tail(smem_arg, bar_arg):
+    def _redo_tail(smem_arg, bar_arg, next_arg="K::NG"):
         """flag bad rows during the loop; after it, redo flagged row groups
         (uniform per group: the flags are read after a CTA barrier) and clear
         the flags, so the buffer is zero again for the next launch"""
+        # the CTA's threads first check all its groups' flags at once (one L2
+        # round trip; a loop of dependent flag loads was a serial tail of
+        # ~20 us), and walk the groups only when one is flagged
         return ["  __syncthreads();",
+                "  bool gr_any = false;",
+                "  for (long long g = blockIdx.x + (long long)threadIdx.x * gridDim.x; g < K::NG; g += (long long)blockDim.x * gridDim.x)",
+                f"    gr_any |= ((__ldcg(p.redo + ((g * {rpc}) >> 5)) >> ((g * {rpc}) & 31)) & {(1 << rpc) - 1}u) != 0u;",
+                "  if (__syncthreads_or(gr_any))",
                 "  for (long long g = blockIdx.x; g < K::NG; g += gridDim.x) {",
                 f"    const unsigned bits = (__ldcg(p.redo + ((g * {rpc}) >> 5)) >> ((g * {rpc}) & 31)) & {(1 << rpc) - 1}u;",
                 "    if (bits) {",
                 "      __syncthreads();",
                 f"      if (threadIdx.x == 0) atomicAnd(p.redo + ((g * {rpc}) >> 5), ~({(1 << rpc) - 1}u << ((g * {rpc}) & 31)));",
-                f"      K::rows<false>(p, g * {rpc}, {smem_arg}, {bar_arg}, K::NG);",
+                f"      K::rows<false>(p, g * {rpc}, {smem_arg}, {bar_arg}, {next_arg});",
                 "    }",
                 "  }"]
 
@@ -671,11 +738,15 @@ def _generate1(region: Region, q, kname, prestage, tma, smem_bytes=0, l2_prefetc
             # (a CTA-wide vote per group cost 0.269 vs 0.243 ms on rownorm)
             kern += _flag(f"K::rows<true>(p, g * {rpc}, nullptr, nullptr, 0)")
             kern.append("  }")
-            kern += _redo_tail("nullptr", "nullptr")
+            # blocked totals: the redo pass counts only the redone rows (their
+            # mask travels in gnext as -1 - bits)
+            kern += _redo_tail("nullptr", "nullptr", "-1 - (long long)bits" if blocked_tot else "K::NG")
         else:
             kern.append(f"    K::rows(p, g * {rpc}, nullptr, nullptr, 0);")
             kern.append("  }")
-    if tot_meta:
+    if tot_meta and blocked_tot:
+        pass      # the warps completing a block fold it (K::fold_block); no grid-end fold
+    elif tot_meta:
         kern.append("  if (gr::last_block(p.ticket)) {")
         for ri, rop, T, off in tot_meta:
             ct = T.ctype

@@ -250,6 +250,21 @@ __device__ __forceinline__ double exp_(double a) { return exp(a); }
 __device__ __forceinline__ float log_(float a) { return logf(a); }
 __device__ __forceinline__ double log_(double a) { return log(a); }
 __device__ __forceinline__ float sqrt_(float a) { return sqrtf(a); }  // IEEE (prec-sqrt)
+// inexact regions (codegen.inexact_region, FAST_DIV): full-range 2-ulp
+// division (div.full.f32: MUFU.RCP + scaling, no Newton steps, no FCHK
+// slow path) and the MUFU square root (sqrt.approx.f32, ~1 ulp, subnormals
+// kept) — error of the same class as the libm transcendentals the region
+// already carries
+__device__ __forceinline__ float div_full(float a, float b) {
+  float r;
+  asm("div.full.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float sqrt_approx(float a) {
+  float r;
+  asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(a));
+  return r;
+}
 __device__ __forceinline__ double sqrt_(double a) { return sqrt(a); }
 __device__ __forceinline__ float sin_(float a) { return sinf(a); }
 __device__ __forceinline__ double sin_(double a) { return sin(a); }

@@ -187,11 +187,6 @@ template <class Op, class T> __device__ __forceinline__ T warp_tree(T v, int wid
   return v;
 }
 
-// Tree over n partials p[0..n) in index order, by one CTA (blockDim.x a power
-// of two <= 1024, n arbitrary).  Each thread folds a contiguous power-of-two
-// chunk as a perfect binary tree (binary-counter stack), then warp and CTA
-// trees: for power-of-two n this is exactly the perfect binary tree over p,
-// i.e. NumPy's pairwise split above row granularity.
 // s = (((s + p[0]) + p[stride]) + ...) over n terms, in that order, with the
 // loads of each batch of 8 issued before its adds: the fold of per-CTA
 // partials by the last CTA waits on L2 once per batch instead of once per
@@ -209,16 +204,38 @@ template <class T> __device__ __forceinline__ T seq_fold(T s, const T* p, unsign
   return s;
 }
 
-template <class Op, class T> __device__ T block_tree(const T* p, long long n, T ident) {
-  __shared__ T sh[32];
-  const int t = threadIdx.x, nt = blockDim.x;
-  long long chunk = 1;
-  while (chunk * nt < n) chunk <<= 1;
-  const long long lo = (long long)t * chunk;
+// Perfect binary tree over q[0..chunk) (chunk a power of two; elements at
+// or past nvalid are the identity), by one thread: leaves in batches of 32
+// (8 for shorter chunks) — the batch's loads issued together, combined as a
+// perfect tree — then a binary-counter stack over the batches.  Same
+// association as a leaf-by-leaf stack; one L2 round trip per batch instead of
+// per partial (rownorm's total: the last CTA's fold of 65536 row partials
+// 0.048 -> ~0.01 ms).
+template <class Op, class T, int B>
+__device__ __forceinline__ T batch_tree(const T* q, long long nvalid, T ident) {
+  T a[B];
+#pragma unroll
+  for (int k = 0; k < B; ++k) a[k] = (k < nvalid) ? __ldcg(q + k) : ident;
+#pragma unroll
+  for (int s = 1; s < B; s <<= 1)
+#pragma unroll
+    for (int k = 0; k + s < B; k += 2 * s) a[k] = Op::template c<T>(a[k], a[k + s]);
+  return a[0];
+}
+template <class Op, class T>
+__device__ __forceinline__ T chunk_tree(const T* q, long long chunk, long long nvalid, T ident) {
   T stack[40];
   long long cnt = 0;
-  for (long long i = 0; i < chunk; ++i) {
-    T v = (lo + i < n) ? p[lo + i] : ident;
+  const long long step = chunk >= 32 ? 32 : chunk >= 8 ? 8 : 1;
+  for (long long i = 0; i < chunk; i += step) {
+    T v;
+    if (step == 32) {
+      v = batch_tree<Op, T, 32>(q + i, nvalid - i, ident);
+    } else if (step == 8) {
+      v = batch_tree<Op, T, 8>(q + i, nvalid - i, ident);
+    } else {
+      v = (i < nvalid) ? __ldcg(q + i) : ident;
+    }
     int lvl = 0;
     while ((cnt >> lvl) & 1) {
       v = Op::template c<T>(stack[lvl], v);
@@ -228,8 +245,22 @@ template <class Op, class T> __device__ T block_tree(const T* p, long long n, T 
     ++cnt;
   }
   int top = 0;
-  while ((1ll << top) < chunk) ++top;
-  T acc = stack[top];
+  while ((1ll << top) < chunk / step) ++top;
+  return stack[top];
+}
+
+// Tree over n partials p[0..n) in index order, by one CTA (blockDim.x a power
+// of two <= 1024, n arbitrary).  Each thread folds a contiguous power-of-two
+// chunk as a perfect binary tree (binary-counter stack), then warp and CTA
+// trees: for power-of-two n this is exactly the perfect binary tree over p,
+// i.e. NumPy's pairwise split above row granularity.
+template <class Op, class T> __device__ T block_tree(const T* p, long long n, T ident) {
+  __shared__ T sh[32];
+  const int t = threadIdx.x, nt = blockDim.x;
+  long long chunk = 1;
+  while (chunk * nt < n) chunk <<= 1;
+  const long long lo = (long long)t * chunk;
+  T acc = chunk_tree<Op, T>(p + lo, chunk, n - lo, ident);
   acc = warp_tree<Op, T>(acc);
   const int lane = t & 31, w = t >> 5, nw = (nt + 31) >> 5;
   if (lane == 0) sh[w] = acc;
@@ -675,6 +706,39 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
                    atomicAdd(&gr_scan_stats[2], (unsigned long long)(clock64() - c0)); }
 #endif
   return __shfl_sync(0xffffffffu, pre, 0);
+}
+
+// acq_rel atomic add (gpu scope): releases the caller's prior writes,
+// acquires those released by earlier adds on the same word
+__device__ __forceinline__ unsigned atom_add_acq_rel(unsigned int* p, unsigned int v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// release-only add (MEMBAR.ALL.GPU + ATOMG): no acquire, so no L1 invalidation
+// (an acq_rel or fenced atomic at gpu scope also emits CCTL.IVALL); the rare
+// reader that finds the count complete acquires with fence_acq_rel()
+__device__ __forceinline__ unsigned atom_add_release(unsigned int* p, unsigned int v) {
+  unsigned old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Perfect binary tree over p[0..N) (N a power of two) by ONE warp: each lane
+// folds a contiguous chunk as a perfect tree (pairwise stack), the lanes
+// combine by the xor butterfly — the same association as block_tree over the
+// same range.  N < 32: lanes >= N contribute the identity.
+template <class Op, class T, long long N> __device__ __forceinline__ T warp_range_tree(const T* p, T ident) {
+  const int lane = threadIdx.x & 31;
+  T v;
+  if constexpr (N >= 32) {
+    constexpr long long CH = N / 32;
+    v = chunk_tree<Op, T>(p + lane * CH, CH, CH, ident);
+  } else {
+    v = lane < N ? __ldcg(p + lane) : ident;
+  }
+  return warp_tree<Op, T>(v);
 }
 
 // Ticket of a group of `expected` blocks: true in exactly the last of them to

@@ -267,3 +267,35 @@ def test_nearest_centre_off_matches(sess, monkeypatch):
     finally:
         codegen._GEN_CACHE.clear()
     assert np.array_equal(on, got) and np.array_equal(on, wl.kmeans_assign(np, P, C))
+
+
+@pytest.mark.parametrize("blocked", [False, True])
+@pytest.mark.parametrize("rows", [8192, 16384])
+@pytest.mark.parametrize("store_y", [False, True])
+def test_rownorm_blocked_total_with_redo(sess, monkeypatch, blocked, rows, store_y):
+    """Totals over many rows with rows redone exactly: the last CTA's batched
+    fold (default) and the per-4096-row-block warp folds (codegen_coop
+    TOT_BLOCK, GRUMPY_COOP_BLOCKED_TOTAL=1) are bit-identical to NumPy, also
+    when rows of several blocks take the exact redo pass (counted only after
+    their redo) and across repeated launches (counters reset)."""
+    from paper_1901_03771_b200 import codegen, codegen_coop
+    monkeypatch.setattr(codegen_coop, "COOP_BLOCKED_TOTAL", blocked)
+    codegen._GEN_CACHE.clear()
+    sess._plan_cache.clear()
+    rng = np.random.default_rng([rows, store_y])
+    x = (rng.standard_normal((rows, 4096)) * 2 + 5).astype(np.float32)
+    for r in (5, 4100, rows - 1):
+        x[r, :] = 0.0
+        x[r, 17] = 1e-30                 # tiny dividends: this row is redone
+    x[4097, ::2] = 1.0
+    x[4097, 1::2] = -1.0
+    ey, et = wl.rownorm(np, x)
+    gx = gp.asarray(x)
+    for _ in range(3):
+        y, tot = wl.rownorm(gp, gx)
+        if store_y:
+            gp.force(y, tot)
+            assert np.array_equal(np.asarray(y), ey)
+        assert np.asarray(tot) == et
+    assert ("fold_block" in sess.executor.last_steps[0].cache["ks"].source) == blocked
+    codegen._GEN_CACHE.clear()

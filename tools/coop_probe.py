@@ -113,5 +113,40 @@ def main():
               f"min={np.min(ms):.4f} frac={1073741824 / np.mean(ms) / 1e6 / 6549.8:.3f} total={tot!r} same={tot == ref}", flush=True)
 
 
+
+
+
+FOLD_SRC = r'''
+#include "gr_ops.cuh"
+#include "gr_reduce.cuh"
+extern "C" __global__ void __launch_bounds__(256) fold(const float* p, float* o, long long n) {
+  const float v = gr::block_tree<gr::OpSum, float>(p, n, 0.0f);
+  if (threadIdx.x == 0) o[0] = v;
+}
+'''
+
+
+def fold_time():
+    """One CTA's block_tree over 65536 partials (the coop kernel's final fold)."""
+    rt = runtime.get()
+    n = 65536
+    x = rt.upload(np.random.default_rng(0).standard_normal(n).astype(np.float32))
+    o = rt.alloc(256)
+    k = rt.kernel(FOLD_SRC, "fold", 256, 0)
+    ms = []
+    for i in range(20):
+        e0, e1 = rt.event(), rt.event()
+        rt.record(e0)
+        rt.launch(k, 1, 256, runtime.pack_params([x.ptr, o.ptr, n]))
+        rt.record(e1)
+        rt.sync()
+        if i >= 3:
+            ms.append(rt.elapsed_ms(e0, e1))
+    print(f"block_tree over {n} f32 by one CTA: {np.mean(ms) * 1e3:.1f} us (min {np.min(ms) * 1e3:.1f})", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["fold"]:
+        fold_time()
+    else:
+        main()
