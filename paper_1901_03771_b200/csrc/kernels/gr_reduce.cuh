@@ -254,11 +254,67 @@ __device__ __forceinline__ T chunk_tree(const T* q, long long chunk, long long n
 // chunk as a perfect binary tree (binary-counter stack), then warp and CTA
 // trees: for power-of-two n this is exactly the perfect binary tree over p,
 // i.e. NumPy's pairwise split above row granularity.
+// Large n: each warp takes a contiguous power-of-two range and walks it in
+// 256-element chunks with coalesced loads (lane i: elements 8i..8i+7 of the
+// chunk, 4 chunks in flight): an 8-leaf tree per lane, the xor butterfly over
+// the lanes (the chunk's perfect tree), a stack over the chunks; the warps'
+// ranges combine in a perfect tree.  Same association as the per-thread
+// chunks below (a perfect tree over the padded range); 65536 f32 partials:
+// 44 -> a few us (the per-thread chunks were 32 lanes x 1 KB strided).
+template <class Op, class T> __device__ T block_tree_wide(const T* p, long long n, T ident, long long S) {
+  __shared__ T shw[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const long long W = S / nw;                       // per-warp range (power of two, >= 1024)
+  const long long base = (long long)w * W;
+  T stack[40];
+  long long cnt = 0;
+  for (long long c0 = 0; c0 < W; c0 += 4 * 256) {
+    T a[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const long long e = base + c0 + u * 256 + lane * 8 + k;
+        a[u][k] = e < n ? __ldcg(p + e) : ident;
+      }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int st = 1; st < 8; st <<= 1)
+#pragma unroll
+        for (int k = 0; k + st < 8; k += 2 * st) a[u][k] = Op::template c<T>(a[u][k], a[u][k + st]);
+      T v = warp_tree<Op, T>(a[u][0]);
+      int lvl = 0;
+      while ((cnt >> lvl) & 1) {
+        v = Op::template c<T>(stack[lvl], v);
+        ++lvl;
+      }
+      stack[lvl] = v;
+      ++cnt;
+    }
+  }
+  int top = 0;
+  while ((1ll << top) < W / 256) ++top;
+  if (lane == 0) shw[w] = stack[top];
+  __syncthreads();
+  if (w == 0) {
+    T v = lane < nw ? shw[lane] : ident;
+    v = warp_tree<Op, T>(v);
+    if (lane == 0) shw[0] = v;
+  }
+  __syncthreads();
+  T r = shw[0];
+  __syncthreads();
+  return r;
+}
+
 template <class Op, class T> __device__ T block_tree(const T* p, long long n, T ident) {
   __shared__ T sh[32];
   const int t = threadIdx.x, nt = blockDim.x;
   long long chunk = 1;
   while (chunk * nt < n) chunk <<= 1;
+  if (chunk * nt >= 1024LL * (nt / 32) && (nt & 31) == 0)
+    return block_tree_wide<Op, T>(p, n, ident, chunk * nt);
   const long long lo = (long long)t * chunk;
   T acc = chunk_tree<Op, T>(p + lo, chunk, n - lo, ident);
   acc = warp_tree<Op, T>(acc);
