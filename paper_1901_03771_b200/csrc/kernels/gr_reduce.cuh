@@ -270,13 +270,27 @@ template <class Op, class T> __device__ T block_tree_wide(const T* p, long long 
   long long cnt = 0;
   for (long long c0 = 0; c0 < W; c0 += 4 * 256) {
     T a[4][8];
+    if (base + c0 + 4 * 256 <= n && (reinterpret_cast<unsigned long long>(p) & 15) == 0) {
+      // whole chunks in range: 16-byte vector loads (the range bases are
+      // multiples of 1024 elements)
 #pragma unroll
-    for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 4; ++u) {
+        const uint4* q = reinterpret_cast<const uint4*>(p + base + c0 + u * 256 + lane * 8);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const long long e = base + c0 + u * 256 + lane * 8 + k;
-        a[u][k] = e < n ? __ldcg(p + e) : ident;
+        for (int h = 0; h < (int)(8 * sizeof(T) / 16); ++h) {
+          const uint4 r = __ldcg(q + h);
+          memcpy(&a[u][h * (16 / sizeof(T))], &r, 16);
+        }
       }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const long long e = base + c0 + u * 256 + lane * 8 + k;
+          a[u][k] = e < n ? __ldcg(p + e) : ident;
+        }
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
 #pragma unroll
