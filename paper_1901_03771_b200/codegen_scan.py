@@ -39,6 +39,7 @@ SCAN_TMA_SMEM = 200 * 1024
 SCAN_TMA_STAGES = int(os.environ.get("GRUMPY_SCAN_STAGES", "6"))
 SCAN_TMA_LAG = int(os.environ.get("GRUMPY_SCAN_LAG", "3"))
 SCAN_TMA_LBW = int(os.environ.get("GRUMPY_SCAN_LBW", "1"))
+SCAN_TMA_ITEMS = int(os.environ.get("GRUMPY_SCAN_ITEMS", "16"))
 
 
 def generate(region: Region, kname="gr_region") -> KernelSource:
@@ -354,9 +355,12 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     if N % W:
         return None
     TPB = 512 if isz == 4 else 256
+    ITEMS = SCAN_TMA_ITEMS                # elements per data thread (16: 32 KB tiles, 32: 64 KB)
     tile = TPB * ITEMS
     tile_b = tile * isz                  # 32 KB
-    rows = tile // W                     # 256 lines per box
+    rows = tile // W                     # 128-byte lines per tile
+    box = min(rows, 256)                 # TMA box: at most 256 lines (32 KB)
+    nbox = rows // box
     ntiles = -(-N // tile)
     NL = len(staged)
     S_ = min(SCAN_TMA_STAGES, SCAN_TMA_SMEM // (NL * tile_b))
@@ -398,8 +402,8 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     M = LAG + NLW                         # mailbox slots
     NTH = TPB + 32 * NLW + 32
     sgs = ", ".join(f"ring + ((long long)s * {NL} + {k}) * {tile_b}" for k in range(NL))
-    loads = "\n".join(f"        gr::tma_load_2d(ring + ((long long)s * {NL} + {k}) * {tile_b}, &p.tmap{k}, 0, (int)(t * {rows}), &full[s]);"
-                      for k in range(NL))
+    loads = "\n".join(f"        gr::tma_load_2d(ring + ((long long)s * {NL} + {k}) * {tile_b} + {b * box * 128}, &p.tmap{k}, 0, (int)(t * {rows} + {b * box}), &full[s]);"
+                      for k in range(NL) for b in range(nbox))
     kern = f"""extern "C" __global__ void __launch_bounds__({NTH}, 1) {kname}(const __grid_constant__ K::Params p) {{
   // warps 0..{NW - 1}: data (scan); warps {NW}..{NW + NLW - 1}: look-back (iteration i
   // goes to warp NW + i % {NLW}); warp {NW + NLW}: TMA producer.  A tile's
@@ -479,7 +483,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     gr::fence_proxy_async();
     asm volatile("bar.sync 1, {TPB};" ::: "memory");
     if (threadIdx.x == 0) {{
-      gr::tma_store_2d(&p.tmap{NL}, 0, (int)(tj * {rows}), ob);
+      for (int b = 0; b < {nbox}; ++b) gr::tma_store_2d(&p.tmap{NL}, 0, (int)(tj * {rows} + b * {box}), ob + b * {box * 128});
       gr::bulk_commit();
       gr::bulk_wait_read<1>();
       if (srel >= 0) gr::mbar_arrive(&empty[srel]);
@@ -544,7 +548,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     src = [pre + HEADER, '#include "gr_reduce.cuh"\n#include "gr_tma.cuh"\n', "struct K {", params, "  " + body.replace("\n", "\n  "), "};", kern]
     scratch = 8 + 8 * (1 if isz <= 4 else 2) * 2 * ntiles + 256
     slots = [region.leaves.index(l) for l in staged]
-    tmaps = [(i, W, N // W, W, rows, 128) for i in slots] + [(len(region.leaves), W, N // W, W, rows, 128)]
+    tmaps = [(i, W, N // W, W, box, 128) for i in slots] + [(len(region.leaves), W, N // W, W, box, 128)]
     return KernelSource("scan", "\n".join(src) + "\n", kname, list(range(len(region.leaves))), [0],
                         block=NTH, groups=ntiles * NTH, vec=1, unroll=1, scratch_bytes=scratch,
                         meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,
