@@ -144,6 +144,12 @@ def _compute(n: Node, a):
             axis = 0
         uf = {ReduceOp.sum: np.add, ReduceOp.prod: np.multiply,
               ReduceOp.max: np.maximum, ReduceOp.min: np.minimum}[rop]
+        if len(a) > 1:
+            # seeded: the fold starts from the seed (a line of the kept axes)
+            seed = np.expand_dims(np.asarray(a[1]).reshape(
+                tuple(d for i, d in enumerate(x.shape) if i != axis)), axis).astype(n.dtype.np)
+            return uf.accumulate(np.concatenate([seed, x.astype(n.dtype.np)], axis=axis), axis=axis,
+                                 dtype=n.dtype.np).take(range(1, x.shape[axis] + 1), axis=axis)
         return uf.accumulate(x, axis=axis, dtype=n.dtype.np)
     if k is OpKind.MATMUL:
         return np.matmul(a[0], a[1])

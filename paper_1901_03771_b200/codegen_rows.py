@@ -58,6 +58,11 @@ NEAREST_MAX_D = 8
 # of line (gr::nearest_exact, __noinline__) the k-means kernel needs 32
 # registers and runs at full occupancy uncapped.
 NEAREST_MIN_BLOCKS = int(os.environ.get("GRUMPY_NEAREST_MINB", "0"))
+# (experiment, off) the kernel's row loop takes two rows per step and
+# searches both rows' centres together (gr::nearest_centre_n<.., 2>): 444
+# instead of 496 hot-loop instructions per point, but 40 registers and the
+# row body's own reload of the point: 1.636 vs 1.601 ms on k-means 2^26 x 64
+NEAREST_PAIR_ROWS = os.environ.get("GRUMPY_NEAREST_PAIR", "0") == "1"
 NEAREST_MAX_K = 256
 
 
@@ -256,6 +261,9 @@ class LoopEmitter(ValueEmitter):
         self.skinny: Optional[tuple] = None
         # centre leaf id -> (K, D, table symbol) of certified nearest-centre searches
         self.nearest: Dict[int, tuple] = {}
+        # two rows per nearest-centre search, done by the kernel loop
+        self.nn_rows2 = False
+        self.nn_pair: Optional[tuple] = None   # (row operand, K, D, table symbol, centre symbol)
 
     # -- scopes ------------------------------------------------------------------
     def emit(self, level, ctype, expr):
@@ -685,6 +693,11 @@ class LoopEmitter(ValueEmitter):
             return None
         tsym = sym + "_nn"
         self.nearest[leaf.id] = (K, D, tsym)
+        if self.nn_rows2 and self.nn_pair is None and kept[0].key() == Aff.of(Var("r", 1)).key():
+            # the kernel loop searches two rows' centres at once (sharing every
+            # table load) and hands this row its label
+            self.nn_pair = (u, K, D, tsym, sym)
+            return self.emit(L, "long long", "nnlab"), L
         pv = self.fresh("P")
         self.stmt(L, f"float {pv}[{D}];")
         iv, s, saved = self.open(L, "for", trip=D, unroll=True)
@@ -962,6 +975,7 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
         cbank = {k: v for k, v in cbank.items() if k != mm.preds[1].id}
     em = LoopEmitter(region, cbank=cbank)
     em.pair_loops = pair
+    em.nn_rows2 = NEAREST_PAIR_ROWS and virtual is None and len(Ts) == 1 and not mms
     rvar = Var("r", 1)
     # row coordinates
     if virtual is None:
@@ -1178,11 +1192,32 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
                 pref.append((i, W))
     lines = ["static __device__ __forceinline__ void row(const Params& p, const long long r, const bool valid"
              + "".join(f", {r.dtype.ctype}* khist{j}" for j, r, _, _ in kmeta)
-             + (f", const float (&zk)[{NZ}]" if mms else "") + ") {",
+             + (f", const float (&zk)[{NZ}]" if mms else "") + (", const int nnlab" if em.nn_pair else "") + ") {",
              "  (void)valid;"]
     lines += ["  " + c for c in em.consts]
     lines += render(em.row, 1)
     lines.append("}")
+    if em.nn_pair:
+        u, K_, D_, tsym, csym = em.nn_pair
+        pe = LoopEmitter(region, cbank=cbank)
+        iv, sc, saved = pe.open(1, "for", trip=D_, unroll=True)
+        v = pe.cast(pe.value(u, [Aff.of(Var("r", 1)), Aff.of(0), Aff.of(iv)]), u.dtype, DType.f32)
+        pe.stmt(iv.level, f"pv[{iv.name}] = {v[0]};")
+        pe.close(sc, saved)
+        lines += [f"static __device__ __forceinline__ void point(const Params& p, const long long r, float (&pv)[{D_}]) {{"]
+        lines += ["  " + c for c in pe.consts]
+        lines += render(pe.row, 1)
+        lines += ["}",
+                  "// two rows' nearest centres: each table record loaded once for both",
+                  "static __device__ __forceinline__ void nn_labels(const Params& p, const long long r0, const long long r1, int (&lab)[2]) {",
+                  f"  float P[2][{D_}];",
+                  "  point(p, r0, P[0]);",
+                  "  point(p, r1, P[1]);",
+                  "  bool ok[2];",
+                  f"  gr::nearest_centre_n<{K_}, {D_}, 2>(P, {tsym}, lab, ok);",
+                  f"  if (!ok[0]) lab[0] = gr::nearest_exact<{K_}, {D_}>(P[0], {csym});",
+                  f"  if (!ok[1]) lab[1] = gr::nearest_exact<{K_}, {D_}>(P[1], {csym});",
+                  "}"]
     params = _params_struct(region).replace("    void* __restrict__ scratch;",
                                              "    void* __restrict__ scratch;\n    unsigned int* ticket;")
     used_cb = []
@@ -1272,12 +1307,25 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
             kern.append(f"  for (int i = threadIdx.x; i < {warps * NBj}; i += blockDim.x) khist{j}[i] = 0;")
         kern.append("  __syncthreads();")
         hargs = "".join(f", khist{j}" for j, _, _, _ in kmeta)
-        kern += ["  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < K::NROWS; base += stride) {",
-                 "    const long long r = base + (threadIdx.x & 31);"]
-        kern += [f"    if (r + stride < K::NROWS) gr::prefetch_l1(p.in{i} + (r + stride) * {W}LL);" for i, W in pref]
-        kern += [f"    K::row(p, r < K::NROWS ? r : K::NROWS - 1, r < K::NROWS{hargs});",
-                 "  }",
-                 "  __syncthreads();"]
+        if em.nn_pair:
+            kern += ["  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < K::NROWS; base += 2 * stride) {",
+                     "    const long long r = base + (threadIdx.x & 31), r1 = r + stride;"]
+            kern += [f"    if (r + 2 * stride < K::NROWS) gr::prefetch_l1(p.in{i} + (r + 2 * stride) * {W}LL);" for i, W in pref]
+            kern += [f"    if (r1 + 2 * stride < K::NROWS) gr::prefetch_l1(p.in{i} + (r1 + 2 * stride) * {W}LL);" for i, W in pref]
+            kern += ["    const long long rc = r < K::NROWS ? r : K::NROWS - 1, r1c = r1 < K::NROWS ? r1 : K::NROWS - 1;",
+                     "    int nl[2];",
+                     "    K::nn_labels(p, rc, r1c, nl);",
+                     f"    K::row(p, rc, r < K::NROWS{hargs}, nl[0]);",
+                     f"    if (base + stride < K::NROWS) K::row(p, r1c, r1 < K::NROWS{hargs}, nl[1]);",
+                     "  }",
+                     "  __syncthreads();"]
+        else:
+            kern += ["  for (long long base = (long long)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < K::NROWS; base += stride) {",
+                     "    const long long r = base + (threadIdx.x & 31);"]
+            kern += [f"    if (r + stride < K::NROWS) gr::prefetch_l1(p.in{i} + (r + stride) * {W}LL);" for i, W in pref]
+            kern += [f"    K::row(p, r < K::NROWS ? r : K::NROWS - 1, r < K::NROWS{hargs});",
+                     "  }",
+                     "  __syncthreads();"]
         for j, r, NBj, off in kmeta:
             ct = r.dtype.ctype
             kern += [f"  for (int b = threadIdx.x; b < {NBj}; b += blockDim.x) {{",
@@ -1285,6 +1333,14 @@ def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:
                      f"    for (int w = 1; w < {warps}; ++w) s += khist{j}[w * {NBj} + b];",
                      f"    reinterpret_cast<{ct}*>(static_cast<char*>(p.scratch) + {off})[(long long)blockIdx.x * {NBj} + b] = s;",
                      "  }"]
+    elif em.nn_pair:
+        kern += ["  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += 2 * stride) {",
+                 "    const long long r1 = r + stride;",
+                 "    int nl[2];",
+                 "    K::nn_labels(p, r, r1 < K::NROWS ? r1 : r, nl);",
+                 "    K::row(p, r, true, nl[0]);",
+                 "    if (r1 < K::NROWS) K::row(p, r1, true, nl[1]);",
+                 "  }"]
     else:
         if pref:
             kern += ["  for (long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x; r < K::NROWS; r += stride) {"]

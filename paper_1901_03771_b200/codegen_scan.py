@@ -23,7 +23,7 @@ from __future__ import annotations
 import os
 from typing import List
 
-from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, c_literal
+from .codegen import HEADER, Aff, KernelSource, Region, Var, _params_struct, bcast_coords, c_literal
 from .codegen_rows import _COMBINE, _IDENT, _OPS, LoopEmitter, NotFusable, render, _flat_coords
 from .dag import OpKind, ReduceOp
 from .errors import UnsupportedNodeInFusedStep
@@ -49,6 +49,7 @@ def generate(region: Region, kname="gr_region") -> KernelSource:
     s = scans[0]
     rop, axis, odt = s.op.attrs
     x = s.preds[0]
+    seed = s.preds[1] if len(s.preds) > 1 else None
     for n in region.nodes:
         if n is not s and n.kind in (OpKind.SCAN, OpKind.REDUCE, OpKind.ARGREDUCE, OpKind.KEYED_SUM):
             raise NotFusable(n, "reductions before a scan run as their own step")
@@ -88,7 +89,14 @@ def _gen_lines(region, s, x, rop, axis, kname, block=128) -> KernelSource:
             kept.append(Aff.of(em.derived_var(1, f"{rest.c()} % {kept_shape[d]}")))
             rest = Aff.of(em.derived_var(1, f"{rest.c()} / {kept_shape[d]}"))
     kept.reverse()
-    acc = em.var_decl(1, ct, c_literal(_IDENT[rop](T), T))
+    seed = s.preds[1] if len(s.preds) > 1 else None
+    if seed is not None:
+        # seeded fold (a streamed chunk's carry): the line starts from its seed
+        sv = em.cast(em.value(seed, bcast_coords(kept, kept_shape, seed.shape) if kept_shape else [Aff.of(0)] * len(seed.shape)),
+                     seed.dtype, T)
+        acc = em.var_decl(1, ct, sv[0])
+    else:
+        acc = em.var_decl(1, ct, c_literal(_IDENT[rop](T), T))
     k, sc, saved = em.open(1, "for", trip=n)
     if axis is None:
         coords = _flat_coords(em, x.shape, Aff.of(k), k)
@@ -101,7 +109,10 @@ def _gen_lines(region, s, x, rop, axis, kname, block=128) -> KernelSource:
             off = off + c.scale(sd)
     v = em.cast(em.value(x, coords), x.dtype, T)
     comb = _COMBINE[rop]
-    em.stmt(k.level, f"{acc} = ({k.name} == 0) ? {v[0]} : {comb}<{ct}>({acc}, {v[0]});")
+    if seed is not None:
+        em.stmt(k.level, f"{acc} = {comb}<{ct}>({acc}, {v[0]});")
+    else:
+        em.stmt(k.level, f"{acc} = ({k.name} == 0) ? {v[0]} : {comb}<{ct}>({acc}, {v[0]});")
     em.stmt(k.level, f"p.out0[{off.c()}] = {acc};")
     em.close(sc, saved)
     lines = ["static __device__ __forceinline__ void line(const Params& p, const long long r) {"]
@@ -137,6 +148,10 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     chunks = ITEMS // vec
     ident = c_literal(_IDENT[rop](T), T)
     comb = _COMBINE[rop]
+    seed = s.preds[1] if len(s.preds) > 1 else None
+    seeded = "true" if seed is not None else "false"
+    seed_fn = _seed_fn(region, seed, T)
+    seedv = "K::seed_value(p)" if seed is not None else c_literal(_IDENT[rop](T), T)
     op = _OPS[rop]
 
     def load_fn(name, full):
@@ -199,7 +214,10 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
 #endif
       const long long t = tids[i & 1];
       if (t < 0) break;
-      const {ct} pre = gr::tile_lookback<{op}, {ct}>(aggs, incs, t, tagg[i & 1], {ident});
+      // a seed (streamed carry) joins tile 0: its inclusive prefix is
+      // seed (+) aggregate, its exclusive prefix the seed
+      const {ct} pre0 = gr::tile_lookback<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? {comb}<{ct}>({seedv}, tagg[i & 1]) : tagg[i & 1], {ident});
+      const {ct} pre = {seeded} && t == 0 ? {seedv} : pre0;
       if (lane == 0) tpre[i & 1] = pre;
       asm volatile("bar.arrive 3, {NTH};" ::: "memory");
     }}
@@ -234,7 +252,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
         const long long e = (long long)j * {TILE_THREADS * vec} + {vec} * threadIdx.x;
         {ct} o[{vec}];
 #pragma unroll
-        for (int v = 0; v < {vec}; ++v) {{ const {ct} x = buf[gr::spad(e + v)]; o[v] = t > 0 ? {comb}<{ct}>(pre, x) : x; }}
+        for (int v = 0; v < {vec}; ++v) {{ const {ct} x = buf[gr::spad(e + v)]; o[v] = (t > 0 || {seeded}) ? {comb}<{ct}>(pre, x) : x; }}
         if (tb + e + {vec} <= {N}LL) {{
           gr::stv<{ct}, {vec}>(p.out0 + tb + e, o);
         }} else {{
@@ -283,7 +301,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
              f"  for (int i = 0; i < {ITEMS}; ++i) buf[gr::spad({ITEMS} * threadIdx.x + i)] = has ? {comb}<{ct}>(loc, vals[i]) : vals[i];",
              f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
              "}"]
-    lines = lines + stage
+    lines = lines + stage + seed_fn
     src = [HEADER, '#include "gr_reduce.cuh"\n', "struct K {", params, "  " + "\n  ".join(lines), "};", kern]
     scratch = 8 + 8 * SW * 2 * ntiles + 256
     return KernelSource("scan", "\n".join(src) + "\n", kname, list(range(len(region.leaves))), [0],
@@ -370,6 +388,10 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     NW = TPB // 32
     ident = c_literal(_IDENT[rop](T), T)
     comb = _COMBINE[rop]
+    seed = s.preds[1] if len(s.preds) > 1 else None
+    seeded = "true" if seed is not None else "false"
+    seed_fn = _seed_fn(region, seed, T)
+    seedv = "K::seed_value(p)" if seed is not None else c_literal(_IDENT[rop](T), T)
     op = _OPS[rop]
 
     # ---- per-thread items: the map prologue on 16 consecutive elements
@@ -453,7 +475,8 @@ def _gen_lookback_tma(region, s, x, rop, kname):
       __threadfence_block();
       const long long t = mb_tid[m];
       if (t < 0) break;
-      const {ct} pre = gr::tile_lookback_buf<{op}, {ct}>(aggs, incs, t, mb_agg[m], {ident}, lbw[k].v);
+      const {ct} pre0 = gr::tile_lookback_buf<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? {comb}<{ct}>({seedv}, mb_agg[m]) : mb_agg[m], {ident}, lbw[k].v);
+      const {ct} pre = {seeded} && t == 0 ? {seedv} : pre0;
       if (lane == 0) {{ mb_pre[m] = pre; __threadfence_block(); mb_done[m] = i + 1; }}
       __syncwarp();
     }}
@@ -474,7 +497,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     for (int q = 0; q < {ITEMS // vec}; ++q) {{
       {ct} o[{vec}];
       gr::lds_sw<{ct}, {vec}>(o, ob, {ITEMS} * threadIdx.x + {vec} * q);
-      if (tj > 0) {{
+      if (tj > 0 || {seeded}) {{
 #pragma unroll
         for (int k2 = 0; k2 < {vec}; ++k2) o[k2] = {comb}<{ct}>(pre, o[k2]);
         gr::sts_sw<{ct}, {vec}>(ob, {ITEMS} * threadIdx.x + {vec} * q, o);
@@ -545,7 +568,8 @@ def _gen_lookback_tma(region, s, x, rop, kname):
   if (threadIdx.x == 0) gr::bulk_wait<0>();
 }}"""
     pre = "".join(f"#define {d.replace('=', ' ', 1)}\n" for d in os.environ.get("GRUMPY_SCAN_DEFINES", "").split(",") if d)  # experiments
-    src = [pre + HEADER, '#include "gr_reduce.cuh"\n#include "gr_tma.cuh"\n', "struct K {", params, "  " + body.replace("\n", "\n  "), "};", kern]
+    src = [pre + HEADER, '#include "gr_reduce.cuh"\n#include "gr_tma.cuh"\n', "struct K {", params,
+           "  " + body.replace("\n", "\n  "), "  " + "\n  ".join(seed_fn), "};", kern]
     scratch = 8 + 8 * (1 if isz <= 4 else 2) * 2 * ntiles + 256
     slots = [region.leaves.index(l) for l in staged]
     tmaps = [(i, W, N // W, W, box, 128) for i in slots] + [(len(region.leaves), W, N // W, W, box, 128)]
@@ -554,3 +578,18 @@ def _gen_lookback_tma(region, s, x, rop, kname):
                         meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,
                               "label": "scan-tma", "smem": S_ * NL * tile_b + 1024, "tmaps": tmaps,
                               "stages": S_})
+
+
+def _seed_fn(region, seed, T):
+    """K::seed_value(p): the value seeding a long scan (a streamed chunk's
+    carry — a view of the previous chunk's result), through the region's
+    index maps."""
+    if seed is None:
+        return []
+    se = LoopEmitter(region)
+    v = se.cast(se.value(seed, [Aff.of(0)] * len(seed.shape)), seed.dtype, T)
+    out = [f"static __device__ __forceinline__ {T.ctype} seed_value(const Params& p) {{"]
+    out += ["  " + c for c in se.consts]
+    out += render(se.row, 1)
+    out += [f"  return {v[0]};", "}"]
+    return out

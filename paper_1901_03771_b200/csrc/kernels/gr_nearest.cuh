@@ -60,50 +60,78 @@ __device__ __forceinline__ float nn_min3(float a, float b, float c) {
   return r;
 }
 
-template <int K, int D>
-__device__ __forceinline__ bool nearest_centre(const float (&p)[D], const float2* __restrict__ tab, int& label) {
+// NPT points at once (each table record loaded once for all of them: the
+// uniform loads and moves per point shrink with NPT); ok[i] / label[i] per
+// point exactly as the one-point search below.
+template <int K, int D, int NPT>
+__device__ __forceinline__ void nearest_centre_n(const float (&p)[NPT][D], const float2* __restrict__ tab,
+                                                 int (&label)[NPT], bool (&ok)[NPT]) {
   using N = Nearest<K, D>;
   const float* hdr = reinterpret_cast<const float*>(tab);
-  float q[D];
-  float pp = 0.0f;
+  float q[NPT][D];
+  float pp[NPT];
 #pragma unroll
-  for (int k = 0; k < D; ++k) {
-    const float pk = __fsub_rn(p[k], hdr[k]);
-    q[k] = -2.0f * pk;
-    pp = __fmaf_rn(pk, pk, pp);
+  for (int i = 0; i < NPT; ++i) {
+    pp[i] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < D; ++k) {
+      const float pk = __fsub_rn(p[i][k], hdr[k]);
+      q[i][k] = -2.0f * pk;
+      pp[i] = __fmaf_rn(pk, pk, pp[i]);
+    }
   }
   // the mask as a register operand (a volatile read of the header word the
   // pack kernel wrote): the LOP3 then takes the index pair as its uniform
   // operand, no per-key index move or LDC
   const unsigned keep = *reinterpret_cast<const volatile unsigned*>(hdr + D + 1);
   const float inf = __int_as_float(0x7f800000);
-  float m1 = inf, m2 = inf;
+  float m1[NPT], m2[NPT];
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) m1[i] = m2[i] = inf;
 #pragma unroll
   for (int jp = 0; jp < K / 2; ++jp) {
     const float2* c = tab + N::H + jp * N::S;
-    float2 acc = __fadd2_rn(make_float2(pp, pp), c[D]);
-#pragma unroll
-    for (int k = 0; k < D; ++k) acc = __ffma2_rn(make_float2(q[k], q[k]), c[k], acc);
     // the record's index pair (2jp, 2jp+1) arrives with its centre words
     const float2 ix = c[D + 1];
-    const float k0 = __uint_as_float(nn_embed(acc.x, keep, __float_as_uint(ix.x)));
-    const float k1 = __uint_as_float(nn_embed(acc.y, keep, __float_as_uint(ix.y)));
-    const float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
-    m2 = nn_min3(m2, fmaxf(m1, lo), hi);
-    m1 = fminf(m1, lo);
+#pragma unroll
+    for (int i = 0; i < NPT; ++i) {
+      float2 acc = __fadd2_rn(make_float2(pp[i], pp[i]), c[D]);
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc = __ffma2_rn(make_float2(q[i][k], q[i][k]), c[k], acc);
+      const float k0 = __uint_as_float(nn_embed(acc.x, keep, __float_as_uint(ix.x)));
+      const float k1 = __uint_as_float(nn_embed(acc.y, keep, __float_as_uint(ix.y)));
+      const float lo = fminf(k0, k1), hi = fmaxf(k0, k1);
+      m2[i] = nn_min3(m2[i], fmaxf(m1[i], lo), hi);
+      m1[i] = fminf(m1[i], lo);
+    }
   }
-  label = (int)(__float_as_uint(m1) & N::MASK);
   constexpr float E = 1.01f * (float)(1u << N::BITS) * 1.1920928955078125e-07f;
-  const float R = pp + 2.0f * hdr[D];
-  const float dc = 24.0f * 5.9604644775390625e-08f * R;
-  const float a1 = fabsf(m1), a2 = fabsf(m2);
   // NumPy's own rounding: a term passes through at most D + 1 roundings (sub,
   // square, the D - 1 adds of the sequential fold; 5 for the n == 8 tree),
   // |D^_j - D_j| <= gamma_(D+1) D_j; 2.1 (D + 2) u covers 2.01 gamma_(D+1)
   constexpr float NP = 2.1f * (D + 2) * 5.9604644775390625e-08f;
-  const float thr = 2.1f * dc + E * (a1 + a2) + NP * fmaxf(m1 + E * a1 + dc, 0.0f) + 1e-35f;
-  // NaN anywhere (p, centres, keys) makes a comparison false: exact scan
-  return R < 1e37f && m2 - m1 > thr;
+#pragma unroll
+  for (int i = 0; i < NPT; ++i) {
+    label[i] = (int)(__float_as_uint(m1[i]) & N::MASK);
+    const float R = pp[i] + 2.0f * hdr[D];
+    const float dc = 24.0f * 5.9604644775390625e-08f * R;
+    const float a1 = fabsf(m1[i]), a2 = fabsf(m2[i]);
+    const float thr = 2.1f * dc + E * (a1 + a2) + NP * fmaxf(m1[i] + E * a1 + dc, 0.0f) + 1e-35f;
+    // NaN anywhere (p, centres, keys) makes a comparison false: exact scan
+    ok[i] = R < 1e37f && m2[i] - m1[i] > thr;
+  }
+}
+
+template <int K, int D>
+__device__ __forceinline__ bool nearest_centre(const float (&p)[D], const float2* __restrict__ tab, int& label) {
+  float pa[1][D];
+#pragma unroll
+  for (int k = 0; k < D; ++k) pa[0][k] = p[k];
+  int l[1];
+  bool ok[1];
+  nearest_centre_n<K, D, 1>(pa, tab, l, ok);
+  label = l[0];
+  return ok[0];
 }
 
 // np.argmin over NumPy's float32 distances, exactly: d_j = ((p0-c0)^2 +

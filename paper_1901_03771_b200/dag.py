@@ -418,6 +418,9 @@ def infer(op: Op, pred_shapes: Sequence[Shape], pred_dtypes: Sequence[DType]) ->
                 tuple(d for i, d in enumerate(s) if i != axis)
         return shape, DType.i64, None
     if k is OpKind.SCAN:
+        # an optional second operand seeds the fold: out[k] = init (+) x[0]
+        # (+) ... (+) x[k], init shaped like one line of the scan (the kept
+        # axes; (1,) for 1-D) — the streamed chunks' carry (streaming.py)
         rop, axis, odt = op.attrs
         s = pred_shapes[0]
         if axis is None:
@@ -426,6 +429,10 @@ def infer(op: Op, pred_shapes: Sequence[Shape], pred_dtypes: Sequence[DType]) ->
             if not 0 <= axis < len(s):
                 raise BadAxis(f"axis {axis} out of range")
             shape = tuple(s)
+        if len(pred_shapes) > 1:
+            kept = (1,) if axis is None or len(s) == 1 else tuple(d for i, d in enumerate(s) if i != axis)
+            if tuple(pred_shapes[1]) != kept:
+                raise ShapeMismatch(f"scan seed of shape {tuple(pred_shapes[1])}, expected {kept}")
         return shape, odt or _reduce_dtype(rop, pred_dtypes[0]), None
     if k is OpKind.MATMUL:
         a, b = pred_shapes

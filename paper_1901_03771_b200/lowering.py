@@ -371,6 +371,8 @@ def lower(step: PlanStep, g=None) -> FusedKernel:
             raise UnsupportedNodeInFusedStep(f"{n.op!r} in the interior of a fused step (SPEC.md:306)")
         if n.kind is OpKind.SCAN and n not in step.roots:
             raise UnsupportedNodeInFusedStep("a scan is only ever a step root (SPEC.md:306)")
+        if n.kind is OpKind.SCAN and len(n.preds) > 1:
+            raise UnsupportedNodeInFusedStep("a seeded scan (streamed carry) has no reference point program")
     kind, vals, extents = _map_values(step)
     b = _PointBuilder(step)
     params = tuple(f"i{k}" for k in range(len(extents)))

@@ -251,11 +251,20 @@ def run(sess, p: StreamPlan, outs: Sequence[np.ndarray]) -> List[np.ndarray]:
             for r in p.roots:
                 if r.id in carried and ci > 0:
                     # continue from the previous chunk's last row (its scan
-                    # result is already on the device, stream-ordered)
+                    # result is already on the device, stream-ordered): the
+                    # chunk's scan is SEEDED with it — one kernel writes the
+                    # chunk once (a second map pass re-read and
+                    # re-wrote every chunk)
                     pf = prev_final[r.id]
                     sl = ((pf.shape[0] - 1, 1, 1),) + tuple((0, 1, e) for e in pf.shape[1:])
                     carry = g.add_op(Op(OpKind.SLICE, None, (sl,)), [pf])
-                    memo[r.id] = g.add_op(Op(OpKind.MAP, _COMBINE[p.dist[r.id][2:]]), [memo[r.id], carry])
+                    sc = memo[r.id]
+                    axis = sc.op.attrs[1]
+                    xs = sc.preds[0].shape
+                    kept = (1,) if axis is None or len(xs) == 1 else tuple(d for i, d in enumerate(xs) if i != axis)
+                    if tuple(carry.shape) != kept:
+                        carry = g.add_op(Op(OpKind.RESHAPE, None, (kept,)), [carry])
+                    memo[r.id] = g.add_op(sc.op, [sc.preds[0], carry])
             croots = [memo[r.id] for r in p.roots]
             views = {}
             for r, cr in zip(p.roots, croots):

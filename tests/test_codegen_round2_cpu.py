@@ -102,3 +102,12 @@ def test_wrow_generator_paired_two_pass(monkeypatch):
     assert ks.family == "wrow"
     assert "gr::p2::div_shr<FAST>" in ks.source and "K::rows<false>" in ks.source
     runtime.compile_cubin(ks.source)
+
+
+def test_kmeans_two_rows_per_search_builds(monkeypatch):
+    monkeypatch.setattr(codegen_rows, "NEAREST_PAIR_ROWS", True)
+    P, C = wl.kmeans_inputs(n=1 << 14)
+    lab, sums, counts = wl.kmeans_partials(gp, gp.asarray(P), gp.asarray(C))
+    ks = _source([lab] + sums + [counts])
+    assert "gr::nearest_centre_n<64, 4, 2>" in ks.source and "K::nn_labels(" in ks.source
+    runtime.compile_cubin(ks.source)

@@ -156,3 +156,49 @@ def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
         assert np.array_equal(outs[0], np.cumsum(xs[0] * 3 + 1))
     if kind == "max":
         assert np.array_equal(outs[0], np.maximum.accumulate(xs[0] * np.float32(2.0)))
+
+
+@pytest.mark.parametrize("case", ["long-f32", "long-i64", "long-tma", "lines-axis0", "short"])
+def test_seeded_scan(sess, monkeypatch, case):
+    """A scan seeded with a value (the streamed chunks' carry, streaming.py)
+    folds from the seed: out[k] = seed (+) x[0] (+) ... (+) x[k]; integers
+    exact, floats within the scan's association bound; the eager oracle
+    agrees."""
+    from paper_1901_03771_b200 import codegen, codegen_scan
+    from paper_1901_03771_b200.dag import Op, OpKind
+    from oracle import eager
+    monkeypatch.setattr(codegen_scan, "SCAN_TMA", case == "long-tma")
+    codegen._GEN_CACHE.clear()
+    rng = np.random.default_rng(len(case))
+    g = sess.graph
+    if case == "lines-axis0":
+        xh = rng.standard_normal((1 << 12, 24))
+        prevh = rng.standard_normal((5, 24))
+        x, prev = gp.asarray(xh), gp.asarray(prevh)
+        c = gp.cumsum(x * 2.0, axis=0)
+        carry = g.add_op(Op(OpKind.SLICE, None, (((4, 1, 1), (0, 1, 24)),)), [prev.node])
+        carry = g.add_op(Op(OpKind.RESHAPE, None, ((24,),)), [carry])
+        ref = np.cumsum(np.concatenate([prevh[4:5], xh * 2.0]), axis=0)[1:]
+    else:
+        n = {"short": 5000, "long-tma": (1 << 21) + 32}.get(case, (1 << 21) + 7)
+        if case == "long-i64":
+            xh, prevh = rng.integers(-50, 50, n), rng.integers(-9, 9, 7)
+        else:
+            xh, prevh = rng.standard_normal(n).astype(np.float32), rng.standard_normal(7).astype(np.float32)
+        x, prev = gp.asarray(xh), gp.asarray(prevh)
+        c = gp.cumsum(x * 3 if case == "long-i64" else x * np.float32(0.5))
+        carry = g.add_op(Op(OpKind.SLICE, None, (((6, 1, 1),),)), [prev.node])
+        t = xh * 3 if case == "long-i64" else xh * np.float32(0.5)
+        ref = np.cumsum(np.concatenate([prevh[6:7], t]).astype(np.float64 if case != "long-i64" else np.int64))[1:]
+    sc = g.add_op(c.node.op, [c.node.preds[0], carry])
+    got = np.asarray(gp.session._wrap(sc, sess))
+    codegen._GEN_CACHE.clear()
+    exp = eager.evaluate(sc)
+    if case == "long-i64":
+        assert np.array_equal(got, ref) and np.array_equal(exp, ref)
+    else:
+        scale = np.cumsum(np.abs(np.concatenate([prevh[-1:] if case != "lines-axis0" else prevh[4:5], xh])), axis=0)[1:]
+        assert np.all(np.abs(got - ref) <= 1e-5 * (scale + 1))
+        assert np.all(np.abs(exp - ref) <= 1e-5 * (scale + 1))
+    label = sess.executor.last_steps[-1].cache["ks"].meta.get("label")
+    assert label == {"long-tma": "scan-tma", "long-f32": "scan-lookback", "long-i64": "scan-lookback"}.get(case, label)
