@@ -732,7 +732,18 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
   if (found >= 0) {
     if (lane == 0) {
       pre = base;
-      for (long long d = tile - 2 - found; d >= 0; --d) pre = Op::template c<T>(pre, lb[d]);
+      // left fold in tile order; the shared-memory reads of each batch of 8
+      // are issued together (a read per add was an LDS latency per tile of
+      // distance on every look-back's critical path)
+      long long d = tile - 2 - found;
+      for (; d >= 7; d -= 8) {
+        T v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = lb[d - k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) pre = Op::template c<T>(pre, v[k]);
+      }
+      for (; d >= 0; --d) pre = Op::template c<T>(pre, lb[d]);
     }
   } else {
     // slow path (more than 32*J*R tiles in flight behind this one): walk the
@@ -766,7 +777,15 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
       __syncwarp();
       if (lane == 0) {
         const int cnt = (int)((tile - b0) < 32 * J ? (tile - b0) : 32 * J);
-        for (int l = 0; l < cnt; ++l) pre = Op::template c<T>(pre, lb[l]);
+        int l = 0;
+        for (; l + 8 <= cnt; l += 8) {
+          T v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = lb[l + k];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) pre = Op::template c<T>(pre, v[k]);
+        }
+        for (; l < cnt; ++l) pre = Op::template c<T>(pre, lb[l]);
       }
     }
   }
