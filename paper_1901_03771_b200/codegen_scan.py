@@ -33,13 +33,18 @@ ITEMS = 16
 
 # Long 1-D scans whose inputs are contiguous arrays of the scan's length: TMA
 # tile ring (see _gen_lookback_tma)
-SCAN_TMA = os.environ.get("GRUMPY_SCAN_TMA", "0") == "1"
+SCAN_TMA = os.environ.get("GRUMPY_SCAN_TMA", "1") == "1"
 SCAN_TMA_MIN = 1 << 20
 SCAN_TMA_SMEM = 200 * 1024
 SCAN_TMA_STAGES = int(os.environ.get("GRUMPY_SCAN_STAGES", "6"))
 SCAN_TMA_LAG = int(os.environ.get("GRUMPY_SCAN_LAG", "3"))
-SCAN_TMA_LBW = int(os.environ.get("GRUMPY_SCAN_LBW", "1"))
+SCAN_TMA_LBW = int(os.environ.get("GRUMPY_SCAN_LBW", "2"))
 SCAN_TMA_ITEMS = int(os.environ.get("GRUMPY_SCAN_ITEMS", "16"))
+# look-back by rounds (gr::tile_lookback_round): the prefix starts from the
+# CTA's own inclusive prefix of one round earlier instead of the nearest one
+# another CTA published
+SCAN_TMA_ROUND = os.environ.get("GRUMPY_SCAN_ROUND", "1") == "1"
+SCAN_TMA_SLEEP = int(os.environ.get("GRUMPY_SCAN_SLEEP", "0"))   # ns backoff in the mailbox waits
 
 
 def generate(region: Region, kname="gr_region") -> KernelSource:
@@ -355,10 +360,19 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     the next tiles are always in flight; 16 data warps read their 16
     consecutive elements per thread straight from the swizzled tile
     (conflict-free 16-byte chunks), evaluate the map prologue in registers and
-    scan (thread run, warp, CTA), and one look-back warp resolves the tile
-    prefix (gr::tile_lookback) while the data warps scan the next tile.  The
-    finished tile is written back into its stage and leaves with one TMA
-    tensor store.  Association is the same as the register-staged kernel
+    scan (thread run, warp, CTA), and look-back warps resolve the tile prefix
+    while the data warps scan the next tiles.  The finished tile is written
+    back into its stage and leaves with one TMA tensor store.
+
+    Tiles go round-robin over a persistent grid of G CTAs (one per SM, all
+    resident), so the look-back is by rounds (gr::round_stage/round_fold):
+    the prefix of tile t is the CTA's own inclusive prefix of tile t - G
+    folded with the G - 1 aggregates in between — one L2 round trip, and it
+    never waits for another CTA's look-back (the nearest-published-prefix
+    walk of gr::tile_lookback made a chain of them: 0.51 ms at 2^28 against
+    0.40).  Two look-back warps alternate tiles, one staging its aggregates
+    while the other folds, and hand the CTA's inclusive prefix over in shared
+    memory.  Association is the left fold of the register-staged kernel
     (_gen_lookback): the results are bit-identical to it."""
     T = s.dtype
     ct = T.ctype
@@ -421,6 +435,39 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     params = params.replace("  struct Params {\n", "  struct Params {\n" + maps, 1)
     LAG = min(SCAN_TMA_LAG, S_ - 2)       # tiles waiting for their prefix
     NLW = SCAN_TMA_LBW                    # look-back warps
+    rounds = SCAN_TMA_ROUND
+    SLEEP = SCAN_TMA_SLEEP
+    if rounds and NLW == 1:
+        # the data warps publish tile 0's aggregate with the seed folded in
+        lb_call = f"""      {ct} pre;
+      if (t == 0) {{ pre = {seedv}; own = mb_agg[m]; }}
+      else {{
+        pre = gr::tile_lookback_round<{op}, {ct}>(aggs, t, (int)gridDim.x, own, {ident}, lbw[k].v);
+        own = {comb}<{ct}>(pre, mb_agg[m]);
+      }}"""
+    elif rounds:
+        # several look-back warps take the iterations in turn: each stages its
+        # tile's aggregates while the previous warp folds, then takes over the
+        # CTA's inclusive prefix (own_v, sequence-numbered) for its own fold
+        lb_call = f"""      {ct} pre;
+      if (t == 0) {{ pre = {seedv}; own = mb_agg[m]; }}
+      else {{
+        gr::round_stage<{op}, {ct}>(aggs, t, (int)gridDim.x, {ident}, lbw[k].v);
+        if (i > 0) {{
+          if (lane == 0) {{ while (own_seq != i) {{ }} }}
+          __syncwarp();
+          __threadfence_block();
+          own = own_v;
+        }}
+        pre = gr::round_fold<{op}, {ct}>(t, (int)gridDim.x, own, {ident}, lbw[k].v);
+        own = {comb}<{ct}>(pre, mb_agg[m]);
+      }}
+      if (lane == 0) {{ own_v = own; __threadfence_block(); own_seq = i + 1; }}"""
+    else:
+        lb_call = (f"      const {ct} pre0 = gr::tile_lookback_buf<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? "
+                   f"{comb}<{ct}>({seedv}, mb_agg[m]) : mb_agg[m], {ident}, lbw[k].v);\n"
+                   f"      const {ct} pre = {seeded} && t == 0 ? {seedv} : pre0;")
+    agg0 = f"{seeded} && t == 0 ? {comb}<{ct}>({seedv}, acc) : acc" if rounds else "acc"
     M = LAG + NLW                         # mailbox slots
     NTH = TPB + 32 * NLW + 32
     sgs = ", ".join(f"ring + ((long long)s * {NL} + {k}) * {tile_b}" for k in range(NL))
@@ -441,12 +488,15 @@ def _gen_lookback_tma(region, s, x, rop, kname):
   __shared__ {ct} mb_agg[{M}], mb_pre[{M}];
   __shared__ volatile int mb_pub[{M}], mb_done[{M}];
   __shared__ gr::LookbackBuf<{ct}> lbw[{NLW}];
+  __shared__ volatile {ct} own_v;
+  __shared__ volatile int own_seq;
   unsigned long long* aggs = reinterpret_cast<unsigned long long*>(p.scratch) + 1;
   unsigned long long* incs = aggs + {ntiles * (1 if isz <= 4 else 2)}LL;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {{
     for (int i = 0; i < {S_}; ++i) {{ gr::mbar_init(&full[i], 1); gr::mbar_init(&empty[i], 1); }}
     for (int i = 0; i < {M}; ++i) {{ mb_pub[i] = 0; mb_done[i] = 0; }}
+    own_seq = 0;
     gr::fence_mbar_init();
   }}
   __syncthreads();
@@ -469,14 +519,31 @@ def _gen_lookback_tma(region, s, x, rop, kname):
   }}
   if (w >= {NW}) {{
     const int k = w - {NW};
+    {ct} own = {ident};   // round look-back: this CTA's inclusive prefix of its previous tile
+    (void)own;
     for (int i = k;; i += {NLW}) {{
       const int m = i % {M};
-      while (mb_pub[m] != i + 1) {{ }}
+#ifdef GR_SCAN_STATS
+      const long long cw = clock64();
+#endif
+      while (mb_pub[m] != i + 1) {{ if ({SLEEP}) __nanosleep({SLEEP}); }}
       __threadfence_block();
+#ifdef GR_SCAN_STATS
+      if (lane == 0 && blockIdx.x == 0) {{ if (i == 0) {{ gr::gr_scan_stats[4] = gr::gr_scan_stats[5] = gr::gr_scan_stats[6] = gr::gr_scan_stats[7] = 0; gr::gr_scan_stats[3] = clock64(); }}
+                                          else gr::gr_scan_stats[7] += clock64() - cw; }}
+#endif
       const long long t = mb_tid[m];
-      if (t < 0) break;
-      const {ct} pre0 = gr::tile_lookback_buf<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? {comb}<{ct}>({seedv}, mb_agg[m]) : mb_agg[m], {ident}, lbw[k].v);
-      const {ct} pre = {seeded} && t == 0 ? {seedv} : pre0;
+      if (t < 0) {{
+#ifdef GR_SCAN_STATS
+        if (blockIdx.x == 0 && lane == 0) {{
+          const unsigned long long* q = gr::gr_scan_stats;
+          printf("GR_SCAN_STATS CTA 0: look-backs=%llu load+wait=%llu fold=%llu mailbox-idle=%llu cycles per look-back, %llu cycles in all\\n",
+                 q[6], q[4] / (q[6] + 1), q[5] / (q[6] + 1), q[7] / (q[6] + 1), (unsigned long long)clock64() - q[3]);
+        }}
+#endif
+        break;
+      }}
+{lb_call}
       if (lane == 0) {{ mb_pre[m] = pre; __threadfence_block(); mb_done[m] = i + 1; }}
       __syncwarp();
     }}
@@ -489,7 +556,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     // tile of iteration j: prefix (+) its tile-local scan (waiting in its
     // stage), back into the stage, one TMA store
     const int m = j % {M};
-    if (threadIdx.x == 0) {{ while (mb_done[m] != j + 1) {{ }} __threadfence_block(); }}
+    if (threadIdx.x == 0) {{ while (mb_done[m] != j + 1) {{ if ({SLEEP}) __nanosleep({SLEEP}); }} __threadfence_block(); }}
     asm volatile("bar.sync 1, {TPB};" ::: "memory");
     const {ct} pre = mb_pre[m];
     unsigned char* ob = ring + (long long)(j % {S_}) * {NL * tile_b};
@@ -541,10 +608,11 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     if (threadIdx.x == 0) {{
       {ct} acc = ws[0];
       for (int k2 = 1; k2 < {NW}; ++k2) {{ acc = {comb}<{ct}>(acc, ws[k2]); ws[k2] = acc; }}
-      gr::stat_put<{ct}>(aggs, t, acc);
+      const {ct} agg = {agg0};
+      gr::stat_put<{ct}>(aggs, t, agg);
       const int m = i % {M};
       mb_tid[m] = t;
-      mb_agg[m] = acc;
+      mb_agg[m] = agg;
       __threadfence_block();
       mb_pub[m] = i + 1;
     }}

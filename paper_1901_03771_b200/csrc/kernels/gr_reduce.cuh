@@ -172,6 +172,9 @@ struct OpMin {
   template <class T> static __device__ __forceinline__ T c(T a, T b) { return (a != a) ? a : ((b != b) ? b : (b < a ? b : a)); }
 };
 
+template <class Op> struct IsSum { static constexpr bool v = false; };
+template <> struct IsSum<OpSum> { static constexpr bool v = true; };
+
 // Perfect binary tree over the lanes of a warp in lane order (pairs (0,1),
 // (2,3), ... then (01,23), ...): the association of NumPy's pairwise split for
 // power-of-two counts.  Every lane ends with the full result.
@@ -662,7 +665,7 @@ __device__ unsigned long long gr_scan_stats[8];
 #ifndef GR_SCAN_R
 #define GR_SCAN_R 8
 #endif
-template <class T> struct LookbackBuf { T v[32 * GR_SCAN_J * GR_SCAN_R]; };
+template <class T> struct __align__(16) LookbackBuf { T v[32 * GR_SCAN_J * GR_SCAN_R]; };
 
 template <class Op, class T>
 __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, unsigned long long* inc,
@@ -795,6 +798,100 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
                    atomicAdd(&gr_scan_stats[2], (unsigned long long)(clock64() - c0)); }
 #endif
   return __shfl_sync(0xffffffffu, pre, 0);
+}
+
+// Look-back of a persistent grid whose G CTAs take the tiles round-robin
+// (tile t on CTA t % G, in its round t / G).  The prefix of tile t > 0 is the
+// left fold, in tile order, of the calling CTA's own inclusive prefix of tile
+// t - G (in the first round: the aggregate of tile 0) and the aggregates of
+// the tiles in between — the same left fold as tile_lookback_buf, so the same
+// bits.  No inclusive prefix crosses CTAs: a look-back waits only for its
+// predecessors' aggregates (published when their tiles are reduced), never
+// for their look-backs, and one L2 round trip reads all G - 1 of them.
+// One full warp calls it; lb: the warp's staging array (>= G - 1 values).
+//
+// Two halves, so that several look-back warps can overlap one tile's loads
+// with the previous tile's fold: round_stage reads the aggregates into lb
+// (padded to a multiple of 8 with a value the combine leaves unchanged:
+// -0.0 for sums, x + -0.0 == x with signed zeros; the identity otherwise),
+// round_fold folds them onto the CTA's previous inclusive prefix.
+template <class Op, class T> __device__ __forceinline__ T round_pad(T ident) {
+  if constexpr (IsSum<Op>::v) return Zero<T>::neg();
+  return ident;
+}
+template <class Op, class T, int J = 5>
+__device__ __forceinline__ void round_stage(const unsigned long long* agg, long long tile, int G, T ident, T* lb) {
+  const int lane = threadIdx.x & 31;
+  const long long lo = tile >= G ? tile - G + 1 : 0;   // first aggregate folded
+  const int n = (int)(tile - lo);                        // aggregates lo .. tile-1
+  const int n8 = (n + 7) & ~7;
+  const T pad = round_pad<Op, T>(ident);
+  for (int w0 = 0; w0 < n8; w0 += 32 * J) {
+    StatRaw<T> ra[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = w0 + lane + 32 * j;
+      if (k < n) ra[j] = stat_ld<T>(agg, lo + k);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = w0 + lane + 32 * j;
+      if (k < n) {
+        while (!stat_ok<T>(ra[j])) ra[j] = stat_ld<T>(agg, lo + k);
+        lb[k] = stat_val<T>(ra[j]);
+      } else if (k < n8) {
+        lb[k] = pad;
+      }
+    }
+  }
+  __syncwarp();
+}
+template <class Op, class T>
+__device__ __forceinline__ T round_fold(long long tile, int G, T own_inc, T ident, T* lb) {
+  const int lane = threadIdx.x & 31;
+  const int n = (int)(tile >= G ? G - 1 : tile);
+  const int n8 = (n + 7) & ~7;
+  const T pad = round_pad<Op, T>(ident);
+  T pre = own_inc;
+  if (lane == 0 && n > 0) {
+    if (tile < G) { pre = lb[0]; lb[0] = pad; }    // first round: the fold starts at tile 0
+    // left fold in tile order; each batch of 8 is read while the previous one
+    // is folded, so the chain is one dependent combine per aggregate
+    T a[8], b[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = lb[q];
+#pragma unroll 1
+    for (int k = 0; k < n8; k += 8) {
+      if (k + 8 < n8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) b[q] = lb[k + 8 + q];
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) pre = Op::template c<T>(pre, a[q]);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = b[q];
+    }
+  }
+  return __shfl_sync(0xffffffffu, pre, 0);
+}
+template <class Op, class T, int J = 5>
+__device__ __forceinline__ T tile_lookback_round(const unsigned long long* agg, long long tile, int G,
+                                                 T own_inc, T ident, T* lb) {
+#ifdef GR_SCAN_NOLB
+  return own_inc;   // experiment: streaming floor without any look-back (wrong results)
+#endif
+#ifdef GR_SCAN_STATS
+  const long long c0 = clock64();
+#endif
+  round_stage<Op, T, J>(agg, tile, G, ident, lb);
+#ifdef GR_SCAN_STATS
+  const long long c1 = clock64();
+#endif
+  const T pre = round_fold<Op, T>(tile, G, own_inc, ident, lb);
+#ifdef GR_SCAN_STATS
+  if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) { gr_scan_stats[4] += c1 - c0; gr_scan_stats[5] += clock64() - c1; gr_scan_stats[6] += 1; }
+#endif
+  return pre;
 }
 
 // acq_rel atomic add (gpu scope): releases the caller's prior writes,

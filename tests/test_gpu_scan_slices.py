@@ -114,11 +114,13 @@ def test_scan_lookback_deterministic(sess):
     assert np.max(np.abs(runs[0] - ref)) <= 1e-6 * np.max(np.abs(ref)) + 1.0
 
 
-@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 32, 3 << 20, (1 << 21) + 7])
+@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 32, 3 << 20, (1 << 21) + 7, (1 << 24) + 96])
 @pytest.mark.parametrize("kind", ["f32", "f64", "i64", "f32x2", "max"])
 def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
     """The TMA-fed look-back scan (codegen_scan._gen_lookback_tma) has the
-    register-staged kernel's association: results bit-identical to it, for
+    register-staged kernel's association (its look-back by rounds folds from
+    the CTA's own prefix of one round earlier — the same left fold): results
+    bit-identical to it, for
     one- and two-leaf map prologues, 4- and 8-byte types, sums and max; lengths
     that are not a multiple of the tile (zero-filled last box) or of the
     128-byte line (register-staged fallback)."""
