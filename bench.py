@@ -273,6 +273,11 @@ WORKLOADS = {
         desc="map-scan cumsum(x*0.5+1) over 2^28 fp32 (SURVEY.md §8(f))",
         program=lambda xp, a: (_programs().scan(xp, *a),),
         elements=lambda n: n, bytes=lambda n: 2 * 4 * n, bound="hbm", shardable=False),
+    "cumsum-rows": dict(
+        label="f32", shape="[65536, 4096]",
+        desc="map-scan cumsum(x*0.5+1, axis=1) over 65536x4096 fp32 rows (SURVEY.md §8(f), scan along the contiguous axis)",
+        program=lambda xp, a: (_programs().scan_rows(xp, *a),),
+        elements=lambda n: n * 4096, bytes=lambda n: 2 * 4 * n * 4096, bound="hbm"),
     "transpose": dict(
         label="f32", shape="[16384, 16384]",
         desc="x.T + y, 16384x16384 fp32: transposed leaf staged through shared-memory tiles (north_star K1 staging)",
@@ -335,7 +340,7 @@ def cpu_sample_n(name):
     """Leading extent of the bounded single-thread CPU sample (~5-20 s)."""
     return {"blackscholes-f32": 1 << 24, "blackscholes-f64": 1 << 24, "listing1": 1 << 24,
             "rownorm": 16384, "rownorm-y": 16384, "mlp": 16384, "kmeans": 1 << 20, "jacobi": 4096, "transpose": 4096,
-            "cumsum": 1 << 24}[name]
+            "cumsum": 1 << 24, "cumsum-rows": 4096}[name]
 
 
 # ---------------------------------------------------------------------------

@@ -20,6 +20,7 @@ bounded for reductions).  Tolerances:
   cumsum f32            |Δ_i| <= (tiles + 32)·eps32·Σ_{j<=i}|t_j| against the
                         float64 prefix of the same f32 terms (the kernel's
                         association: a sequential chain over 8192-element tiles)
+  cumsum-rows           bit-exact (a sequential fold per row, NumPy's order)
 
 ``comm_sum`` sums a float64 vector over ranks (gloo) for results that were
 allreduced on the device (totals, k-means partials); identity on one rank.
@@ -235,6 +236,22 @@ def _check_cumsum(wl, name, inp, out, threads, comm_sum, world, tile=8192):
         bad += int(np.count_nonzero(~(d <= gamma * ab)))
         off, aoff = ref[-1], ab[-1]
     return _result(bad == 0, n, bad, worst, f"|d_i| <= {gamma:.3g}*prefix sum|t|", err_unit="|d_i|/prefix sum|t|")
+
+
+def _check_cumsum_rows(wl, name, inp, out, threads, comm_sum, world):
+    """Per-row sequential fold: NumPy's own association, bit-exact."""
+    (x,) = inp
+    got = out[0]
+
+    def f(blk):
+        lo, hi = blk
+        e = wl.scan_rows(np, x[lo:hi])
+        g = got[lo:hi]
+        return int(np.count_nonzero(e.view(np.uint32) != g.view(np.uint32))), float(np.max(np.abs(e - g), initial=0))
+
+    r = _map_blocks(threads, len(x), f)
+    mm = sum(v[0] for v in r)
+    return _result(mm == 0, x.size, mm, max(v[1] for v in r), "bit-exact")
 
 
 def _check_jacobi(wl, name, inp, out, threads, comm_sum, world):

@@ -178,6 +178,10 @@ def cumsum(a, axis=None, dtype=None):
     return _arr(a).cumsum(axis=axis, dtype=dtype)
 
 
+def cumprod(a, axis=None, dtype=None):
+    return _arr(a).cumprod(axis=axis, dtype=dtype)
+
+
 def transpose(a, axes=None):
     return _arr(a).transpose(*(axes or ()))
 

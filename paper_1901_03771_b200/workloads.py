@@ -170,6 +170,12 @@ def scan(xp, x):
     return xp.cumsum(x * 0.5 + 1.0)
 
 
+def scan_rows(xp, x):
+    """Map-scan along the contiguous axis of a matrix (one scan
+    axis of the operand): every row its own sequential fold."""
+    return xp.cumsum(x * 0.5 + 1.0, axis=1)
+
+
 # ---- named-shape inputs generated in fixed row blocks ---------------------------
 # The bench shards the named shape along its leading axis (SURVEY.md §8(e)).
 # Generating the global array from fixed row blocks, block b from
@@ -227,6 +233,9 @@ NAMED = {
     "kmeans": (1 << 26, 1 << 20, lambda s: _km_rows(s), lambda s: [_km_centres(s)[1]], "SR"),
     "cumsum": (1 << 28, 1 << 22, lambda s: (lambda rng, r: [rng.standard_normal(r, dtype=np.float32)]),
                lambda s: [], "S"),
+    "cumsum-rows": (65536, 1024,
+                    lambda s: (lambda rng, r: [rng.standard_normal((r, 4096), dtype=np.float32)]),
+                    lambda s: [], "S"),
     "jacobi": (16384, 256, lambda s: (lambda rng, r: [rng.random((r, 16384), dtype=np.float32)]),
                lambda s: [], "S"),
 }

@@ -117,3 +117,17 @@ def test_kmeans_two_rows_per_search_builds(monkeypatch):
     ks = _source([lab] + sums + [counts])
     assert "gr::nearest_centre_n<64, 4, 2>" in ks.source and "K::nn_labels(" in ks.source
     runtime.compile_cubin(ks.source)
+
+
+@pytest.mark.parametrize("dt", [np.float32, np.float64, np.int32])
+def test_scan_rows_generator_builds(dt):
+    """Scans along the last axis go to the warp-per-32-lines kernel (coalesced
+    through a padded shared tile; the 48 KB static limit sizes the CTA); other
+    axes and short line counts stay thread-per-line."""
+    x = gp.asarray(np.ones((1000, 300), dt))
+    ks = _source([gp.cumsum(x * 3 + 1, axis=1)])
+    assert ks.meta["label"] == "scan-rows" and "K::val(p, r, k)" in ks.source
+    runtime.compile_cubin(ks.source)
+    assert _source([gp.cumsum(x * 3 + 1, axis=0)]).meta.get("label") is None          # lines
+    assert _source([gp.cumsum(gp.asarray(np.ones((31, 300), dt)), axis=1)]).meta.get("label") is None
+

@@ -13,7 +13,7 @@ from oracle import fullsize, programs
 wl = programs.load()
 
 SMALL = {"listing1": 1 << 14, "blackscholes-f32": 1 << 14, "blackscholes-f64": 1 << 14, "rownorm": 256,
-         "rownorm-y": 256, "mlp": 512, "kmeans": 1 << 14, "cumsum": 1 << 16, "jacobi": 64}
+         "rownorm-y": 256, "mlp": 512, "kmeans": 1 << 14, "cumsum": 1 << 16, "cumsum-rows": 64, "jacobi": 64}
 
 
 def _outputs(name, inp):
@@ -33,6 +33,8 @@ def _outputs(name, inp):
         return [lab, *sums, counts]
     if name == "cumsum":
         return [wl.scan(np, *inp)]
+    if name == "cumsum-rows":
+        return [wl.scan_rows(np, *inp)]
     if name == "jacobi":
         a = inp[0]
         return [wl.jacobi(np, a)]
@@ -52,13 +54,13 @@ def test_numpy_outputs_pass(name):
     kw = {"tile": 1} if name == "cumsum" else {}
     r = fullsize.check(name, inp, _outputs(name, inp), threads=4, **kw)
     assert r["ok"], r
-    if name in ("listing1", "jacobi", "kmeans"):
+    if name in ("listing1", "jacobi", "kmeans", "cumsum-rows"):
         assert r["mismatches"] == 0
     if name.startswith("rownorm"):
         assert r["total_bitexact"], r
 
 
-@pytest.mark.parametrize("name", ["listing1", "blackscholes-f32", "rownorm-y", "kmeans", "cumsum", "mlp"])
+@pytest.mark.parametrize("name", ["listing1", "blackscholes-f32", "rownorm-y", "kmeans", "cumsum", "cumsum-rows", "mlp"])
 def test_perturbed_outputs_fail(name):
     inp = _inputs(name)
     out = [np.array(o, copy=True) for o in _outputs(name, inp)]

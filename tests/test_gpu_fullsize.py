@@ -84,6 +84,12 @@ def test_cumsum_2p28_f32_lookback_slow_path(sess):
     assert r["ok"], r
 
 
+def test_cumsum_rows_65536x4096_bitexact(sess):
+    inp, got = _run(sess, "cumsum-rows", lambda d: [wl.scan_rows(gp, *d)], expect_kernels=1)
+    r = fullsize.check("cumsum-rows", inp, got)
+    assert r["ok"] and r["mismatches"] == 0, r
+
+
 def test_cumsum_2p28_int64_exact(sess):
     """Integer prefix sums are exact in any association: any look-back bug at
     32768 tiles (slow path, deep windows) shows as a wrong value."""

@@ -24,6 +24,43 @@ def test_scan_lines_exact(sess, shape, axis):
     assert np.array_equal(np.asarray(g), (x * 2 + 1).cumsum(axis=axis))   # sequential fold = NumPy
 
 
+@pytest.mark.parametrize("shape", [(1000, 300), (33, 65), (4096, 64), (5, 40, 129), (64, 2), (2048, 1000)])
+@pytest.mark.parametrize("kind", ["f32", "f64", "i64", "i32", "prod", "max", "rowvec", "colvec"])
+def test_scan_rows_contiguous_axis(sess, shape, kind):
+    """Scans along the last axis (codegen_scan._gen_rows_t: a warp per 32
+    lines, coalesced through a shared tile) keep NumPy's sequential fold per
+    line: bit-identical to np.cumsum / cumprod / maximum.accumulate, including
+    NaN propagation, broadcast operands along either axis, and line counts and
+    lengths that are not multiples of 32 or of the 64-column chunk."""
+    from paper_1901_03771_b200 import codegen
+    rng = np.random.default_rng([len(shape), shape[-1], len(kind)])
+    if kind in ("i64", "i32"):
+        x = rng.integers(-50, 50, shape).astype(np.int64 if kind == "i64" else np.int32)
+    elif kind == "f64":
+        x = rng.standard_normal(shape)
+    else:
+        x = rng.standard_normal(shape).astype(np.float32)
+    g = gp.asarray(x)
+    if kind == "prod":
+        xs = (x * np.float32(0.01) + np.float32(1.0))
+        got, ref = gp.cumprod(g * 0.01 + 1.0, axis=-1), np.cumprod(xs, axis=-1)
+    elif kind == "max":
+        x[..., shape[-1] // 2] = np.nan
+        got, ref = np.maximum.accumulate(gp.asarray(x), axis=-1), np.maximum.accumulate(x, axis=-1)
+    elif kind == "rowvec":
+        c = rng.standard_normal(shape[-1]).astype(np.float32)
+        got, ref = gp.cumsum(g * 2.0 + gp.asarray(c), axis=-1), np.cumsum(x * np.float32(2.0) + c, axis=-1)
+    elif kind == "colvec":
+        c = rng.standard_normal(shape[:-1] + (1,)).astype(np.float32)
+        got, ref = gp.cumsum(g - gp.asarray(c), axis=-1), np.cumsum(x - c, axis=-1)
+    else:
+        got, ref = gp.cumsum(g * 3 + 1, axis=-1), np.cumsum(x * 3 + 1, axis=-1)
+    out = np.asarray(got)
+    assert sess.executor.last_steps[-1].cache["ks"].meta.get("label") == "scan-rows"
+    assert out.dtype == ref.dtype and out.shape == ref.shape
+    assert np.array_equal(out, ref, equal_nan=kind not in ("i64", "i32"))
+
+
 @pytest.mark.parametrize("n", [8193, 100000, 1 << 22])
 def test_scan_lookback(sess, n):
     rng = np.random.default_rng(6)
