@@ -70,9 +70,19 @@ def generate(region: Region, kname="gr_region") -> KernelSource:
         if n > 8192:
             return _gen_lookback(region, s, x, rop, kname)
         return _gen_lines(region, s, x, rop, None, kname)
-    if (ROWS_T and axis == len(x.shape) - 1 and seed is None and x.shape[-1] > 1
-            and element_count(x.shape[:-1]) >= 32):
-        return _gen_rows_t(region, s, x, rop, kname)
+    if axis == len(x.shape) - 1 and seed is None and x.shape[-1] > 1:
+        lines = element_count(x.shape[:-1])
+        if SCAN_TMA and lines < ROWS_T_MIN_LINES and element_count(x.shape) >= SCAN_TMA_MIN:
+            # too few lines for a warp per 16 of them to fill the GPU: one
+            # look-back scan per line (tolerance instead of NumPy's order)
+            try:
+                ks = _gen_lookback_tma(region, s, x, rop, kname)
+                if ks is not None:
+                    return ks
+            except NotFusable:
+                pass
+        if ROWS_T and lines >= 32:
+            return _gen_rows_t(region, s, x, rop, kname)
     return _gen_lines(region, s, x, rop, axis, kname)
 
 
@@ -80,6 +90,9 @@ def generate(region: Region, kname="gr_region") -> KernelSource:
 # shared memory so loads and stores are coalesced (see _gen_rows_t)
 ROWS_T = os.environ.get("GRUMPY_SCAN_ROWS_T", "1") == "1"
 ROWS_T_CW = int(os.environ.get("GRUMPY_SCAN_ROWS_CW", "64"))       # columns per chunk
+# below this many lines a scan along the last axis whose lines are whole
+# look-back tiles runs as one look-back scan per line (_gen_lookback_tma)
+ROWS_T_MIN_LINES = int(os.environ.get("GRUMPY_SCAN_ROWS_MIN_LINES", str(148 * 16 * 4)))
 ROWS_T_RPW = int(os.environ.get("GRUMPY_SCAN_ROWS_RPW", "16"))     # lines per warp (16 lanes fold; measured 0.415 vs 0.427 ms for 32)
 ROWS_T_WPB = int(os.environ.get("GRUMPY_SCAN_ROWS_WPB", "1"))      # warps per CTA (1: even spread of the 32-line groups over the SMs)
 
@@ -432,10 +445,10 @@ class _StagedEmitter(LoopEmitter):
     """Loop emitter whose staged leaves are read from a swizzled shared-memory
     tile (16-byte chunks, gr::lds_sw) instead of global memory."""
 
-    def __init__(self, region, staged, tb):
+    def __init__(self, region, staged, tvars):
         super().__init__(region, vec_loads=True)
         self.staged = staged      # leaf id -> name of the tile's base pointer
-        self.tb = tb
+        self.tvars = tvars        # [(var, coef)]: the tile's first element = sum(coef * var)
 
     def load_leaf(self, leaf, off):
         sym = self.staged.get(leaf.id)
@@ -448,9 +461,11 @@ class _StagedEmitter(LoopEmitter):
         if sc is None or sc.kind != "for" or not sc.unroll or sc.var is None or off.coef(sc.var) != 1:
             raise NotFusable(leaf, "staged leaf not read along the item loop")
         rest = off.without(sc.var)
-        if rest.coef(self.tb) != 1 or sc.trip * leaf.dtype.itemsize != 16:
+        if any(rest.coef(tv) != c for tv, c in self.tvars) or sc.trip * leaf.dtype.itemsize != 16:
             raise NotFusable(leaf, "staged leaf read off the tile")
-        rel = rest.without(self.tb)
+        rel = rest
+        for tv, _ in self.tvars:
+            rel = rel.without(tv)
         key = ("svec", leaf.id, rel.key())
         hit = self.memo.get(key)
         if hit is not None and (hit[1] == 0 or (hit[1] < len(self.stack) and self.stack[hit[1]] is hit[2])):
@@ -493,7 +508,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     isz = T.itemsize
     if isz not in (4, 8):
         return None
-    staged = [l for l in region.leaves if tuple(l.shape) == (N,)]
+    staged = [l for l in region.leaves if tuple(l.shape) == tuple(x.shape)]
     if not staged or any(l.dtype.itemsize != isz for l in staged):
         return None
     W = 128 // isz                       # elements per 128-byte line
@@ -502,6 +517,12 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     TPB = 512 if isz == 4 else 256
     ITEMS = SCAN_TMA_ITEMS                # elements per data thread (16: 32 KB tiles, 32: 64 KB)
     tile = TPB * ITEMS
+    # segments: a scan along the last axis of a matrix is one scan per line;
+    # lines made of whole tiles keep every tile inside one line
+    seg = x.shape[-1] if len(x.shape) > 1 else N
+    if seg % tile and len(x.shape) > 1:
+        return None
+    TPL = seg // tile if len(x.shape) > 1 else -(-N // tile)     # tiles per segment
     tile_b = tile * isz                  # 32 KB
     rows = tile // W                     # 128-byte lines per tile
     box = min(rows, 256)                 # TMA box: at most 256 lines (32 KB)
@@ -524,17 +545,38 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     # ---- per-thread items: the map prologue on 16 consecutive elements
     tb = Var("tb", 1, align=tile)
     tt = Var("tt", 1)
-    em = _StagedEmitter(region, {l.id: f"sg{k}" for k, l in enumerate(staged)}, tb)
+    if len(x.shape) == 1:
+        em = _StagedEmitter(region, {l.id: f"sg{k}" for k, l in enumerate(staged)}, [(tb, 1)])
+        tile_coords = lambda e_: [Aff.of(tb) + e_]        # noqa: E731
+    else:
+        # the tile's line and first column; the line's kept coordinates
+        tln, tkb = Var("tln", 1), Var("tkb", 1, align=tile)
+        em = _StagedEmitter(region, {l.id: f"sg{k}" for k, l in enumerate(staged)}, [])
+        kept_shape = x.shape[:-1]
+        kept, rest_, stride = [], tln, seg
+        for d in range(len(kept_shape) - 1, -1, -1):
+            # the tile's base is sum(coordinate_d * stride_d) over the line's coordinates
+            cv = rest_ if d == 0 else em.derived_var(1, f"{rest_.name} % {kept_shape[d]}")
+            kept.append(Aff.of(cv))
+            em.tvars.append((cv, stride))
+            stride *= kept_shape[d]
+            if d:
+                rest_ = em.derived_var(1, f"{rest_.name} / {kept_shape[d]}")
+        kept.reverse()
+        em.tvars.append((tkb, 1))
+        tile_coords = lambda e_: kept + [Aff.of(tkb) + e_]    # noqa: E731
     j, sj, a = em.open(1, "for", trip=ITEMS // vec, unroll=True)
     v, sv, b = em.open(j.level, "for", trip=vec, unroll=True)
     e = Aff.of(tt).scale(ITEMS) + Aff.of(j).scale(vec) + Aff.of(v)
-    val = em.cast(em.value(x, [Aff.of(tb) + e]), x.dtype, T)
+    val = em.cast(em.value(x, tile_coords(e)), x.dtype, T)
     em.stmt(v.level, f"vals[{vec} * {j.name} + {v.name}] = {val[0]};")
     em.close(sv, b)
     em.close(sj, a)
     args = "".join(f", const unsigned char* sg{k}" for k in range(NL))
     items = [f"static __device__ __forceinline__ void items(const Params& p, const long long tb{args}, {ct} (&vals)[{ITEMS}]) {{",
              "  const long long tt = threadIdx.x; (void)tb;"]
+    if len(x.shape) > 1:
+        items.append(f"  const long long tln = tb / {seg}LL, tkb = tb % {seg}LL;")
     items += ["  " + c for c in em.consts]
     items += render(em.row, 1)
     items.append("}")
@@ -549,13 +591,15 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     LAG = min(SCAN_TMA_LAG, S_ - 2)       # tiles waiting for their prefix
     NLW = SCAN_TMA_LBW                    # look-back warps
     rounds = SCAN_TMA_ROUND
+    if len(x.shape) > 1 and not rounds:
+        return None                      # segments need the look-back by rounds
     SLEEP = SCAN_TMA_SLEEP
     if rounds and NLW == 1:
         # the data warps publish tile 0's aggregate with the seed folded in
         lb_call = f"""      {ct} pre;
-      if (t == 0) {{ pre = {seedv}; own = mb_agg[m]; }}
+      if (t % {TPL}LL == 0) {{ pre = {seedv}; own = mb_agg[m]; }}
       else {{
-        pre = gr::tile_lookback_round<{op}, {ct}>(aggs, t, (int)gridDim.x, own, {ident}, lbw[k].v);
+        pre = gr::tile_lookback_round<{op}, {ct}>(aggs, t, (int)gridDim.x, (t / {TPL}LL) * {TPL}LL, own, {ident}, lbw[k].v);
         own = {comb}<{ct}>(pre, mb_agg[m]);
       }}"""
     elif rounds:
@@ -563,16 +607,19 @@ def _gen_lookback_tma(region, s, x, rop, kname):
         # tile's aggregates while the previous warp folds, then takes over the
         # CTA's inclusive prefix (own_v, sequence-numbered) for its own fold
         lb_call = f"""      {ct} pre;
-      if (t == 0) {{ pre = {seedv}; own = mb_agg[m]; }}
+      // a segment's first tile has no prefix, but it still takes its turn in
+      // the CTA's sequence of inclusive prefixes (own_seq counts iterations)
+      const bool s0 = t % {TPL}LL == 0;
+      if (!s0) gr::round_stage<{op}, {ct}>(aggs, t, (int)gridDim.x, (t / {TPL}LL) * {TPL}LL, {ident}, lbw[k].v);
+      if (i > 0) {{
+        if (lane == 0) {{ while (own_seq != i) {{ }} }}
+        __syncwarp();
+        __threadfence_block();
+        own = own_v;
+      }}
+      if (s0) {{ pre = {seedv}; own = mb_agg[m]; }}
       else {{
-        gr::round_stage<{op}, {ct}>(aggs, t, (int)gridDim.x, {ident}, lbw[k].v);
-        if (i > 0) {{
-          if (lane == 0) {{ while (own_seq != i) {{ }} }}
-          __syncwarp();
-          __threadfence_block();
-          own = own_v;
-        }}
-        pre = gr::round_fold<{op}, {ct}>(t, (int)gridDim.x, own, {ident}, lbw[k].v);
+        pre = gr::round_fold<{op}, {ct}>(t, (int)gridDim.x, (t / {TPL}LL) * {TPL}LL, own, {ident}, lbw[k].v);
         own = {comb}<{ct}>(pre, mb_agg[m]);
       }}
       if (lane == 0) {{ own_v = own; __threadfence_block(); own_seq = i + 1; }}"""
@@ -677,7 +724,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     for (int q = 0; q < {ITEMS // vec}; ++q) {{
       {ct} o[{vec}];
       gr::lds_sw<{ct}, {vec}>(o, ob, {ITEMS} * threadIdx.x + {vec} * q);
-      if (tj > 0 || {seeded}) {{
+      if (tj % {TPL}LL != 0 || {seeded}) {{
 #pragma unroll
         for (int k2 = 0; k2 < {vec}; ++k2) o[k2] = {comb}<{ct}>(pre, o[k2]);
         gr::sts_sw<{ct}, {vec}>(ob, {ITEMS} * threadIdx.x + {vec} * q, o);

@@ -819,10 +819,14 @@ template <class Op, class T> __device__ __forceinline__ T round_pad(T ident) {
   if constexpr (IsSum<Op>::v) return Zero<T>::neg();
   return ident;
 }
+// ls: the first tile of the tile's segment (0 for one long scan; the first
+// tile of its line for a scan along the rows of a matrix): the fold never
+// reaches below it
 template <class Op, class T, int J = 5>
-__device__ __forceinline__ void round_stage(const unsigned long long* agg, long long tile, int G, T ident, T* lb) {
+__device__ __forceinline__ void round_stage(const unsigned long long* agg, long long tile, int G, long long ls,
+                                            T ident, T* lb) {
   const int lane = threadIdx.x & 31;
-  const long long lo = tile >= G ? tile - G + 1 : 0;   // first aggregate folded
+  const long long lo = tile - G + 1 > ls ? tile - G + 1 : ls;   // first aggregate folded
   const int n = (int)(tile - lo);                        // aggregates lo .. tile-1
   const int n8 = (n + 7) & ~7;
   const T pad = round_pad<Op, T>(ident);
@@ -847,14 +851,15 @@ __device__ __forceinline__ void round_stage(const unsigned long long* agg, long 
   __syncwarp();
 }
 template <class Op, class T>
-__device__ __forceinline__ T round_fold(long long tile, int G, T own_inc, T ident, T* lb) {
+__device__ __forceinline__ T round_fold(long long tile, int G, long long ls, T own_inc, T ident, T* lb) {
   const int lane = threadIdx.x & 31;
-  const int n = (int)(tile >= G ? G - 1 : tile);
+  const bool first = tile - G < ls;                // no own prefix inside the segment
+  const int n = (int)(first ? tile - ls : G - 1);
   const int n8 = (n + 7) & ~7;
   const T pad = round_pad<Op, T>(ident);
   T pre = own_inc;
   if (lane == 0 && n > 0) {
-    if (tile < G) { pre = lb[0]; lb[0] = pad; }    // first round: the fold starts at tile 0
+    if (first) { pre = lb[0]; lb[0] = pad; }       // first round: the fold starts at the segment's first tile
     // left fold in tile order; each batch of 8 is read while the previous one
     // is folded, so the chain is one dependent combine per aggregate
     T a[8], b[8];
@@ -875,7 +880,7 @@ __device__ __forceinline__ T round_fold(long long tile, int G, T own_inc, T iden
   return __shfl_sync(0xffffffffu, pre, 0);
 }
 template <class Op, class T, int J = 5>
-__device__ __forceinline__ T tile_lookback_round(const unsigned long long* agg, long long tile, int G,
+__device__ __forceinline__ T tile_lookback_round(const unsigned long long* agg, long long tile, int G, long long ls,
                                                  T own_inc, T ident, T* lb) {
 #ifdef GR_SCAN_NOLB
   return own_inc;   // experiment: streaming floor without any look-back (wrong results)
@@ -883,11 +888,11 @@ __device__ __forceinline__ T tile_lookback_round(const unsigned long long* agg, 
 #ifdef GR_SCAN_STATS
   const long long c0 = clock64();
 #endif
-  round_stage<Op, T, J>(agg, tile, G, ident, lb);
+  round_stage<Op, T, J>(agg, tile, G, ls, ident, lb);
 #ifdef GR_SCAN_STATS
   const long long c1 = clock64();
 #endif
-  const T pre = round_fold<Op, T>(tile, G, own_inc, ident, lb);
+  const T pre = round_fold<Op, T>(tile, G, ls, own_inc, ident, lb);
 #ifdef GR_SCAN_STATS
   if ((threadIdx.x & 31) == 0 && blockIdx.x == 0) { gr_scan_stats[4] += c1 - c0; gr_scan_stats[5] += clock64() - c1; gr_scan_stats[6] += 1; }
 #endif
