@@ -44,7 +44,6 @@ SCAN_TMA_ITEMS = int(os.environ.get("GRUMPY_SCAN_ITEMS", "16"))
 # CTA's own inclusive prefix of one round earlier instead of the nearest one
 # another CTA published
 SCAN_TMA_ROUND = os.environ.get("GRUMPY_SCAN_ROUND", "1") == "1"
-SCAN_TMA_SLEEP = int(os.environ.get("GRUMPY_SCAN_SLEEP", "0"))   # ns backoff in the mailbox waits
 
 
 def generate(region: Region, kname="gr_region") -> KernelSource:
@@ -593,7 +592,6 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     rounds = SCAN_TMA_ROUND
     if len(x.shape) > 1 and not rounds:
         return None                      # segments need the look-back by rounds
-    SLEEP = SCAN_TMA_SLEEP
     if rounds and NLW == 1:
         # the data warps publish tile 0's aggregate with the seed folded in
         lb_call = f"""      {ct} pre;
@@ -686,7 +684,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
 #ifdef GR_SCAN_STATS
       const long long cw = clock64();
 #endif
-      while (mb_pub[m] != i + 1) {{ if ({SLEEP}) __nanosleep({SLEEP}); }}
+      while (mb_pub[m] != i + 1) {{ }}
       __threadfence_block();
 #ifdef GR_SCAN_STATS
       if (lane == 0 && blockIdx.x == 0) {{ if (i == 0) {{ gr::gr_scan_stats[4] = gr::gr_scan_stats[5] = gr::gr_scan_stats[6] = gr::gr_scan_stats[7] = 0; gr::gr_scan_stats[3] = clock64(); }}
@@ -716,7 +714,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     // tile of iteration j: prefix (+) its tile-local scan (waiting in its
     // stage), back into the stage, one TMA store
     const int m = j % {M};
-    if (threadIdx.x == 0) {{ while (mb_done[m] != j + 1) {{ if ({SLEEP}) __nanosleep({SLEEP}); }} __threadfence_block(); }}
+    if (threadIdx.x == 0) {{ while (mb_done[m] != j + 1) {{ }} __threadfence_block(); }}
     asm volatile("bar.sync 1, {TPB};" ::: "memory");
     const {ct} pre = mb_pre[m];
     unsigned char* ob = ring + (long long)(j % {S_}) * {NL * tile_b};
