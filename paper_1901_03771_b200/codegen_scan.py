@@ -511,7 +511,10 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     if not staged or any(l.dtype.itemsize != isz for l in staged):
         return None
     W = 128 // isz                       # elements per 128-byte line
-    if N % W:
+    # TMA moves whole 128-byte lines: the last N % W elements of a 1-D scan
+    # (the tail) are read and written by the threads that own them
+    NM = N - N % W
+    if N % W and (len(x.shape) > 1 or NM < 2 * 8192):
         return None
     TPB = 512 if isz == 4 else 256
     ITEMS = SCAN_TMA_ITEMS                # elements per data thread (16: 32 KB tiles, 32: 64 KB)
@@ -583,6 +586,28 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     for i, l in enumerate(region.leaves):
         if l in staged and f"p.in{i}" in body:
             raise NotFusable(l, "staged leaf also read from global memory")
+    tail_fn, tail_load, tail_store = [], "", ""
+    if NM < N:
+        # the tail's mapped values straight from global memory
+        te = LoopEmitter(region)
+        ix = Var("ix", 1)
+        tv = te.cast(te.value(x, [Aff.of(ix)]), x.dtype, T)
+        tail_fn = [f"static __device__ __forceinline__ {ct} tail_value(const Params& p, const long long ix) {{"]
+        tail_fn += ["  " + c for c in te.consts] + render(te.row, 1) + [f"  return {tv[0]};", "}"]
+        tail_load = f'''    if (t == {ntiles - 1}LL) {{
+#pragma unroll
+      for (int k2 = 0; k2 < {ITEMS}; ++k2) {{
+        const long long ix = t * {tile}LL + {ITEMS} * threadIdx.x + k2;
+        if (ix >= {NM}LL && ix < {N}LL) vals[k2] = K::tail_value(p, ix);
+      }}
+    }}'''
+        tail_store = f'''      if (tj == {ntiles - 1}LL) {{
+#pragma unroll
+        for (int k2 = 0; k2 < {vec}; ++k2) {{
+          const long long ix = tj * {tile}LL + {ITEMS} * threadIdx.x + {vec} * q + k2;
+          if (ix >= {NM}LL && ix < {N}LL) p.out0[ix] = o[k2];
+        }}
+      }}'''
 
     params = _params_struct(region)
     maps = "".join(f"    gr::TMap tmap{k};\n" for k in range(NL + 1))
@@ -727,6 +752,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
         for (int k2 = 0; k2 < {vec}; ++k2) o[k2] = {comb}<{ct}>(pre, o[k2]);
         gr::sts_sw<{ct}, {vec}>(ob, {ITEMS} * threadIdx.x + {vec} * q, o);
       }}
+{tail_store}
     }}
     gr::fence_proxy_async();
     asm volatile("bar.sync 1, {TPB};" ::: "memory");
@@ -752,6 +778,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     {ct} vals[{ITEMS}];
     unsigned char* sb = ring + (long long)s * {NL * tile_b};
     K::items(p, t * {tile}LL, {sgs}, vals);
+{tail_load}
 #pragma unroll
     for (int k2 = 1; k2 < {ITEMS}; ++k2) vals[k2] = {comb}<{ct}>(vals[k2 - 1], vals[k2]);
     {ct} inc = vals[{ITEMS - 1}];
@@ -795,10 +822,10 @@ def _gen_lookback_tma(region, s, x, rop, kname):
 }}"""
     pre = "".join(f"#define {d.replace('=', ' ', 1)}\n" for d in os.environ.get("GRUMPY_SCAN_DEFINES", "").split(",") if d)  # experiments
     src = [pre + HEADER, '#include "gr_reduce.cuh"\n#include "gr_tma.cuh"\n', "struct K {", params,
-           "  " + body.replace("\n", "\n  "), "  " + "\n  ".join(seed_fn), "};", kern]
+           "  " + body.replace("\n", "\n  "), "  " + "\n  ".join(seed_fn + tail_fn), "};", kern]
     scratch = 8 + 8 * (1 if isz <= 4 else 2) * 2 * ntiles + 256
     slots = [region.leaves.index(l) for l in staged]
-    tmaps = [(i, W, N // W, W, box, 128) for i in slots] + [(len(region.leaves), W, N // W, W, box, 128)]
+    tmaps = [(i, W, NM // W, W, box, 128) for i in slots] + [(len(region.leaves), W, NM // W, W, box, 128)]
     return KernelSource("scan", "\n".join(src) + "\n", kname, list(range(len(region.leaves))), [0],
                         block=NTH, groups=ntiles * NTH, vec=1, unroll=1, scratch_bytes=scratch,
                         meta={"tiles": ntiles, "scratch_zero": True, "exact": not T.is_float,

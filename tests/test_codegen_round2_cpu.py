@@ -97,7 +97,10 @@ def test_scan_tma_generator_builds(monkeypatch):
     assert "gr::tile_lookback_round<" in one and "own_seq != i" not in one
     runtime.compile_cubin(one)
     odd = gp.asarray(np.arange((1 << 20) + 7, dtype=np.float32))
-    assert _source([gp.cumsum(odd)]).meta["label"] == "scan-lookback"    # not a multiple of a line
+    tail = _source([gp.cumsum(odd)])
+    assert tail.meta["label"] == "scan-tma" and "K::tail_value(p, ix)" in tail.source   # tail past the last line
+    assert tail.meta["tmaps"][0][2] == ((1 << 20) + 7) // 32
+    runtime.compile_cubin(tail.source)
 
 
 def test_wrow_generator_paired_two_pass(monkeypatch):

@@ -188,7 +188,7 @@ def test_scan_lookback_deterministic(sess):
     assert np.max(np.abs(runs[0] - ref)) <= 1e-6 * np.max(np.abs(ref)) + 1.0
 
 
-@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 32, 3 << 20, (1 << 21) + 7, (1 << 24) + 96])
+@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 32, 3 << 20, (1 << 21) + 7, (1 << 24) + 96, (1 << 20) + 8191, 5 * 8192 * 148 + 33])
 @pytest.mark.parametrize("kind", ["f32", "f64", "i64", "f32x2", "max"])
 def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
     """The TMA-fed look-back scan (codegen_scan._gen_lookback_tma) has the
@@ -197,7 +197,7 @@ def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
     bit-identical to it, for
     one- and two-leaf map prologues, 4- and 8-byte types, sums and max; lengths
     that are not a multiple of the tile (zero-filled last box) or of the
-    128-byte line (register-staged fallback)."""
+    128-byte line (the tail elements loaded and stored by their threads)."""
     from paper_1901_03771_b200 import codegen, codegen_scan
     rng = np.random.default_rng([n, len(kind)])
     if kind == "i64":
@@ -226,7 +226,7 @@ def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
     codegen._GEN_CACHE.clear()
     sess._plan_cache.clear()
     assert labels[1] == "scan-lookback"
-    assert labels[0] == ("scan-tma" if n % 32 == 0 else "scan-lookback")
+    assert labels[0] == "scan-tma"      # a tail past the last 128-byte line: read and written by its threads
     assert np.array_equal(outs[0], outs[1])
     if kind in ("i64",):
         assert np.array_equal(outs[0], np.cumsum(xs[0] * 3 + 1))

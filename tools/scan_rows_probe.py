@@ -1,5 +1,7 @@
 """Experiment: scans along the last axis of a matrix with few long lines —
-the segmented TMA look-back scan against the warp-per-16-lines kernel.
+the segmented TMA look-back scan against the warp-per-16-lines kernel — and
+a 1-D scan whose length is not a multiple of a 128-byte line (TMA kernel with
+a tail).
 Run under ncu (--metrics gpu__time_duration.sum) for kernel times; prints the
 kernel label per case.  usage: scan_rows_probe.py"""
 import os
@@ -23,3 +25,9 @@ for shape in [(1024, 262144), (64, 1 << 22), (8192, 32768)]:
             gp.force(y)
         print(shape, mode, sess.executor.last_steps[-1].cache["ks"].meta.get("label"), flush=True)
         del y
+x = gp.asarray(np.random.default_rng(2).standard_normal((1 << 28) + 7, dtype=np.float32))
+for _ in range(3):
+    y = gp.cumsum(x * 0.5 + 1.0)
+    gp.force(y)
+print("2^28+7", sess.executor.last_steps[-1].cache["ks"].meta.get("label"), flush=True)
+
