@@ -22,4 +22,6 @@ for w in blackscholes-f32 mlp transpose rownorm kmeans cumsum cumsum-rows; do
   timeout 900 ncu --set full --clock-control none --import-source on -k regex:gr_region -s 3 -c 1 \
     -o $OUT/full_$w python bench.py --workload $w --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 > /dev/null 2>&1
 done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/scan_rows_probe.csv \
+  python tools/scan_rows_probe.py > $OUT/scan_rows_probe.txt 2>&1
 echo done
