@@ -665,21 +665,30 @@ def _e2e(args, dist, gp, rt, sess, prog, host, inputs_of, elements, pinned):
     d2h = sum(x.nbytes for x in dst)
     steps = max(1, min(args.steps, args.e2e_steps))
     sc0 = sess.stats.streamed_chunks
-    WARM = 2   # first call compiles the chunk kernels, second reaches the pool's steady state
+    # the first call compiles the chunk kernels, the next two reach the
+    # pool's and the copy engines' steady state (tools/e2e_probe.py: 11, 5.6,
+    # then 4.8 ms per MLP step)
+    WARM = 3
+    per_step = []
     for it in range(WARM + steps):
         if it == WARM:
             dist.barrier()
             rt.sync()
             t0 = time.perf_counter()
+        ts = time.perf_counter()
         outs = prog(gp, inputs_of(src))
         # to_external of every output into host buffers; regions reading host
         # inputs row-locally stream (H2D / kernel / D2H overlap)
         gp.materialize(*outs, out=dst)
+        if it >= WARM:
+            per_step.append(time.perf_counter() - ts)
     rt.sync()
     s = dist.max(time.perf_counter() - t0)
     return {"value": elements * steps / s, "unit": "elements/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "steps": steps, "host_memory": "page-locked" if pinned else "pageable",
-            "streamed_chunks_per_step": (sess.stats.streamed_chunks - sc0) / (WARM + steps)}
+            "streamed_chunks_per_step": (sess.stats.streamed_chunks - sc0) / (WARM + steps),
+            "step_ms": {"mean": 1e3 * s / steps, "median": 1e3 * float(np.median(per_step)),
+                        "max": 1e3 * max(per_step)}}
 
 
 def _compute_roofline(w, n, kernel_ms, clk):
@@ -720,7 +729,7 @@ def main():
     ap.add_argument("--impl", default="grumpy", choices=["grumpy", "reference"])
     ap.add_argument("--workload", default="blackscholes-f32", choices=sorted(WORKLOADS))
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"])
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -71,15 +71,18 @@ def generate(region: Region, kname="gr_region") -> KernelSource:
         return _gen_lines(region, s, x, rop, None, kname)
     if axis == len(x.shape) - 1 and seed is None and x.shape[-1] > 1:
         lines = element_count(x.shape[:-1])
-        if SCAN_TMA and lines < ROWS_T_MIN_LINES and element_count(x.shape) >= SCAN_TMA_MIN:
+        if lines < ROWS_T_MIN_LINES and element_count(x.shape) >= SCAN_TMA_MIN and x.shape[-1] >= 8192:
             # too few lines for a warp per 16 of them to fill the GPU: one
-            # look-back scan per line (tolerance instead of NumPy's order)
-            try:
-                ks = _gen_lookback_tma(region, s, x, rop, kname)
-                if ks is not None:
-                    return ks
-            except NotFusable:
-                pass
+            # look-back scan per line (tolerance instead of NumPy's order) —
+            # the TMA kernel when lines are whole tiles, else register-staged
+            if SCAN_TMA:
+                try:
+                    ks = _gen_lookback_tma(region, s, x, rop, kname)
+                    if ks is not None:
+                        return ks
+                except NotFusable:
+                    pass
+            return _gen_lookback(region, s, x, rop, kname, segments=True)
         if ROWS_T and lines >= 32:
             return _gen_rows_t(region, s, x, rop, kname)
     return _gen_lines(region, s, x, rop, axis, kname)
@@ -259,12 +262,17 @@ def _gen_lines(region, s, x, rop, axis, kname, block=128) -> KernelSource:
                         block=block, groups=L, vec=1, unroll=1, meta={"lines": L, "length": n, "exact": True})
 
 
-def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
+def _gen_lookback(region, s, x, rop, kname, segments=False) -> KernelSource:
     """One pass over a long 1-D scan: 4096-element tiles, coalesced (vector)
     loads of the map prologue into a padded shared tile, a thread-sequential
     run per thread, warp and CTA combines, and the deterministic look-back of
     gr::tile_lookback; results leave through the shared tile as coalesced
-    vector stores."""
+    vector stores.
+
+    A matrix scanned along its last axis runs as one such scan per line
+    (segments): every line starts at a tile boundary (ceil(n / tile) tiles per
+    line, the last one partial) and the look-back stops at the line's first
+    tile."""
     T = s.dtype
     ct = T.ctype
     N = element_count(x.shape)
@@ -272,9 +280,12 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     # 4096 for 8-byte types so the shared tile stays within 48 KB
     TILE_THREADS = int(os.environ.get("GRUMPY_SCAN_TPB", "512")) if T.itemsize <= 4 else 256
     tile = TILE_THREADS * ITEMS
-    ntiles = -(-N // tile)
+    n_seg = x.shape[-1] if segments else N               # segment (line) length
+    TPL = -(-n_seg // tile)                              # tiles per segment
+    ntiles = TPL * (N // n_seg)
     SW = 1 if T.itemsize <= 4 else 2      # 64-bit status words per published value
     vec = max(1, min(4, 16 // max(T.itemsize, x.dtype.itemsize)))
+    aligned = n_seg % vec == 0            # every tile starts on a vector boundary
     chunks = ITEMS // vec
     ident = c_literal(_IDENT[rop](T), T)
     comb = _COMBINE[rop]
@@ -296,16 +307,16 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
             lin = Aff.of(tb) + e
         else:
             raw = em.emit(v.level, "long long", f"tb + {e.c()}")
-            lin = Aff.of(Var(em.emit(v.level, "long long", f"{raw} < {N}LL ? {raw} : {N - 1}LL"), v.level))
+            lin = Aff.of(Var(em.emit(v.level, "long long", f"{raw} < lim ? {raw} : lim - 1"), v.level))
         coords = _flat_coords(em, x.shape, lin, v)
         val = em.cast(em.value(x, coords), x.dtype, T)
-        keep = "" if full else f"(tb + {e.c()} < {N}LL) ? "
+        keep = "" if full else f"(tb + {e.c()} < lim) ? "
         tail = "" if full else f" : {ident}"
         em.stmt(v.level, f"buf[gr::spad({e.c()})] = {keep}{val[0]}{tail};")
         em.close(sv, b)
         em.close(sj, a)
-        out = [f"static __device__ __forceinline__ void {name}(const Params& p, const long long tb, {ct}* buf) {{",
-               "  const long long tt = threadIdx.x;"]
+        out = [f"static __device__ __forceinline__ void {name}(const Params& p, const long long tb, const long long lim, {ct}* buf) {{",
+               "  const long long tt = threadIdx.x; (void)lim;"]
         out += ["  " + c for c in em.consts]
         out += render(em.row, 1)
         out.append("}")
@@ -346,7 +357,7 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
       if (t < 0) break;
       // a seed (streamed carry) joins tile 0: its inclusive prefix is
       // seed (+) aggregate, its exclusive prefix the seed
-      const {ct} pre0 = gr::tile_lookback<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? {comb}<{ct}>({seedv}, tagg[i & 1]) : tagg[i & 1], {ident});
+      const {ct} pre0 = gr::tile_lookback<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? {comb}<{ct}>({seedv}, tagg[i & 1]) : tagg[i & 1], {ident}, (t / {TPL}LL) * {TPL}LL);
       const {ct} pre = {seeded} && t == 0 ? {seedv} : pre0;
       if (lane == 0) tpre[i & 1] = pre;
       asm volatile("bar.arrive 3, {NTH};" ::: "memory");
@@ -376,17 +387,19 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
     {{
       const {ct}* buf = bufs + b * {TP}LL;
       const {ct} pre = tpre[b];
-      const long long tb = t * {tile}LL;
+      const long long ln = t / {TPL}LL, tc = t % {TPL}LL;
+      const long long tb = ln * {n_seg}LL + tc * {tile}LL;
+      const long long lim = ln * {n_seg}LL + ({n_seg}LL < (tc + 1) * {tile}LL ? {n_seg}LL : (tc + 1) * {tile}LL);
 #pragma unroll
       for (int j = 0; j < {chunks}; ++j) {{
         const long long e = (long long)j * {TILE_THREADS * vec} + {vec} * threadIdx.x;
         {ct} o[{vec}];
 #pragma unroll
-        for (int v = 0; v < {vec}; ++v) {{ const {ct} x = buf[gr::spad(e + v)]; o[v] = (t > 0 || {seeded}) ? {comb}<{ct}>(pre, x) : x; }}
-        if (tb + e + {vec} <= {N}LL) {{
+        for (int v = 0; v < {vec}; ++v) {{ const {ct} x = buf[gr::spad(e + v)]; o[v] = (tc > 0 || {seeded}) ? {comb}<{ct}>(pre, x) : x; }}
+        if ({"true" if aligned else "false"} && tb + e + {vec} <= lim) {{
           gr::stv<{ct}, {vec}>(p.out0 + tb + e, o);
         }} else {{
-          for (int v = 0; v < {vec}; ++v) if (tb + e + v < {N}LL) p.out0[tb + e + v] = o[v];
+          for (int v = 0; v < {vec}; ++v) if (tb + e + v < lim) p.out0[tb + e + v] = o[v];
         }}
       }}
     }}
@@ -398,8 +411,10 @@ def _gen_lookback(region, s, x, rop, kname) -> KernelSource:
   }}
 }}'''
     stage = [f"static __device__ __forceinline__ void stage(const Params& p, const long long t, {ct}* buf, {ct}* ws, {ct}* agg_s, long long* tid_s, unsigned long long* aggs, const int lane, const int w) {{",
-             f"  const long long tb = t * {tile}LL;",
-             f"  if (tb + {tile}LL <= {N}LL) load_full(p, tb, buf); else load_tail(p, tb, buf);",
+             f"  const long long ln = t / {TPL}LL, tc = t % {TPL}LL;",
+             f"  const long long tb = ln * {n_seg}LL + tc * {tile}LL;",
+             f"  const long long lim = ln * {n_seg}LL + ({n_seg}LL < (tc + 1) * {tile}LL ? {n_seg}LL : (tc + 1) * {tile}LL);",
+             f"  if ({'true' if aligned else 'false'} && tb + {tile}LL <= lim) load_full(p, tb, lim, buf); else load_tail(p, tb, lim, buf);",
              f'  asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");',
              f"  {ct} vals[{ITEMS}];",
              "#pragma unroll",

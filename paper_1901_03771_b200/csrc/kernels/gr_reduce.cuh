@@ -669,24 +669,26 @@ template <class T> struct __align__(16) LookbackBuf { T v[32 * GR_SCAN_J * GR_SC
 
 template <class Op, class T>
 __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, unsigned long long* inc,
-                                               long long tile, T tile_agg, T ident, T* lb);
+                                               long long tile, T tile_agg, T ident, T* lb, long long ls = 0);
 template <class Op, class T>
 __device__ __forceinline__ T tile_lookback(const unsigned long long* agg, unsigned long long* inc,
-                                           long long tile, T tile_agg, T ident) {
+                                           long long tile, T tile_agg, T ident, long long ls = 0) {
   __shared__ LookbackBuf<T> lbs;
-  return tile_lookback_buf<Op, T>(agg, inc, tile, tile_agg, ident, lbs.v);
+  return tile_lookback_buf<Op, T>(agg, inc, tile, tile_agg, ident, lbs.v, ls);
 }
 // lb: the calling warp's own staging array (32 * J * R values); several
-// look-back warps of one CTA each pass their own
+// look-back warps of one CTA each pass their own.  ls: the first tile of the
+// tile's segment (a line of a matrix scanned along its rows): the walk never
+// goes below it, and the segment's first tile starts its own prefix chain.
 template <class Op, class T>
 __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, unsigned long long* inc,
-                                               long long tile, T tile_agg, T ident, T* lb) {
+                                               long long tile, T tile_agg, T ident, T* lb, long long ls) {
   const int lane = threadIdx.x & 31;
 #ifdef GR_SCAN_NOLB
   return ident;   // experiment: streaming floor without any look-back (wrong results)
 #endif
-  if (tile == 0) {
-    if (lane == 0) stat_put<T>(inc, 0, tile_agg);
+  if (tile == ls) {
+    if (lane == 0) stat_put<T>(inc, tile, tile_agg);
     return ident;
   }
 #ifdef GR_SCAN_STATS
@@ -706,8 +708,8 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const long long q = top - lane - 32 * j;
-      ri[j] = q >= 0 ? stat_ld<T>(inc, q) : StatRaw<T>{0, 0};
-      ra[j] = q >= 0 ? stat_ld<T>(agg, q) : StatRaw<T>{0, 0};
+      ri[j] = q >= ls ? stat_ld<T>(inc, q) : StatRaw<T>{0, 0};
+      ra[j] = q >= ls ? stat_ld<T>(agg, q) : StatRaw<T>{0, 0};
     }
     long long fw = -1;
 #pragma unroll
@@ -718,7 +720,7 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
 #pragma unroll
     for (int j = 0; j < J; ++j) {
       const long long q = top - lane - 32 * j;
-      if (q >= 0 && q > fw) {
+      if (q >= ls && q > fw) {
         while (!stat_ok<T>(ra[j])) ra[j] = stat_ld<T>(agg, q);
         lb[tile - 1 - q] = stat_val<T>(ra[j]);
       }
@@ -728,7 +730,7 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
       found = fw;
       base = __shfl_sync(0xffffffffu, base, (int)((top - fw) & 31));
     }
-    if (top - 32 * J < 0 && found < 0) { top = tile - 1 + 32 * J; w = -1; }   // nothing published down to tile 0 yet: poll again
+    if (top - 32 * J < ls && found < 0) { top = tile - 1 + 32 * J; w = -1; }   // nothing published down to the segment's start yet: poll again
   }
   __syncwarp();
   T pre = ident;
@@ -755,13 +757,13 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const long long q = top - lane - 32 * j;
-        const StatRaw<T> r = q >= 0 ? stat_ld<T>(inc, q) : StatRaw<T>{0, 0};
+        const StatRaw<T> r = q >= ls ? stat_ld<T>(inc, q) : StatRaw<T>{0, 0};
         const unsigned m = __ballot_sync(0xffffffffu, stat_ok<T>(r));
         if (found < 0 && m) found = top - (__ffs(m) - 1) - 32 * j;
       }
       if (found < 0) {
         top -= 32 * J;
-        if (top < 0) top = tile - 1;
+        if (top < ls) top = tile - 1;
       }
     }
     StatRaw<T> rf = stat_ld<T>(inc, found);

@@ -134,3 +134,17 @@ def test_scan_rows_generator_builds(dt):
     assert _source([gp.cumsum(x * 3 + 1, axis=0)]).meta.get("label") is None          # lines
     assert _source([gp.cumsum(gp.asarray(np.ones((31, 300), dt)), axis=1)]).meta.get("label") is None
 
+
+
+@pytest.mark.parametrize("shape,label,tiles", [((64, 65536), "scan-tma", 512), ((64, 100003), "scan-lookback", 64 * 13),
+                                               ((16, 70001), "scan-lookback", 16 * 9)])
+def test_scan_few_long_lines_segmented(shape, label, tiles):
+    """Few long lines along the last axis: one look-back scan per line — TMA
+    when lines are whole 8192-element tiles, else register-staged with a
+    partial last tile per line; the look-back stops at the line's first tile."""
+    x = gp.asarray(np.ones(shape, np.float32))
+    ks = _source([gp.cumsum(x * 3 + 1, axis=-1)])
+    assert ks.meta["label"] == label and ks.meta["tiles"] == tiles
+    tpl = -(-shape[-1] // 8192)
+    assert f"(t / {tpl}LL) * {tpl}LL" in ks.source
+    runtime.compile_cubin(ks.source)

@@ -61,13 +61,15 @@ def test_scan_rows_contiguous_axis(sess, shape, kind):
     assert np.array_equal(out, ref, equal_nan=kind not in ("i64", "i32"))
 
 
-@pytest.mark.parametrize("shape", [(64, 65536), (4, 8, 1 << 16), (1024, 16384), (3, 1 << 20)])
+@pytest.mark.parametrize("shape", [(64, 65536), (4, 8, 1 << 16), (1024, 16384), (3, 1 << 20),
+                                   (64, 100003), (16, 70001), (300, 16388), (7, 3, 50021)])
 @pytest.mark.parametrize("kind", ["f32", "f64", "i64", "max", "colvec"])
 def test_scan_rows_segmented_lookback(sess, shape, kind):
     """Few long lines scanned along the last axis run as one look-back scan per
-    line (the TMA kernel with segments: a tile's fold never reaches below its
-    line's first tile).  Integers and max exact; float sums within the
-    reassociation bound of the 1-D scan, per line."""
+    line (segments: a tile's fold never reaches below its line's first tile) —
+    the TMA kernel when every line is whole tiles, else the register-staged
+    kernel with a partial last tile per line.  Integers and max exact; float
+    sums within the reassociation bound of the 1-D scan, per line."""
     rng = np.random.default_rng([shape[-1], len(kind)])
     if kind == "i64":
         x = rng.integers(-50, 50, shape)
@@ -79,7 +81,7 @@ def test_scan_rows_segmented_lookback(sess, shape, kind):
     if kind == "max":
         x.reshape(-1)[x.size // 3] = np.nan
         out = np.asarray(np.maximum.accumulate(gp.asarray(x), axis=-1))
-        assert sess.executor.last_steps[-1].cache["ks"].meta.get("label") == "scan-tma"
+        assert sess.executor.last_steps[-1].cache["ks"].meta.get("label") in ("scan-tma", "scan-lookback")
         assert np.array_equal(out, np.maximum.accumulate(x, axis=-1), equal_nan=True)
         return
     if kind == "colvec":
@@ -87,14 +89,15 @@ def test_scan_rows_segmented_lookback(sess, shape, kind):
         out, t = np.asarray(gp.cumsum(g * 0.5 - gp.asarray(c), axis=-1)), x * np.float32(0.5) - c
     else:
         out, t = np.asarray(gp.cumsum(g * 3 + 1, axis=-1)), x * 3 + 1
-    assert sess.executor.last_steps[-1].cache["ks"].meta.get("label") == "scan-tma"
+    whole = shape[-1] % (8192 if x.dtype.itemsize == 4 else 4096) == 0
+    assert sess.executor.last_steps[-1].cache["ks"].meta.get("label") == ("scan-tma" if whole else "scan-lookback")
     if kind == "i64":
         assert np.array_equal(out, np.cumsum(t, axis=-1))
         return
     ref = np.cumsum(t.astype(np.float64), axis=-1)
     bound = np.cumsum(np.abs(t.astype(np.float64)), axis=-1)
     eps = np.finfo(t.dtype).eps
-    tiles = shape[-1] // (8192 if t.dtype == np.float32 else 4096)
+    tiles = -(-shape[-1] // (8192 if t.dtype == np.float32 else 4096))
     assert np.all(np.abs(out - ref) <= (tiles + 32) * eps * bound)
 
 
