@@ -14,7 +14,7 @@ import paper_1901_03771_b200 as gp  # noqa: E402
 from paper_1901_03771_b200 import codegen, codegen_scan  # noqa: E402
 
 sess = gp.default_session()
-for shape in [(1024, 262144), (64, 1 << 22), (8192, 32768)]:
+for shape in [(1024, 262144), (64, 1 << 22), (8192, 32768), (1024, 262147)]:
     x = gp.asarray(np.random.default_rng(1).standard_normal(shape, dtype=np.float32))
     for mode in ("tma", "rows"):
         codegen_scan.ROWS_T_MIN_LINES = 148 * 16 * 4 if mode == "tma" else 0
