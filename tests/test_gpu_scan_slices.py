@@ -61,6 +61,23 @@ def test_scan_rows_contiguous_axis(sess, shape, kind):
     assert np.array_equal(out, ref, equal_nan=kind not in ("i64", "i32"))
 
 
+@pytest.mark.parametrize("view", ["T", "step", "cols", "big-T"])
+def test_scan_last_axis_of_views(sess, view):
+    """Scans along the last axis of transposed / strided / column-sliced views
+    (the leaves are read through their index maps, not staged): NumPy's
+    sequential fold per line, bit-exact, whichever kernel takes them."""
+    rng = np.random.default_rng(len(view))
+    x = rng.standard_normal((2048, 3000) if view == "big-T" else (600, 700)).astype(np.float32)
+    g = gp.asarray(x)
+    if view in ("T", "big-T"):
+        got, ref = gp.cumsum(g.T * 2.0, axis=-1), np.cumsum(x.T * np.float32(2.0), axis=-1)
+    elif view == "step":
+        got, ref = gp.cumsum(g[:, ::2] + 1.0, axis=1), np.cumsum(x[:, ::2] + np.float32(1.0), axis=1)
+    else:
+        got, ref = gp.cumsum(g[100:, 5:605] - 0.5, axis=1), np.cumsum(x[100:, 5:605] - np.float32(0.5), axis=1)
+    assert np.array_equal(np.asarray(got), ref)
+
+
 @pytest.mark.parametrize("shape", [(64, 65536), (4, 8, 1 << 16), (1024, 16384), (3, 1 << 20),
                                    (64, 100003), (16, 70001), (300, 16388), (7, 3, 50021)])
 @pytest.mark.parametrize("kind", ["f32", "f64", "i64", "max", "colvec"])
