@@ -285,7 +285,9 @@ def _gen_lookback(region, s, x, rop, kname, segments=False) -> KernelSource:
     ntiles = TPL * (N // n_seg)
     SW = 1 if T.itemsize <= 4 else 2      # 64-bit status words per published value
     vec = max(1, min(4, 16 // max(T.itemsize, x.dtype.itemsize)))
-    aligned = n_seg % vec == 0            # every tile starts on a vector boundary
+    # every tile starts on a vector boundary (tile bases are multiples of the
+    # tile in one long scan; a line's tiles start at multiples of its length)
+    aligned = not segments or n_seg % vec == 0
     chunks = ITEMS // vec
     ident = c_literal(_IDENT[rop](T), T)
     comb = _COMBINE[rop]

@@ -254,7 +254,7 @@ def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
         assert np.array_equal(outs[0], np.maximum.accumulate(xs[0] * np.float32(2.0)))
 
 
-@pytest.mark.parametrize("case", ["long-f32", "long-i64", "long-tma", "lines-axis0", "short"])
+@pytest.mark.parametrize("case", ["long-f32", "long-i64", "long-tma", "long-tma-tail", "lines-axis0", "short"])
 def test_seeded_scan(sess, monkeypatch, case):
     """A scan seeded with a value (the streamed chunks' carry, streaming.py)
     folds from the seed: out[k] = seed (+) x[0] (+) ... (+) x[k]; integers
@@ -263,7 +263,7 @@ def test_seeded_scan(sess, monkeypatch, case):
     from paper_1901_03771_b200 import codegen, codegen_scan
     from paper_1901_03771_b200.dag import Op, OpKind
     from oracle import eager
-    monkeypatch.setattr(codegen_scan, "SCAN_TMA", case == "long-tma")
+    monkeypatch.setattr(codegen_scan, "SCAN_TMA", case.startswith("long-tma"))
     codegen._GEN_CACHE.clear()
     rng = np.random.default_rng(len(case))
     g = sess.graph
@@ -276,7 +276,7 @@ def test_seeded_scan(sess, monkeypatch, case):
         carry = g.add_op(Op(OpKind.RESHAPE, None, ((24,),)), [carry])
         ref = np.cumsum(np.concatenate([prevh[4:5], xh * 2.0]), axis=0)[1:]
     else:
-        n = {"short": 5000, "long-tma": (1 << 21) + 32}.get(case, (1 << 21) + 7)
+        n = {"short": 5000, "long-tma": (1 << 21) + 32}.get(case, (1 << 21) + 7)      # long-tma-tail: + 7
         if case == "long-i64":
             xh, prevh = rng.integers(-50, 50, n), rng.integers(-9, 9, 7)
         else:
@@ -297,4 +297,5 @@ def test_seeded_scan(sess, monkeypatch, case):
         assert np.all(np.abs(got - ref) <= 1e-5 * (scale + 1))
         assert np.all(np.abs(exp - ref) <= 1e-5 * (scale + 1))
     label = sess.executor.last_steps[-1].cache["ks"].meta.get("label")
-    assert label == {"long-tma": "scan-tma", "long-f32": "scan-lookback", "long-i64": "scan-lookback"}.get(case, label)
+    assert label == {"long-tma": "scan-tma", "long-tma-tail": "scan-tma", "long-f32": "scan-lookback",
+                     "long-i64": "scan-lookback"}.get(case, label)
