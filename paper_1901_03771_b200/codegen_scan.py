@@ -531,11 +531,11 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     # TMA moves whole 128-byte lines: the last N % W elements of a 1-D scan
     # (the tail) are read and written by the threads that own them
     NM = N - N % W
-    if N % W and (len(x.shape) > 1 or NM < 2 * 8192):
-        return None
     TPB = 512 if isz == 4 else 256
     ITEMS = SCAN_TMA_ITEMS                # elements per data thread (16: 32 KB tiles, 32: 64 KB)
     tile = TPB * ITEMS
+    if N % W and (len(x.shape) > 1 or NM < 2 * tile):
+        return None
     # segments: a scan along the last axis of a matrix is one scan per line;
     # lines made of whole tiles keep every tile inside one line
     seg = x.shape[-1] if len(x.shape) > 1 else N
