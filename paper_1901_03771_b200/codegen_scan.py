@@ -37,13 +37,15 @@ SCAN_TMA = os.environ.get("GRUMPY_SCAN_TMA", "1") == "1"
 SCAN_TMA_MIN = 1 << 20
 SCAN_TMA_SMEM = 200 * 1024
 SCAN_TMA_STAGES = int(os.environ.get("GRUMPY_SCAN_STAGES", "6"))
-SCAN_TMA_LAG = int(os.environ.get("GRUMPY_SCAN_LAG", "3"))
-SCAN_TMA_LBW = int(os.environ.get("GRUMPY_SCAN_LBW", "2"))
+SCAN_TMA_LAG = int(os.environ.get("GRUMPY_SCAN_LAG", "2"))   # 3 with the left fold (GRUMPY_SCAN_TREE=0)
+SCAN_TMA_LBW = int(os.environ.get("GRUMPY_SCAN_LBW", "1"))   # 2 with the left fold
 SCAN_TMA_ITEMS = int(os.environ.get("GRUMPY_SCAN_ITEMS", "16"))
 # look-back by rounds (gr::tile_lookback_round): the prefix starts from the
 # CTA's own inclusive prefix of one round earlier instead of the nearest one
 # another CTA published
 SCAN_TMA_ROUND = os.environ.get("GRUMPY_SCAN_ROUND", "1") == "1"
+# the aggregates of a round combined as a warp tree (not a left fold)
+SCAN_TMA_TREE = os.environ.get("GRUMPY_SCAN_TREE", "1") == "1"
 
 
 def generate(region: Region, kname="gr_region") -> KernelSource:
@@ -509,15 +511,18 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     back into its stage and leaves with one TMA tensor store.
 
     Tiles go round-robin over a persistent grid of G CTAs (one per SM, all
-    resident), so the look-back is by rounds (gr::round_stage/round_fold):
-    the prefix of tile t is the CTA's own inclusive prefix of tile t - G
-    folded with the G - 1 aggregates in between — one L2 round trip, and it
-    never waits for another CTA's look-back (the nearest-published-prefix
-    walk of gr::tile_lookback made a chain of them: 0.51 ms at 2^28 against
-    0.40).  Two look-back warps alternate tiles, one staging its aggregates
-    while the other folds, and hand the CTA's inclusive prefix over in shared
-    memory.  Association is the left fold of the register-staged kernel
-    (_gen_lookback): the results are bit-identical to it."""
+    resident), so the look-back is by rounds: the prefix of tile t is the
+    CTA's own inclusive prefix of tile t - G combined with the G - 1
+    aggregates in between — one L2 round trip, and it never waits for
+    another CTA's look-back (the nearest-published-prefix walk of
+    gr::tile_lookback made a chain of them: 0.51 ms at 2^28).  The default
+    combines those aggregates as a warp tree (gr::round_tree: ~100 cycles
+    after the loads, so two tiles of lag hide the look-back; 0.341 ms, more
+    accurate than a left fold, deterministic for a given grid).  With
+    GRUMPY_SCAN_TREE=0 they are left-folded by one lane (gr::round_stage /
+    round_fold, the register-staged kernel's association, bit-identical to
+    it; 1.8k cycles per fold, two look-back warps alternate tiles and hand
+    the CTA's prefix over in shared memory: 0.40 ms)."""
     T = s.dtype
     ct = T.ctype
     N = element_count(x.shape)
@@ -634,7 +639,28 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     rounds = SCAN_TMA_ROUND
     if len(x.shape) > 1 and not rounds:
         return None                      # segments need the look-back by rounds
-    if rounds and NLW == 1:
+    ls_expr = f"(t / {TPL}LL) * {TPL}LL"
+    if rounds and SCAN_TMA_TREE:
+        # the aggregates since the CTA's previous tile combined as a warp tree
+        # (gr::round_tree) before the CTA's inclusive prefix is needed
+        take_own = ("" if NLW == 1 else
+                    f"""        if (i > 0) {{
+          if (lane == 0) {{ while (own_seq != i) {{ }} }}
+          __syncwarp();
+          __threadfence_block();
+          own = own_v;
+        }}
+""")
+        give_own = "" if NLW == 1 else "\n      if (lane == 0) { own_v = own; __threadfence_block(); own_seq = i + 1; }"
+        lb_call = f"""      {ct} pre;
+      if (t % {TPL}LL == 0) {{
+{take_own}        pre = {seedv}; own = mb_agg[m];
+      }} else {{
+        const {ct} tree = gr::round_tree<{op}, {ct}>(aggs, t, (int)gridDim.x, {ls_expr}, {ident});
+{take_own}        pre = t - (long long)gridDim.x < {ls_expr} ? tree : {comb}<{ct}>(own, tree);
+        own = {comb}<{ct}>(pre, mb_agg[m]);
+      }}{give_own}"""
+    elif rounds and NLW == 1:
         # the data warps publish tile 0's aggregate with the seed folded in
         lb_call = f"""      {ct} pre;
       if (t % {TPL}LL == 0) {{ pre = {seedv}; own = mb_agg[m]; }}

@@ -827,6 +827,9 @@ template <class Op, class T> __device__ __forceinline__ T round_pad(T ident) {
 template <class Op, class T, int J = 5>
 __device__ __forceinline__ void round_stage(const unsigned long long* agg, long long tile, int G, long long ls,
                                             T ident, T* lb) {
+#ifdef GR_SCAN_NOLB
+  return;           // experiment: streaming floor without any look-back (wrong results)
+#endif
   const int lane = threadIdx.x & 31;
   const long long lo = tile - G + 1 > ls ? tile - G + 1 : ls;   // first aggregate folded
   const int n = (int)(tile - lo);                        // aggregates lo .. tile-1
@@ -854,6 +857,9 @@ __device__ __forceinline__ void round_stage(const unsigned long long* agg, long 
 }
 template <class Op, class T>
 __device__ __forceinline__ T round_fold(long long tile, int G, long long ls, T own_inc, T ident, T* lb) {
+#ifdef GR_SCAN_NOLB
+  return own_inc;   // experiment: streaming floor without any look-back (wrong results)
+#endif
   const int lane = threadIdx.x & 31;
   const bool first = tile - G < ls;                // no own prefix inside the segment
   const int n = (int)(first ? tile - ls : G - 1);
@@ -881,6 +887,51 @@ __device__ __forceinline__ T round_fold(long long tile, int G, long long ls, T o
   }
   return __shfl_sync(0xffffffffu, pre, 0);
 }
+// The same look-back with the aggregates between the CTA's previous tile and
+// this one combined as a tree across the warp instead of a left fold: each
+// lane folds the aggregates k = lane + 32 j (j ascending), then a butterfly
+// over the lanes (fixed pattern), then own (+) that — one dependent combine
+// per aggregate became ~J + 5, so the look-back is a round trip plus ~100
+// cycles.  The association depends only on the tile index and G (the grid,
+// one CTA per SM): deterministic on a given GPU, more accurate than the left
+// fold, no longer the register-staged kernel's bits.  Returns the tree of
+// the aggregates; the caller's prefix is own (+) tree, or the tree alone for
+// a segment's first round (tile - G < ls: no own prefix inside the segment).
+template <class Op, class T, int J = 5>
+__device__ __forceinline__ T round_tree(const unsigned long long* agg, long long tile, int G, long long ls, T ident) {
+#ifdef GR_SCAN_NOLB
+  return ident;     // experiment: streaming floor without any look-back (wrong results)
+#endif
+  const int lane = threadIdx.x & 31;
+  const bool first = tile - G < ls;
+  const long long lo = first ? ls : tile - G + 1;
+  const int n = (int)(tile - lo);
+  const T pad = round_pad<Op, T>(ident);
+  T acc = pad;
+  for (int w0 = 0; w0 < n; w0 += 32 * J) {
+    StatRaw<T> ra[J];
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = w0 + lane + 32 * j;
+      if (k < n) ra[j] = stat_ld<T>(agg, lo + k);
+    }
+#pragma unroll
+    for (int j = 0; j < J; ++j) {
+      const int k = w0 + lane + 32 * j;
+      if (k < n) {
+        while (!stat_ok<T>(ra[j])) ra[j] = stat_ld<T>(agg, lo + k);
+        acc = Op::template c<T>(acc, stat_val<T>(ra[j]));
+      }
+    }
+  }
+#pragma unroll
+  for (int m = 1; m < 32; m <<= 1) {
+    const T o = shfl_xor<T>(acc, m);
+    acc = (lane & m) ? Op::template c<T>(o, acc) : Op::template c<T>(acc, o);
+  }
+  return acc;
+}
+
 template <class Op, class T, int J = 5>
 __device__ __forceinline__ T tile_lookback_round(const unsigned long long* agg, long long tile, int G, long long ls,
                                                  T own_inc, T ident, T* lb) {

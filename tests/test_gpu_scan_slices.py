@@ -210,15 +210,19 @@ def test_scan_lookback_deterministic(sess):
 
 @pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 32, 3 << 20, (1 << 21) + 7, (1 << 24) + 96, (1 << 20) + 8191, 5 * 8192 * 148 + 33])
 @pytest.mark.parametrize("kind", ["f32", "f64", "i64", "f32x2", "max"])
-def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
-    """The TMA-fed look-back scan (codegen_scan._gen_lookback_tma) has the
-    register-staged kernel's association (its look-back by rounds folds from
-    the CTA's own prefix of one round earlier — the same left fold): results
-    bit-identical to it, for
-    one- and two-leaf map prologues, 4- and 8-byte types, sums and max; lengths
-    that are not a multiple of the tile (zero-filled last box) or of the
-    128-byte line (the tail elements loaded and stored by their threads)."""
+@pytest.mark.parametrize("tree", [True, False])
+def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind, tree):
+    """The TMA-fed look-back scan (codegen_scan._gen_lookback_tma) against the
+    register-staged kernel, for one- and two-leaf map prologues, 4- and 8-byte
+    types, sums and max; lengths that are not a multiple of the tile
+    (zero-filled last box) or of the 128-byte line (the tail elements loaded
+    and stored by their threads).  With the left fold of a round's aggregates
+    (tree=False) the association is the register-staged kernel's: bits
+    identical.  With the warp tree (the default) integers and max are still
+    identical and float sums stay within the 1-D scan's reassociation bound,
+    the same bits on every run."""
     from paper_1901_03771_b200 import codegen, codegen_scan
+    monkeypatch.setattr(codegen_scan, "SCAN_TMA_TREE", tree)
     rng = np.random.default_rng([n, len(kind)])
     if kind == "i64":
         xs = [rng.integers(-1000, 1000, n)]
@@ -236,7 +240,7 @@ def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
         return gp.cumsum(g[0] * 3 + 1)
 
     outs, labels = [], []
-    for tma in (True, False):
+    for tma in (True, True, False):
         monkeypatch.setattr(codegen_scan, "SCAN_TMA", tma)
         codegen._GEN_CACHE.clear()
         sess._plan_cache.clear()
@@ -245,9 +249,18 @@ def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind):
         labels.append(sess.executor.last_steps[-1].cache["ks"].meta.get("label"))
     codegen._GEN_CACHE.clear()
     sess._plan_cache.clear()
-    assert labels[1] == "scan-lookback"
-    assert labels[0] == "scan-tma"      # a tail past the last 128-byte line: read and written by its threads
-    assert np.array_equal(outs[0], outs[1])
+    assert labels == ["scan-tma", "scan-tma", "scan-lookback"]
+    assert np.array_equal(outs[0], outs[1])                      # deterministic
+    if kind in ("i64", "max") or not tree:
+        assert np.array_equal(outs[0], outs[2])
+    else:
+        t = (xs[0] * xs[1] + np.float32(1.0)) if kind == "f32x2" else xs[0] * 3 + 1
+        ref = np.cumsum(t.astype(np.float64))
+        bound = np.cumsum(np.abs(t.astype(np.float64)))
+        tiles = -(-n // (8192 if t.dtype == np.float32 else 4096))
+        eps = np.finfo(t.dtype).eps
+        for o in (outs[0], outs[2]):
+            assert np.all(np.abs(o - ref) <= (tiles + 32) * eps * bound)
     if kind in ("i64",):
         assert np.array_equal(outs[0], np.cumsum(xs[0] * 3 + 1))
     if kind == "max":
