@@ -46,6 +46,9 @@ SCAN_TMA_ITEMS = int(os.environ.get("GRUMPY_SCAN_ITEMS", "16"))
 SCAN_TMA_ROUND = os.environ.get("GRUMPY_SCAN_ROUND", "1") == "1"
 # the aggregates of a round combined as a warp tree (not a left fold)
 SCAN_TMA_TREE = os.environ.get("GRUMPY_SCAN_TREE", "1") == "1"
+# the register-staged kernel with the same look-back (static round-robin
+# tiles over its persistent grid); off: dynamic claims + nearest-prefix walk
+SCAN_REG_ROUNDS = os.environ.get("GRUMPY_SCAN_REG_ROUNDS", "1") == "1"
 
 
 def generate(region: Region, kname="gr_region") -> KernelSource:
@@ -333,6 +336,37 @@ def _gen_lookback(region, s, x, rop, kname, segments=False) -> KernelSource:
     # residency: two shared tiles per CTA; cap registers so the shared memory,
     # not the register file, sets the CTAs per SM
     minb = max(1, min(int(os.environ.get("GRUMPY_SCAN_MINB", "8")), (227 * 1024) // (2 * TP * T.itemsize + 1024)))
+    REG_ROUNDS_C = "true" if SCAN_REG_ROUNDS else "false"
+    if SCAN_REG_ROUNDS:
+        # static round-robin tiles over the persistent grid (every CTA
+        # resident) and the look-back by rounds with a warp tree, as in the
+        # TMA kernel (gr::round_tree)
+        ls_expr = f"(t / {TPL}LL) * {TPL}LL"
+        lookback = f'''      {ct} pre;
+      if (t % {TPL}LL == 0) {{ pre = {seedv}; own = tagg[i & 1]; }}
+      else {{
+        const {ct} tree = gr::round_tree<{op}, {ct}>(aggs, t, (int)gridDim.x, {ls_expr}, {ident});
+        pre = t - (long long)gridDim.x < {ls_expr} ? tree : {comb}<{ct}>(own, tree);
+        own = {comb}<{ct}>(pre, tagg[i & 1]);
+      }}'''
+        first_tile = f"  t = blockIdx.x < {ntiles}LL ? (long long)blockIdx.x : -1;"
+        next_tile = f"    const long long tn = t + gridDim.x < {ntiles}LL ? t + gridDim.x : -1;"
+    else:
+        # dynamic tile claims and the nearest-published-prefix walk
+        # (gr::tile_lookback); a seed (streamed carry) joins tile 0: its
+        # inclusive prefix is seed (+) aggregate, its exclusive prefix the seed
+        lookback = f'''      const {ct} pre0 = gr::tile_lookback<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? {comb}<{ct}>({seedv}, tagg[i & 1]) : tagg[i & 1], {ident}, (t / {TPL}LL) * {TPL}LL);
+      const {ct} pre = {seeded} && t == 0 ? {seedv} : pre0;'''
+        first_tile = f'''  {{
+    if (threadIdx.x == 0) next_id = (long long)atomicAdd(counter, 1ull);
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+    t = next_id < {ntiles}LL ? next_id : -1;
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+  }}'''
+        next_tile = f'''    if (threadIdx.x == 0) next_id = (long long)atomicAdd(counter, 1ull);
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+    const long long tn = next_id < {ntiles}LL ? next_id : -1;
+    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");'''
     kern = f'''extern "C" __global__ void __launch_bounds__({NTH}, {minb}) {kname}(const K::Params p) {{
   // warps 0..{TILE_THREADS // 32 - 1}: data (load, tile-local scan, store) over two shared tiles;
   // warp {TILE_THREADS // 32}: look-back — tile i's prefix is resolved while the data warps
@@ -349,6 +383,8 @@ def _gen_lookback(region, s, x, rop, kname, segments=False) -> KernelSource:
   unsigned long long* incs = aggs + {ntiles * SW}LL;            // tile inclusive prefixes
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (w == {TILE_THREADS // 32}) {{
+    {ct} own = {ident};   // rounds: this CTA's inclusive prefix of its previous tile
+    (void)own;
     for (int i = 0;; ++i) {{
 #ifdef GR_SCAN_STATS
       const long long cw = clock64();
@@ -359,10 +395,7 @@ def _gen_lookback(region, s, x, rop, kname, segments=False) -> KernelSource:
 #endif
       const long long t = tids[i & 1];
       if (t < 0) break;
-      // a seed (streamed carry) joins tile 0: its inclusive prefix is
-      // seed (+) aggregate, its exclusive prefix the seed
-      const {ct} pre0 = gr::tile_lookback<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? {comb}<{ct}>({seedv}, tagg[i & 1]) : tagg[i & 1], {ident}, (t / {TPL}LL) * {TPL}LL);
-      const {ct} pre = {seeded} && t == 0 ? {seedv} : pre0;
+{lookback}
       if (lane == 0) tpre[i & 1] = pre;
       asm volatile("bar.arrive 3, {NTH};" ::: "memory");
     }}
@@ -370,21 +403,13 @@ def _gen_lookback(region, s, x, rop, kname, segments=False) -> KernelSource:
   }}
   // ---- data warps
   long long t;
-  {{
-    if (threadIdx.x == 0) next_id = (long long)atomicAdd(counter, 1ull);
-    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
-    t = next_id < {ntiles}LL ? next_id : -1;
-    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
-  }}
+{first_tile}
   int b = 0;
   if (t >= 0) K::stage(p, t, bufs, wsum[0], &tagg[0], &tids[0], aggs, lane, w);
   else if (threadIdx.x == 0) tids[0] = -1;
   asm volatile("bar.arrive 2, {NTH};" ::: "memory");
   while (t >= 0) {{
-    if (threadIdx.x == 0) next_id = (long long)atomicAdd(counter, 1ull);
-    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
-    const long long tn = next_id < {ntiles}LL ? next_id : -1;
-    asm volatile("bar.sync 1, {TILE_THREADS};" ::: "memory");
+{next_tile}
     if (tn >= 0) K::stage(p, tn, bufs + (b ^ 1) * {TP}LL, wsum[b ^ 1], &tagg[b ^ 1], &tids[b ^ 1], aggs, lane, w);
     asm volatile("bar.sync 3, {NTH};" ::: "memory");
     // tile t: prefix (+) tile-local inclusive scan, coalesced stores
@@ -436,6 +461,7 @@ def _gen_lookback(region, s, x, rop, kname, segments=False) -> KernelSource:
              "  if (threadIdx.x == 0) {",
              f"    {ct} acc = ws[0];",
              f"    for (int i = 1; i < {TILE_THREADS // 32}; ++i) {{ acc = {comb}<{ct}>(acc, ws[i]); ws[i] = acc; }}",
+             f"    if ({seeded} && {REG_ROUNDS_C} && t == 0) acc = {comb}<{ct}>({seedv}, acc);   // rounds: tile 0's aggregate carries the seed",
              "    *agg_s = acc;",
              "    *tid_s = t;",
              f"    gr::stat_put<{ct}>(aggs, t, acc);",

@@ -217,12 +217,13 @@ def test_scan_tma_matches_register_staged(sess, monkeypatch, n, kind, tree):
     types, sums and max; lengths that are not a multiple of the tile
     (zero-filled last box) or of the 128-byte line (the tail elements loaded
     and stored by their threads).  With the left fold of a round's aggregates
-    (tree=False) the association is the register-staged kernel's: bits
-    identical.  With the warp tree (the default) integers and max are still
+    (tree=False) the association is that of the register-staged kernel's
+    nearest-prefix walk: bits identical.  With the warp tree (the default) integers and max are still
     identical and float sums stay within the 1-D scan's reassociation bound,
     the same bits on every run."""
     from paper_1901_03771_b200 import codegen, codegen_scan
     monkeypatch.setattr(codegen_scan, "SCAN_TMA_TREE", tree)
+    monkeypatch.setattr(codegen_scan, "SCAN_REG_ROUNDS", tree)     # left fold: the nearest-prefix walk
     rng = np.random.default_rng([n, len(kind)])
     if kind == "i64":
         xs = [rng.integers(-1000, 1000, n)]

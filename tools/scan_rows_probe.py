@@ -30,4 +30,9 @@ for _ in range(3):
     y = gp.cumsum(x * 0.5 + 1.0)
     gp.force(y)
 print("2^28+7", sess.executor.last_steps[-1].cache["ks"].meta.get("label"), flush=True)
+x2 = gp.asarray(np.random.default_rng(3).standard_normal((16384, 16384), dtype=np.float32))
+for _ in range(3):
+    y = gp.cumsum(x2 * 0.5 + 1.0)          # flattened (axis=None) scan of a matrix
+    gp.force(y)
+print("16384x16384 flat", sess.executor.last_steps[-1].cache["ks"].meta.get("label"), flush=True)
 
