@@ -64,9 +64,10 @@ def generate(region: Region, kname="gr_region") -> KernelSource:
             raise NotFusable(n, "reductions before a scan run as their own step")
     if axis is None or len(x.shape) == 1:
         n = element_count(x.shape)
-        if SCAN_TMA and len(x.shape) == 1 and n >= SCAN_TMA_MIN:
+        if SCAN_TMA and n >= SCAN_TMA_MIN:
             try:
-                ks = _gen_lookback_tma(region, s, x, rop, kname)
+                # an n-D operand is scanned in its flat row-major order
+                ks = _gen_lookback_tma(region, s, x, rop, kname, flat=len(x.shape) > 1)
                 if ks is not None:
                     return ks
             except NotFusable:
@@ -489,10 +490,15 @@ class _StagedEmitter(LoopEmitter):
     """Loop emitter whose staged leaves are read from a swizzled shared-memory
     tile (16-byte chunks, gr::lds_sw) instead of global memory."""
 
-    def __init__(self, region, staged, tvars):
+    def __init__(self, region, staged, tvars, flat=None):
         super().__init__(region, vec_loads=True)
         self.staged = staged      # leaf id -> name of the tile's base pointer
         self.tvars = tvars        # [(var, coef)]: the tile's first element = sum(coef * var)
+        # flat scans of an n-D operand: (the operand's row-major offset of the
+        # element, its offset within the tile without the vector lane, the
+        # vector-lane loop variable); a staged leaf read at exactly that
+        # offset is the tile's element
+        self.flat = flat
 
     def load_leaf(self, leaf, off):
         sym = self.staged.get(leaf.id)
@@ -500,6 +506,11 @@ class _StagedEmitter(LoopEmitter):
             if off.level >= 2:
                 raise NotFusable(leaf, "unstaged leaf read per element")
             return super().load_leaf(leaf, off)
+        if self.flat is not None:
+            expect, rel, vv, trip = self.flat
+            if off.key() != expect.key():
+                raise NotFusable(leaf, "staged leaf read off the tile")
+            return self._staged_vec(leaf, sym, rel, vv, trip)
         lvl = off.level
         sc = self.stack[lvl] if lvl >= 2 else None
         if sc is None or sc.kind != "for" or not sc.unroll or sc.var is None or off.coef(sc.var) != 1:
@@ -510,20 +521,26 @@ class _StagedEmitter(LoopEmitter):
         rel = rest
         for tv, _ in self.tvars:
             rel = rel.without(tv)
+        return self._staged_vec(leaf, sym, rel, sc.var, sc.trip)
+
+    def _staged_vec(self, leaf, sym, rel, vv, trip):
+        """The staged leaf's vector at tile offset ``rel`` (one 16-byte chunk,
+        loaded once per chunk), indexed by the vector-lane loop ``vv``."""
+        lvl = vv.level
         key = ("svec", leaf.id, rel.key())
         hit = self.memo.get(key)
         if hit is not None and (hit[1] == 0 or (hit[1] < len(self.stack) and self.stack[hit[1]] is hit[2])):
-            return f"{hit[0]}[{sc.var.name}]", lvl
+            return f"{hit[0]}[{vv.name}]", lvl
         T = leaf.dtype.ctype
         name = self.fresh("L")
         plvl = max(rel.level, 1)
-        self.stmt(plvl, f"{T} {name}[{sc.trip}];")
-        self.stmt(plvl, f"gr::lds_sw<{T}, {sc.trip}>({name}, {sym}, (unsigned){rel.c()});")
+        self.stmt(plvl, f"{T} {name}[{trip}];")
+        self.stmt(plvl, f"gr::lds_sw<{T}, {trip}>({name}, {sym}, (unsigned){rel.c()});")
         self.memo[key] = (name, plvl, self.stack[plvl] if plvl > 0 else None)
-        return f"{name}[{sc.var.name}]", lvl
+        return f"{name}[{vv.name}]", lvl
 
 
-def _gen_lookback_tma(region, s, x, rop, kname):
+def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
     """Single-pass look-back scan fed by TMA (sm_100a).
 
     A producer warp streams each input leaf's 32 KB tile into a ring of
@@ -565,14 +582,15 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     TPB = 512 if isz == 4 else 256
     ITEMS = SCAN_TMA_ITEMS                # elements per data thread (16: 32 KB tiles, 32: 64 KB)
     tile = TPB * ITEMS
-    if N % W and (len(x.shape) > 1 or NM < 2 * tile):
+    segmented = len(x.shape) > 1 and not flat
+    if N % W and (segmented or NM < 2 * tile):
         return None
     # segments: a scan along the last axis of a matrix is one scan per line;
     # lines made of whole tiles keep every tile inside one line
-    seg = x.shape[-1] if len(x.shape) > 1 else N
-    if seg % tile and len(x.shape) > 1:
+    seg = x.shape[-1] if segmented else N
+    if seg % tile and segmented:
         return None
-    TPL = seg // tile if len(x.shape) > 1 else -(-N // tile)     # tiles per segment
+    TPL = seg // tile if segmented else -(-N // tile)     # tiles per segment
     tile_b = tile * isz                  # 32 KB
     rows = tile // W                     # 128-byte lines per tile
     box = min(rows, 256)                 # TMA box: at most 256 lines (32 KB)
@@ -598,6 +616,9 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     if len(x.shape) == 1:
         em = _StagedEmitter(region, {l.id: f"sg{k}" for k, l in enumerate(staged)}, [(tb, 1)])
         tile_coords = lambda e_: [Aff.of(tb) + e_]        # noqa: E731
+    elif flat:
+        em = _StagedEmitter(region, {l.id: f"sg{k}" for k, l in enumerate(staged)}, [])
+        tile_coords = None
     else:
         # the tile's line and first column; the line's kept coordinates
         tln, tkb = Var("tln", 1), Var("tkb", 1, align=tile)
@@ -618,6 +639,16 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     j, sj, a = em.open(1, "for", trip=ITEMS // vec, unroll=True)
     v, sv, b = em.open(j.level, "for", trip=vec, unroll=True)
     e = Aff.of(tt).scale(ITEMS) + Aff.of(j).scale(vec) + Aff.of(v)
+    if tile_coords is None:
+        # flat order of an n-D operand: its coordinates from the flat index;
+        # identity-mapped contiguous leaves are read at exactly the operand's
+        # row-major offset, i.e. the tile's element
+        coords = _flat_coords(em, x.shape, Aff.of(tb) + e, v)
+        expect = Aff.of(0)
+        for c, sd in zip(coords, row_major_strides(x.shape)):
+            expect = expect + c.scale(sd)
+        em.flat = (expect, Aff.of(tt).scale(ITEMS) + Aff.of(j).scale(vec), v, vec)
+        tile_coords = lambda e_: coords     # noqa: E731
     val = em.cast(em.value(x, tile_coords(e)), x.dtype, T)
     em.stmt(v.level, f"vals[{vec} * {j.name} + {v.name}] = {val[0]};")
     em.close(sv, b)
@@ -625,7 +656,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     args = "".join(f", const unsigned char* sg{k}" for k in range(NL))
     items = [f"static __device__ __forceinline__ void items(const Params& p, const long long tb{args}, {ct} (&vals)[{ITEMS}]) {{",
              "  const long long tt = threadIdx.x; (void)tb;"]
-    if len(x.shape) > 1:
+    if segmented:
         items.append(f"  const long long tln = tb / {seg}LL, tkb = tb % {seg}LL;")
     items += ["  " + c for c in em.consts]
     items += render(em.row, 1)
@@ -639,7 +670,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
         # the tail's mapped values straight from global memory
         te = LoopEmitter(region)
         ix = Var("ix", 1)
-        tv = te.cast(te.value(x, [Aff.of(ix)]), x.dtype, T)
+        tv = te.cast(te.value(x, _flat_coords(te, x.shape, Aff.of(ix), ix)), x.dtype, T)
         tail_fn = [f"static __device__ __forceinline__ {ct} tail_value(const Params& p, const long long ix) {{"]
         tail_fn += ["  " + c for c in te.consts] + render(te.row, 1) + [f"  return {tv[0]};", "}"]
         tail_load = f'''    if (t == {ntiles - 1}LL) {{
@@ -663,7 +694,7 @@ def _gen_lookback_tma(region, s, x, rop, kname):
     LAG = min(SCAN_TMA_LAG, S_ - 2)       # tiles waiting for their prefix
     NLW = SCAN_TMA_LBW                    # look-back warps
     rounds = SCAN_TMA_ROUND
-    if len(x.shape) > 1 and not rounds:
+    if segmented and not rounds:
         return None                      # segments need the look-back by rounds
     ls_expr = f"(t / {TPL}LL) * {TPL}LL"
     if rounds and SCAN_TMA_TREE:

@@ -61,6 +61,41 @@ def test_scan_rows_contiguous_axis(sess, shape, kind):
     assert np.array_equal(out, ref, equal_nan=kind not in ("i64", "i32"))
 
 
+@pytest.mark.parametrize("case", ["f32", "f64-3d", "i64", "tail", "rowvec", "transposed"])
+def test_scan_flat_nd(sess, case):
+    """cumsum of an n-D operand without an axis scans its flat row-major
+    order: identity-mapped contiguous leaves are staged by TMA like a 1-D
+    scan (tail past the last 128-byte line included); broadcast or
+    transposed leaves fall back to the register-staged kernel.  Integers
+    exact, floats within the 1-D scan's bound."""
+    rng = np.random.default_rng(len(case))
+    shape = {"f64-3d": (4, 512, 1001), "tail": (1025, 1031)}.get(case, (1024, 1500))
+    if case == "i64":
+        a, b = rng.integers(-50, 50, shape), rng.integers(-3, 3, shape)
+    else:
+        dt = np.float64 if case == "f64-3d" else np.float32
+        a, b = rng.standard_normal(shape).astype(dt), rng.standard_normal(shape).astype(dt)
+    ga, gb = gp.asarray(a), gp.asarray(b)
+    if case == "rowvec":
+        c = rng.standard_normal(shape[-1]).astype(np.float32)
+        got, t = gp.cumsum(ga + gp.asarray(c)), a + c
+    elif case == "transposed":
+        bt = np.ascontiguousarray(b.T)
+        got, t = gp.cumsum(ga * gp.asarray(bt).T), a * bt.T
+    else:
+        got, t = gp.cumsum(ga * gb + 1), a * b + 1
+    out = np.asarray(got)
+    label = sess.executor.last_steps[-1].cache["ks"].meta.get("label")
+    assert label == ("scan-lookback" if case in ("rowvec", "transposed") else "scan-tma")
+    if case == "i64":
+        assert np.array_equal(out, np.cumsum(t))
+        return
+    ref = np.cumsum(t.astype(np.float64))
+    bound = np.cumsum(np.abs(t.astype(np.float64)))
+    tiles = -(-t.size // (8192 if t.dtype == np.float32 else 4096))
+    assert np.all(np.abs(out - ref) <= (tiles + 32) * np.finfo(t.dtype).eps * bound)
+
+
 @pytest.mark.parametrize("view", ["T", "step", "cols", "big-T"])
 def test_scan_last_axis_of_views(sess, view):
     """Scans along the last axis of transposed / strided / column-sliced views
