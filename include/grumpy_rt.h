@@ -132,6 +132,12 @@ int grumpy_rt_launch(uint64_t fn, unsigned gx, unsigned gy, unsigned gz,
 /* Waits for all work of the runtime's context (every stream). */
 int grumpy_rt_sync(void);
 
+/* ---- profiler ranges (NVTX 3) ----------------------------------------------
+ * Named, nestable ranges around plan steps for Nsight Systems / Compute
+ * (SURVEY.md §5 tracing); no-ops unless a tool injects itself. */
+int grumpy_rt_range_push(const char* name);
+int grumpy_rt_range_pop(void);
+
 /* ---- streams: copy/compute overlap for streamed materialisation ---------
  * Async work (launch, h2d, d2h_async, d2d, memset, event_record, gemm, NCCL)
  * goes to the "current" stream: the runtime's own stream unless

@@ -294,6 +294,10 @@ class ValueEmitter:
     def load_leaf(self, leaf: Node, offset: Aff) -> Tuple[str, int]:
         raise NotImplementedError
 
+    def bounds_exempt(self, leaf: Node) -> bool:
+        """Leaves not read from global memory at ``offset`` (staged copies)."""
+        return False
+
     # -- shared
     def const(self, value, dtype: DType) -> Tuple[str, int]:
         key = (value, dtype)
@@ -325,6 +329,11 @@ class ValueEmitter:
             for c, s, ext in zip(coords, st, n.shape):
                 if ext != 1:
                     off = off + c.scale(s)
+            if DEBUG_BOUNDS and not self.bounds_exempt(n):
+                # debug runs: every leaf read checked against its extent
+                # (SPEC.md:286, 314); a violation prints and traps
+                self.emit(off.level, "bool", f"gr::bounds_ok((long long)({off.c()}), {element_count(n.shape)}LL, "
+                                              f"{self.leaf_index[n.id]})")
             return self.load_leaf(n, off)
         k = n.op.kind
         if k is OpKind.MAP:
@@ -716,6 +725,8 @@ CONTRACT = os.environ.get("GRUMPY_CONTRACT", "1") == "1"
 # inexact f32 regions also divide with div.full.f32 (2 ulp) and take square
 # roots with sqrt.approx.f32 (the same choice in the packed body and the tail)
 FAST_DIV = os.environ.get("GRUMPY_FAST_DIV", "1") == "1"
+# debug runs: bounds-check every leaf read in generated kernels
+DEBUG_BOUNDS = os.environ.get("GRUMPY_DEBUG_BOUNDS", "0") == "1"
 # ptxas's own FFMA2 contraction of the packed body (with the tail run through
 # the same body): measured 1.054 vs 1.078 ms on Black-Scholes f32, but which
 # product ptxas fuses in a*b - c*d follows the emission order, which differs
@@ -973,7 +984,7 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
     # ---- group body (vectorised); f32 regions evaluate lane pairs packed
     pair = False
     packed_tail = False
-    if vec % 2 == 0 and os.environ.get("GRUMPY_PAIR", "1") != "0":
+    if vec % 2 == 0 and os.environ.get("GRUMPY_PAIR", "1") != "0" and not DEBUG_BOUNDS:
         try:
             if PTXAS_CONTRACT and CONTRACT and inexact_region(region) and (tail == 0 or rank == 1):
                 # ptxas contraction, provided the tail (if any) can run this
@@ -1022,7 +1033,7 @@ def gen_map(region: Region, kname="gr_region", unroll=None, block=256) -> Kernel
     fast_fn = []
     if unroll == 1 and vec > 1 and any(n_.kind is OpKind.SLICE_ASSIGN for n_ in region.nodes):
         fem = fouts = None
-        for fpair in ((True, False) if vec % 2 == 0 and os.environ.get("GRUMPY_PAIR", "1") != "0" else (False,)):
+        for fpair in ((True, False) if vec % 2 == 0 and os.environ.get("GRUMPY_PAIR", "1") != "0" and not DEBUG_BOUNDS else (False,)):
             try:
                 fem, fouts = build("group", pair=fpair, fast=True)
                 fp = fpair

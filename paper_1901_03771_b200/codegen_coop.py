@@ -391,6 +391,9 @@ def try_generate(region: Region, kname="gr_region") -> Optional[KernelSource]:
 
 
 COOP_PAIR = os.environ.get("GRUMPY_COOP_PAIR", "1") == "1"
+# debug bounds checks run the unpaired element loops
+if os.environ.get("GRUMPY_DEBUG_BOUNDS", "0") == "1":
+    COOP_PAIR = False
 COOP_BLOCKED_TOTAL = os.environ.get("GRUMPY_COOP_BLOCKED_TOTAL", "0") == "1"
 TOT_BLOCK = 4096          # rows per first-level block of a cooperative kernel's total
 COOP_BLOCK = int(os.environ.get("GRUMPY_COOP_BLOCK", "256"))

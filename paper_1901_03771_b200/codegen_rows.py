@@ -960,6 +960,9 @@ def gen_rows(region: Region, kname="gr_region", block=128) -> KernelSource:
 # 4.14 ms (254 regs, refused now); pairs from a pair-adjacent smem copy
 # 2.99 ms; pair-adjacent constant bank 2.41 ms (profiles/r01s2_kmeans_variants.md).
 PAIR_LOOPS = os.environ.get("GRUMPY_PAIR_LOOPS", "1") == "1"
+# debug bounds checks run the unpaired element loops
+if os.environ.get("GRUMPY_DEBUG_BOUNDS", "0") == "1":
+    PAIR_LOOPS = False
 
 
 def _gen_rows(region: Region, kname, block, cbank, pair=False) -> KernelSource:

@@ -500,6 +500,11 @@ class _StagedEmitter(LoopEmitter):
         # offset is the tile's element
         self.flat = flat
 
+    def bounds_exempt(self, leaf):
+        # staged leaves come from the TMA tile (out-of-range lanes of the
+        # last tile read zero fill, never global memory)
+        return leaf.id in self.staged
+
     def load_leaf(self, leaf, off):
         sym = self.staged.get(leaf.id)
         if sym is None:

@@ -18,6 +18,7 @@
 #include <cublas_v2.h>
 #include <dlfcn.h>
 #include <nvrtc.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <chrono>
 #include <cstdio>
@@ -722,6 +723,17 @@ int grumpy_rt_sync(void) {
   int r = need_init();
   if (r) return r;
   CU_CHECK(D.p_cuCtxSynchronize(), "cuCtxSynchronize");
+  return GR_OK;
+}
+
+// ---- profiler ranges ----------------------------------------------------------
+int grumpy_rt_range_push(const char* name) {
+  nvtxRangePushA(name ? name : "");
+  return GR_OK;
+}
+
+int grumpy_rt_range_pop(void) {
+  nvtxRangePop();
   return GR_OK;
 }
 

@@ -255,6 +255,16 @@ __device__ __forceinline__ float sqrt_(float a) { return sqrtf(a); }  // IEEE (p
 // slow path) and the MUFU square root (sqrt.approx.f32, ~1 ulp, subnormals
 // kept) — error of the same class as the libm transcendentals the region
 // already carries
+// Debug runs (GRUMPY_DEBUG_BOUNDS=1): a leaf read outside [0, n) prints the
+// leaf slot and offset and traps ("bounds-checked in debug runs").
+__device__ __noinline__ bool bounds_ok(long long off, long long n, int leaf) {
+  if ((unsigned long long)off >= (unsigned long long)n) {
+    printf("grumpy: leaf %d read at %lld, outside [0, %lld)\n", leaf, off, n);
+    __trap();
+  }
+  return true;
+}
+
 __device__ __forceinline__ float div_full(float a, float b) {
   float r;
   asm("div.full.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));

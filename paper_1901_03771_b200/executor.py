@@ -24,6 +24,8 @@ from .tensor import DType, TensorBuffer, element_count
 
 
 PRECOMPILE = os.environ.get("GRUMPY_PRECOMPILE", "1") == "1"
+# NVTX ranges around every plan step (kind, kernel family or library call)
+NVTX = os.environ.get("GRUMPY_NVTX", "0") == "1"
 
 
 class Executor:
@@ -57,7 +59,6 @@ class Executor:
     # -- steps ------------------------------------------------------------------------
     def run(self, steps: List[PlanStep], dist=None, comm=None):
         self.last_steps = steps
-        g = self.session.graph
         cold = [st for st in steps if st.kind == "Fused" and "kernel" not in st.cache]
         if len(cold) >= 2 and PRECOMPILE:
             # JIT/execute pipelining: generate every uncompiled step's source
@@ -70,24 +71,41 @@ class Executor:
                     srcs.append(st.cache["ks"].source)
             self.rt.precompile(srcs)
         for st in steps:
-            if st.kind == "Library":
-                if self.profile is not None:
-                    e0, e1 = self._event_pair()
-                    self.rt.record(e0)
-                    outs = [self.run_library(st)]
-                    self.rt.record(e1)
-                    label = st.call + (f"+{st.epilogue[0]}" if st.epilogue else "")
-                    self.profile.append(("library", label, e0, e1))
-                else:
-                    outs = [self.run_library(st)]
-                self.session.stats.library_calls += 1
+            if NVTX:
+                self.rt.range_push(self._step_name(st))
+            try:
+                self._run_step(st, dist, comm)
+            finally:
+                if NVTX:
+                    self.rt.range_pop()
+
+    @staticmethod
+    def _step_name(st: PlanStep) -> str:
+        if st.kind == "Library":
+            return "grumpy:" + st.call
+        ks = st.cache.get("ks")     # generated source (prepared by run()'s precompile or earlier runs)
+        return "grumpy:" + (ks.meta.get("label") or ks.family if ks is not None else "fused")
+
+    def _run_step(self, st: PlanStep, dist, comm):
+        g = self.session.graph
+        if st.kind == "Library":
+            if self.profile is not None:
+                e0, e1 = self._event_pair()
+                self.rt.record(e0)
+                outs = [self.run_library(st)]
+                self.rt.record(e1)
+                label = st.call + (f"+{st.epilogue[0]}" if st.epilogue else "")
+                self.profile.append(("library", label, e0, e1))
             else:
-                outs = self.run_fused(st)
-            if dist is not None:
-                self._combine_partials(st.roots, outs, dist, comm)
-            for r, b in zip(st.roots, outs):
-                g.mark_materialized(r, b)
-            self.session.stats.nodes_materialized += len(st.roots)
+                outs = [self.run_library(st)]
+            self.session.stats.library_calls += 1
+        else:
+            outs = self.run_fused(st)
+        if dist is not None:
+            self._combine_partials(st.roots, outs, dist, comm)
+        for r, b in zip(st.roots, outs):
+            g.mark_materialized(r, b)
+        self.session.stats.nodes_materialized += len(st.roots)
 
     def _combine_partials(self, roots, outs, dist, comm):
         """Allreduce partial roots in place on the runtime stream (NCCL), right

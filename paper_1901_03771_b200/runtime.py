@@ -74,6 +74,8 @@ SIGNATURES = {
     "grumpy_rt_launch": [_u64, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint,
                          ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, ctypes.c_uint, _p, _sz],
     "grumpy_rt_sync": [],
+    "grumpy_rt_range_push": [_cp],
+    "grumpy_rt_range_pop": [],
     "grumpy_rt_stream_create": [_u64p],
     "grumpy_rt_stream_destroy": [_u64],
     "grumpy_rt_set_stream": [_u64],
@@ -274,6 +276,13 @@ class Runtime:
 
     def sync(self):
         _check(self.lib.grumpy_rt_sync())
+
+    def range_push(self, name: str):
+        """NVTX range around host-side work (Nsight Systems / Compute)."""
+        _check(self.lib.grumpy_rt_range_push(name.encode()))
+
+    def range_pop(self):
+        _check(self.lib.grumpy_rt_range_pop())
 
     def function(self, k: "Kernel", name: str) -> "Kernel":
         """Another kernel of ``k``'s module (e.g. a leaf repack kernel)."""

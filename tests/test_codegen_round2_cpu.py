@@ -154,3 +154,29 @@ def test_scan_few_long_lines_segmented(shape, label, tiles):
     tpl = -(-shape[-1] // 8192)
     assert f"(t / {tpl}LL) * {tpl}LL" in ks.source
     runtime.compile_cubin(ks.source)
+
+
+def test_debug_bounds_checks_every_family(monkeypatch):
+    """GRUMPY_DEBUG_BOUNDS=1: every leaf read of the
+    generated kernels goes through gr::bounds_ok (print + trap); the sources
+    still compile.  Staged TMA tiles are exempt (they read zero fill, not
+    global memory)."""
+    from paper_1901_03771_b200 import codegen_coop
+    monkeypatch.setattr(codegen, "DEBUG_BOUNDS", True)
+    monkeypatch.setattr(codegen_coop, "COOP_PAIR", False)
+    monkeypatch.setattr(codegen_rows, "PAIR_LOOPS", False)
+    monkeypatch.setattr(codegen, "_GEN_CACHE", {})
+    S, X, T = wl.blackscholes_inputs(n=(1 << 12) + 3)
+    (x,) = wl.rownorm_inputs(rows=64, cols=4096)
+    P, C = wl.kmeans_inputs(n=1 << 12)
+    lab, sums, cnt = wl.kmeans_partials(gp, gp.asarray(P), gp.asarray(C))
+    a = gp.asarray(np.ones((256, 256), np.float32))
+    progs = [list(wl.blackscholes(gp, *map(gp.asarray, (S, X, T)))), list(wl.rownorm(gp, gp.asarray(x))),
+             [lab] + sums + [cnt], [a.T + a], [gp.cumsum(a, axis=1)]]
+    for roots in progs:
+        ks = _source(roots)
+        assert "gr::bounds_ok(" in ks.source, ks.family
+        runtime.compile_cubin(ks.source)
+    tma = _source([gp.cumsum(gp.asarray(np.ones(1 << 21, np.float32)) * 2)])
+    assert tma.meta["label"] == "scan-tma" and "gr::bounds_ok(" not in tma.source
+
