@@ -774,7 +774,9 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
   __shared__ {ct} wsum[2][{NW}];
   __shared__ long long mb_tid[{M}];
   __shared__ {ct} mb_agg[{M}], mb_pre[{M}];
-  __shared__ volatile int mb_pub[{M}], mb_done[{M}];
+  // mailbox slot m carries iterations m, m + {M}, ...: its k-th use is phase
+  // k of mb_pub[m] (tile published) and mb_done[m] (prefix ready)
+  __shared__ unsigned long long mb_pub[{M}], mb_done[{M}];
   __shared__ gr::LookbackBuf<{ct}> lbw[{NLW}];
   __shared__ volatile {ct} own_v;
   __shared__ volatile int own_seq;
@@ -783,7 +785,7 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {{
     for (int i = 0; i < {S_}; ++i) {{ gr::mbar_init(&full[i], 1); gr::mbar_init(&empty[i], 1); }}
-    for (int i = 0; i < {M}; ++i) {{ mb_pub[i] = 0; mb_done[i] = 0; }}
+    for (int i = 0; i < {M}; ++i) {{ gr::mbar_init(&mb_pub[i], 1); gr::mbar_init(&mb_done[i], 1); }}
     own_seq = 0;
     gr::fence_mbar_init();
   }}
@@ -814,8 +816,7 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
 #ifdef GR_SCAN_STATS
       const long long cw = clock64();
 #endif
-      while (mb_pub[m] != i + 1) {{ }}
-      __threadfence_block();
+      gr::mbar_wait(&mb_pub[m], (i / {M}) & 1);
 #ifdef GR_SCAN_STATS
       if (lane == 0 && blockIdx.x == 0) {{ if (i == 0) {{ gr::gr_scan_stats[4] = gr::gr_scan_stats[5] = gr::gr_scan_stats[6] = gr::gr_scan_stats[7] = 0; gr::gr_scan_stats[3] = clock64(); }}
                                           else gr::gr_scan_stats[7] += clock64() - cw; }}
@@ -832,7 +833,7 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
         break;
       }}
 {lb_call}
-      if (lane == 0) {{ mb_pre[m] = pre; __threadfence_block(); mb_done[m] = i + 1; }}
+      if (lane == 0) {{ mb_pre[m] = pre; gr::mbar_arrive(&mb_done[m]); }}
       __syncwarp();
     }}
     return;
@@ -844,7 +845,7 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
     // tile of iteration j: prefix (+) its tile-local scan (waiting in its
     // stage), back into the stage, one TMA store
     const int m = j % {M};
-    if (threadIdx.x == 0) {{ while (mb_done[m] != j + 1) {{ }} __threadfence_block(); }}
+    if (threadIdx.x == 0) gr::mbar_wait(&mb_done[m], (j / {M}) & 1);
     asm volatile("bar.sync 1, {TPB};" ::: "memory");
     const {ct} pre = mb_pre[m];
     unsigned char* ob = ring + (long long)(j % {S_}) * {NL * tile_b};
@@ -875,7 +876,7 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
     const long long t = stid[s];
     if (t < 0) {{
       if (threadIdx.x == 0) {{
-        for (int e = 0; e < {NLW}; ++e) {{ mb_tid[(i + e) % {M}] = -1; __threadfence_block(); mb_pub[(i + e) % {M}] = i + e + 1; }}
+        for (int e = 0; e < {NLW}; ++e) {{ mb_tid[(i + e) % {M}] = -1; gr::mbar_arrive(&mb_pub[(i + e) % {M}]); }}
       }}
       for (int j = (i > {LAG} ? i - {LAG} : 0); j < i; ++j) finalize(j, ptid[j % {LAG + 1}]);
       break;
@@ -903,8 +904,7 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
       const int m = i % {M};
       mb_tid[m] = t;
       mb_agg[m] = agg;
-      __threadfence_block();
-      mb_pub[m] = i + 1;
+      gr::mbar_arrive(&mb_pub[m]);          // release: the waiting look-back warp sees tid and agg
     }}
     asm volatile("bar.sync 1, {TPB};" ::: "memory");
     const {ct} lane_ex = __shfl_up_sync(0xffffffffu, inc, 1);

@@ -86,6 +86,15 @@ def _():
     assert np.array_equal(np.asarray(gp.asarray(xi).cumsum()), xi.cumsum())
     xf = np.random.default_rng(5).standard_normal((33, 70))
     assert np.array_equal(np.asarray(gp.cumsum(gp.asarray(xf) * 2, axis=1)), np.cumsum(xf * 2, axis=1))
+    # TMA ring + round-tree look-back: 1-D with a tail, segmented lines,
+    # flat n-D; register-staged with segments and with a broadcast operand
+    rng = np.random.default_rng(6)
+    for shape, axis in [((1 << 20) + 7, None), ((16, 65536), 1), ((1024, 1024), None), ((16, 70001), 1)]:
+        v = rng.integers(-50, 50, shape)
+        assert np.array_equal(np.asarray(gp.cumsum(gp.asarray(v) * 3, axis=axis)), np.cumsum(v * 3, axis=axis))
+    m = rng.integers(-50, 50, (1024, 1024))
+    r = rng.integers(-5, 5, 1024)
+    assert np.array_equal(np.asarray(gp.cumsum(gp.asarray(m) + gp.asarray(r))), np.cumsum(m + r))
 
 
 @case("stream")
