@@ -348,3 +348,72 @@ def test_seeded_scan(sess, monkeypatch, case):
     label = sess.executor.last_steps[-1].cache["ks"].meta.get("label")
     assert label == {"long-tma": "scan-tma", "long-tma-tail": "scan-tma", "long-f32": "scan-lookback",
                      "long-i64": "scan-lookback"}.get(case, label)
+
+
+def _scan_case(rng, i):
+    """A random scan program: shape, axis, op and dtype chosen to reach every
+    scan kernel (lines, warp-per-lines, segmented TMA / register-staged,
+    flat TMA with and without a tail, 1-D register-staged)."""
+    kind = i % 8
+    if kind == 0:
+        shape, axis = (int(rng.integers(2, 40)), int(rng.integers(2, 300))), 0
+    elif kind == 1:
+        shape, axis = (int(rng.integers(32, 3000)), int(rng.integers(2, 700))), 1
+    elif kind == 2:
+        shape, axis = (int(rng.integers(1, 40)), 8192 * int(rng.integers(4, 40))), -1
+    elif kind == 3:
+        shape, axis = (int(rng.integers(1, 40)), int(rng.integers(20000, 200000))), -1
+    elif kind == 4:
+        shape, axis = (int(rng.integers(300, 1500)), int(rng.integers(700, 3000))), None
+    elif kind == 5:
+        shape, axis = (int(rng.integers(1 << 20, 3 << 20)),), None
+    elif kind == 6:
+        shape, axis = (int(rng.integers(9000, 1 << 20)),), None
+    else:
+        shape, axis = (int(rng.integers(2, 6)), int(rng.integers(2, 9)), int(rng.integers(20000, 90000))), -1
+    dt = [np.float32, np.float64, np.int64, np.int32][int(rng.integers(0, 4))]
+    op = ["sum", "max", "prod"][int(rng.integers(0, 3))] if dt != np.float64 else "sum"
+    return shape, axis, dt, op
+
+
+@pytest.mark.parametrize("i", range(40))
+def test_scan_random_shapes(sess, i):
+    """Randomized scans against NumPy: integers and max exact, sums and
+    products of floats within the look-back's reassociation bound (exact
+    where the kernel keeps NumPy's sequential order)."""
+    rng = np.random.default_rng([7, i])
+    shape, axis, dt, op = _scan_case(rng, i)
+    if np.issubdtype(dt, np.integer):
+        x = rng.integers(-3, 4, shape).astype(dt) if op == "prod" else rng.integers(-100, 100, shape).astype(dt)
+    else:
+        x = (rng.standard_normal(shape) * (0.01 if op == "prod" else 1) + (1 if op == "prod" else 0)).astype(dt)
+    g = gp.asarray(x)
+    if op == "sum":
+        got, ref = gp.cumsum(g, axis=axis), np.cumsum(x, axis=axis)
+    elif op == "prod":
+        got, ref = gp.cumprod(g, axis=axis), np.cumprod(x, axis=axis)
+    else:
+        flat = x.reshape(-1) if axis is None else x
+        got = np.maximum.accumulate(gp.asarray(flat), axis=0 if axis is None else axis)
+        ref = np.maximum.accumulate(flat, axis=0 if axis is None else axis)
+    out = np.asarray(got)
+    assert out.shape == ref.shape and out.dtype == ref.dtype, (out.shape, ref.shape, out.dtype, ref.dtype)
+    label = sess.executor.last_steps[-1].cache["ks"].meta.get("label")
+    if np.issubdtype(dt, np.integer) or op == "max" or label in (None, "scan-rows"):
+        assert np.array_equal(out, ref), (shape, axis, dt, op, label)
+        return
+    w = np.float64 if dt == np.float32 else np.longdouble
+    if op == "sum":
+        wide = np.cumsum(x.astype(w), axis=axis)
+        mag = np.cumsum(np.abs(x).astype(w), axis=axis)
+    else:
+        wide = np.cumprod(x.astype(w), axis=axis)
+        mag = np.abs(wide)
+    n = x.size if axis is None else x.shape[axis]
+    tiles = -(-n // (8192 if dt == np.float32 else 4096))
+    eps = np.finfo(dt).eps
+    # long products reach the subnormal range, where the storage type (as
+    # NumPy's own) keeps only an absolute precision of ~tiny
+    atol = 4 * np.finfo(dt).tiny if op == "prod" else 0.0
+    assert np.all(np.abs(out.astype(w) - wide) <= (tiles + 32) * eps * mag * (4 if op == "prod" else 1) + atol), \
+        (shape, axis, dt, op, label)
