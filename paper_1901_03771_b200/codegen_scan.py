@@ -5,17 +5,20 @@ the mapped values along one axis, a three-phase blocked scan on CPU threads
 (SPEC.md:385); PAPER.md:545-551 (map-scan primitive).  NumPy's accumulate is a
 sequential left fold along the axis (out[k] = out[k-1] ⊕ x[k]).
 
-* scans along an axis with many independent lines: one thread per line, the
-  line folded sequentially — exactly NumPy's association (bit-identical);
-* long 1-D scans (axis=None or a single long line): a single-pass scan with
-  decoupled look-back — 8192-element tiles (a warp-specialised CTA: data warps
-  load, scan and store; one warp resolves the tile prefix), each tile
-  publishes its aggregate and then its inclusive prefix inside 64-bit status
-  words (value and flag in one word: no fences), and ``gr::tile_lookback``
-  folds the aggregates above the nearest published inclusive prefix left to
-  right, so the result does not depend on timing — deterministic; float
-  results within tolerance of NumPy's sequential fold (reassociation),
-  integers exact.
+* scans along an axis with many independent lines keep that order exactly
+  (bit-identical to NumPy): a thread per line when lines are strided
+  (``_gen_lines``), a warp per 16 lines through a padded shared tile when
+  they are contiguous (``_gen_rows_t``);
+* long scans (1-D, flat n-D, or few long lines as segments) run as one
+  single-pass kernel: tiles dealt round-robin over a persistent grid, each
+  tile's aggregate published in a 64-bit status word (value and flag, no
+  fences), and a look-back by rounds — the prefix of tile t is the CTA's own
+  inclusive prefix of tile t - G combined with a warp tree of the G - 1
+  aggregates in between (``gr::round_tree``), so no look-back waits for
+  another.  ``_gen_lookback_tma`` feeds the tiles by TMA through a shared
+  ring (the default); ``_gen_lookback`` stages them through registers for the
+  layouts TMA cannot take.  Deterministic; float results within the
+  reassociation bound of NumPy's sequential fold, integers and max exact.
 """
 
 from __future__ import annotations
