@@ -649,6 +649,16 @@ template <class T> __device__ __forceinline__ T stat_val(const StatRaw<T>& r) {
 #ifdef GR_SCAN_STATS
 __device__ unsigned long long gr_scan_stats[8];
 #endif
+// A look-back waits for other CTAs' tile aggregates; those CTAs are resident
+// by construction (persistent grids sized by the occupancy calculator).  If
+// that ever fails (another tenant holding SMs), fail loudly instead of
+// hanging: ~2^24 polls of an L2 word is seconds, a normal wait microseconds.
+__device__ __forceinline__ void spin_guard(unsigned& polls) {
+  if (++polls == (1u << 24)) {
+    printf("grumpy: scan look-back waited 2^24 polls for a predecessor tile (grid not co-resident?)\n");
+    __trap();
+  }
+}
 // Exclusive prefix of tile `tile` of a single-pass scan; one full warp calls
 // it after the tile's aggregate was published (stat_put(agg, tile, .)), and it
 // publishes the tile's inclusive prefix (stat_put(inc, tile, .)).
@@ -721,7 +731,7 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
     for (int j = 0; j < J; ++j) {
       const long long q = top - lane - 32 * j;
       if (q >= ls && q > fw) {
-        while (!stat_ok<T>(ra[j])) ra[j] = stat_ld<T>(agg, q);
+        for (unsigned polls = 0; !stat_ok<T>(ra[j]); spin_guard(polls)) ra[j] = stat_ld<T>(agg, q);
         lb[tile - 1 - q] = stat_val<T>(ra[j]);
       }
       if (q == fw) base = stat_val<T>(ri[j]);
@@ -775,7 +785,7 @@ __device__ __forceinline__ T tile_lookback_buf(const unsigned long long* agg, un
         const long long q = b0 + lane + 32 * j;
         if (q <= tile - 1) {
           StatRaw<T> r = stat_ld<T>(agg, q);
-          while (!stat_ok<T>(r)) r = stat_ld<T>(agg, q);
+          for (unsigned polls = 0; !stat_ok<T>(r); spin_guard(polls)) r = stat_ld<T>(agg, q);
           lb[lane + 32 * j] = stat_val<T>(r);
         }
       }
@@ -846,7 +856,7 @@ __device__ __forceinline__ void round_stage(const unsigned long long* agg, long 
     for (int j = 0; j < J; ++j) {
       const int k = w0 + lane + 32 * j;
       if (k < n) {
-        while (!stat_ok<T>(ra[j])) ra[j] = stat_ld<T>(agg, lo + k);
+        for (unsigned polls = 0; !stat_ok<T>(ra[j]); spin_guard(polls)) ra[j] = stat_ld<T>(agg, lo + k);
         lb[k] = stat_val<T>(ra[j]);
       } else if (k < n8) {
         lb[k] = pad;
@@ -919,7 +929,7 @@ __device__ __forceinline__ T round_tree(const unsigned long long* agg, long long
     for (int j = 0; j < J; ++j) {
       const int k = w0 + lane + 32 * j;
       if (k < n) {
-        while (!stat_ok<T>(ra[j])) ra[j] = stat_ld<T>(agg, lo + k);
+        for (unsigned polls = 0; !stat_ok<T>(ra[j]); spin_guard(polls)) ra[j] = stat_ld<T>(agg, lo + k);
         acc = Op::template c<T>(acc, stat_val<T>(ra[j]));
       }
     }
