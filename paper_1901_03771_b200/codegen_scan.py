@@ -103,7 +103,10 @@ ROWS_T = os.environ.get("GRUMPY_SCAN_ROWS_T", "1") == "1"
 ROWS_T_CW = int(os.environ.get("GRUMPY_SCAN_ROWS_CW", "64"))       # columns per chunk
 # below this many lines a scan along the last axis whose lines are whole
 # look-back tiles runs as one look-back scan per line (_gen_lookback_tma)
-ROWS_T_MIN_LINES = int(os.environ.get("GRUMPY_SCAN_ROWS_MIN_LINES", str(148 * 16 * 4)))
+# (the warp-per-16-lines kernel keeps one 64-column chunk per line in flight:
+# it needs ~28 warps per SM to stream at full rate — 16384x16384 took 0.95 ms
+# there against 0.34 segmented, 65536x4096 0.41 ms; tools/rows_mid_probe.py)
+ROWS_T_MIN_LINES = int(os.environ.get("GRUMPY_SCAN_ROWS_MIN_LINES", str(148 * 16 * 28)))
 ROWS_T_RPW = int(os.environ.get("GRUMPY_SCAN_ROWS_RPW", "16"))     # lines per warp (16 lanes fold; measured 0.415 vs 0.427 ms for 32)
 ROWS_T_WPB = int(os.environ.get("GRUMPY_SCAN_ROWS_WPB", "1"))      # warps per CTA (1: even spread of the 32-line groups over the SMs)
 
