@@ -713,13 +713,11 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
         # (gr::round_tree) before the CTA's inclusive prefix is needed
         take_own = ("" if NLW == 1 else
                     f"""        if (i > 0) {{
-          if (lane == 0) {{ while (own_seq != i) {{ }} }}
-          __syncwarp();
-          __threadfence_block();
+          gr::mbar_wait(&own_bar, (i - 1) & 1);
           own = own_v;
         }}
 """)
-        give_own = "" if NLW == 1 else "\n      if (lane == 0) { own_v = own; __threadfence_block(); own_seq = i + 1; }"
+        give_own = "" if NLW == 1 else "\n      __syncwarp();   // every lane has read own_v\n      if (lane == 0) { own_v = own; gr::mbar_arrive(&own_bar); }"
         lb_call = f"""      {ct} pre;
       if (t % {TPL}LL == 0) {{
 {take_own}        pre = {seedv}; own = mb_agg[m];
@@ -742,13 +740,11 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
         # CTA's inclusive prefix (own_v, sequence-numbered) for its own fold
         lb_call = f"""      {ct} pre;
       // a segment's first tile has no prefix, but it still takes its turn in
-      // the CTA's sequence of inclusive prefixes (own_seq counts iterations)
+      // the CTA's sequence of inclusive prefixes (own_bar counts iterations)
       const bool s0 = t % {TPL}LL == 0;
       if (!s0) gr::round_stage<{op}, {ct}>(aggs, t, (int)gridDim.x, (t / {TPL}LL) * {TPL}LL, {ident}, lbw[k].v);
       if (i > 0) {{
-        if (lane == 0) {{ while (own_seq != i) {{ }} }}
-        __syncwarp();
-        __threadfence_block();
+        gr::mbar_wait(&own_bar, (i - 1) & 1);
         own = own_v;
       }}
       if (s0) {{ pre = {seedv}; own = mb_agg[m]; }}
@@ -756,7 +752,8 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
         pre = gr::round_fold<{op}, {ct}>(t, (int)gridDim.x, (t / {TPL}LL) * {TPL}LL, own, {ident}, lbw[k].v);
         own = {comb}<{ct}>(pre, mb_agg[m]);
       }}
-      if (lane == 0) {{ own_v = own; __threadfence_block(); own_seq = i + 1; }}"""
+      __syncwarp();   // every lane has read own_v
+      if (lane == 0) {{ own_v = own; gr::mbar_arrive(&own_bar); }}"""
     else:
         lb_call = (f"      const {ct} pre0 = gr::tile_lookback_buf<{op}, {ct}>(aggs, incs, t, {seeded} && t == 0 ? "
                    f"{comb}<{ct}>({seedv}, mb_agg[m]) : mb_agg[m], {ident}, lbw[k].v);\n"
@@ -784,15 +781,17 @@ def _gen_lookback_tma(region, s, x, rop, kname, flat=False):
   // k of mb_pub[m] (tile published) and mb_done[m] (prefix ready)
   __shared__ unsigned long long mb_pub[{M}], mb_done[{M}];
   __shared__ gr::LookbackBuf<{ct}> lbw[{NLW}];
-  __shared__ volatile {ct} own_v;
-  __shared__ volatile int own_seq;
+  // several look-back warps: the CTA's inclusive prefix handed from
+  // iteration i to i + 1 (phase i of own_bar)
+  __shared__ {ct} own_v;
+  __shared__ unsigned long long own_bar;
   unsigned long long* aggs = reinterpret_cast<unsigned long long*>(p.scratch) + 1;
   unsigned long long* incs = aggs + {ntiles * (1 if isz <= 4 else 2)}LL;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   if (threadIdx.x == 0) {{
     for (int i = 0; i < {S_}; ++i) {{ gr::mbar_init(&full[i], 1); gr::mbar_init(&empty[i], 1); }}
     for (int i = 0; i < {M}; ++i) {{ gr::mbar_init(&mb_pub[i], 1); gr::mbar_init(&mb_done[i], 1); }}
-    own_seq = 0;
+    gr::mbar_init(&own_bar, 1);
     gr::fence_mbar_init();
   }}
   __syncthreads();

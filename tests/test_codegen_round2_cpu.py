@@ -90,17 +90,17 @@ def test_scan_tma_generator_builds(monkeypatch):
     assert ks.meta["label"] == "scan-tma"
     assert len(ks.meta["tmaps"]) == 2 and ks.meta["tmaps"][-1][0] == 1     # leaf map + output map
     # look-back by rounds: the round's aggregates as a warp tree, one warp
-    assert "gr::round_tree<" in ks.source and "own_seq != i" not in ks.source
+    assert "gr::round_tree<" in ks.source and "mbar_wait(&own_bar" not in ks.source
     runtime.compile_cubin(ks.source)
     # the left-fold alternative: two warps handing the CTA's prefix over
     monkeypatch.setattr(codegen_scan, "SCAN_TMA_TREE", False)
     monkeypatch.setattr(codegen_scan, "SCAN_TMA_LBW", 2)
     two = _source([gp.cumsum(x * 0.5 + 1.0 + 0.0)]).source
-    assert "gr::round_stage<" in two and "gr::round_fold<" in two and "own_seq != i" in two
+    assert "gr::round_stage<" in two and "gr::round_fold<" in two and "mbar_wait(&own_bar" in two
     runtime.compile_cubin(two)
     monkeypatch.setattr(codegen_scan, "SCAN_TMA_LBW", 1)
     one = _source([gp.cumsum(x * 0.5 + 2.0)]).source
-    assert "gr::tile_lookback_round<" in one and "own_seq != i" not in one
+    assert "gr::tile_lookback_round<" in one and "mbar_wait(&own_bar" not in one
     runtime.compile_cubin(one)
     odd = gp.asarray(np.arange((1 << 20) + 7, dtype=np.float32))
     tail = _source([gp.cumsum(odd)])
